@@ -1,0 +1,183 @@
+/* nasch.h -- C interface of the B200 NaSch engine (libnasch_b200.so).
+ *
+ * Drop-in for the reference's C ABI /root/reference/proj/include/nasch/nasch.h
+ * (36 symbols, reference nasch.h:16-127): same names, signatures, enum
+ * values, ownership and error conventions.  Each declaration below cites
+ * the reference declaration it replaces.  The agent engine runs on the
+ * current CUDA device; there is no CPU fallback -- without a GPU,
+ * nasch_sim_new* fails with NASCH_ERR_INVALID.
+ *
+ * Every fallible entry point returns a nasch_status; on failure
+ * nasch_last_error() describes it for the calling thread.  Handles are
+ * opaque and owned by the caller until the matching _free.
+ */
+#ifndef NASCH_H
+#define NASCH_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* reference nasch.h:16-21 */
+typedef enum nasch_status {
+  NASCH_OK = 0,
+  NASCH_ERR_INVALID = 1, /* bad argument, parameter combination or device failure */
+  NASCH_ERR_PARSE = 2,   /* malformed parameter text */
+  NASCH_ERR_IO = 3       /* file could not be read or written */
+} nasch_status;
+
+/* reference nasch.h:23-27 */
+typedef enum nasch_output_mode {
+  NASCH_OUTPUT_NONE = 0,
+  NASCH_OUTPUT_ASCII = 1,
+  NASCH_OUTPUT_PGM = 2
+} nasch_output_mode;
+
+/* reference nasch.h:29-32, plus the explicit CUDA kind (additive: the
+ * reference rejects unknown kinds, capi.cpp:203-207). */
+typedef enum nasch_engine_kind {
+  NASCH_ENGINE_AGENT = 0,          /* car-array engine (runs on the GPU here) */
+  NASCH_ENGINE_GRID_REFERENCE = 1, /* cell-array engine, workers must be 1 */
+  NASCH_ENGINE_CUDA = 2            /* same as AGENT, named explicitly */
+} nasch_engine_kind;
+
+typedef struct nasch_params nasch_params;
+typedef struct nasch_sim nasch_sim;
+
+/* reference nasch.h:37-40 */
+const char* nasch_last_error(void);
+
+/* ---- parameter sets (reference nasch.h:42-78) ------------------------ */
+
+/* reference nasch.h:44-47: defaults vmax=5, p=0.13, output=none, stride=1. */
+nasch_status nasch_params_new(nasch_params** out);
+/* reference nasch.h:49-55: `key = value` text / file. */
+nasch_status nasch_params_parse(const char* text, nasch_params** out,
+                                unsigned* out_threads);
+nasch_status nasch_params_load(const char* path, nasch_params** out,
+                               unsigned* out_threads);
+void nasch_params_free(nasch_params* params);
+
+/* reference nasch.h:58-66 */
+nasch_status nasch_params_set_length(nasch_params* params, uint64_t length);
+nasch_status nasch_params_set_ncars(nasch_params* params, uint64_t ncars);
+nasch_status nasch_params_set_vmax(nasch_params* params, uint64_t vmax);
+nasch_status nasch_params_set_p(nasch_params* params, double p);
+nasch_status nasch_params_set_steps(nasch_params* params, uint64_t steps);
+nasch_status nasch_params_set_seed(nasch_params* params, uint64_t seed);
+nasch_status nasch_params_set_output(nasch_params* params,
+                                     nasch_output_mode mode);
+nasch_status nasch_params_set_stride(nasch_params* params, uint64_t stride);
+
+/* reference nasch.h:68-75 (0 / NONE for a NULL set) */
+uint64_t nasch_params_length(const nasch_params* params);
+uint64_t nasch_params_ncars(const nasch_params* params);
+uint64_t nasch_params_vmax(const nasch_params* params);
+double nasch_params_p(const nasch_params* params);
+uint64_t nasch_params_steps(const nasch_params* params);
+uint64_t nasch_params_seed(const nasch_params* params);
+nasch_output_mode nasch_params_output(const nasch_params* params);
+uint64_t nasch_params_stride(const nasch_params* params);
+
+/* reference nasch.h:77-78 */
+nasch_status nasch_params_validate(const nasch_params* params);
+
+/* ---- simulations (reference nasch.h:80-122) -------------------------- */
+
+/* reference nasch.h:82-86.  workers >= 1; results are bit-identical for
+ * every value (the B200 engine is geometry-independent). */
+nasch_status nasch_sim_new(const nasch_params* params, unsigned workers,
+                           nasch_sim** out);
+/* reference nasch.h:88-90 */
+nasch_status nasch_sim_new_kind(const nasch_params* params, unsigned workers,
+                                nasch_engine_kind kind, nasch_sim** out);
+void nasch_sim_free(nasch_sim* sim);
+
+/* reference nasch.h:93-97: synchronous; clamps at the configured total. */
+nasch_status nasch_sim_advance(nasch_sim* sim, uint64_t steps);
+nasch_status nasch_sim_run(nasch_sim* sim);
+
+/* reference nasch.h:99-107 (0 for NULL) */
+uint64_t nasch_sim_steps_done(const nasch_sim* sim);
+uint64_t nasch_sim_checksum(const nasch_sim* sim);
+uint64_t nasch_sim_draws(const nasch_sim* sim);
+uint64_t nasch_sim_frame_count(const nasch_sim* sim);
+
+/* reference nasch.h:109-113 */
+nasch_status nasch_sim_observables(const nasch_sim* sim, double* out_density,
+                                   double* out_mean_velocity,
+                                   double* out_flow);
+
+/* reference nasch.h:115-118: increasing-position order. */
+nasch_status nasch_sim_state(const nasch_sim* sim, uint64_t* positions,
+                             uint64_t* velocities, size_t capacity);
+
+/* reference nasch.h:120-122 */
+nasch_status nasch_sim_write_ascii(const nasch_sim* sim, const char* path);
+nasch_status nasch_sim_write_pgm(const nasch_sim* sim, const char* path);
+
+/* reference nasch.h:126-127 */
+unsigned nasch_physical_cores(void);
+
+/* ---- B200 extensions (additive; absent from the reference) ----------- */
+
+/* Replaces the current state with a rank-ordered one: strictly increasing
+ * positions < length, velocities <= vmax (and <= length-1).  steps_done,
+ * draws and checksum are kept, so it doubles as checkpoint restore; the
+ * velocity series restarts.  The reference can only start from its
+ * equally spaced init (engine.cpp:52). */
+nasch_status nasch_sim_set_state(nasch_sim* sim, const uint64_t* positions,
+                                 const uint64_t* velocities, size_t count);
+nasch_status nasch_sim_set_state32(nasch_sim* sim, const uint32_t* positions,
+                                   const uint32_t* velocities, size_t count);
+
+/* The per-step trajectory checksum needs every step's state on the host
+ * (serial FNV-1a, engine.cpp:173-181).  On by default, as in the
+ * reference; pass 0 to stop folding further steps (checksum() then keeps
+ * the value reached). */
+nasch_status nasch_sim_set_checksum(nasch_sim* sim, int enabled);
+
+/* Exact velocity sum / mean velocity after each completed step since the
+ * last set_state (or since step 0).  *count receives the series length;
+ * at most `capacity` values are written. */
+nasch_status nasch_sim_sumv_series(const nasch_sim* sim, uint64_t* out,
+                                   size_t capacity, size_t* count);
+nasch_status nasch_sim_mean_velocity_series(const nasch_sim* sim, double* out,
+                                            size_t capacity, size_t* count);
+/* Number of cars that crossed the origin in each step. */
+nasch_status nasch_sim_wrap_series(const nasch_sim* sim, uint64_t* out,
+                                   size_t capacity, size_t* count);
+
+/* Asynchronous advance on the engine's CUDA stream; nasch_sim_synchronize
+ * completes it.  Steps that need host work (checksum, frames) still
+ * synchronise internally. */
+nasch_status nasch_sim_enqueue(nasch_sim* sim, uint64_t steps);
+nasch_status nasch_sim_synchronize(nasch_sim* sim);
+
+/* The cudaStream_t the engine launches on (for event timing). */
+void* nasch_sim_cuda_stream(const nasch_sim* sim);
+/* Kernel launches issued by this simulation so far. */
+uint64_t nasch_sim_kernel_launches(const nasch_sim* sim);
+
+/* Seeded synthetic input: N distinct uniformly chosen cells of [0, L)
+ * in increasing order, velocities uniform in [0, vmax_init].  Host-only. */
+nasch_status nasch_fill_uniform_state(uint64_t length, uint64_t ncars,
+                                      uint64_t vmax_init, uint64_t seed,
+                                      uint32_t* positions, uint32_t* velocities);
+
+/* Build identification string. */
+const char* nasch_b200_version(void);
+
+/* The integer form of the deceleration test: a draw s decelerates iff
+ * s < threshold, which equals double(s)/double(2^31-1) < p for every s
+ * (src/model.cpp:51). */
+uint32_t nasch_b200_draw_threshold(double p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NASCH_H */

@@ -1,0 +1,523 @@
+// engine.cu -- host side of the B200 ring engine (GpuRing) and the uniform
+// initial-state generator.  Kernels: step_kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "minstd.hpp"
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(call) check((call), #call)
+
+constexpr int kTPB = 256;
+constexpr int kCPT = 4;
+constexpr uint32_t kTile = kTPB * kCPT;
+constexpr int kGraphSteps = 32;
+
+// FNV-1a-64 of one value given as 8 little-endian bytes; values < 2^32 take
+// the 4-byte fold plus four zero-byte multiplies (src/engine.hpp:15-36).
+inline uint64_t fnv_u32(uint64_t h, uint32_t value) {
+  constexpr uint64_t p4 = kFnvPrime * kFnvPrime * kFnvPrime * kFnvPrime;
+  h = (h ^ (value & 0xffu)) * kFnvPrime;
+  h = (h ^ ((value >> 8) & 0xffu)) * kFnvPrime;
+  h = (h ^ ((value >> 16) & 0xffu)) * kFnvPrime;
+  h = (h ^ (value >> 24)) * kFnvPrime;
+  return h * p4;
+}
+
+}  // namespace
+
+struct GpuRing::Impl {
+  SimParams params;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t n = 0, L = 0, vmax_eff = 0, npad = 0;
+  int vbytes = 1;  // 1 => u8 velocities, 4 => u32
+  uint32_t* x[2] = {nullptr, nullptr};
+  void* v[2] = {nullptr, nullptr};
+  uint32_t* blkpow = nullptr;
+  uint32_t* thrpow = nullptr;
+  Ctl* ctl = nullptr;
+  StepRec* rec = nullptr;
+  unsigned long long* dsum = nullptr;
+  int grid = 1;
+  RingArgs args{};
+  cudaGraphExec_t graph = nullptr;
+
+  // host bookkeeping
+  uint64_t steps_done = 0;      // steps enqueued
+  uint64_t drained = 0;         // steps whose records are in sumv_host
+  uint64_t hash = kFnvBasis;
+  bool checksum_on = true;
+  uint64_t sumv0 = 0;           // velocity sum of the state at steps_done == drained base
+  std::vector<uint64_t> sumv_host;  // [k] = sum v after step k+1
+  std::vector<uint64_t> wraps_host;
+  uint64_t series_base = 0;     // step index of sumv_host[0]
+  uint32_t W_host = 0;          // rank offset after `drained` steps
+  uint64_t launches = 0;
+  std::vector<Frame> frames;
+
+  // pinned staging
+  uint32_t* hx = nullptr;
+  void* hv = nullptr;
+  StepRec* hrec = nullptr;
+  Ctl* hctl = nullptr;
+
+  void step_launch() {
+    if (vbytes == 1) {
+      nasch_step_kernel<uint8_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+    } else {
+      nasch_step_kernel<uint32_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+    }
+    ++launches;
+  }
+
+  void build_graph() {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kGraphSteps; ++i) step_launch();
+    launches -= kGraphSteps;
+    CK(cudaStreamEndCapture(stream, &g));
+    CK(cudaGraphInstantiate(&graph, g, 0));
+    CK(cudaGraphDestroy(g));
+  }
+
+  void reset_ctl() {
+    Ctl c{};
+    c.t = steps_done;
+    c.W = 0;
+    c.E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, n, 0)));
+    c.E2 = mulmod(c.E, args.an_inv);
+    c.ticket = 0;
+    *hctl = c;
+    CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+    CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
+    W_host = 0;
+  }
+
+  void compute_sumv0() {
+    CK(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long), stream));
+    const int blocks = std::max(1, std::min<int>((n + kTPB - 1) / kTPB, 1024));
+    const int cur = static_cast<int>(steps_done & 1);
+    if (vbytes == 1) {
+      sum_velocity_kernel<uint8_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint8_t*>(v[cur]), n, dsum);
+    } else {
+      sum_velocity_kernel<uint32_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint32_t*>(v[cur]), n, dsum);
+    }
+    CK(cudaGetLastError());
+    unsigned long long s = 0;
+    CK(cudaMemcpyAsync(&s, dsum, sizeof s, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    sumv0 = s;
+  }
+
+  // Pull per-step records of steps [drained, steps_done) into the host series.
+  void drain() {
+    if (drained == steps_done) return;
+    const uint64_t first = drained, count = steps_done - drained;
+    // records live at t mod kRecCap; copy in at most two segments
+    uint64_t done = 0;
+    while (done < count) {
+      const uint64_t t = first + done;
+      const uint64_t slot = t % kRecCap;
+      const uint64_t seg = std::min<uint64_t>(count - done, kRecCap - slot);
+      CK(cudaMemcpyAsync(hrec + done, rec + slot, seg * sizeof(StepRec), cudaMemcpyDeviceToHost, stream));
+      done += seg;
+    }
+    CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    for (uint64_t k = 0; k < count; ++k) {
+      sumv_host.push_back(hrec[k].sumv);
+      wraps_host.push_back(hrec[k].c);
+    }
+    if (hctl->t != steps_done) {
+      throw std::runtime_error("device step counter out of sync (" + std::to_string(hctl->t) +
+                               " vs " + std::to_string(steps_done) + ")");
+    }
+    W_host = hctl->W;
+    drained = steps_done;
+  }
+
+  // Current state in rank order into pinned staging (hx, hv) -- requires
+  // drained == steps_done.
+  void fetch_rank_order() {
+    const int cur = static_cast<int>(steps_done & 1);
+    const uint32_t head = (n - W_host) % n;  // id of the rank-0 car
+    const uint32_t first = n - head;         // ids head..n-1 -> ranks 0..first-1
+    CK(cudaMemcpyAsync(hx, x[cur] + head, size_t(first) * 4, cudaMemcpyDeviceToHost, stream));
+    if (head) CK(cudaMemcpyAsync(hx + first, x[cur], size_t(head) * 4, cudaMemcpyDeviceToHost, stream));
+    char* hvb = static_cast<char*>(hv);
+    const char* dv = static_cast<const char*>(v[cur]);
+    CK(cudaMemcpyAsync(hvb, dv + size_t(head) * vbytes, size_t(first) * vbytes, cudaMemcpyDeviceToHost, stream));
+    if (head)
+      CK(cudaMemcpyAsync(hvb + size_t(first) * vbytes, dv, size_t(head) * vbytes, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  uint32_t hvel(size_t i) const {
+    return vbytes == 1 ? static_cast<const uint8_t*>(hv)[i] : static_cast<const uint32_t*>(hv)[i];
+  }
+
+  void hash_staged() {
+    uint64_t h = hash;
+    for (uint32_t i = 0; i < n; ++i) h = fnv_u32(h, hx[i]);
+    for (uint32_t i = 0; i < n; ++i) h = fnv_u32(h, hvel(i));
+    hash = h;
+  }
+
+  void record_frame_staged() {
+    Frame f;
+    f.step = steps_done;
+    f.positions.assign(hx, hx + n);
+    f.velocities.resize(n);
+    for (uint32_t i = 0; i < n; ++i) f.velocities[i] = hvel(i);
+    frames.push_back(std::move(f));
+  }
+
+  bool frame_due() const {
+    return params.output_mode != OutputMode::none && steps_done < params.steps &&
+           steps_done % params.output_stride == 0;
+  }
+
+  // src/engine.cpp:81-86
+  void record_frame_if_due() {
+    if (!frame_due()) return;
+    drain();
+    fetch_rank_order();
+    record_frame_staged();
+  }
+
+  void enqueue_steps(uint64_t count) {
+    while (count > 0) {
+      // keep at most kRecCap-1 undrained steps in flight (the last block of
+      // step t zeroes slot (t+1) mod kRecCap)
+      if (steps_done - drained + std::min<uint64_t>(count, kGraphSteps) > kRecCap - 1) drain();
+      if (count >= static_cast<uint64_t>(kGraphSteps)) {
+        if (!graph) build_graph();
+        CK(cudaGraphLaunch(graph, stream));
+        launches += kGraphSteps;
+        steps_done += kGraphSteps;
+        count -= kGraphSteps;
+      } else {
+        step_launch();
+        CK(cudaGetLastError());
+        ++steps_done;
+        --count;
+      }
+    }
+  }
+
+  void advance(uint64_t steps, bool sync) {
+    const uint64_t count = std::min(steps, params.steps - steps_done);
+    if (count == 0) return;
+    const bool per_step = checksum_on || params.output_mode != OutputMode::none;
+    if (!per_step) {
+      enqueue_steps(count);
+      if (sync) drain();
+      return;
+    }
+    // Checksum and frames need every step's rank-ordered state on the host
+    // (src/engine.cpp:173-181); the reference pays this serially too.
+    for (uint64_t k = 0; k < count; ++k) {
+      enqueue_steps(1);
+      const bool frame = frame_due();
+      if (checksum_on || frame) {
+        drain();
+        fetch_rank_order();
+        if (checksum_on) hash_staged();
+        if (frame) record_frame_staged();
+      }
+    }
+    if (sync) drain();
+  }
+
+  void load_state(const uint32_t* hx_in, const uint32_t* hv_in) {
+    // validation (rank order): strictly ascending positions < L,
+    // velocities <= vmax (acceptance.cpp:118-123 invariants) and <= L-1.
+    for (uint32_t i = 0; i < n; ++i) {
+      if (hx_in[i] >= L) throw std::invalid_argument("position out of range [0, length)");
+      if (i && hx_in[i - 1] >= hx_in[i])
+        throw std::invalid_argument("positions must be strictly increasing");
+      if (hv_in[i] > params.v_max) throw std::invalid_argument("velocity above vmax");
+      if (hv_in[i] > vmax_eff)
+        throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+    }
+    drain();
+    const int cur = static_cast<int>(steps_done & 1);
+    std::memcpy(hx, hx_in, size_t(n) * 4);
+    CK(cudaMemcpyAsync(x[cur], hx, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
+    if (vbytes == 4) {
+      std::memcpy(hv, hv_in, size_t(n) * 4);
+      CK(cudaMemcpyAsync(v[cur], hv, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
+    } else {
+      uint8_t* hb = static_cast<uint8_t*>(hv);
+      for (uint32_t i = 0; i < n; ++i) hb[i] = static_cast<uint8_t>(hv_in[i]);
+      CK(cudaMemcpyAsync(v[cur], hv, size_t(n), cudaMemcpyHostToDevice, stream));
+    }
+    reset_ctl();
+    compute_sumv0();
+    series_base = steps_done;
+    sumv_host.clear();
+    wraps_host.clear();
+    if (steps_done == 0) {
+      frames.clear();
+      record_frame_if_due();
+    }
+  }
+};
+
+GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
+  Impl& d = *impl_;
+  params.validate();
+  d.params = params;
+  if (params.road_length > 2147483647ull) {
+    throw std::invalid_argument("length above 2^31-1 is not supported by the B200 engine");
+  }
+  int ndev = 0;
+  const cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    throw std::runtime_error(std::string("no CUDA device available for the B200 engine (") +
+                             cudaGetErrorString(e) + ")");
+  }
+  CK(cudaGetDevice(&d.device));
+  d.n = static_cast<uint32_t>(params.car_count);
+  d.L = static_cast<uint32_t>(params.road_length);
+  d.vmax_eff = static_cast<uint32_t>(std::min<uint64_t>(params.v_max, params.road_length - 1));
+  d.vbytes = d.vmax_eff <= 255 ? 1 : 4;
+  d.npad = ((d.n + kTile - 1) / kTile) * kTile;
+
+  CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    CK(cudaMalloc(&d.x[b], size_t(d.npad) * 4));
+    CK(cudaMalloc(&d.v[b], size_t(d.npad) * d.vbytes));
+  }
+  CK(cudaMalloc(&d.ctl, sizeof(Ctl)));
+  CK(cudaMalloc(&d.rec, sizeof(StepRec) * kRecCap));
+  CK(cudaMalloc(&d.dsum, sizeof(unsigned long long)));
+  CK(cudaMallocHost(&d.hx, size_t(d.n) * 4));
+  CK(cudaMallocHost(&d.hv, size_t(d.n) * d.vbytes));
+  CK(cudaMallocHost(&d.hrec, sizeof(StepRec) * kRecCap));
+  CK(cudaMallocHost(&d.hctl, sizeof(Ctl)));
+
+  // Persistent grid: resident blocks on every SM, never more than tiles.
+  int sms = 0, per_sm = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
+  if (d.vbytes == 1) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB>, kTPB, 0));
+  } else {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint32_t, kTPB>, kTPB, 0));
+  }
+  const uint32_t ntiles = d.npad / kTile;
+  d.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
+  // Test knob: force a grid size, to show results do not depend on the
+  // launch geometry (the reference's W-invariance, test_engine.cpp:136-152).
+  if (const char* g = std::getenv("NASCH_B200_GRID")) {
+    const long want = std::strtol(g, nullptr, 10);
+    if (want > 0) d.grid = static_cast<int>(std::min<long>(want, 1 << 20));
+  }
+
+  // Geometry-dependent draw multipliers.
+  std::vector<uint32_t> blk(d.grid), thr(kTPB);
+  for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * kTile);
+  for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, uint64_t(t) * kCPT);
+  CK(cudaMalloc(&d.blkpow, blk.size() * 4));
+  CK(cudaMalloc(&d.thrpow, thr.size() * 4));
+  CK(cudaMemcpy(d.blkpow, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d.thrpow, thr.data(), thr.size() * 4, cudaMemcpyHostToDevice));
+
+  RingArgs& a = d.args;
+  a.x[0] = d.x[0];
+  a.x[1] = d.x[1];
+  a.v[0] = d.v[0];
+  a.v[1] = d.v[1];
+  a.n = d.n;
+  a.L = d.L;
+  a.vmax = d.vmax_eff;
+  a.tp = deceleration_threshold(params.p);
+  a.s0 = seeded(params.seed);
+  a.an_inv = powmod(kA, kOrder - (d.n % kOrder));
+  a.a1 = powmod(kA, (1 + kOrder - (d.n % kOrder)) % kOrder);
+  a.g = powmod(kA, uint64_t(d.grid) * kTile);
+  a.blkpow = d.blkpow;
+  a.thrpow = d.thrpow;
+  a.ctl = d.ctl;
+  a.rec = d.rec;
+
+  // init_state (model.cpp:30-40) on the device.
+  const int ib = std::max(1, std::min<int>((d.npad + kTPB - 1) / kTPB, 4096));
+  if (d.vbytes == 1) {
+    init_state_kernel<uint8_t><<<ib, kTPB, 0, d.stream>>>(d.x[0], static_cast<uint8_t*>(d.v[0]), d.n, d.npad, d.L);
+    init_state_kernel<uint8_t><<<ib, kTPB, 0, d.stream>>>(d.x[1], static_cast<uint8_t*>(d.v[1]), d.n, d.npad, d.L);
+  } else {
+    init_state_kernel<uint32_t><<<ib, kTPB, 0, d.stream>>>(d.x[0], static_cast<uint32_t*>(d.v[0]), d.n, d.npad, d.L);
+    init_state_kernel<uint32_t><<<ib, kTPB, 0, d.stream>>>(d.x[1], static_cast<uint32_t*>(d.v[1]), d.n, d.npad, d.L);
+  }
+  CK(cudaGetLastError());
+  d.reset_ctl();
+  d.sumv0 = 0;
+  CK(cudaStreamSynchronize(d.stream));
+  d.record_frame_if_due();
+}
+
+GpuRing::~GpuRing() {
+  Impl& d = *impl_;
+  if (d.stream) cudaStreamSynchronize(d.stream);
+  if (d.graph) cudaGraphExecDestroy(d.graph);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(d.x[b]);
+    cudaFree(d.v[b]);
+  }
+  cudaFree(d.ctl);
+  cudaFree(d.rec);
+  cudaFree(d.dsum);
+  cudaFree(d.blkpow);
+  cudaFree(d.thrpow);
+  cudaFreeHost(d.hx);
+  cudaFreeHost(d.hv);
+  cudaFreeHost(d.hrec);
+  cudaFreeHost(d.hctl);
+  if (d.stream) cudaStreamDestroy(d.stream);
+}
+
+void GpuRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  if (n != d.n) throw std::invalid_argument("state length must equal ncars");
+  std::vector<uint32_t> x32(n), v32(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (x[i] >= d.L) throw std::invalid_argument("position out of range [0, length)");
+    if (v[i] > d.params.v_max) throw std::invalid_argument("velocity above vmax");
+    if (v[i] > d.vmax_eff) throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+    x32[i] = static_cast<uint32_t>(x[i]);
+    v32[i] = static_cast<uint32_t>(v[i]);
+  }
+  d.load_state(x32.data(), v32.data());
+}
+
+void GpuRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  if (n != d.n) throw std::invalid_argument("state length must equal ncars");
+  d.load_state(x, v);
+}
+
+void GpuRing::advance(uint64_t steps) {
+  CK(cudaSetDevice(impl_->device));
+  impl_->advance(steps, true);
+}
+
+void GpuRing::enqueue(uint64_t steps) {
+  CK(cudaSetDevice(impl_->device));
+  impl_->advance(steps, false);
+}
+
+void GpuRing::synchronize() {
+  CK(cudaSetDevice(impl_->device));
+  impl_->drain();
+}
+
+uint64_t GpuRing::steps_done() const { return impl_->steps_done; }
+uint64_t GpuRing::checksum() const { return impl_->hash; }
+uint64_t GpuRing::draws() const { return impl_->steps_done * impl_->params.car_count; }
+const std::vector<Frame>& GpuRing::frames() const { return impl_->frames; }
+const SimParams& GpuRing::params() const { return impl_->params; }
+
+void GpuRing::observables(double* density, double* mean_velocity, double* flow) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  d.drain();
+  const uint64_t total = d.sumv_host.empty() ? d.sumv0 : d.sumv_host.back();
+  const double n = static_cast<double>(d.params.car_count);
+  const double mean = static_cast<double>(total) / n;
+  const double dens = n / static_cast<double>(d.params.road_length);
+  if (density) *density = dens;
+  if (mean_velocity) *mean_velocity = mean;
+  if (flow) *flow = dens * mean;
+}
+
+void GpuRing::state(uint64_t* positions, uint64_t* velocities) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  d.drain();
+  d.fetch_rank_order();
+  if (positions)
+    for (uint32_t i = 0; i < d.n; ++i) positions[i] = d.hx[i];
+  if (velocities)
+    for (uint32_t i = 0; i < d.n; ++i) velocities[i] = d.hvel(i);
+}
+
+size_t GpuRing::sumv_series(uint64_t* out, size_t cap) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  d.drain();
+  const size_t k = std::min(cap, d.sumv_host.size());
+  if (out) std::memcpy(out, d.sumv_host.data(), k * sizeof(uint64_t));
+  return d.sumv_host.size();
+}
+
+size_t GpuRing::wrap_series(uint64_t* out, size_t cap) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  d.drain();
+  const size_t k = std::min(cap, d.wraps_host.size());
+  if (out) std::memcpy(out, d.wraps_host.data(), k * sizeof(uint64_t));
+  return d.wraps_host.size();
+}
+
+void GpuRing::set_checksum(bool enabled) { impl_->checksum_on = enabled; }
+bool GpuRing::checksum_enabled() const { return impl_->checksum_on; }
+void* GpuRing::cuda_stream() const { return impl_->stream; }
+uint64_t GpuRing::kernel_launches() const { return impl_->launches; }
+int GpuRing::velocity_bytes() const { return impl_->vbytes; }
+
+// Selection sampling (Knuth Vol. 2, Algorithm S): cell c is chosen with
+// probability need/(L - c), which yields every N-subset of [0, L) with
+// equal probability, already sorted.  splitmix64 streams, Lemire's
+// multiply-shift for the bounded draw.  Velocities come from a second
+// stream.  Deterministic for (L, N, vmax_init, seed).
+void fill_uniform_state(uint64_t L, uint64_t N, uint64_t vmax_init, uint64_t seed,
+                        uint32_t* x, uint32_t* v) {
+  if (N > L || L > 0xffffffffull) throw std::invalid_argument("need N <= L < 2^32");
+  auto mix = [](uint64_t& s) {
+    uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  uint64_t s = seed * 0x2545f4914f6cdd1dull + 0x1234567ull;
+  uint64_t need = N;
+  uint64_t k = 0;
+  for (uint64_t c = 0; c < L && need > 0; ++c) {
+    const uint64_t left = L - c;
+    if (need == left) {  // must take every remaining cell
+      for (uint64_t r = c; r < L; ++r) x[k++] = static_cast<uint32_t>(r);
+      break;
+    }
+    const uint64_t r = mix(s) >> 32;  // 32 random bits
+    if (((r * left) >> 32) < need) {
+      x[k++] = static_cast<uint32_t>(c);
+      --need;
+    }
+  }
+  uint64_t sv = seed ^ 0xa5a5a5a5deadbeefull;
+  for (uint64_t i = 0; i < N; ++i) {
+    v[i] = vmax_init ? static_cast<uint32_t>(((mix(sv) >> 32) * (vmax_init + 1)) >> 32) : 0u;
+  }
+}
+
+}  // namespace nb200

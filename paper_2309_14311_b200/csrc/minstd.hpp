@@ -1,0 +1,77 @@
+// minstd.hpp -- counter-based restatement of the reference's single
+// shared minstd stream (a = 48271, c = 0, m = 2^31-1; src/lcg.hpp:21-56).
+//
+// The reference draws the (t*N + r + 1)-th generator output for the car of
+// rank r at step t (one draw per car per step in rank order,
+// src/model.cpp:42-75, src/engine.cpp:62-72 + 115-145).  With c = 0 and m
+// prime that output is s0 * a^(t*N + r + 1) mod m, with exponents reducible
+// mod (m-1) (Fermat), so any draw is O(1) mulmods away from any other --
+// this is what makes the GPU step independent of launch geometry and GPU
+// count, as the reference's jump-ahead does for OpenMP team size.
+//
+// The Bernoulli test `double(s)/double(m) < p` (src/model.cpp:51) is
+// replaced by the exact integer test `s < threshold(p)`: IEEE division is
+// correctly rounded hence monotone in s, so {s : fl(s/m) < p} is a prefix
+// [0, T_p) of the integers, and T_p is found by bisection with the very
+// same binary64 expression (tests/test_minstd.py checks the boundary).
+#pragma once
+#include <cstdint>
+
+#if defined(__CUDACC__)
+#define NB_HD __host__ __device__ __forceinline__
+#else
+#define NB_HD inline
+#endif
+
+namespace nb200 {
+
+constexpr uint32_t kA = 48271u;         // src/lcg.hpp:22
+constexpr uint32_t kM = 2147483647u;    // src/lcg.hpp:23
+constexpr uint64_t kOrder = kM - 1ull;  // multiplicative order bound
+
+// x*y mod (2^31-1) for x, y < 2^31: Mersenne fold of the <2^62 product.
+NB_HD uint32_t mulmod(uint32_t x, uint32_t y) {
+  const uint64_t p = static_cast<uint64_t>(x) * y;
+  uint32_t r = static_cast<uint32_t>(p & kM) + static_cast<uint32_t>(p >> 31);
+  return r >= kM ? r - kM : r;
+}
+
+// a^e mod m by square-and-multiply (host side / one-off device use).
+NB_HD uint32_t powmod(uint32_t base, uint64_t e) {
+  e %= kOrder;
+  uint32_t result = 1, b = base % kM;
+  while (e) {
+    if (e & 1) result = mulmod(result, b);
+    b = mulmod(b, b);
+    e >>= 1;
+  }
+  return result;
+}
+
+// src/lcg.cpp:11-16: state = seed mod m, zero escapes to one.
+NB_HD uint32_t seeded(uint64_t seed) {
+  const uint32_t s = static_cast<uint32_t>(seed % kM);
+  return s == 0 ? 1u : s;
+}
+
+// Exponent (t*N + 1 + w) mod (m-1) without overflow; t, n arbitrary u64.
+NB_HD uint64_t draw_exponent(uint64_t t, uint64_t n, uint64_t w) {
+  const uint64_t tn = ((t % kOrder) * (n % kOrder)) % kOrder;
+  return (tn + 1 + (w % kOrder)) % kOrder;
+}
+
+// Host-only: smallest s in [0, m] with double(s)/double(m) >= p.
+inline uint32_t deceleration_threshold(double p) {
+  uint64_t lo = 0, hi = kM;  // invariant: answer in [lo, hi]
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) / 2;
+    if (static_cast<double>(mid) / static_cast<double>(kM) < p) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  return static_cast<uint32_t>(lo);
+}
+
+}  // namespace nb200

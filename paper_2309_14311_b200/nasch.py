@@ -1,0 +1,247 @@
+"""Python mirror of the reference's simulation interface over the C ABI.
+
+Class and method names follow the reference C++ types so parity tests read
+like the reference's own tests:
+
+* ``SimParams``  -- nasch::SimParams / nasch_params (src/model.hpp:16-28,
+  include/nasch/nasch.h:42-78)
+* ``Engine``     -- nasch::Engine / nasch_sim (src/engine.hpp:84-126,
+  include/nasch/nasch.h:80-122): advance, run, steps_done, checksum,
+  draws_consumed, frames, snapshot, observables
+
+Errors surface as exceptions carrying the ABI status: ``ParamError``
+(NASCH_ERR_PARSE), ``IoError`` (NASCH_ERR_IO), ``NaschError``
+(NASCH_ERR_INVALID), as the reference folds its exceptions
+(src/capi.cpp:27-44).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import capi as _capi
+
+_MODES = {"none": 0, "ascii": 1, "pgm": 2}
+_MODE_NAMES = {v: k for k, v in _MODES.items()}
+
+
+class NaschError(RuntimeError):
+    status = _capi.NASCH_ERR_INVALID
+
+
+class ParamError(NaschError):
+    status = _capi.NASCH_ERR_PARSE
+
+
+class IoError(NaschError):
+    status = _capi.NASCH_ERR_IO
+
+
+def _lib():
+    return _capi.load()
+
+
+def _check(status: int) -> None:
+    if status == _capi.NASCH_OK:
+        return
+    msg = _lib().nasch_last_error().decode()
+    cls = {_capi.NASCH_ERR_PARSE: ParamError, _capi.NASCH_ERR_IO: IoError}.get(status, NaschError)
+    raise cls(msg)
+
+
+def _u64p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def _u32p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_uint32))
+
+
+class SimParams:
+    """Owned nasch_params handle (defaults vmax=5, p=0.13, output none)."""
+
+    def __init__(self, length: int = 0, ncars: int = 0, vmax: int = 5, p: float = 0.13,
+                 steps: int = 0, seed: int = 0, output: str = "none", stride: int = 1,
+                 *, _handle=None):
+        lib = _lib()
+        if _handle is None:
+            h = C.c_void_p()
+            _check(lib.nasch_params_new(C.byref(h)))
+            self._h = h
+            self.length, self.ncars, self.vmax, self.p = length, ncars, vmax, p
+            self.steps, self.seed, self.output, self.stride = steps, seed, output, stride
+        else:
+            self._h = _handle
+
+    @classmethod
+    def parse(cls, text: str) -> tuple["SimParams", int]:
+        h, threads = C.c_void_p(), C.c_uint(0)
+        _check(_lib().nasch_params_parse(text.encode(), C.byref(h), C.byref(threads)))
+        return cls(_handle=h), threads.value
+
+    @classmethod
+    def load(cls, path: str) -> tuple["SimParams", int]:
+        h, threads = C.c_void_p(), C.c_uint(0)
+        _check(_lib().nasch_params_load(str(path).encode(), C.byref(h), C.byref(threads)))
+        return cls(_handle=h), threads.value
+
+    def validate(self) -> None:
+        _check(_lib().nasch_params_validate(self._h))
+
+    def _set(self, name, value):
+        _check(getattr(_lib(), "nasch_params_set_" + name)(self._h, value))
+
+    def _get(self, name):
+        return getattr(_lib(), "nasch_params_" + name)(self._h)
+
+    length = property(lambda s: s._get("length"), lambda s, v: s._set("length", v))
+    ncars = property(lambda s: s._get("ncars"), lambda s, v: s._set("ncars", v))
+    vmax = property(lambda s: s._get("vmax"), lambda s, v: s._set("vmax", v))
+    p = property(lambda s: s._get("p"), lambda s, v: s._set("p", float(v)))
+    steps = property(lambda s: s._get("steps"), lambda s, v: s._set("steps", v))
+    seed = property(lambda s: s._get("seed"), lambda s, v: s._set("seed", v))
+    stride = property(lambda s: s._get("stride"), lambda s, v: s._set("stride", v))
+    output = property(lambda s: _MODE_NAMES[s._get("output")],
+                      lambda s, v: s._set("output", _MODES[v]))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().nasch_params_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Engine:
+    """A simulation on the B200 engine (nasch_sim)."""
+
+    AGENT, GRID_REFERENCE, CUDA = 0, 1, 2
+
+    def __init__(self, params: SimParams, workers: int = 1, kind: int = 0):
+        h = C.c_void_p()
+        _check(_lib().nasch_sim_new_kind(params._h, workers, kind, C.byref(h)))
+        self._h = h
+        self.ncars = params.ncars
+        self.length = params.length
+
+    # -- stepping ------------------------------------------------------
+    def advance(self, steps: int) -> None:
+        _check(_lib().nasch_sim_advance(self._h, steps))
+
+    def run(self) -> None:
+        _check(_lib().nasch_sim_run(self._h))
+
+    def enqueue(self, steps: int) -> None:
+        _check(_lib().nasch_sim_enqueue(self._h, steps))
+
+    def synchronize(self) -> None:
+        _check(_lib().nasch_sim_synchronize(self._h))
+
+    # -- accessors -------------------------------------------------------
+    @property
+    def steps_done(self) -> int:
+        return _lib().nasch_sim_steps_done(self._h)
+
+    @property
+    def checksum(self) -> int:
+        return _lib().nasch_sim_checksum(self._h)
+
+    @property
+    def draws_consumed(self) -> int:
+        return _lib().nasch_sim_draws(self._h)
+
+    @property
+    def frame_count(self) -> int:
+        return _lib().nasch_sim_frame_count(self._h)
+
+    @property
+    def kernel_launches(self) -> int:
+        return _lib().nasch_sim_kernel_launches(self._h)
+
+    @property
+    def cuda_stream(self) -> int:
+        return _lib().nasch_sim_cuda_stream(self._h) or 0
+
+    def set_checksum(self, enabled: bool) -> None:
+        _check(_lib().nasch_sim_set_checksum(self._h, 1 if enabled else 0))
+
+    def snapshot(self, *, out_x=None, out_v=None):
+        """Current (positions, velocities) in increasing-position order."""
+        x = np.empty(self.ncars, np.uint64) if out_x is None else out_x
+        v = np.empty(self.ncars, np.uint64) if out_v is None else out_v
+        _check(_lib().nasch_sim_state(self._h, _u64p(x), _u64p(v), self.ncars))
+        return x, v
+
+    def observables(self) -> tuple[float, float, float]:
+        """(density, mean_velocity, flow) as nasch_sim_observables."""
+        d, m, f = C.c_double(), C.c_double(), C.c_double()
+        _check(_lib().nasch_sim_observables(self._h, C.byref(d), C.byref(m), C.byref(f)))
+        return d.value, m.value, f.value
+
+    def set_state(self, x, v) -> None:
+        x = np.ascontiguousarray(x)
+        v = np.ascontiguousarray(v)
+        if x.dtype == np.uint32 and v.dtype == np.uint32:
+            _check(_lib().nasch_sim_set_state32(self._h, _u32p(x), _u32p(v), len(x)))
+        else:
+            x = np.ascontiguousarray(x, np.uint64)
+            v = np.ascontiguousarray(v, np.uint64)
+            _check(_lib().nasch_sim_set_state(self._h, _u64p(x), _u64p(v), len(x)))
+
+    def _series(self, fn, dtype, ptr):
+        n = C.c_size_t()
+        _check(fn(self._h, None, 0, C.byref(n)))
+        out = np.empty(n.value, dtype)
+        _check(fn(self._h, ptr(out), n.value, C.byref(n)))
+        return out
+
+    def sumv_series(self) -> np.ndarray:
+        return self._series(_lib().nasch_sim_sumv_series, np.uint64, _u64p)
+
+    def wrap_series(self) -> np.ndarray:
+        return self._series(_lib().nasch_sim_wrap_series, np.uint64, _u64p)
+
+    def mean_velocity_series(self) -> np.ndarray:
+        return self._series(_lib().nasch_sim_mean_velocity_series, np.float64,
+                            lambda a: a.ctypes.data_as(C.POINTER(C.c_double)))
+
+    def write_ascii(self, path: str) -> None:
+        _check(_lib().nasch_sim_write_ascii(self._h, str(path).encode()))
+
+    def write_pgm(self, path: str) -> None:
+        _check(_lib().nasch_sim_write_pgm(self._h, str(path).encode()))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().nasch_sim_free(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fill_uniform_state(length: int, ncars: int, vmax_init: int, seed: int):
+    """BASELINE inputs: sorted distinct uniform positions (u32) and
+    velocities uniform in [0, vmax_init] (u32)."""
+    x = np.empty(ncars, np.uint32)
+    v = np.empty(ncars, np.uint32)
+    _check(_lib().nasch_fill_uniform_state(length, ncars, vmax_init, seed, _u32p(x), _u32p(v)))
+    return x, v
+
+
+def physical_cores() -> int:
+    return _lib().nasch_physical_cores()
