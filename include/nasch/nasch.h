@@ -161,6 +161,9 @@ nasch_status nasch_sim_synchronize(nasch_sim* sim);
 void* nasch_sim_cuda_stream(const nasch_sim* sim);
 /* Kernel launches issued by this simulation so far. */
 uint64_t nasch_sim_kernel_launches(const nasch_sim* sim);
+/* Steps one step-kernel launch advances (temporal-blocking depth K, or 1
+ * for rings too small to block; env NASCH_B200_K caps K). */
+unsigned nasch_sim_steps_per_launch(const nasch_sim* sim);
 
 /* Seeded synthetic input: N distinct uniformly chosen cells of [0, L)
  * in increasing order, velocities uniform in [0, vmax_init].  Host-only. */

@@ -1,5 +1,12 @@
 // engine.cu -- host side of the B200 ring engine (GpuRing) and the uniform
 // initial-state generator.  Kernels: step_kernels.cuh.
+//
+// Mode selection (per simulation, fixed at construction):
+//   TB  -- nasch_tb_kernel, K steps per launch (temporal blocking) with the
+//          origin-cone plan; used when the ring is long enough
+//          (N >= 2*2048, L > K*vmax, K*(vmax+1) <= 256).
+//   K1  -- nasch_step_kernel, one step per launch; any ring.
+// Both are bit-identical to the reference; tests cover each.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,9 +32,21 @@ void check(cudaError_t e, const char* what) {
 #define CK(call) check((call), #call)
 
 constexpr int kTPB = 256;
-constexpr int kCPT = 4;
-constexpr uint32_t kTile = kTPB * kCPT;
-constexpr int kGraphSteps = 32;
+// single-step kernel geometry
+constexpr int kCPT1 = 4;
+constexpr uint32_t kTile1 = kTPB * kCPT1;
+// temporal-blocked kernel geometry
+constexpr int kCPTB = 8;
+constexpr int kHalo = 16;
+constexpr uint32_t kLoadTB = kTPB * kCPTB;       // 2048 cars loaded per tile
+constexpr uint32_t kStoreTB = kLoadTB - kHalo;   // 2032 cars owned per tile
+constexpr int kGraphLaunches = 16;
+
+long env_long(const char* name, long fallback) {
+  const char* s = std::getenv(name);
+  if (!s || !*s) return fallback;
+  return std::strtol(s, nullptr, 10);
+}
 
 // FNV-1a-64 of one value given as 8 little-endian bytes; values < 2^32 take
 // the 4-byte fold plus four zero-byte multiplies (src/engine.hpp:15-36).
@@ -47,7 +66,9 @@ struct GpuRing::Impl {
   int device = 0;
   cudaStream_t stream = nullptr;
   uint32_t n = 0, L = 0, vmax_eff = 0, npad = 0;
-  int vbytes = 1;  // 1 => u8 velocities, 4 => u32
+  int vbytes = 1;   // 1 => u8 velocities, 4 => u32
+  bool tb = false;  // temporal-blocked mode
+  uint32_t K = 1;   // steps per TB launch
   uint32_t* x[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
   uint32_t* blkpow = nullptr;
@@ -60,15 +81,16 @@ struct GpuRing::Impl {
   cudaGraphExec_t graph = nullptr;
 
   // host bookkeeping
-  uint64_t steps_done = 0;      // steps enqueued
-  uint64_t drained = 0;         // steps whose records are in sumv_host
+  uint64_t steps_done = 0;  // steps enqueued
+  uint64_t drained = 0;     // steps whose records are in the host series
   uint64_t hash = kFnvBasis;
   bool checksum_on = true;
-  uint64_t sumv0 = 0;           // velocity sum of the state at steps_done == drained base
-  std::vector<uint64_t> sumv_host;  // [k] = sum v after step k+1
+  uint64_t sumv0 = 0;       // velocity sum of the state at the last set_state
+  std::vector<uint64_t> sumv_host;  // [k] = sum v after step series_base+k+1
   std::vector<uint64_t> wraps_host;
-  uint64_t series_base = 0;     // step index of sumv_host[0]
-  uint32_t W_host = 0;          // rank offset after `drained` steps
+  uint64_t series_base = 0;
+  uint32_t W_host = 0;      // rank offset after `drained` steps
+  uint32_t buf_host = 0;    // buffer holding the state after `drained` steps
   uint64_t launches = 0;
   std::vector<Frame> frames;
 
@@ -78,46 +100,66 @@ struct GpuRing::Impl {
   StepRec* hrec = nullptr;
   Ctl* hctl = nullptr;
 
-  void step_launch() {
-    if (vbytes == 1) {
-      nasch_step_kernel<uint8_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+  template <typename VT>
+  void launch_tb(uint32_t k) {
+    nasch_tb_kernel<VT, kTPB, kCPTB, kHalo><<<grid, kTPB, 0, stream>>>(args, k);
+  }
+
+  // One launch advancing k steps (k == 1 in single-step mode).
+  void launch(uint32_t k) {
+    if (tb) {
+      if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
     } else {
-      nasch_step_kernel<uint32_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+      if (vbytes == 1) {
+        nasch_step_kernel<uint8_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+      } else {
+        nasch_step_kernel<uint32_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+      }
     }
     ++launches;
   }
 
+  uint32_t steps_per_launch() const { return tb ? K : 1u; }
+
   void build_graph() {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < kGraphSteps; ++i) step_launch();
-    launches -= kGraphSteps;
+    for (int i = 0; i < kGraphLaunches; ++i) launch(steps_per_launch());
+    launches -= kGraphLaunches;
     CK(cudaStreamEndCapture(stream, &g));
     CK(cudaGraphInstantiate(&graph, g, 0));
     CK(cudaGraphDestroy(g));
   }
 
+  // Control block for the current state (W = 0: ids are ranks again).
   void reset_ctl() {
     Ctl c{};
     c.t = steps_done;
     c.W = 0;
+    c.buf = buf_host;
     c.E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, n, 0)));
     c.E2 = mulmod(c.E, args.an_inv);
-    c.ticket = 0;
     *hctl = c;
     CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
     CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
+    if (tb) {
+      if (vbytes == 1) {
+        cone_init_kernel<uint8_t, kTPB><<<1, kTPB, 0, stream>>>(args);
+      } else {
+        cone_init_kernel<uint32_t, kTPB><<<1, kTPB, 0, stream>>>(args);
+      }
+      CK(cudaGetLastError());
+    }
     W_host = 0;
   }
 
   void compute_sumv0() {
     CK(cudaMemsetAsync(dsum, 0, sizeof(unsigned long long), stream));
     const int blocks = std::max(1, std::min<int>((n + kTPB - 1) / kTPB, 1024));
-    const int cur = static_cast<int>(steps_done & 1);
     if (vbytes == 1) {
-      sum_velocity_kernel<uint8_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint8_t*>(v[cur]), n, dsum);
+      sum_velocity_kernel<uint8_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint8_t*>(v[buf_host]), n, dsum);
     } else {
-      sum_velocity_kernel<uint32_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint32_t*>(v[cur]), n, dsum);
+      sum_velocity_kernel<uint32_t><<<blocks, kTPB, 0, stream>>>(static_cast<uint32_t*>(v[buf_host]), n, dsum);
     }
     CK(cudaGetLastError());
     unsigned long long s = 0;
@@ -130,33 +172,36 @@ struct GpuRing::Impl {
   void drain() {
     if (drained == steps_done) return;
     const uint64_t first = drained, count = steps_done - drained;
-    // records live at t mod kRecCap; copy in at most two segments
     uint64_t done = 0;
-    while (done < count) {
-      const uint64_t t = first + done;
-      const uint64_t slot = t % kRecCap;
+    while (done < count) {  // records live at t mod kRecCap
+      const uint64_t slot = (first + done) % kRecCap;
       const uint64_t seg = std::min<uint64_t>(count - done, kRecCap - slot);
       CK(cudaMemcpyAsync(hrec + done, rec + slot, seg * sizeof(StepRec), cudaMemcpyDeviceToHost, stream));
       done += seg;
     }
     CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    for (uint64_t k = 0; k < count; ++k) {
-      sumv_host.push_back(hrec[k].sumv);
-      wraps_host.push_back(hrec[k].c);
+    if (hctl->err) {
+      throw std::runtime_error("origin-cone plan contradicted at step " +
+                               std::to_string(hctl->err_step) + " (engine state is invalid)");
     }
     if (hctl->t != steps_done) {
       throw std::runtime_error("device step counter out of sync (" + std::to_string(hctl->t) +
                                " vs " + std::to_string(steps_done) + ")");
     }
+    for (uint64_t k = 0; k < count; ++k) {
+      sumv_host.push_back(hrec[k].sumv);
+      wraps_host.push_back(hrec[k].c);
+    }
     W_host = hctl->W;
+    buf_host = hctl->buf;
     drained = steps_done;
   }
 
-  // Current state in rank order into pinned staging (hx, hv) -- requires
+  // Current state in rank order into pinned staging (hx, hv); requires
   // drained == steps_done.
   void fetch_rank_order() {
-    const int cur = static_cast<int>(steps_done & 1);
+    const int cur = static_cast<int>(buf_host);
     const uint32_t head = (n - W_host) % n;  // id of the rank-0 car
     const uint32_t first = n - head;         // ids head..n-1 -> ranks 0..first-1
     CK(cudaMemcpyAsync(hx, x[cur] + head, size_t(first) * 4, cudaMemcpyDeviceToHost, stream));
@@ -202,22 +247,26 @@ struct GpuRing::Impl {
     record_frame_staged();
   }
 
+  // Enqueue `count` steps: graph chains of full launches, then a remainder
+  // launch.  Keeps the undrained record window well inside kRecCap (each
+  // launch's last block zeroes the slots of the next plan).
   void enqueue_steps(uint64_t count) {
+    const uint64_t per = steps_per_launch();
+    const uint64_t chunk = per * kGraphLaunches;
     while (count > 0) {
-      // keep at most kRecCap-1 undrained steps in flight (the last block of
-      // step t zeroes slot (t+1) mod kRecCap)
-      if (steps_done - drained + std::min<uint64_t>(count, kGraphSteps) > kRecCap - 1) drain();
-      if (count >= static_cast<uint64_t>(kGraphSteps)) {
+      if (steps_done - drained + std::min(count, chunk) > kRecCap / 2) drain();
+      if (count >= chunk) {
         if (!graph) build_graph();
         CK(cudaGraphLaunch(graph, stream));
-        launches += kGraphSteps;
-        steps_done += kGraphSteps;
-        count -= kGraphSteps;
+        launches += kGraphLaunches;
+        steps_done += chunk;
+        count -= chunk;
       } else {
-        step_launch();
+        const uint32_t k = static_cast<uint32_t>(std::min(count, per));
+        launch(k);
         CK(cudaGetLastError());
-        ++steps_done;
-        --count;
+        steps_done += k;
+        count -= k;
       }
     }
   }
@@ -234,11 +283,13 @@ struct GpuRing::Impl {
     // Checksum and frames need every step's rank-ordered state on the host
     // (src/engine.cpp:173-181); the reference pays this serially too.
     for (uint64_t k = 0; k < count; ++k) {
-      enqueue_steps(1);
+      launch(1);
+      CK(cudaGetLastError());
+      ++steps_done;
       const bool frame = frame_due();
-      if (checksum_on || frame) {
+      if (checksum_on || frame || steps_done - drained > kRecCap / 2) {
         drain();
-        fetch_rank_order();
+        if (checksum_on || frame) fetch_rank_order();
         if (checksum_on) hash_staged();
         if (frame) record_frame_staged();
       }
@@ -258,7 +309,7 @@ struct GpuRing::Impl {
         throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
     }
     drain();
-    const int cur = static_cast<int>(steps_done & 1);
+    const int cur = static_cast<int>(buf_host);
     std::memcpy(hx, hx_in, size_t(n) * 4);
     CK(cudaMemcpyAsync(x[cur], hx, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
     if (vbytes == 4) {
@@ -299,7 +350,18 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   d.L = static_cast<uint32_t>(params.road_length);
   d.vmax_eff = static_cast<uint32_t>(std::min<uint64_t>(params.v_max, params.road_length - 1));
   d.vbytes = d.vmax_eff <= 255 ? 1 : 4;
-  d.npad = ((d.n + kTile - 1) / kTile) * kTile;
+
+  // Temporal blocking: K steps per launch when the origin cone fits one
+  // block and the ring holds at least two full tiles.
+  const long kreq = env_long("NASCH_B200_K", 8);
+  uint32_t K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
+  K = std::min<uint32_t>(K, kTPB / (d.vmax_eff + 1));
+  d.tb = K >= 2 && d.n >= 2 * kLoadTB && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
+  d.K = d.tb ? K : 1;
+  const uint32_t tile = d.tb ? kStoreTB : kTile1;
+  const uint32_t cpt = d.tb ? kCPTB : kCPT1;
+  const uint32_t ntiles = (d.n + tile - 1) / tile;
+  d.npad = ntiles * tile + kLoadTB;  // vector loads of the last tile stay in bounds
 
   CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
@@ -317,24 +379,27 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // Persistent grid: resident blocks on every SM, never more than tiles.
   int sms = 0, per_sm = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
-  if (d.vbytes == 1) {
+  if (d.tb) {
+    if (d.vbytes == 1) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTPB, kCPTB, kHalo>, kTPB, 0));
+    } else {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTPB, kCPTB, kHalo>, kTPB, 0));
+    }
+  } else if (d.vbytes == 1) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB>, kTPB, 0));
   } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint32_t, kTPB>, kTPB, 0));
   }
-  const uint32_t ntiles = d.npad / kTile;
   d.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
   // Test knob: force a grid size, to show results do not depend on the
   // launch geometry (the reference's W-invariance, test_engine.cpp:136-152).
-  if (const char* g = std::getenv("NASCH_B200_GRID")) {
-    const long want = std::strtol(g, nullptr, 10);
-    if (want > 0) d.grid = static_cast<int>(std::min<long>(want, 1 << 20));
-  }
+  const long gwant = env_long("NASCH_B200_GRID", 0);
+  if (gwant > 0) d.grid = static_cast<int>(std::min<long>(gwant, 1 << 20));
 
-  // Geometry-dependent draw multipliers.
+  // Geometry-dependent draw multipliers a^(first id of block / thread).
   std::vector<uint32_t> blk(d.grid), thr(kTPB);
-  for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * kTile);
-  for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, uint64_t(t) * kCPT);
+  for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * tile);
+  for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, uint64_t(t) * cpt);
   CK(cudaMalloc(&d.blkpow, blk.size() * 4));
   CK(cudaMalloc(&d.thrpow, thr.size() * 4));
   CK(cudaMemcpy(d.blkpow, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));
@@ -350,9 +415,11 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   a.vmax = d.vmax_eff;
   a.tp = deceleration_threshold(params.p);
   a.s0 = seeded(params.seed);
+  a.an = powmod(kA, d.n);
   a.an_inv = powmod(kA, kOrder - (d.n % kOrder));
   a.a1 = powmod(kA, (1 + kOrder - (d.n % kOrder)) % kOrder);
-  a.g = powmod(kA, uint64_t(d.grid) * kTile);
+  a.g = powmod(kA, uint64_t(d.grid) * tile);
+  a.kplan = d.tb ? d.K : 0;
   a.blkpow = d.blkpow;
   a.thrpow = d.thrpow;
   a.ctl = d.ctl;
@@ -360,14 +427,15 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
 
   // init_state (model.cpp:30-40) on the device.
   const int ib = std::max(1, std::min<int>((d.npad + kTPB - 1) / kTPB, 4096));
-  if (d.vbytes == 1) {
-    init_state_kernel<uint8_t><<<ib, kTPB, 0, d.stream>>>(d.x[0], static_cast<uint8_t*>(d.v[0]), d.n, d.npad, d.L);
-    init_state_kernel<uint8_t><<<ib, kTPB, 0, d.stream>>>(d.x[1], static_cast<uint8_t*>(d.v[1]), d.n, d.npad, d.L);
-  } else {
-    init_state_kernel<uint32_t><<<ib, kTPB, 0, d.stream>>>(d.x[0], static_cast<uint32_t*>(d.v[0]), d.n, d.npad, d.L);
-    init_state_kernel<uint32_t><<<ib, kTPB, 0, d.stream>>>(d.x[1], static_cast<uint32_t*>(d.v[1]), d.n, d.npad, d.L);
+  for (int b = 0; b < 2; ++b) {
+    if (d.vbytes == 1) {
+      init_state_kernel<uint8_t><<<ib, kTPB, 0, d.stream>>>(d.x[b], static_cast<uint8_t*>(d.v[b]), d.n, d.npad, d.L);
+    } else {
+      init_state_kernel<uint32_t><<<ib, kTPB, 0, d.stream>>>(d.x[b], static_cast<uint32_t*>(d.v[b]), d.n, d.npad, d.L);
+    }
   }
   CK(cudaGetLastError());
+  d.buf_host = 0;
   d.reset_ctl();
   d.sumv0 = 0;
   CK(cudaStreamSynchronize(d.stream));
@@ -484,6 +552,7 @@ bool GpuRing::checksum_enabled() const { return impl_->checksum_on; }
 void* GpuRing::cuda_stream() const { return impl_->stream; }
 uint64_t GpuRing::kernel_launches() const { return impl_->launches; }
 int GpuRing::velocity_bytes() const { return impl_->vbytes; }
+int GpuRing::steps_per_launch() const { return static_cast<int>(impl_->steps_per_launch()); }
 
 // Selection sampling (Knuth Vol. 2, Algorithm S): cell c is chosen with
 // probability need/(L - c), which yields every N-subset of [0, L) with

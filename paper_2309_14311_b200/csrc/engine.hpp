@@ -56,6 +56,9 @@ class GpuRing {
   void* cuda_stream() const;
   uint64_t kernel_launches() const;
   int velocity_bytes() const;
+  // Steps advanced per step-kernel launch: K in temporal-blocked mode, 1
+  // in single-step mode (small rings).
+  int steps_per_launch() const;
 
  private:
   struct Impl;

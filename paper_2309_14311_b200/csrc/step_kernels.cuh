@@ -1,33 +1,38 @@
 // step_kernels.cuh -- sm_100a kernels of the NaSch agent step.
 //
-// One launch = one synchronous time step of the whole ring, i.e. the
-// reference's Phase A + Phase B + `omp single` tail of
-// Engine::advance_agent (src/engine.cpp:115-181) and step_serial
-// (src/model.cpp:42-75), fused:
+// The reference's time step (step_serial, src/model.cpp:42-75; the OpenMP
+// form Engine::advance_agent, src/engine.cpp:101-184) for car i in rank
+// order is
+//     gap = (x[i+1] - x[i] - 1) mod L            (model.hpp:60-65)
+//     v   = min(v+1, vmax); v = min(v, gap)       (model.cpp:48-50)
+//     u   = next draw; if (u < p && v > 0) --v   (model.cpp:51-53)
+//     x   = (x + v) mod L, then the wrapped suffix rotates to the front.
 //
-//   per car id (ID order, never rotated; rank(id) = (id + W_t) mod N):
-//     gap   = (x[id+1] - x[id] - 1) mod L          (model.hpp:60-65)
-//     v     = min(v+1, vmax); v = min(v, gap)       (model.cpp:48-50)
-//     s     = minstd output #(t*N + rank + 1)       (counter-based draw)
-//     if (s < T_p && v > 0) --v                     (model.cpp:51-53)
-//     x'    = (x + v) mod L                          (model.cpp:57-66)
-//   reductions: c_t = #cars with x+v >= L  (the reference's wrap count,
-//   engine.cpp:138/150-153) and sum(v') (measure, model.cpp:131-142).
+// B200 restatement:
+//  * Cars are stored in ID order and never rotated.  The rotation only
+//    shifts every rank by the step's wrap count c_t, so
+//    rank(id, t) = (id + W_t) mod N with W_{t+1} = W_t + c_t (mod N), and
+//    the leader of id is always id+1 (mod N).
+//  * The draw of rank r at step t is minstd output #(t*N + r + 1) =
+//    s0 * a^(t*N + 1 + W_t) * a^id  [* a^-N when id >= N - W_t]  (mod m):
+//    one mulmod per car from per-step bases E_t, E2_t = E_t * a^-N.
+//  * u < p  <=>  s < T_p  (integer threshold, minstd.hpp).
 //
-// The rotation of the wrapped suffix (model.cpp:70-73) is never performed:
-// it only shifts every rank by c_t, which W_{t+1} = W_t + c_t absorbs.
-//
-// HBM layout: x as u32[Npad], v as VT[Npad] (u8 when vmax_eff <= 255),
-// ping-pong buffers selected by step parity.  Each thread owns CPT=4
-// consecutive cars per tile: one 16-byte x load, one 4-byte (u8) v load,
-// the leader of its last car via a warp shuffle (lane 31: one extra 4-byte
-// load that hits the line the next warp streams), so HBM sees exactly
-// 4+1 bytes read and 4+1 bytes written per car-update.
-//
-// Step control (W_t, E_t) lives on the device: the LAST block of launch t
-// (ticket pattern) folds the step's wrap count into W_{t+1} and the next
-// draw base, so consecutive launches (a CUDA graph chain) need no host
-// round trip.
+// Two step kernels:
+//  nasch_step_kernel  one launch = one step, streaming (x,v) through HBM
+//                     once; the launch's last block folds c_t into W_{t+1}.
+//  nasch_tb_kernel    one launch = k <= 16 steps (temporal blocking): each
+//                     tile of 2048 consecutive cars (2032 owned + a 16-car
+//                     halo ahead) is loaded once into registers, advanced k
+//                     steps, and the 2032 owned cars stored once, so HBM
+//                     moves ~10/k bytes per car-update.  The k per-step
+//                     rank offsets come from the ORIGIN CONE planner, run
+//                     by the previous launch's last block: only cars with
+//                     x >= L - k*vmax can cross the origin within k steps
+//                     (they are the last k*vmax ranks), and simulating them
+//                     plus the k cars ahead of the origin for k steps
+//                     yields c_t .. c_{t+k-1} exactly.  Every launch
+//                     re-counts the crossings and flags any disagreement.
 #pragma once
 #include <cstdint>
 
@@ -35,12 +40,22 @@
 
 namespace nb200 {
 
+constexpr int kPlanMax = 16;
+
 struct Ctl {
   unsigned long long t;  // steps completed on the device
-  unsigned int W;        // rank offset: rank(id) = (id + W) mod N
-  unsigned int E;        // s0 * a^(t*N + 1 + W) mod m: draw of id 0 if 0 < N-W
-  unsigned int E2;       // E * a^(-N): draw base for ids >= N - W
+  unsigned int W;        // rank offset at step t: rank(id) = (id + W) mod N
+  unsigned int buf;      // which ping-pong buffer holds the state at step t
   unsigned int ticket;   // last-block-done counter
+  unsigned int err;      // != 0: a launch's crossing count contradicted the plan
+  unsigned int E;        // s0 * a^(t*N + 1 + W): draw base of ids < N - W
+  unsigned int E2;       // E * a^(-N): draw base of ids >= N - W
+  unsigned int kplan;    // steps the plan below covers (temporal blocking)
+  unsigned int err_step;
+  unsigned int Wk[kPlanMax];   // W_{t+j}
+  unsigned int Ek[kPlanMax];   // E_{t+j}
+  unsigned int E2k[kPlanMax];  // E2_{t+j}
+  unsigned int ck[kPlanMax];   // predicted c_{t+j}
 };
 
 struct StepRec {
@@ -59,63 +74,87 @@ struct RingArgs {
   uint32_t vmax;    // effective vmax = min(vmax, L-1)
   uint32_t tp;      // deceleration iff draw < tp
   uint32_t s0;      // seeded generator state
+  uint32_t an;      // a^N mod m
   uint32_t an_inv;  // a^(-N) mod m
   uint32_t a1;      // a^(1-N) mod m (step across the rank seam)
-  uint32_t g;       // a^(gridDim.x * TILE) mod m (grid-stride advance)
-  const uint32_t* blkpow;  // a^(blockIdx.x * TILE)
-  const uint32_t* thrpow;  // a^(threadIdx.x * CPT)
+  uint32_t g;       // a^(gridDim.x * tile stride) mod m (grid-stride advance)
+  uint32_t kplan;   // temporal-blocking plan length (0: single-step mode)
+  const uint32_t* blkpow;  // a^(blockIdx.x * tile stride)
+  const uint32_t* thrpow;  // a^(threadIdx.x * cars per thread)
   Ctl* ctl;
   StepRec* rec;     // kRecCap ring indexed by t mod kRecCap
 };
 
-template <typename VT>
-struct VPack;
+// ---- vector access helpers ----------------------------------------------
 
-template <>
-struct VPack<uint8_t> {
-  using raw = uint32_t;
-  static __device__ __forceinline__ raw load(const uint8_t* p) {
-    raw r;
-    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-    return r;
-  }
-  static __device__ __forceinline__ uint32_t get(raw r, int j) { return (r >> (8 * j)) & 0xffu; }
-  static __device__ __forceinline__ void put(raw& r, int j, uint32_t v) { r |= v << (8 * j); }
-  static __device__ __forceinline__ void store(uint8_t* p, raw r) {
-    *reinterpret_cast<uint32_t*>(p) = r;
-  }
-};
-
-template <>
-struct VPack<uint32_t> {
-  using raw = uint4;
-  static __device__ __forceinline__ raw load(const uint32_t* p) {
-    raw r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-    return r;
-  }
-  static __device__ __forceinline__ uint32_t get(const raw& r, int j) {
-    return j == 0 ? r.x : j == 1 ? r.y : j == 2 ? r.z : r.w;
-  }
-  static __device__ __forceinline__ void put(raw& r, int j, uint32_t v) {
-    if (j == 0) r.x = v; else if (j == 1) r.y = v; else if (j == 2) r.z = v; else r.w = v;
-  }
-  static __device__ __forceinline__ void store(uint32_t* p, const raw& r) {
-    *reinterpret_cast<uint4*>(p) = r;
-  }
-};
-
-__device__ __forceinline__ uint4 ld_x4(const uint32_t* p) {
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
   asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
   return r;
 }
-
+__device__ __forceinline__ uint2 ld_nc_v2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_nc_u32(const void* p) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint32_t get4(const uint4& r, int j) {
   return j == 0 ? r.x : j == 1 ? r.y : j == 2 ? r.z : r.w;
 }
+
+// Loads/stores CPT consecutive velocities of type VT into u32 registers.
+template <typename VT, int CPT>
+struct VLanes;
+
+template <>
+struct VLanes<uint8_t, 4> {
+  static __device__ __forceinline__ void load(const uint8_t* p, uint32_t* v) {
+    const uint32_t r = ld_nc_u32(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] = (r >> (8 * j)) & 0xffu;
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+    *reinterpret_cast<uint32_t*>(p) = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+  }
+};
+template <>
+struct VLanes<uint8_t, 8> {
+  static __device__ __forceinline__ void load(const uint8_t* p, uint32_t* v) {
+    const uint2 r = ld_nc_v2(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[j] = (r.x >> (8 * j)) & 0xffu;
+      v[4 + j] = (r.y >> (8 * j)) & 0xffu;
+    }
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+    uint2 r;
+    r.x = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
+    r.y = v[4] | (v[5] << 8) | (v[6] << 16) | (v[7] << 24);
+    *reinterpret_cast<uint2*>(p) = r;
+  }
+};
+template <int CPT>
+struct VLanes<uint32_t, CPT> {
+  static __device__ __forceinline__ void load(const uint32_t* p, uint32_t* v) {
+#pragma unroll
+    for (int q = 0; q < CPT / 4; ++q) {
+      const uint4 r = ld_nc_v4(p + 4 * q);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[4 * q + j] = get4(r, j);
+    }
+  }
+  static __device__ __forceinline__ void store(uint32_t* p, const uint32_t* v) {
+#pragma unroll
+    for (int q = 0; q < CPT / 4; ++q)
+      *reinterpret_cast<uint4*>(p + 4 * q) = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+};
 
 // One car: returns the new velocity; writes the new position and whether
 // it crossed the origin.  All u32: x + v < 2L < 2^32 and xl + (L - x) - 1
@@ -134,22 +173,121 @@ __device__ __forceinline__ uint32_t car_rule(uint32_t x, uint32_t xl, uint32_t v
   return v;
 }
 
+template <typename VT>
+__device__ __forceinline__ const VT* vbuf(const RingArgs& ra, int b) {
+  return static_cast<const VT*>(b ? ra.v[1] : ra.v[0]);
+}
+template <typename VT>
+__device__ __forceinline__ VT* vbuf_w(const RingArgs& ra, int b) {
+  return static_cast<VT*>(b ? ra.v[1] : ra.v[0]);
+}
+__device__ __forceinline__ uint32_t* xbuf(const RingArgs& ra, int b) { return b ? ra.x[1] : ra.x[0]; }
+
+// Ticket pattern: returns true in every thread of the block that finished
+// last (all other blocks' global writes are visible to it).
+__device__ __forceinline__ bool last_block_done(Ctl* ctl) {
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t ticket = atomicAdd(&ctl->ticket, 1u);
+    s_last = (ticket == gridDim.x - 1) ? 1u : 0u;
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  return s_last != 0;
+}
+
+// ---- origin cone planner ---------------------------------------------------
+//
+// Run by ONE block of TPB threads (TPB >= kk*(vmax+1)).  From the state
+// (X, V) at step t with rank offset W, simulates cone cars
+//   i in [0, M)      : the M = kk*vmax highest ranks (ids just behind the
+//                      rank-0 car h = (N - W) mod N) -- every car that can
+//                      reach the origin within kk steps is among them;
+//   i in [M, M + kk) : ranks 0..kk-1, the leaders those cars need;
+// for kk steps with exact draws, and writes W, E, E2 and the crossing count
+// of each step into the plan.  Requires L > kk*vmax and N >= M + kk.
+template <typename VT, int TPB>
+__device__ void cone_plan(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t,
+                          uint32_t W, uint32_t kk, Ctl* ctl) {
+  __shared__ uint32_t s_x[TPB];
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax;
+  const uint32_t M = kk * vmax;
+  const uint32_t C = M + kk;
+  const uint32_t i = threadIdx.x;
+  const bool act = i < C;
+  const uint32_t h = W == 0 ? 0u : N - W;
+  const uint32_t id = static_cast<uint32_t>((uint64_t(h) + (N - M) + i) % N);
+  // .cg loads: the state was just written by other blocks of this launch
+  uint32_t x = act ? __ldcg(X + id) : 0u;
+  uint32_t v = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+  const uint32_t apw = act ? powmod(kA, id) : 1u;
+  uint32_t E = mulmod(ra.s0, powmod(kA, draw_exponent(t, N, W)));
+  uint32_t Wj = W;
+  for (uint32_t j = 0; j < kk; ++j) {
+    s_x[i] = x;
+    __syncthreads();
+    const uint32_t xl = (i + 1 < C) ? s_x[i + 1] : x;  // front-most car: unused
+    const uint32_t E2 = mulmod(E, ra.an_inv);
+    const uint32_t s = mulmod(apw, id < N - Wj ? E : E2);
+    uint32_t xn, cr;
+    v = car_rule(x, xl, v, s, L, vmax, ra.tp, xn, cr);
+    x = xn;
+    const uint32_t c = __syncthreads_count(act && i < M && cr);
+    if (i == 0) {
+      ctl->Wk[j] = Wj;
+      ctl->Ek[j] = E;
+      ctl->E2k[j] = E2;
+      ctl->ck[j] = c;
+    }
+    uint32_t Wn = Wj + c;
+    const bool wrap = Wn >= N;
+    if (wrap) Wn -= N;
+    // E_{t+j+1} = E_{t+j} * a^(N + W_{j+1} - W_j)
+    const uint32_t ac = powmod(kA, c);
+    E = mulmod(E, wrap ? ac : mulmod(ra.an, ac));
+    Wj = Wn;
+  }
+  if (i == 0) {
+    ctl->kplan = kk;
+    ctl->E = ctl->Ek[0];
+    ctl->E2 = ctl->E2k[0];
+  }
+}
+
+// Plan for the current state (after set_state / construction).
+template <typename VT, int TPB>
+__global__ void __launch_bounds__(TPB) cone_init_kernel(const RingArgs ra) {
+  Ctl* ctl = ra.ctl;
+  const int b = static_cast<int>(ctl->buf);
+  const uint64_t t = ctl->t;
+  const uint32_t W = ctl->W;
+  cone_plan<VT, TPB>(ra, xbuf(ra, b), vbuf<VT>(ra, b), t, W, ra.kplan, ctl);
+  for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
+    StepRec* r = ra.rec + ((t + j) % kRecCap);
+    r->sumv = 0;
+    r->c = 0;
+  }
+}
+
+// ---- single-step streaming kernel -----------------------------------------
+
 template <typename VT, int TPB>
 __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
   constexpr int CPT = 4;
   constexpr uint32_t TILE = TPB * CPT;
   const uint32_t N = ra.n;
-  const uint64_t t = ra.ctl->t;
-  const uint32_t W = ra.ctl->W;
-  const uint32_t E = ra.ctl->E;
-  const uint32_t E2 = ra.ctl->E2;
-  const int par = static_cast<int>(t & 1);
-  // select with ternaries: indexing the by-value parameter array with a
-  // runtime index would spill it to local memory
-  const uint32_t* __restrict__ X = par ? ra.x[1] : ra.x[0];
-  const VT* __restrict__ V = static_cast<const VT*>(par ? ra.v[1] : ra.v[0]);
-  uint32_t* __restrict__ Xo = par ? ra.x[0] : ra.x[1];
-  VT* __restrict__ Vo = static_cast<VT*>(par ? ra.v[0] : ra.v[1]);
+  Ctl* ctl = ra.ctl;
+  const uint64_t t = ctl->t;
+  const uint32_t W = ctl->W;
+  const uint32_t E = ctl->E;
+  const uint32_t E2 = ctl->E2;
+  const int b = static_cast<int>(ctl->buf);
+  const uint32_t* __restrict__ X = xbuf(ra, b);
+  const VT* __restrict__ V = vbuf<VT>(ra, b);
+  uint32_t* __restrict__ Xo = xbuf(ra, b ^ 1);
+  VT* __restrict__ Vo = vbuf_w<VT>(ra, b ^ 1);
   const uint32_t bound = N - W;  // ids >= bound draw from E2 (none when W == 0)
   const uint32_t L = ra.L, vmax = ra.vmax, tp = ra.tp;
   const uint32_t lane = threadIdx.x & 31u;
@@ -160,33 +298,31 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
   uint32_t cross = 0;
   const uint32_t ntiles = (N + TILE - 1) / TILE;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t b = tile * TILE + threadIdx.x * CPT;
-    const uint4 xs = ld_x4(X + b);
-    const typename VPack<VT>::raw vs = VPack<VT>::load(V + b);
+    const uint32_t base = tile * TILE + threadIdx.x * CPT;
+    const uint4 xs = ld_nc_v4(X + base);
+    uint32_t vv[CPT];
+    VLanes<VT, CPT>::load(V + base, vv);
     uint32_t xnext = __shfl_down_sync(0xffffffffu, xs.x, 1);
-    if (lane == 31 && b + CPT < N) xnext = __ldg(X + b + CPT);
-    uint32_t s = mulmod(P, b < bound ? E : E2);
+    if (lane == 31 && base + CPT < N) xnext = __ldg(X + base + CPT);
+    uint32_t s = mulmod(P, base < bound ? E : E2);
     P = mulmod(P, ra.g);
 
-    uint4 xo;
-    typename VPack<VT>::raw vo{};
+    uint32_t xo[CPT];
     uint32_t tsum = 0, tcross = 0;
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
-      const uint32_t id = b + j;
+      const uint32_t id = base + j;
       if (j > 0) s = mulmod(s, id == bound ? ra.a1 : kA);
       const uint32_t x = get4(xs, j);
       const uint32_t xl = (id + 1 < N) ? (j + 1 < CPT ? get4(xs, j + 1) : xnext) : x_head;
-      uint32_t xn, cr;
-      const uint32_t vn = car_rule(x, xl, VPack<VT>::get(vs, j), s, L, vmax, tp, xn, cr);
-      if (j == 0) xo.x = xn; else if (j == 1) xo.y = xn; else if (j == 2) xo.z = xn; else xo.w = xn;
-      VPack<VT>::put(vo, j, vn);
+      uint32_t cr;
+      vv[j] = car_rule(x, xl, vv[j], s, L, vmax, tp, xo[j], cr);
       const bool live = id < N;
-      tsum += live ? vn : 0u;
+      tsum += live ? vv[j] : 0u;
       tcross += live ? cr : 0u;
     }
-    *reinterpret_cast<uint4*>(Xo + b) = xo;
-    VPack<VT>::store(Vo + b, vo);
+    *reinterpret_cast<uint4*>(Xo + base) = make_uint4(xo[0], xo[1], xo[2], xo[3]);
+    VLanes<VT, CPT>::store(Vo + base, vv);
     sumv += tsum;
     cross += tcross;
   }
@@ -204,6 +340,7 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
     s_cross[threadIdx.x / 32] = cross;
   }
   __syncthreads();
+  StepRec* rec = ra.rec + (t % kRecCap);
   if (threadIdx.x == 0) {
     unsigned long long bs = 0;
     uint32_t bc = 0;
@@ -212,30 +349,189 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
       bs += s_sum[w];
       bc += s_cross[w];
     }
-    StepRec* rec = ra.rec + (t % kRecCap);
     if (bs) atomicAdd(&rec->sumv, bs);
     if (bc) atomicAdd(&rec->c, bc);
-    __threadfence();
-    const uint32_t ticket = atomicAdd(&ra.ctl->ticket, 1u);
-    if (ticket == gridDim.x - 1) {
-      // Last block: every block's wrap count is in; fold it into the next
-      // step's rank offset and draw base (the rotation, model.cpp:70-73).
-      __threadfence();
-      const uint32_t c = atomicAdd(&rec->c, 0u);
-      uint32_t Wn = W + c;  // W < N, c <= N
-      if (Wn >= N) Wn -= N;
-      const uint32_t En = mulmod(ra.s0, powmod(kA, draw_exponent(t + 1, N, Wn)));
-      rec->W = W;
-      StepRec* nrec = ra.rec + ((t + 1) % kRecCap);
-      nrec->sumv = 0;
-      nrec->c = 0;
-      nrec->W = Wn;
-      ra.ctl->W = Wn;
-      ra.ctl->E = En;
-      ra.ctl->E2 = mulmod(En, ra.an_inv);
-      ra.ctl->t = t + 1;
-      ra.ctl->ticket = 0;
+  }
+  if (last_block_done(ctl) && threadIdx.x == 0) {
+    // Every block's wrap count is in: fold it into the next step's rank
+    // offset and draw base (the rotation, model.cpp:70-73).
+    const uint32_t c = atomicAdd(&rec->c, 0u);
+    uint32_t Wn = W + c;  // W < N, c <= N
+    if (Wn >= N) Wn -= N;
+    const uint32_t En = mulmod(ra.s0, powmod(kA, draw_exponent(t + 1, N, Wn)));
+    rec->W = W;
+    StepRec* nrec = ra.rec + ((t + 1) % kRecCap);
+    nrec->sumv = 0;
+    nrec->c = 0;
+    nrec->W = Wn;
+    ctl->W = Wn;
+    ctl->E = En;
+    ctl->E2 = mulmod(En, ra.an_inv);
+    ctl->t = t + 1;
+    ctl->buf = static_cast<unsigned int>(b ^ 1);
+    ctl->ticket = 0;
+  }
+}
+
+// ---- temporal-blocked kernel ------------------------------------------------
+
+template <typename VT, int TPB, int CPT, int HALO>
+__global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
+  constexpr uint32_t LOAD = TPB * CPT;     // cars loaded per tile
+  constexpr uint32_t STORE = LOAD - HALO;  // cars owned (stored) per tile
+  constexpr int NW = TPB / 32;
+  static_assert(HALO >= kPlanMax && HALO % 16 == 0, "halo must cover the plan");
+  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax];
+  __shared__ unsigned long long s_sum[kPlanMax];
+  __shared__ uint32_t s_cr[kPlanMax];
+  __shared__ uint32_t s_lead[2][NW];
+
+  Ctl* ctl = ra.ctl;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint64_t t = ctl->t;
+  const int b = static_cast<int>(ctl->buf);
+  if (threadIdx.x < kPlanMax) {
+    s_W[threadIdx.x] = ctl->Wk[threadIdx.x];
+    s_E[threadIdx.x] = ctl->Ek[threadIdx.x];
+    s_E2[threadIdx.x] = ctl->E2k[threadIdx.x];
+    s_sum[threadIdx.x] = 0;
+    s_cr[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  const uint32_t* __restrict__ X = xbuf(ra, b);
+  const VT* __restrict__ V = vbuf<VT>(ra, b);
+  uint32_t* __restrict__ Xo = xbuf(ra, b ^ 1);
+  VT* __restrict__ Vo = vbuf_w<VT>(ra, b ^ 1);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t i0 = threadIdx.x * CPT;  // first car of this thread within the tile
+
+  uint32_t P = mulmod(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
+  uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
+  const uint32_t ntiles = (N + STORE - 1) / STORE;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t a0 = tile * STORE;
+    const uint32_t base = a0 + i0;  // id of car 0 (may exceed N in the wrap tile)
+    const bool fast = a0 + LOAD <= N;  // block-uniform
+    uint32_t x[CPT], v[CPT], ap[CPT];
+    if (fast) {
+#pragma unroll
+      for (int q = 0; q < CPT / 4; ++q) {
+        const uint4 r = ld_nc_v4(X + base + 4 * q);
+        x[4 * q] = r.x;
+        x[4 * q + 1] = r.y;
+        x[4 * q + 2] = r.z;
+        x[4 * q + 3] = r.w;
+      }
+      VLanes<VT, CPT>::load(V + base, v);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        uint32_t id = base + c;
+        if (id >= N) id -= N;
+        x[c] = X[id];
+        v[c] = V[id];
+      }
     }
+    // a^id for this thread's cars (id wrapped past N multiplies by a^-N)
+    uint32_t u = P;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (c) u = mulmod(u, kA);
+      ap[c] = (base + c >= N) ? mulmod(u, ra.an_inv) : u;
+    }
+    P = mulmod(P, ra.g);
+    uint32_t own = 0;  // bit c: car c is stored by this tile
+#pragma unroll
+    for (int c = 0; c < CPT; ++c)
+      own |= (i0 + c < STORE && base + c < N) ? (1u << c) : 0u;
+
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t E = s_E[j], E2 = s_E2[j];
+      const uint32_t bound = N - s_W[j];
+      // leader of each warp's last car: lane 0 of the next warp.  Slots
+      // alternate with the running step count, so one barrier per step
+      // suffices (a slot is rewritten only after the next barrier).
+      const uint32_t slot = phase++ & 1u;
+      if (lane == 0) s_lead[slot][warp] = x[0];
+      __syncthreads();
+      uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+      if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
+      uint32_t sum = 0, crs = 0;
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        uint32_t id = base + c;
+        if (id >= N) id -= N;
+        const uint32_t s = mulmod(ap[c], id < bound ? E : E2);
+        const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+        uint32_t xnew, cr;
+        v[c] = car_rule(x[c], xl, v[c], s, L, vmax, tp, xnew, cr);
+        x[c] = xnew;
+        const bool mine = (own >> c) & 1u;
+        sum += mine ? v[c] : 0u;
+        crs += mine ? cr : 0u;
+      }
+      sum = __reduce_add_sync(0xffffffffu, sum);
+      crs = __reduce_add_sync(0xffffffffu, crs);
+      if (lane == 0) {
+        if (sum) atomicAdd(&s_sum[j], static_cast<unsigned long long>(sum));
+        if (crs) atomicAdd(&s_cr[j], crs);
+      }
+    }
+    if (fast) {
+      if (i0 + CPT <= STORE) {
+#pragma unroll
+        for (int q = 0; q < CPT / 4; ++q)
+          *reinterpret_cast<uint4*>(Xo + base + 4 * q) =
+              make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        VLanes<VT, CPT>::store(Vo + base, v);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if ((own >> c) & 1u) {
+          Xo[base + c] = x[c];
+          Vo[base + c] = static_cast<VT>(v[c]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    StepRec* r = ra.rec + ((t + threadIdx.x) % kRecCap);
+    if (s_sum[threadIdx.x]) atomicAdd(&r->sumv, s_sum[threadIdx.x]);
+    if (s_cr[threadIdx.x]) atomicAdd(&r->c, s_cr[threadIdx.x]);
+  }
+  if (!last_block_done(ctl)) return;
+
+  // Last block: check the plan, advance the control block, plan the next k.
+  __shared__ uint32_t s_Wnext;
+  if (threadIdx.x == 0) {
+    for (uint32_t j = 0; j < k; ++j) {
+      StepRec* r = ra.rec + ((t + j) % kRecCap);
+      const uint32_t c = atomicAdd(&r->c, 0u);
+      r->W = ctl->Wk[j];
+      if (c != ctl->ck[j] && !ctl->err) {
+        ctl->err = 1;
+        ctl->err_step = static_cast<unsigned int>(t + j);
+      }
+    }
+    uint32_t Wn = ctl->Wk[k - 1] + ctl->ck[k - 1];
+    if (Wn >= N) Wn -= N;
+    s_Wnext = Wn;
+  }
+  __syncthreads();
+  const uint32_t Wn = s_Wnext;
+  cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
+  for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
+    StepRec* r = ra.rec + ((t + k + j) % kRecCap);
+    r->sumv = 0;
+    r->c = 0;
+  }
+  if (threadIdx.x == 0) {
+    ctl->W = Wn;
+    ctl->t = t + k;
+    ctl->buf = static_cast<unsigned int>(b ^ 1);
+    ctl->ticket = 0;
   }
 }
 
@@ -259,13 +555,6 @@ __global__ void sum_velocity_kernel(const VT* v, uint32_t n, unsigned long long*
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
-}
-
-// u32 staging -> VT narrowing for set_state (velocities validated on host).
-template <typename VT>
-__global__ void narrow_velocity_kernel(const uint32_t* src, VT* dst, uint32_t n) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    dst[i] = static_cast<VT>(src[i]);
 }
 
 }  // namespace nb200

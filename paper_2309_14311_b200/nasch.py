@@ -164,6 +164,10 @@ class Engine:
         return _lib().nasch_sim_kernel_launches(self._h)
 
     @property
+    def steps_per_launch(self) -> int:
+        return _lib().nasch_sim_steps_per_launch(self._h)
+
+    @property
     def cuda_stream(self) -> int:
         return _lib().nasch_sim_cuda_stream(self._h) or 0
 

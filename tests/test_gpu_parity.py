@@ -325,3 +325,66 @@ def test_config3_prefix_vs_oracle(port):
     x, v = e.snapshot()
     assert (np.diff(x.astype(np.int64)) > 0).all() and int(x[-1]) < L and int(v.max()) <= 5
     assert int(v.sum()) == int(e.sumv_series()[-1])
+
+
+# ---- temporal blocking (origin-cone plan) vs single-step vs oracle -------
+
+@pytest.fixture
+def k_env():
+    old = os.environ.get("NASCH_B200_K")
+    yield
+    if old is None:
+        os.environ.pop("NASCH_B200_K", None)
+    else:
+        os.environ["NASCH_B200_K"] = old
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 8, 16])
+def test_temporal_blocking_depths(port, k_env, K):
+    """Rings long enough for the temporal-blocked kernel: every depth K
+    (and the single-step kernel, K=1) is bit-exact with the oracle,
+    including K not dividing the step count and chunked advances."""
+    os.environ["NASCH_B200_K"] = str(K)
+    rng = np.random.default_rng(100 + K)
+    cases = [(20000, 4096, 5, 0.13), (5000, 4100, 5, 0.5), (4096, 4096, 5, 0.3),
+             (300000, 9000, 20, 0.2), (70000, 12000, 40, 0.35), (1 << 20, 70001, 5, 0.7)]
+    for trial, (L, N, vmax, p) in enumerate(cases):
+        x0 = np.sort(rng.choice(L, N, replace=False)).astype(np.uint64)
+        v0 = rng.integers(0, min(vmax, L - 1) + 1, N).astype(np.uint64)
+        T = 53
+        o = port.run(L, vmax, p, 7 + trial, T, x0, v0)
+        e = nasch.Engine(params(L, N, vmax, p, T, 7 + trial))
+        e.set_checksum(False)
+        e.set_state(x0, v0)
+        kk = e.steps_per_launch
+        if K == 1:
+            assert kk == 1
+        e.advance(17)
+        e.advance(36)
+        x, v = e.snapshot()
+        assert (x == o["x"]).all() and (v == o["v"]).all(), (K, kk, trial)
+        assert (e.sumv_series() == o["sumv"]).all()
+        assert (e.wrap_series() == o["wraps"]).all()
+        e.close()
+
+
+def test_temporal_blocking_checksum_mode(port, k_env):
+    """Checksum mode steps one at a time through the TB kernel."""
+    os.environ["NASCH_B200_K"] = "8"
+    L, N = 40000, 6000
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 1)
+    o = port.run(L, 5, 0.25, 1, 40, x0.astype(np.uint64), v0.astype(np.uint64))
+    g = gpu_run(L, N, 5, 0.25, 1, 40, x0, v0)
+    assert_same(g, o)
+
+
+def test_temporal_blocking_long_run_vs_reference(ref, k_env):
+    """Thousands of steps of a dense jammed ring (many crossings per plan)
+    against the reference Engine."""
+    os.environ["NASCH_B200_K"] = "16"
+    L, N = 12000, 7000
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 8)
+    r = ref.run(L, N, 5, 0.5, 8, 3000, x0=x0, v0=v0, workers=4)
+    g = gpu_run(L, N, 5, 0.5, 8, 3000, x0, v0, checksum=False)
+    assert (g["x"] == r["x"]).all() and (g["v"] == r["v"]).all()
+    assert (g["sumv"] == r["sumv"]).all()
