@@ -33,7 +33,7 @@ void check(cudaError_t e, const char* what) {
 
 constexpr int kTPB = 256;
 // single-step kernel geometry
-constexpr int kCPT1 = 4;
+constexpr int kCPT1 = 8;
 constexpr uint32_t kTile1 = kTPB * kCPT1;
 // temporal-blocked kernel geometry
 constexpr int kCPTB = 8;
@@ -111,9 +111,9 @@ struct GpuRing::Impl {
       if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
     } else {
       if (vbytes == 1) {
-        nasch_step_kernel<uint8_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+        nasch_step_kernel<uint8_t, kTPB, kCPT1><<<grid, kTPB, 0, stream>>>(args);
       } else {
-        nasch_step_kernel<uint32_t, kTPB><<<grid, kTPB, 0, stream>>>(args);
+        nasch_step_kernel<uint32_t, kTPB, kCPT1><<<grid, kTPB, 0, stream>>>(args);
       }
     }
     ++launches;
@@ -274,9 +274,25 @@ struct GpuRing::Impl {
   void advance(uint64_t steps, bool sync) {
     const uint64_t count = std::min(steps, params.steps - steps_done);
     if (count == 0) return;
-    const bool per_step = checksum_on || params.output_mode != OutputMode::none;
-    if (!per_step) {
-      enqueue_steps(count);
+    if (!checksum_on) {
+      // Run at full speed between frame steps (every output_stride steps,
+      // src/engine.cpp:81-86); each frame is one rank-ordered D2H.
+      uint64_t left = count;
+      while (left > 0) {
+        uint64_t chunk = left;
+        if (params.output_mode != OutputMode::none) {
+          const uint64_t stride = params.output_stride;
+          const uint64_t next = (steps_done / stride + 1) * stride;  // next frame step
+          chunk = std::min(chunk, next - steps_done);
+        }
+        enqueue_steps(chunk);
+        left -= chunk;
+        if (frame_due()) {
+          drain();
+          fetch_rank_order();
+          record_frame_staged();
+        }
+      }
       if (sync) drain();
       return;
     }
@@ -353,7 +369,7 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
 
   // Temporal blocking: K steps per launch when the origin cone fits one
   // block and the ring holds at least two full tiles.
-  const long kreq = env_long("NASCH_B200_K", 8);
+  const long kreq = env_long("NASCH_B200_K", kPlanMax);
   uint32_t K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
   K = std::min<uint32_t>(K, kTPB / (d.vmax_eff + 1));
   d.tb = K >= 2 && d.n >= 2 * kLoadTB && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
@@ -386,9 +402,9 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTPB, kCPTB, kHalo>, kTPB, 0));
     }
   } else if (d.vbytes == 1) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB>, kTPB, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB, kCPT1>, kTPB, 0));
   } else {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint32_t, kTPB>, kTPB, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint32_t, kTPB, kCPT1>, kTPB, 0));
   }
   d.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
   // Test knob: force a grid size, to show results do not depend on the

@@ -127,16 +127,19 @@ struct VLanes<uint8_t, 8> {
   static __device__ __forceinline__ void load(const uint8_t* p, uint32_t* v) {
     const uint2 r = ld_nc_v2(p);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      v[j] = (r.x >> (8 * j)) & 0xffu;
-      v[4 + j] = (r.y >> (8 * j)) & 0xffu;
+    for (int j = 0; j < 4; ++j) {  // one PRMT per byte
+      v[j] = __byte_perm(r.x, 0u, 0x4440u | j);
+      v[4 + j] = __byte_perm(r.y, 0u, 0x4440u | j);
     }
   }
-  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+  static __device__ __forceinline__ uint2 pack(const uint32_t* v) {
     uint2 r;
-    r.x = v[0] | (v[1] << 8) | (v[2] << 16) | (v[3] << 24);
-    r.y = v[4] | (v[5] << 8) | (v[6] << 16) | (v[7] << 24);
-    *reinterpret_cast<uint2*>(p) = r;
+    r.x = __byte_perm(__byte_perm(v[0], v[1], 0x0040u), __byte_perm(v[2], v[3], 0x0040u), 0x5410u);
+    r.y = __byte_perm(__byte_perm(v[4], v[5], 0x0040u), __byte_perm(v[6], v[7], 0x0040u), 0x5410u);
+    return r;
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+    *reinterpret_cast<uint2*>(p) = pack(v);
   }
 };
 template <int CPT>
@@ -170,6 +173,58 @@ __device__ __forceinline__ uint32_t car_rule(uint32_t x, uint32_t xl, uint32_t v
   const uint32_t nx = x + v;
   crossed = nx >= L ? 1u : 0u;
   xnew = crossed ? nx - L : nx;
+  return v;
+}
+
+// Sum of CPT velocities (u8 lanes: two byte dot-products of the packed
+// store words).
+template <typename VT, int CPT>
+struct VSum {
+  static __device__ __forceinline__ uint32_t sum(const uint32_t* v) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) s += v[c];
+    return s;
+  }
+};
+template <>
+struct VSum<uint8_t, 8> {
+  static __device__ __forceinline__ uint32_t sum(const uint32_t* v) {
+    const uint2 p = VLanes<uint8_t, 8>::pack(v);
+    return static_cast<uint32_t>(__dp4a(static_cast<int>(p.y), 0x01010101,
+                                        __dp4a(static_cast<int>(p.x), 0x01010101, 0)));
+  }
+};
+
+// Interior car: its leader is strictly ahead without wrapping (xl > x),
+// which holds for every car except rank N-1.  Counts a crossing into cnt.
+__device__ __forceinline__ uint32_t car_fast(uint32_t x, uint32_t xl, uint32_t v, uint32_t s,
+                                             uint32_t L, uint32_t vmax, uint32_t tp,
+                                             uint32_t& xnew, uint32_t& cnt) {
+  v = min(min(v + 1, vmax), xl - x - 1);
+  if (s < tp) v = static_cast<uint32_t>(max(static_cast<int>(v) - 1, 0));
+  uint32_t nx = x + v;
+  if (nx >= L) {
+    nx -= L;
+    ++cnt;
+  }
+  xnew = nx;
+  return v;
+}
+
+// Any car (the leader may sit behind the origin): gap taken mod L.
+__device__ __forceinline__ uint32_t car_any(uint32_t x, uint32_t xl, uint32_t v, uint32_t s,
+                                            uint32_t L, uint32_t vmax, uint32_t tp,
+                                            uint32_t& xnew, uint32_t& cnt) {
+  const uint32_t gap = xl > x ? xl - x - 1 : xl + (L - x) - 1;
+  v = min(min(v + 1, vmax), gap);
+  if (s < tp) v = static_cast<uint32_t>(max(static_cast<int>(v) - 1, 0));
+  uint32_t nx = x + v;
+  if (nx >= L) {
+    nx -= L;
+    ++cnt;
+  }
+  xnew = nx;
   return v;
 }
 
@@ -273,9 +328,8 @@ __global__ void __launch_bounds__(TPB) cone_init_kernel(const RingArgs ra) {
 
 // ---- single-step streaming kernel -----------------------------------------
 
-template <typename VT, int TPB>
+template <typename VT, int TPB, int CPT>
 __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
-  constexpr int CPT = 4;
   constexpr uint32_t TILE = TPB * CPT;
   const uint32_t N = ra.n;
   Ctl* ctl = ra.ctl;
@@ -293,38 +347,62 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t x_head = __ldg(X);  // leader of car N-1 is car 0
 
-  uint32_t P = mulmod(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
+  uint32_t P = mulmod_d(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
   unsigned long long sumv = 0;
   uint32_t cross = 0;
   const uint32_t ntiles = (N + TILE - 1) / TILE;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t base = tile * TILE + threadIdx.x * CPT;
-    const uint4 xs = ld_nc_v4(X + base);
-    uint32_t vv[CPT];
-    VLanes<VT, CPT>::load(V + base, vv);
-    uint32_t xnext = __shfl_down_sync(0xffffffffu, xs.x, 1);
-    if (lane == 31 && base + CPT < N) xnext = __ldg(X + base + CPT);
-    uint32_t s = mulmod(P, base < bound ? E : E2);
-    P = mulmod(P, ra.g);
-
-    uint32_t xo[CPT];
-    uint32_t tsum = 0, tcross = 0;
+    uint32_t x[CPT], v[CPT];
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) {
-      const uint32_t id = base + j;
-      if (j > 0) s = mulmod(s, id == bound ? ra.a1 : kA);
-      const uint32_t x = get4(xs, j);
-      const uint32_t xl = (id + 1 < N) ? (j + 1 < CPT ? get4(xs, j + 1) : xnext) : x_head;
-      uint32_t cr;
-      vv[j] = car_rule(x, xl, vv[j], s, L, vmax, tp, xo[j], cr);
-      const bool live = id < N;
-      tsum += live ? vv[j] : 0u;
-      tcross += live ? cr : 0u;
+    for (int q = 0; q < CPT / 4; ++q) {
+      const uint4 r = ld_nc_v4(X + base + 4 * q);
+      x[4 * q] = r.x;
+      x[4 * q + 1] = r.y;
+      x[4 * q + 2] = r.z;
+      x[4 * q + 3] = r.w;
     }
-    *reinterpret_cast<uint4*>(Xo + base) = make_uint4(xo[0], xo[1], xo[2], xo[3]);
-    VLanes<VT, CPT>::store(Vo + base, vv);
+    VLanes<VT, CPT>::load(V + base, v);
+    uint32_t xnext = __shfl_down_sync(0xffffffffu, x[0], 1);
+    if (lane == 31 && base + CPT < N) xnext = __ldg(X + base + CPT);
+    const uint32_t ap = P;  // a^base
+    P = mulmod_d(P, ra.g);
+    uint32_t cnt = 0, tsum = 0;
+    if (base + CPT < N && !(base < bound && bound < base + CPT)) {
+      // Interior group: all cars live, one draw base, positions increasing
+      // except possibly across the last car's leader (the rank seam).
+      uint32_t s = mulmod_d(ap, base < bound ? E : E2);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if (c) s = mulmod_d(s, kA);
+        if (c + 1 < CPT) {
+          v[c] = car_fast(x[c], x[c + 1], v[c], s, L, vmax, tp, x[c], cnt);
+        } else {
+          v[c] = car_any(x[c], xnext, v[c], s, L, vmax, tp, x[c], cnt);
+        }
+      }
+      tsum = VSum<VT, CPT>::sum(v);
+    } else {
+      uint32_t s = mulmod_d(ap, base < bound ? E : E2);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        const uint32_t id = base + c;
+        if (c) s = mulmod_d(s, id == bound ? ra.a1 : kA);
+        const uint32_t xl = (id + 1 < N) ? (c + 1 < CPT ? x[c + 1] : xnext) : x_head;
+        uint32_t cc = 0;
+        v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cc);
+        const bool live = id < N;
+        tsum += live ? v[c] : 0u;
+        cnt += live ? cc : 0u;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < CPT / 4; ++q)
+      *reinterpret_cast<uint4*>(Xo + base + 4 * q) =
+          make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+    VLanes<VT, CPT>::store(Vo + base, v);
     sumv += tsum;
-    cross += tcross;
+    cross += cnt;
   }
 
   // Block reduction, then one atomic per block for each of c_t and sum(v).
@@ -457,18 +535,37 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
       uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
       if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
       uint32_t sum = 0, crs = 0;
+      if (fast && !(base < bound && bound < base + CPT)) {
+        // Interior thread: ids contiguous and on one side of the rank seam;
+        // only the last car's leader can sit behind the origin.
+        const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        uint32_t id = base + c;
-        if (id >= N) id -= N;
-        const uint32_t s = mulmod(ap[c], id < bound ? E : E2);
-        const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-        uint32_t xnew, cr;
-        v[c] = car_rule(x[c], xl, v[c], s, L, vmax, tp, xnew, cr);
-        x[c] = xnew;
-        const bool mine = (own >> c) & 1u;
-        sum += mine ? v[c] : 0u;
-        crs += mine ? cr : 0u;
+        for (int c = 0; c < CPT; ++c) {
+          const uint32_t s = mulmod_d(ap[c], Es);
+          if (c + 1 < CPT) {
+            v[c] = car_fast(x[c], x[c + 1], v[c], s, L, vmax, tp, x[c], crs);
+          } else {
+            v[c] = car_any(x[c], xn, v[c], s, L, vmax, tp, x[c], crs);
+          }
+        }
+        if (own) {
+          sum = VSum<uint32_t, CPT>::sum(v);
+        } else {
+          crs = 0;
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          uint32_t id = base + c;
+          if (id >= N) id -= N;
+          const uint32_t s = mulmod_d(ap[c], id < bound ? E : E2);
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+          uint32_t cr = 0;
+          v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);
+          const bool mine = (own >> c) & 1u;
+          sum += mine ? v[c] : 0u;
+          crs += mine ? cr : 0u;
+        }
       }
       sum = __reduce_add_sync(0xffffffffu, sum);
       crs = __reduce_add_sync(0xffffffffu, crs);
