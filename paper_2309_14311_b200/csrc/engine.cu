@@ -19,6 +19,7 @@
 #include "engine.hpp"
 #include "minstd.hpp"
 #include "step_kernels.cuh"
+#include "tb_kernel.cuh"
 
 namespace nb200 {
 

@@ -451,186 +451,7 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
   }
 }
 
-// ---- temporal-blocked kernel ------------------------------------------------
-
-template <typename VT, int TPB, int CPT, int HALO>
-__global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
-  constexpr uint32_t LOAD = TPB * CPT;     // cars loaded per tile
-  constexpr uint32_t STORE = LOAD - HALO;  // cars owned (stored) per tile
-  constexpr int NW = TPB / 32;
-  static_assert(HALO >= kPlanMax && HALO % 16 == 0, "halo must cover the plan");
-  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax];
-  __shared__ unsigned long long s_sum[kPlanMax];
-  __shared__ uint32_t s_cr[kPlanMax];
-  __shared__ uint32_t s_lead[2][NW];
-
-  Ctl* ctl = ra.ctl;
-  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
-  const uint64_t t = ctl->t;
-  const int b = static_cast<int>(ctl->buf);
-  if (threadIdx.x < kPlanMax) {
-    s_W[threadIdx.x] = ctl->Wk[threadIdx.x];
-    s_E[threadIdx.x] = ctl->Ek[threadIdx.x];
-    s_E2[threadIdx.x] = ctl->E2k[threadIdx.x];
-    s_sum[threadIdx.x] = 0;
-    s_cr[threadIdx.x] = 0;
-  }
-  __syncthreads();
-  const uint32_t* __restrict__ X = xbuf(ra, b);
-  const VT* __restrict__ V = vbuf<VT>(ra, b);
-  uint32_t* __restrict__ Xo = xbuf(ra, b ^ 1);
-  VT* __restrict__ Vo = vbuf_w<VT>(ra, b ^ 1);
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t i0 = threadIdx.x * CPT;  // first car of this thread within the tile
-
-  uint32_t P = mulmod(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
-  uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
-  const uint32_t ntiles = (N + STORE - 1) / STORE;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t a0 = tile * STORE;
-    const uint32_t base = a0 + i0;  // id of car 0 (may exceed N in the wrap tile)
-    const bool fast = a0 + LOAD <= N;  // block-uniform
-    uint32_t x[CPT], v[CPT], ap[CPT];
-    if (fast) {
-#pragma unroll
-      for (int q = 0; q < CPT / 4; ++q) {
-        const uint4 r = ld_nc_v4(X + base + 4 * q);
-        x[4 * q] = r.x;
-        x[4 * q + 1] = r.y;
-        x[4 * q + 2] = r.z;
-        x[4 * q + 3] = r.w;
-      }
-      VLanes<VT, CPT>::load(V + base, v);
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        uint32_t id = base + c;
-        if (id >= N) id -= N;
-        x[c] = X[id];
-        v[c] = V[id];
-      }
-    }
-    // a^id for this thread's cars (id wrapped past N multiplies by a^-N)
-    uint32_t u = P;
-#pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if (c) u = mulmod(u, kA);
-      ap[c] = (base + c >= N) ? mulmod(u, ra.an_inv) : u;
-    }
-    P = mulmod(P, ra.g);
-    uint32_t own = 0;  // bit c: car c is stored by this tile
-#pragma unroll
-    for (int c = 0; c < CPT; ++c)
-      own |= (i0 + c < STORE && base + c < N) ? (1u << c) : 0u;
-
-    for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t E = s_E[j], E2 = s_E2[j];
-      const uint32_t bound = N - s_W[j];
-      // leader of each warp's last car: lane 0 of the next warp.  Slots
-      // alternate with the running step count, so one barrier per step
-      // suffices (a slot is rewritten only after the next barrier).
-      const uint32_t slot = phase++ & 1u;
-      if (lane == 0) s_lead[slot][warp] = x[0];
-      __syncthreads();
-      uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
-      if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
-      uint32_t sum = 0, crs = 0;
-      if (fast && !(base < bound && bound < base + CPT)) {
-        // Interior thread: ids contiguous and on one side of the rank seam;
-        // only the last car's leader can sit behind the origin.
-        const uint32_t Es = base < bound ? E : E2;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          const uint32_t s = mulmod_d(ap[c], Es);
-          if (c + 1 < CPT) {
-            v[c] = car_fast(x[c], x[c + 1], v[c], s, L, vmax, tp, x[c], crs);
-          } else {
-            v[c] = car_any(x[c], xn, v[c], s, L, vmax, tp, x[c], crs);
-          }
-        }
-        if (own) {
-          sum = VSum<uint32_t, CPT>::sum(v);
-        } else {
-          crs = 0;
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          uint32_t id = base + c;
-          if (id >= N) id -= N;
-          const uint32_t s = mulmod_d(ap[c], id < bound ? E : E2);
-          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t cr = 0;
-          v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);
-          const bool mine = (own >> c) & 1u;
-          sum += mine ? v[c] : 0u;
-          crs += mine ? cr : 0u;
-        }
-      }
-      sum = __reduce_add_sync(0xffffffffu, sum);
-      crs = __reduce_add_sync(0xffffffffu, crs);
-      if (lane == 0) {
-        if (sum) atomicAdd(&s_sum[j], static_cast<unsigned long long>(sum));
-        if (crs) atomicAdd(&s_cr[j], crs);
-      }
-    }
-    if (fast) {
-      if (i0 + CPT <= STORE) {
-#pragma unroll
-        for (int q = 0; q < CPT / 4; ++q)
-          *reinterpret_cast<uint4*>(Xo + base + 4 * q) =
-              make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
-        VLanes<VT, CPT>::store(Vo + base, v);
-      }
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        if ((own >> c) & 1u) {
-          Xo[base + c] = x[c];
-          Vo[base + c] = static_cast<VT>(v[c]);
-        }
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x < k) {
-    StepRec* r = ra.rec + ((t + threadIdx.x) % kRecCap);
-    if (s_sum[threadIdx.x]) atomicAdd(&r->sumv, s_sum[threadIdx.x]);
-    if (s_cr[threadIdx.x]) atomicAdd(&r->c, s_cr[threadIdx.x]);
-  }
-  if (!last_block_done(ctl)) return;
-
-  // Last block: check the plan, advance the control block, plan the next k.
-  __shared__ uint32_t s_Wnext;
-  if (threadIdx.x == 0) {
-    for (uint32_t j = 0; j < k; ++j) {
-      StepRec* r = ra.rec + ((t + j) % kRecCap);
-      const uint32_t c = atomicAdd(&r->c, 0u);
-      r->W = ctl->Wk[j];
-      if (c != ctl->ck[j] && !ctl->err) {
-        ctl->err = 1;
-        ctl->err_step = static_cast<unsigned int>(t + j);
-      }
-    }
-    uint32_t Wn = ctl->Wk[k - 1] + ctl->ck[k - 1];
-    if (Wn >= N) Wn -= N;
-    s_Wnext = Wn;
-  }
-  __syncthreads();
-  const uint32_t Wn = s_Wnext;
-  cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
-  for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
-    StepRec* r = ra.rec + ((t + k + j) % kRecCap);
-    r->sumv = 0;
-    r->c = 0;
-  }
-  if (threadIdx.x == 0) {
-    ctl->W = Wn;
-    ctl->t = t + k;
-    ctl->buf = static_cast<unsigned int>(b ^ 1);
-    ctl->ticket = 0;
-  }
-}
+// The temporal-blocked kernel lives in tb_kernel.cuh.
 
 // x_i = floor(i*L/N), v_i = 0 (model.cpp:30-40), in ID order (= rank order
 // at W = 0).

@@ -1,0 +1,206 @@
+// tb_kernel.cuh -- temporal-blocked NaSch step kernel (k <= 16 steps per
+// launch).  See step_kernels.cuh for the shared reformulation (ID order,
+// counter-based draws, integer threshold) and DESIGN.md section 4.2.
+//
+// Tile = LOAD consecutive cars (STORE owned + HALO ahead), held in registers
+// (CPT cars per thread) for all k steps; one __syncthreads per step hands
+// each warp's first position to the warp behind it.  Per step a thread takes
+// one of two paths:
+//   plain  -- its cars cannot reach the origin within the launch
+//             (max x < L - k*vmax at tile start) and the rank seam is not at
+//             or inside its cars: gap = leader - x - 1, no mod L, no crossing
+//             bookkeeping, one draw base.  This is every thread but a handful
+//             near the origin.
+//   general-- per-car seam/wrap handling (car_any) and an exact crossing
+//             count, added straight to the step's record.
+// Exact per-step velocity sums are kept per thread in shared memory (one
+// writer per slot, no atomics) and reduced once per launch.  The launch's
+// last block verifies the counted crossings against the origin-cone plan and
+// plans the next launch (cone_plan, step_kernels.cuh).
+#pragma once
+#include <cstdint>
+#include <type_traits>
+
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+template <typename VT, int TPB, int CPT, int HALO>
+__global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
+  constexpr uint32_t LOAD = TPB * CPT;     // cars loaded per tile
+  constexpr uint32_t STORE = LOAD - HALO;  // cars owned (stored) per tile
+  constexpr int NW = TPB / 32;
+  static_assert(HALO >= kPlanMax && HALO % 16 == 0, "halo must cover the plan");
+  using Acc = typename std::conditional<sizeof(VT) == 1, uint32_t, unsigned long long>::type;
+  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax];
+  __shared__ uint32_t s_lead[2][NW];
+  __shared__ Acc s_acc[kPlanMax][TPB];  // per-thread, per-step velocity sums
+
+  Ctl* ctl = ra.ctl;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint64_t t = ctl->t;
+  const int b = static_cast<int>(ctl->buf);
+  if (threadIdx.x < kPlanMax) {
+    s_W[threadIdx.x] = ctl->Wk[threadIdx.x];
+    s_E[threadIdx.x] = ctl->Ek[threadIdx.x];
+    s_E2[threadIdx.x] = ctl->E2k[threadIdx.x];
+  }
+#pragma unroll
+  for (int j = 0; j < kPlanMax; ++j) s_acc[j][threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t* __restrict__ X = xbuf(ra, b);
+  const VT* __restrict__ V = vbuf<VT>(ra, b);
+  uint32_t* __restrict__ Xo = xbuf(ra, b ^ 1);
+  VT* __restrict__ Vo = vbuf_w<VT>(ra, b ^ 1);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t i0 = threadIdx.x * CPT;  // first car of this thread within the tile
+  const uint32_t reach = k * vmax;        // farthest any car moves in this launch (< L)
+
+  uint32_t P = mulmod_d(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
+  uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
+  const uint32_t ntiles = (N + STORE - 1) / STORE;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t a0 = tile * STORE;
+    const uint32_t base = a0 + i0;     // id of car 0 (may exceed N in the wrap tile)
+    const bool fast = a0 + LOAD <= N;  // block-uniform: no id wraps in this tile
+    uint32_t x[CPT], v[CPT], ap[CPT];
+    if (fast) {
+#pragma unroll
+      for (int q = 0; q < CPT / 4; ++q) {
+        const uint4 r = ld_nc_v4(X + base + 4 * q);
+        x[4 * q] = r.x;
+        x[4 * q + 1] = r.y;
+        x[4 * q + 2] = r.z;
+        x[4 * q + 3] = r.w;
+      }
+      VLanes<VT, CPT>::load(V + base, v);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        uint32_t id = base + c;
+        if (id >= N) id -= N;
+        x[c] = X[id];
+        v[c] = V[id];
+      }
+    }
+    // a^id for this thread's cars (an id wrapped past N multiplies by a^-N)
+    uint32_t u = P;
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      if (c) u = mulmod_d(u, kA);
+      ap[c] = (base + c >= N) ? mulmod_d(u, ra.an_inv) : u;
+    }
+    P = mulmod_d(P, ra.g);
+    uint32_t own = 0;  // bit c: car c is stored by this tile
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) own |= (i0 + c < STORE && base + c < N) ? (1u << c) : 0u;
+    const bool own_all = own == (1u << CPT) - 1u;
+    uint32_t xmax = x[0];
+#pragma unroll
+    for (int c = 1; c < CPT; ++c) xmax = max(xmax, x[c]);
+    const bool plain = fast && xmax < L - reach;
+
+    for (uint32_t j = 0; j < k; ++j) {
+      const uint32_t E = s_E[j], E2 = s_E2[j];
+      const uint32_t bound = N - s_W[j];  // id of the rank-0 car (N when W = 0)
+      // Slots alternate with the running step count, so one barrier per step
+      // suffices (a slot is rewritten only after the next barrier).
+      const uint32_t slot = phase++ & 1u;
+      if (lane == 0) s_lead[slot][warp] = x[0];
+      __syncthreads();
+      uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+      if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
+      if (plain && !(base < bound && bound <= base + CPT)) {
+        const uint32_t Es = base < bound ? E : E2;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          const uint32_t s = mulmod_d(ap[c], Es);
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+          uint32_t vc = min(min(v[c] + 1, vmax), xl - x[c] - 1);
+          if (s < tp) vc = static_cast<uint32_t>(max(static_cast<int>(vc) - 1, 0));
+          v[c] = vc;
+          x[c] += vc;
+        }
+        if (own_all) s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+      } else {
+        Acc sum = 0;
+        uint32_t crs = 0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          uint32_t id = base + c;
+          if (id >= N) id -= N;
+          const uint32_t s = mulmod_d(ap[c], id < bound ? E : E2);
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+          uint32_t cr = 0;
+          v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);
+          const bool mine = (own >> c) & 1u;
+          sum += mine ? v[c] : 0u;
+          crs += mine ? cr : 0u;
+        }
+        s_acc[j][threadIdx.x] += sum;
+        if (crs) atomicAdd(&ra.rec[(t + j) % kRecCap].c, crs);
+      }
+    }
+    if (fast) {
+      if (i0 + CPT <= STORE) {
+#pragma unroll
+        for (int q = 0; q < CPT / 4; ++q)
+          *reinterpret_cast<uint4*>(Xo + base + 4 * q) =
+              make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+        VLanes<VT, CPT>::store(Vo + base, v);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if ((own >> c) & 1u) {
+          Xo[base + c] = x[c];
+          Vo[base + c] = static_cast<VT>(v[c]);
+        }
+      }
+    }
+  }
+  // Per-step velocity sums: warp w reduces steps w, w+NW, ...
+  __syncthreads();
+  for (uint32_t j = warp; j < k; j += NW) {
+    unsigned long long acc = 0;
+#pragma unroll
+    for (int q = 0; q < TPB / 32; ++q) acc += s_acc[j][lane + 32 * q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(&ra.rec[(t + j) % kRecCap].sumv, acc);
+  }
+  if (!last_block_done(ctl)) return;
+
+  // Last block: check the plan, advance the control block, plan the next k.
+  __shared__ uint32_t s_Wnext;
+  if (threadIdx.x == 0) {
+    for (uint32_t j = 0; j < k; ++j) {
+      StepRec* r = ra.rec + ((t + j) % kRecCap);
+      const uint32_t c = atomicAdd(&r->c, 0u);
+      r->W = ctl->Wk[j];
+      if (c != ctl->ck[j] && !ctl->err) {
+        ctl->err = 1;
+        ctl->err_step = static_cast<unsigned int>(t + j);
+      }
+    }
+    uint32_t Wn = ctl->Wk[k - 1] + ctl->ck[k - 1];
+    if (Wn >= N) Wn -= N;
+    s_Wnext = Wn;
+  }
+  __syncthreads();
+  const uint32_t Wn = s_Wnext;
+  cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
+  for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
+    StepRec* r = ra.rec + ((t + k + j) % kRecCap);
+    r->sumv = 0;
+    r->c = 0;
+  }
+  if (threadIdx.x == 0) {
+    ctl->W = Wn;
+    ctl->t = t + k;
+    ctl->buf = static_cast<unsigned int>(b ^ 1);
+    ctl->ticket = 0;
+  }
+}
+
+}  // namespace nb200
