@@ -1,0 +1,458 @@
+// ensemble.cu -- GpuEnsemble: many independent rings, each resident in one
+// SM's shared memory for a whole launch (see ensemble.hpp).
+//
+// Kernel: persistent, one 1024-thread CTA per SM with ~227 KB of shared
+// memory, pulling rings from an atomic queue in decreasing-N order (longest
+// processing time first).  A ring's cars are packed as x | v << bx into one
+// u32 per car (bx = bits of L-1; needs bx + bits(vmax) <= 32), so a 57k-car
+// ring fits; each thread owns an odd-sized run of consecutive cars (odd
+// stride => conflict-free shared-memory banks).  Per step: read the leader
+// of the run's last car, barrier, update the run in place (each car reads
+// its own word and its leader's old word before overwriting its own),
+// warp-reduce the crossing count and velocity sum into per-warp slots,
+// barrier.  Every warp then folds the 32 crossing slots into its own copy of
+// W and the draw base E (c <= vmax <= 255, so a^c is a table lookup) --
+// the rank/draw bookkeeping of the single-ring kernels (step_kernels.cuh)
+// with no global round trip.  Rings that do not fit run on a GpuRing each.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "ensemble.hpp"
+#include "minstd.hpp"
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+namespace {
+
+void check_e(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+#define CKE(call) check_e((call), #call)
+
+constexpr int kEnsTPB = 1024;
+constexpr int kEnsHeaderWords = 256 + 64 + 64 + 16;  // a^c table, slots, scalars
+
+struct RingDesc {
+  unsigned long long off;         // first car of the ring in X / V
+  unsigned long long t;           // steps done
+  unsigned long long steps;       // configured total
+  unsigned long long sumv_total;  // sum over completed steps of sum(v)
+  uint32_t n, L, vmax, tp, s0, an, an_inv, a1;
+  uint32_t W, E, bx, last_sumv;
+};
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(0xffffffffu, v); }
+
+template <int TPB>
+__global__ void __launch_bounds__(TPB, 1)
+    ensemble_kernel(RingDesc* __restrict__ rings, const uint32_t* __restrict__ order, uint32_t nrings,
+                    unsigned long long steps, uint32_t* counter, uint32_t* __restrict__ X,
+                    uint8_t* __restrict__ V) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* apw = sm;               // a^c, c < 256
+  uint32_t* slot_c = sm + 256;      // [2][32] crossing counts per warp
+  uint32_t* slot_v = slot_c + 64;   // [2][32] velocity sums per warp
+  uint32_t* sc = slot_v + 64;       // scalars
+  uint32_t* packed = sm + kEnsHeaderWords;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  if (tid < 256) apw[tid] = powmod(kA, tid);
+
+  for (;;) {
+    __syncthreads();  // previous ring fully written back; sc reusable
+    if (tid == 0) sc[0] = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t qi = sc[0];
+    if (qi >= nrings) break;
+    const uint32_t r = order[qi];
+    const RingDesc d = rings[r];
+    const unsigned long long remain = d.steps - d.t;
+    const unsigned long long todo = steps < remain ? steps : remain;
+    if (todo == 0) continue;
+    const uint32_t N = d.n, L = d.L, vmax = d.vmax, tp = d.tp, bx = d.bx;
+    const uint32_t xmask = (1u << bx) - 1u;
+    for (uint32_t i = tid; i < N; i += TPB)
+      packed[i] = X[d.off + i] | (static_cast<uint32_t>(V[d.off + i]) << bx);
+    uint32_t cpt = (N + TPB - 1) / TPB;
+    cpt |= 1u;  // odd stride: conflict-free banks
+    const uint32_t first = tid * cpt;
+    const uint32_t cnt = first < N ? min(cpt, N - first) : 0u;
+    const uint32_t lead_idx = (first + cnt >= N) ? 0u : first + cnt;
+    const uint32_t ap0 = cnt ? powmod(kA, first) : 1u;
+    uint32_t W = d.W, E = d.E;
+    unsigned long long total = 0;  // meaningful in warp 0 lane 0
+    uint32_t last = d.last_sumv;
+    __syncthreads();
+    for (unsigned long long st = 0; st <= todo; ++st) {
+      if (st > 0) {
+        // fold the previous step's crossings into W and E (every warp)
+        const uint32_t p = static_cast<uint32_t>((st - 1) & 1);
+        const uint32_t c = warp_sum(slot_c[p * 32 + lane]);
+        const uint32_t sv = warp_sum(slot_v[p * 32 + lane]);
+        total += sv;
+        last = sv;
+        uint32_t Wn = W + c;
+        const bool wrap = Wn >= N;
+        if (wrap) Wn -= N;
+        E = mulmod_d(E, wrap ? apw[c] : mulmod_d(d.an, apw[c]));
+        W = Wn;
+      }
+      if (st == todo) break;
+      const uint32_t E2 = mulmod_d(E, d.an_inv);
+      const uint32_t bound = N - W;
+      const uint32_t lead = cnt ? (packed[lead_idx] & xmask) : 0u;
+      __syncthreads();
+      uint32_t crs = 0, sum = 0;
+      if (cnt) {
+        uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
+        uint32_t cur = packed[first];
+        for (uint32_t c = 0; c < cnt; ++c) {
+          const uint32_t id = first + c;
+          if (c) s = mulmod_d(s, id == bound ? d.a1 : kA);
+          const uint32_t nxt = (c + 1 < cnt) ? packed[id + 1] : lead;
+          uint32_t xn;
+          const uint32_t vn = car_any(cur & xmask, nxt & xmask, cur >> bx, s, L, vmax, tp, xn, crs);
+          packed[id] = xn | (vn << bx);
+          sum += vn;
+          cur = nxt;
+        }
+      }
+      crs = warp_sum(crs);
+      sum = warp_sum(sum);
+      if (lane == 0) {
+        slot_c[(st & 1) * 32 + warp] = crs;
+        slot_v[(st & 1) * 32 + warp] = sum;
+      }
+      __syncthreads();
+    }
+    for (uint32_t i = tid; i < N; i += TPB) {
+      const uint32_t w = packed[i];
+      X[d.off + i] = w & xmask;
+      V[d.off + i] = static_cast<uint8_t>(w >> bx);
+    }
+    if (tid == 0) {
+      rings[r].t = d.t + todo;
+      rings[r].W = W;
+      rings[r].E = E;
+      rings[r].sumv_total = d.sumv_total + total;
+      rings[r].last_sumv = last;
+    }
+  }
+}
+
+// init_state (model.cpp:30-40) for every resident ring: block per ring.
+__global__ void ensemble_init_kernel(const RingDesc* __restrict__ rings, uint32_t nrings,
+                                     uint32_t* __restrict__ X, uint8_t* __restrict__ V) {
+  for (uint32_t r = blockIdx.x; r < nrings; r += gridDim.x) {
+    const RingDesc d = rings[r];
+    for (uint32_t i = threadIdx.x; i < d.n; i += blockDim.x) {
+      X[d.off + i] = static_cast<uint32_t>(uint64_t(i) * d.L / d.n);
+      V[d.off + i] = 0;
+    }
+  }
+}
+
+__global__ void ensemble_sumv_kernel(const RingDesc* __restrict__ rings, uint32_t r,
+                                     const uint8_t* __restrict__ V, unsigned long long* out) {
+  const RingDesc d = rings[r];
+  unsigned long long s = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x)
+    s += V[d.off + i];
+  s = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(s));
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
+}
+
+uint32_t bits_for(uint64_t max_value) {
+  uint32_t b = 0;
+  while (b < 32 && (uint64_t(1) << b) <= max_value) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct GpuEnsemble::Impl {
+  std::vector<SimParams> params;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::vector<int> slot;                    // ring -> resident index or -1
+  std::vector<RingDesc> desc;               // resident descriptors (host copy)
+  std::vector<std::unique_ptr<GpuRing>> overflow;  // ring -> engine if not resident
+  std::vector<uint32_t> order;              // resident indices by decreasing N
+  RingDesc* d_desc = nullptr;
+  uint32_t* d_order = nullptr;
+  uint32_t* d_counter = nullptr;
+  uint32_t* X = nullptr;
+  uint8_t* V = nullptr;
+  unsigned long long* d_sum = nullptr;
+  RingDesc* h_desc = nullptr;  // pinned mirror
+  int grid = 1;
+  size_t smem = 0;
+  size_t cap_cars = 0;
+  uint64_t launches = 0;
+  bool dirty = false;  // device descriptors newer than host mirror
+
+  void pull() {
+    if (!dirty || desc.empty()) return;
+    CKE(cudaMemcpyAsync(h_desc, d_desc, desc.size() * sizeof(RingDesc), cudaMemcpyDeviceToHost, stream));
+    CKE(cudaStreamSynchronize(stream));
+    std::memcpy(desc.data(), h_desc, desc.size() * sizeof(RingDesc));
+    dirty = false;
+  }
+
+  void push() {
+    std::memcpy(h_desc, desc.data(), desc.size() * sizeof(RingDesc));
+    CKE(cudaMemcpyAsync(d_desc, h_desc, desc.size() * sizeof(RingDesc), cudaMemcpyHostToDevice, stream));
+    CKE(cudaStreamSynchronize(stream));
+  }
+
+  void launch(uint64_t steps) {
+    if (desc.empty()) return;
+    CKE(cudaMemsetAsync(d_counter, 0, sizeof(uint32_t), stream));
+    ensemble_kernel<kEnsTPB><<<grid, kEnsTPB, smem, stream>>>(
+        d_desc, d_order, static_cast<uint32_t>(desc.size()), steps, d_counter, X, V);
+    CKE(cudaGetLastError());
+    ++launches;
+    dirty = true;
+  }
+};
+
+GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) {
+  Impl& d = *impl_;
+  int ndev = 0;
+  const cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    throw std::runtime_error(std::string("no CUDA device available for the B200 engine (") +
+                             cudaGetErrorString(e) + ")");
+  }
+  if (rings.empty()) throw std::invalid_argument("ensemble needs at least one ring");
+  for (const SimParams& p : rings) {
+    p.validate();
+    if (p.road_length > 2147483647ull)
+      throw std::invalid_argument("length above 2^31-1 is not supported by the B200 engine");
+  }
+  CKE(cudaGetDevice(&d.device));
+  d.params = rings;
+  CKE(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  int max_optin = 0, sms = 0;
+  CKE(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
+  CKE(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
+  d.cap_cars = static_cast<size_t>(max_optin) / 4 - kEnsHeaderWords;
+
+  // Which rings are resident, and their packing.
+  d.slot.assign(rings.size(), -1);
+  d.overflow.resize(rings.size());
+  uint64_t total_cars = 0;
+  size_t max_cars = 0;
+  for (size_t r = 0; r < rings.size(); ++r) {
+    const SimParams& p = rings[r];
+    const uint64_t vmax_eff = std::min<uint64_t>(p.v_max, p.road_length - 1);
+    const uint32_t bx = std::max<uint32_t>(1, bits_for(p.road_length - 1));
+    const bool fits = p.car_count <= d.cap_cars && vmax_eff <= 255 &&
+                      bx + bits_for(vmax_eff) <= 32;
+    if (!fits) continue;
+    RingDesc rd{};
+    rd.off = total_cars;
+    rd.t = 0;
+    rd.steps = p.steps;
+    rd.n = static_cast<uint32_t>(p.car_count);
+    rd.L = static_cast<uint32_t>(p.road_length);
+    rd.vmax = static_cast<uint32_t>(vmax_eff);
+    rd.tp = deceleration_threshold(p.p);
+    rd.s0 = seeded(p.seed);
+    rd.an = powmod(kA, rd.n);
+    rd.an_inv = powmod(kA, kOrder - (rd.n % kOrder));
+    rd.a1 = powmod(kA, (1 + kOrder - (rd.n % kOrder)) % kOrder);
+    rd.W = 0;
+    rd.E = mulmod(rd.s0, powmod(kA, draw_exponent(0, rd.n, 0)));
+    rd.bx = bx;
+    d.slot[r] = static_cast<int>(d.desc.size());
+    d.desc.push_back(rd);
+    total_cars += rd.n;
+    max_cars = std::max<size_t>(max_cars, rd.n);
+  }
+  for (size_t r = 0; r < rings.size(); ++r) {
+    if (d.slot[r] < 0) {
+      SimParams p = rings[r];
+      p.output_mode = OutputMode::none;
+      d.overflow[r].reset(new GpuRing(p));
+      d.overflow[r]->set_checksum(false);
+    }
+  }
+  if (!d.desc.empty()) {
+    d.order.resize(d.desc.size());
+    std::iota(d.order.begin(), d.order.end(), 0u);
+    std::stable_sort(d.order.begin(), d.order.end(),
+                     [&](uint32_t a, uint32_t b) { return d.desc[a].n > d.desc[b].n; });
+    CKE(cudaMalloc(&d.X, total_cars * 4 + 16));
+    CKE(cudaMalloc(&d.V, total_cars + 16));
+    CKE(cudaMalloc(&d.d_desc, d.desc.size() * sizeof(RingDesc)));
+    CKE(cudaMallocHost(&d.h_desc, d.desc.size() * sizeof(RingDesc)));
+    CKE(cudaMalloc(&d.d_order, d.order.size() * 4));
+    CKE(cudaMalloc(&d.d_counter, 4));
+    CKE(cudaMalloc(&d.d_sum, sizeof(unsigned long long)));
+    CKE(cudaMemcpy(d.d_order, d.order.data(), d.order.size() * 4, cudaMemcpyHostToDevice));
+    d.push();
+    d.smem = (kEnsHeaderWords + max_cars) * 4;
+    CKE(cudaFuncSetAttribute(ensemble_kernel<kEnsTPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(d.smem)));
+    int per_sm = 0;
+    CKE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ensemble_kernel<kEnsTPB>, kEnsTPB, d.smem));
+    d.grid = static_cast<int>(std::min<size_t>(d.desc.size(), size_t(sms) * std::max(per_sm, 1)));
+    ensemble_init_kernel<<<static_cast<int>(std::min<size_t>(d.desc.size(), 4096)), 256, 0, d.stream>>>(
+        d.d_desc, static_cast<uint32_t>(d.desc.size()), d.X, d.V);
+    CKE(cudaGetLastError());
+    CKE(cudaStreamSynchronize(d.stream));
+  }
+}
+
+GpuEnsemble::~GpuEnsemble() {
+  Impl& d = *impl_;
+  if (d.stream) cudaStreamSynchronize(d.stream);
+  cudaFree(d.X);
+  cudaFree(d.V);
+  cudaFree(d.d_desc);
+  cudaFree(d.d_order);
+  cudaFree(d.d_counter);
+  cudaFree(d.d_sum);
+  cudaFreeHost(d.h_desc);
+  if (d.stream) cudaStreamDestroy(d.stream);
+}
+
+size_t GpuEnsemble::size() const { return impl_->params.size(); }
+size_t GpuEnsemble::resident_capacity_cars() const { return impl_->cap_cars; }
+void* GpuEnsemble::cuda_stream() const { return impl_->stream; }
+
+uint64_t GpuEnsemble::kernel_launches() const {
+  uint64_t n = impl_->launches;
+  for (const auto& o : impl_->overflow)
+    if (o) n += o->kernel_launches();
+  return n;
+}
+
+void GpuEnsemble::set_state32(size_t ring, const uint32_t* x, const uint32_t* v, size_t n) {
+  Impl& d = *impl_;
+  if (ring >= d.params.size()) throw std::invalid_argument("ring index out of range");
+  CKE(cudaSetDevice(d.device));
+  if (d.overflow[ring]) {
+    d.overflow[ring]->set_state32(x, v, n);
+    return;
+  }
+  const SimParams& p = d.params[ring];
+  if (n != p.car_count) throw std::invalid_argument("state length must equal ncars");
+  d.pull();
+  RingDesc& rd = d.desc[d.slot[ring]];
+  std::vector<uint8_t> v8(n);
+  for (size_t i = 0; i < n; ++i) {
+    if (x[i] >= rd.L) throw std::invalid_argument("position out of range [0, length)");
+    if (i && x[i - 1] >= x[i]) throw std::invalid_argument("positions must be strictly increasing");
+    if (v[i] > p.v_max) throw std::invalid_argument("velocity above vmax");
+    if (v[i] > rd.vmax) throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+    v8[i] = static_cast<uint8_t>(v[i]);
+  }
+  CKE(cudaMemcpyAsync(d.X + rd.off, x, n * 4, cudaMemcpyHostToDevice, d.stream));
+  CKE(cudaMemcpyAsync(d.V + rd.off, v8.data(), n, cudaMemcpyHostToDevice, d.stream));
+  rd.W = 0;
+  rd.E = mulmod(rd.s0, powmod(kA, draw_exponent(rd.t, rd.n, 0)));
+  uint64_t s = 0;
+  for (size_t i = 0; i < n; ++i) s += v[i];
+  rd.last_sumv = static_cast<uint32_t>(s);
+  d.push();
+}
+
+void GpuEnsemble::enqueue(uint64_t steps) {
+  Impl& d = *impl_;
+  CKE(cudaSetDevice(d.device));
+  d.launch(steps);
+  for (auto& o : d.overflow)
+    if (o) o->enqueue(steps);
+}
+
+void GpuEnsemble::synchronize() {
+  Impl& d = *impl_;
+  CKE(cudaSetDevice(d.device));
+  CKE(cudaStreamSynchronize(d.stream));
+  for (auto& o : d.overflow)
+    if (o) o->synchronize();
+}
+
+void GpuEnsemble::advance(uint64_t steps) {
+  enqueue(steps);
+  synchronize();
+}
+
+uint64_t GpuEnsemble::steps_done(size_t ring) {
+  Impl& d = *impl_;
+  if (ring >= d.params.size()) throw std::invalid_argument("ring index out of range");
+  if (d.overflow[ring]) return d.overflow[ring]->steps_done();
+  d.pull();
+  return d.desc[d.slot[ring]].t;
+}
+
+void GpuEnsemble::sumv_totals(uint64_t* out, size_t cap) {
+  Impl& d = *impl_;
+  CKE(cudaSetDevice(d.device));
+  d.pull();
+  for (size_t r = 0; r < d.params.size() && r < cap; ++r) {
+    if (d.overflow[r]) {
+      const size_t k = d.overflow[r]->sumv_series(nullptr, 0);
+      std::vector<uint64_t> s(k);
+      d.overflow[r]->sumv_series(s.data(), k);
+      uint64_t tot = 0;
+      for (uint64_t x : s) tot += x;
+      out[r] = tot;
+    } else {
+      out[r] = d.desc[d.slot[r]].sumv_total;
+    }
+  }
+}
+
+void GpuEnsemble::sumv_last(uint64_t* out, size_t cap) {
+  Impl& d = *impl_;
+  CKE(cudaSetDevice(d.device));
+  d.pull();
+  for (size_t r = 0; r < d.params.size() && r < cap; ++r) {
+    if (d.overflow[r]) {
+      const size_t k = d.overflow[r]->sumv_series(nullptr, 0);
+      std::vector<uint64_t> s(k);
+      d.overflow[r]->sumv_series(s.data(), k);
+      out[r] = k ? s.back() : 0;
+    } else {
+      out[r] = d.desc[d.slot[r]].last_sumv;
+    }
+  }
+}
+
+void GpuEnsemble::state(size_t ring, uint64_t* x, uint64_t* v) {
+  Impl& d = *impl_;
+  if (ring >= d.params.size()) throw std::invalid_argument("ring index out of range");
+  CKE(cudaSetDevice(d.device));
+  if (d.overflow[ring]) {
+    d.overflow[ring]->state(x, v);
+    return;
+  }
+  d.pull();
+  const RingDesc& rd = d.desc[d.slot[ring]];
+  std::vector<uint32_t> hx(rd.n);
+  std::vector<uint8_t> hv(rd.n);
+  CKE(cudaMemcpyAsync(hx.data(), d.X + rd.off, size_t(rd.n) * 4, cudaMemcpyDeviceToHost, d.stream));
+  CKE(cudaMemcpyAsync(hv.data(), d.V + rd.off, rd.n, cudaMemcpyDeviceToHost, d.stream));
+  CKE(cudaStreamSynchronize(d.stream));
+  const uint32_t head = (rd.n - rd.W) % rd.n;  // rank-0 car
+  for (uint32_t k = 0; k < rd.n; ++k) {
+    uint32_t id = head + k;
+    if (id >= rd.n) id -= rd.n;
+    if (x) x[k] = hx[id];
+    if (v) v[k] = hv[id];
+  }
+}
+
+}  // namespace nb200
