@@ -179,6 +179,39 @@ const char* nasch_b200_version(void);
  * (src/model.cpp:51). */
 uint32_t nasch_b200_draw_threshold(double p);
 
+/* ---- ensembles of independent rings (extension) ------------------------
+ * One handle advances many independent simulations at once -- BASELINE
+ * config 4's fundamental-diagram sweep.  Each ring is exactly the
+ * single-ring model with its own parameter set and minstd stream; rings
+ * that fit one SM's shared memory (about 57k cars, vmax <= 255) run in one
+ * persistent launch, the others on their own engine.  For multi-GPU runs
+ * each rank builds an ensemble of its share of the rings. */
+typedef struct nasch_ensemble nasch_ensemble;
+nasch_status nasch_ensemble_new(const nasch_params* const* params, size_t count,
+                                nasch_ensemble** out);
+void nasch_ensemble_free(nasch_ensemble* ens);
+size_t nasch_ensemble_size(const nasch_ensemble* ens);
+nasch_status nasch_ensemble_set_state32(nasch_ensemble* ens, size_t ring,
+                                        const uint32_t* positions,
+                                        const uint32_t* velocities, size_t count);
+/* Every ring advances min(steps, its remaining steps). */
+nasch_status nasch_ensemble_advance(nasch_ensemble* ens, uint64_t steps);
+nasch_status nasch_ensemble_enqueue(nasch_ensemble* ens, uint64_t steps);
+nasch_status nasch_ensemble_synchronize(nasch_ensemble* ens);
+uint64_t nasch_ensemble_steps_done(const nasch_ensemble* ens, size_t ring);
+/* Per ring: exact sum over completed steps of the velocity sum
+ * (time-averaged flux = total / (steps * length)). */
+nasch_status nasch_ensemble_sumv_totals(const nasch_ensemble* ens, uint64_t* out,
+                                        size_t capacity);
+/* Per ring: velocity sum after the last completed step. */
+nasch_status nasch_ensemble_sumv_last(const nasch_ensemble* ens, uint64_t* out,
+                                      size_t capacity);
+nasch_status nasch_ensemble_state(const nasch_ensemble* ens, size_t ring,
+                                  uint64_t* positions, uint64_t* velocities,
+                                  size_t capacity);
+void* nasch_ensemble_cuda_stream(const nasch_ensemble* ens);
+uint64_t nasch_ensemble_kernel_launches(const nasch_ensemble* ens);
+
 #ifdef __cplusplus
 }
 #endif

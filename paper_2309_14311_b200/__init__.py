@@ -6,6 +6,7 @@ C++ + sm_100a CUDA in csrc/).  This package only builds and binds it.
 from .capi import build, load, LIB_PATH  # noqa: F401
 from .nasch import (  # noqa: F401
     Engine,
+    Ensemble,
     IoError,
     NaschError,
     ParamError,

@@ -80,6 +80,20 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_fill_uniform_state": (C.c_int, [_u64, _u64, _u64, _u64, _u32p, _u32p]),
     "nasch_b200_version": (C.c_char_p, []),
     "nasch_b200_draw_threshold": (C.c_uint32, [C.c_double]),
+    # ensembles
+    "nasch_ensemble_new": (C.c_int, [C.POINTER(_P), C.c_size_t, C.POINTER(_P)]),
+    "nasch_ensemble_free": (None, [_P]),
+    "nasch_ensemble_size": (C.c_size_t, [_P]),
+    "nasch_ensemble_set_state32": (C.c_int, [_P, C.c_size_t, _u32p, _u32p, C.c_size_t]),
+    "nasch_ensemble_advance": (C.c_int, [_P, _u64]),
+    "nasch_ensemble_enqueue": (C.c_int, [_P, _u64]),
+    "nasch_ensemble_synchronize": (C.c_int, [_P]),
+    "nasch_ensemble_steps_done": (_u64, [_P, C.c_size_t]),
+    "nasch_ensemble_sumv_totals": (C.c_int, [_P, _u64p, C.c_size_t]),
+    "nasch_ensemble_sumv_last": (C.c_int, [_P, _u64p, C.c_size_t]),
+    "nasch_ensemble_state": (C.c_int, [_P, C.c_size_t, _u64p, _u64p, C.c_size_t]),
+    "nasch_ensemble_cuda_stream": (C.c_void_p, [_P]),
+    "nasch_ensemble_kernel_launches": (_u64, [_P]),
 }
 REFERENCE_SYMBOLS = list(SIGNATURES)[:36]
 

@@ -10,10 +10,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -42,6 +44,26 @@ constexpr int kHalo = 16;
 constexpr uint32_t kLoadTB = kTPB * kCPTB;       // 2048 cars loaded per tile
 constexpr uint32_t kStoreTB = kLoadTB - kHalo;   // 2032 cars owned per tile
 constexpr int kGraphLaunches = 16;
+
+// Runs f(lo, hi) over [0, n) in parallel host chunks (input validation and
+// u64 <-> u32 conversion at the ABI; large rings only).
+template <typename F>
+void parallel_chunks(size_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const unsigned nt = static_cast<unsigned>(std::min<size_t>(std::min(hw, 32u), n / (1u << 20) + 1));
+  if (nt <= 1) {
+    f(size_t(0), n);
+    return;
+  }
+  const size_t chunk = (n + nt - 1) / nt;
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nt; ++t) {
+    const size_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    pool.emplace_back([&f, lo, hi] { f(lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+}
 
 long env_long(const char* name, long fallback) {
   const char* s = std::getenv(name);
@@ -314,29 +336,42 @@ struct GpuRing::Impl {
     if (sync) drain();
   }
 
-  void load_state(const uint32_t* hx_in, const uint32_t* hv_in) {
-    // validation (rank order): strictly ascending positions < L,
-    // velocities <= vmax (acceptance.cpp:118-123 invariants) and <= L-1.
-    for (uint32_t i = 0; i < n; ++i) {
-      if (hx_in[i] >= L) throw std::invalid_argument("position out of range [0, length)");
-      if (i && hx_in[i - 1] >= hx_in[i])
-        throw std::invalid_argument("positions must be strictly increasing");
-      if (hv_in[i] > params.v_max) throw std::invalid_argument("velocity above vmax");
-      if (hv_in[i] > vmax_eff)
-        throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+  // Validates a rank-ordered state (strictly ascending positions < L,
+  // velocities <= vmax -- the invariants of acceptance.cpp:118-123 -- and
+  // <= L-1) while narrowing it into the pinned staging buffers, in parallel
+  // host chunks, then uploads it.
+  template <typename T>
+  void load_state(const T* hx_in, const T* hv_in) {
+    std::atomic<int> err{0};
+    const uint64_t vlim = std::min<uint64_t>(params.v_max, vmax_eff);
+    parallel_chunks(n, [&](size_t lo, size_t hi) {
+      int e = 0;
+      for (size_t i = lo; i < hi && !e; ++i) {
+        const uint64_t xi = hx_in[i], vi = hv_in[i];
+        if (xi >= L) e = 1;
+        else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
+        else if (vi > params.v_max) e = 3;
+        else if (vi > vlim) e = 4;
+        hx[i] = static_cast<uint32_t>(xi);
+        if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
+        else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
+      }
+      if (e) {
+        int expected = 0;
+        err.compare_exchange_strong(expected, e);
+      }
+    });
+    switch (err.load()) {
+      case 1: throw std::invalid_argument("position out of range [0, length)");
+      case 2: throw std::invalid_argument("positions must be strictly increasing");
+      case 3: throw std::invalid_argument("velocity above vmax");
+      case 4: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      default: break;
     }
     drain();
     const int cur = static_cast<int>(buf_host);
-    std::memcpy(hx, hx_in, size_t(n) * 4);
     CK(cudaMemcpyAsync(x[cur], hx, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
-    if (vbytes == 4) {
-      std::memcpy(hv, hv_in, size_t(n) * 4);
-      CK(cudaMemcpyAsync(v[cur], hv, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
-    } else {
-      uint8_t* hb = static_cast<uint8_t*>(hv);
-      for (uint32_t i = 0; i < n; ++i) hb[i] = static_cast<uint8_t>(hv_in[i]);
-      CK(cudaMemcpyAsync(v[cur], hv, size_t(n), cudaMemcpyHostToDevice, stream));
-    }
+    CK(cudaMemcpyAsync(v[cur], hv, size_t(n) * vbytes, cudaMemcpyHostToDevice, stream));
     reset_ctl();
     compute_sumv0();
     series_base = steps_done;
@@ -483,22 +518,14 @@ void GpuRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   Impl& d = *impl_;
   CK(cudaSetDevice(d.device));
   if (n != d.n) throw std::invalid_argument("state length must equal ncars");
-  std::vector<uint32_t> x32(n), v32(n);
-  for (size_t i = 0; i < n; ++i) {
-    if (x[i] >= d.L) throw std::invalid_argument("position out of range [0, length)");
-    if (v[i] > d.params.v_max) throw std::invalid_argument("velocity above vmax");
-    if (v[i] > d.vmax_eff) throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
-    x32[i] = static_cast<uint32_t>(x[i]);
-    v32[i] = static_cast<uint32_t>(v[i]);
-  }
-  d.load_state(x32.data(), v32.data());
+  d.load_state<uint64_t>(x, v);
 }
 
 void GpuRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) {
   Impl& d = *impl_;
   CK(cudaSetDevice(d.device));
   if (n != d.n) throw std::invalid_argument("state length must equal ncars");
-  d.load_state(x, v);
+  d.load_state<uint32_t>(x, v);
 }
 
 void GpuRing::advance(uint64_t steps) {
@@ -540,10 +567,12 @@ void GpuRing::state(uint64_t* positions, uint64_t* velocities) {
   CK(cudaSetDevice(d.device));
   d.drain();
   d.fetch_rank_order();
-  if (positions)
-    for (uint32_t i = 0; i < d.n; ++i) positions[i] = d.hx[i];
-  if (velocities)
-    for (uint32_t i = 0; i < d.n; ++i) velocities[i] = d.hvel(i);
+  parallel_chunks(d.n, [&](size_t lo, size_t hi) {
+    if (positions)
+      for (size_t i = lo; i < hi; ++i) positions[i] = d.hx[i];
+    if (velocities)
+      for (size_t i = lo; i < hi; ++i) velocities[i] = d.hvel(i);
+  });
 }
 
 size_t GpuRing::sumv_series(uint64_t* out, size_t cap) {

@@ -161,16 +161,6 @@ __global__ void ensemble_init_kernel(const RingDesc* __restrict__ rings, uint32_
   }
 }
 
-__global__ void ensemble_sumv_kernel(const RingDesc* __restrict__ rings, uint32_t r,
-                                     const uint8_t* __restrict__ V, unsigned long long* out) {
-  const RingDesc d = rings[r];
-  unsigned long long s = 0;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < d.n; i += gridDim.x * blockDim.x)
-    s += V[d.off + i];
-  s = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(s));
-  if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
-}
-
 uint32_t bits_for(uint64_t max_value) {
   uint32_t b = 0;
   while (b < 32 && (uint64_t(1) << b) <= max_value) ++b;
@@ -192,7 +182,6 @@ struct GpuEnsemble::Impl {
   uint32_t* d_counter = nullptr;
   uint32_t* X = nullptr;
   uint8_t* V = nullptr;
-  unsigned long long* d_sum = nullptr;
   RingDesc* h_desc = nullptr;  // pinned mirror
   int grid = 1;
   size_t smem = 0;
@@ -298,7 +287,6 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
     CKE(cudaMallocHost(&d.h_desc, d.desc.size() * sizeof(RingDesc)));
     CKE(cudaMalloc(&d.d_order, d.order.size() * 4));
     CKE(cudaMalloc(&d.d_counter, 4));
-    CKE(cudaMalloc(&d.d_sum, sizeof(unsigned long long)));
     CKE(cudaMemcpy(d.d_order, d.order.data(), d.order.size() * 4, cudaMemcpyHostToDevice));
     d.push();
     d.smem = (kEnsHeaderWords + max_cars) * 4;
@@ -322,7 +310,6 @@ GpuEnsemble::~GpuEnsemble() {
   cudaFree(d.d_desc);
   cudaFree(d.d_order);
   cudaFree(d.d_counter);
-  cudaFree(d.d_sum);
   cudaFreeHost(d.h_desc);
   if (d.stream) cudaStreamDestroy(d.stream);
 }

@@ -238,6 +238,75 @@ class Engine:
             pass
 
 
+class Ensemble:
+    """Many independent rings advanced together (nasch_ensemble)."""
+
+    def __init__(self, params: list[SimParams]):
+        self._params = list(params)  # keep handles alive during construction
+        arr = (C.c_void_p * len(params))(*[p._h.value for p in params])
+        h = C.c_void_p()
+        _check(_lib().nasch_ensemble_new(arr, len(params), C.byref(h)))
+        self._h = h
+        self.ncars = [p.ncars for p in params]
+        self.length = [p.length for p in params]
+
+    def __len__(self):
+        return _lib().nasch_ensemble_size(self._h)
+
+    def set_state(self, ring: int, x, v) -> None:
+        x = np.ascontiguousarray(x, np.uint32)
+        v = np.ascontiguousarray(v, np.uint32)
+        _check(_lib().nasch_ensemble_set_state32(self._h, ring, _u32p(x), _u32p(v), len(x)))
+
+    def advance(self, steps: int) -> None:
+        _check(_lib().nasch_ensemble_advance(self._h, steps))
+
+    def enqueue(self, steps: int) -> None:
+        _check(_lib().nasch_ensemble_enqueue(self._h, steps))
+
+    def synchronize(self) -> None:
+        _check(_lib().nasch_ensemble_synchronize(self._h))
+
+    def steps_done(self, ring: int) -> int:
+        return _lib().nasch_ensemble_steps_done(self._h, ring)
+
+    def sumv_totals(self) -> np.ndarray:
+        out = np.empty(len(self.ncars), np.uint64)
+        _check(_lib().nasch_ensemble_sumv_totals(self._h, _u64p(out), len(out)))
+        return out
+
+    def sumv_last(self) -> np.ndarray:
+        out = np.empty(len(self.ncars), np.uint64)
+        _check(_lib().nasch_ensemble_sumv_last(self._h, _u64p(out), len(out)))
+        return out
+
+    def snapshot(self, ring: int):
+        n = self.ncars[ring]
+        x = np.empty(n, np.uint64)
+        v = np.empty(n, np.uint64)
+        _check(_lib().nasch_ensemble_state(self._h, ring, _u64p(x), _u64p(v), n))
+        return x, v
+
+    @property
+    def cuda_stream(self) -> int:
+        return _lib().nasch_ensemble_cuda_stream(self._h) or 0
+
+    @property
+    def kernel_launches(self) -> int:
+        return _lib().nasch_ensemble_kernel_launches(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().nasch_ensemble_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def fill_uniform_state(length: int, ncars: int, vmax_init: int, seed: int):
     """BASELINE inputs: sorted distinct uniform positions (u32) and
     velocities uniform in [0, vmax_init] (u32)."""

@@ -1,0 +1,99 @@
+"""GPU parity of the ensemble engine (BASELINE config 4 shape) against the
+oracle: every ring is the reference's single-ring model with its own
+parameters and minstd stream (src/model.cpp:42-75, src/lcg.cpp:11-16)."""
+import numpy as np
+import pytest
+
+from paper_2309_14311_b200 import nasch
+
+pytestmark = pytest.mark.gpu
+
+
+def mk(L, N, vmax, p, steps, seed):
+    return nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=steps, seed=seed)
+
+
+def oracle_ring(port, L, N, vmax, p, seed, T, x0=None, v0=None):
+    if x0 is None:
+        x0, v0 = port.init_state(L, N)
+    return port.run(L, vmax, p, seed, T, np.asarray(x0, np.uint64), np.asarray(v0, np.uint64),
+                    want_checksum=False)
+
+
+def test_ensemble_matches_oracle_per_ring(port):
+    rng = np.random.default_rng(3)
+    specs = []
+    for i in range(40):
+        L = int(rng.integers(20, 60000))
+        N = int(rng.integers(1, min(L, 50000) + 1))
+        vmax = int(rng.integers(1, 12))
+        p = float(rng.choice([0.0, 0.1, 0.13, 0.3, 0.5, 0.7, 1.0]))
+        specs.append((L, N, vmax, p, 120, int(rng.integers(0, 2**40))))
+    ens = nasch.Ensemble([mk(*s) for s in specs])
+    ens.advance(45)
+    ens.advance(1000)  # clamps at 120
+    tot = ens.sumv_totals()
+    last = ens.sumv_last()
+    for r, (L, N, vmax, p, T, seed) in enumerate(specs):
+        o = oracle_ring(port, L, N, vmax, p, seed, T)
+        x, v = ens.snapshot(r)
+        assert ens.steps_done(r) == T
+        assert (x == o["x"]).all() and (v == o["v"]).all(), r
+        assert int(tot[r]) == int(o["sumv"].sum()), r
+        assert int(last[r]) == int(o["sumv"][-1]), r
+
+
+def test_ensemble_per_step_series_and_injected_state(port):
+    specs = [(100000, 5000, 5, 0.13, 60, 11), (100000, 50000, 5, 0.7, 60, 12),
+             (100000, 27500, 5, 0.0, 60, 13), (1000, 1000, 5, 0.4, 60, 14)]
+    ens = nasch.Ensemble([mk(*s) for s in specs])
+    inits = []
+    for r, (L, N, vmax, p, T, seed) in enumerate(specs):
+        x0, v0 = nasch.fill_uniform_state(L, N, 0, 100 + r)
+        ens.set_state(r, x0, v0)
+        inits.append((x0, v0))
+    orc = [oracle_ring(port, L, N, vmax, p, seed, T, *inits[r])
+           for r, (L, N, vmax, p, T, seed) in enumerate(specs)]
+    for t in range(60):
+        ens.advance(1)
+        last = ens.sumv_last()
+        for r in range(len(specs)):
+            assert int(last[r]) == int(orc[r]["sumv"][t]), (r, t)
+    for r in range(len(specs)):
+        x, v = ens.snapshot(r)
+        assert (x == orc[r]["x"]).all() and (v == orc[r]["v"]).all()
+
+
+def test_ensemble_overflow_ring_and_order_invariance(port):
+    """A ring too large for shared memory runs on its own engine; results do
+    not depend on which rings share the launch or in which order."""
+    specs = [(300000, 90000, 5, 0.2, 40, 5), (5000, 2000, 5, 0.2, 40, 6),
+             (20000, 15000, 200, 0.25, 40, 7)]
+    a = nasch.Ensemble([mk(*s) for s in specs])
+    a.advance(40)
+    b = nasch.Ensemble([mk(*s) for s in reversed(specs)])
+    b.advance(17)
+    b.advance(23)
+    ta, tb = a.sumv_totals(), b.sumv_totals()[::-1]
+    assert (ta == tb).all()
+    for r, (L, N, vmax, p, T, seed) in enumerate(specs):
+        o = oracle_ring(port, L, N, vmax, p, seed, T)
+        x, v = a.snapshot(r)
+        assert (x == o["x"]).all() and (v == o["v"]).all()
+        assert int(ta[r]) == int(o["sumv"].sum())
+
+
+def test_ensemble_equals_single_ring_engine():
+    L, N = 100000, 35000
+    x0, v0 = nasch.fill_uniform_state(L, N, 0, 9)
+    e = nasch.Engine(mk(L, N, 5, 0.3, 500, 77))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.run()
+    ens = nasch.Ensemble([mk(L, N, 5, 0.3, 500, 77)])
+    ens.set_state(0, x0, v0)
+    ens.advance(500)
+    xe, ve = e.snapshot()
+    xs, vs = ens.snapshot(0)
+    assert (xe == xs).all() and (ve == vs).all()
+    assert int(ens.sumv_totals()[0]) == int(e.sumv_series().sum())
