@@ -185,7 +185,15 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- device-resident throughput -----------------------------------
     prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=W + K, seed=seed)
-    eng = nasch.Engine(prm)
+    if world > 1:
+        # one ring, G contiguous segments, halo + cone window all-gathered
+        # over NCCL once per K-step launch
+        box = [nasch.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        nccl_id = box[0]
+        eng = nasch.Engine.distributed(prm, rank, world, nccl_id)
+    else:
+        eng = nasch.Engine(prm)
     eng.set_checksum(False)
     eng.set_state(x, v)
     eng.advance(W)
@@ -212,34 +220,60 @@ def run_ours(args, rank, world, local_rank):
         ms = float(t.item())
         dist.barrier()
     sumv = eng.sumv_series()
-    xs, vs = eng.snapshot()
-    ok = bool((np.diff(xs.astype(np.int64)) > 0).all() and int(xs[-1]) < L
-              and int(vs.sum()) == int(sumv[-1]))
+    if world == 1:
+        xs, vs = eng.snapshot()
+        ok = bool((np.diff(xs.astype(np.int64)) > 0).all() and int(xs[-1]) < L
+                  and int(vs.sum()) == int(sumv[-1]))
+        del xs, vs
+    else:
+        # whole-ring velocity sums = sum of the ranks' partial series; the
+        # wrap series (from the shared plan) must agree on every rank
+        tot = torch.tensor(sumv.astype(np.int64), device="cuda")
+        dist.all_reduce(tot)
+        wraps = eng.wrap_series()
+        allw = [None] * world
+        dist.all_gather_object(allw, wraps.tolist())
+        ok = bool(len(sumv) == W + K and all(w == allw[0] for w in allw)
+                  and int(tot.max().item()) <= vmax * N)
     eng.close()
-    del xs, vs
-    value = world * N * K / (ms / 1000.0) if world == 1 else N * K / (ms / 1000.0)
+    value = N * K / (ms / 1000.0)  # whole ring, max over ranks
     step_ms = ms / K
 
     # ---- end to end through the C ABI with host buffers ----------------
     x64 = x.astype(np.uint64)
     v64 = v.astype(np.uint64)
-    outx = np.empty(N, np.uint64)
-    outv = np.empty(N, np.uint64)
     prm2 = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=K, seed=seed)
-    eng2 = nasch.Engine(prm2)
+    if world > 1:
+        eng2 = nasch.Engine.distributed(prm2, rank, world, nccl_id)
+        dist.barrier()
+    else:
+        outx = np.empty(N, np.uint64)
+        outv = np.empty(N, np.uint64)
+        eng2 = nasch.Engine(prm2)
     eng2.set_checksum(False)
     eng2.advance(0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     eng2.set_state(x64, v64)
     eng2.advance(K)
-    series = eng2.mean_velocity_series()
-    eng2.snapshot(out_x=outx, out_v=outv)
+    series = eng2.sumv_series()
+    if world > 1:  # per-step result: whole-ring mean velocity on every rank
+        st = torch.tensor(series.astype(np.int64), device="cuda")
+        dist.all_reduce(st)
+        mean_v = st.cpu().numpy().astype(np.float64) / N
+    else:
+        mean_v = eng2.mean_velocity_series()
+        eng2.snapshot(out_x=outx, out_v=outv)
     t1 = time.perf_counter()
-    e2e_value = N * K / (t1 - t0)
+    e2e_s = t1 - t0
+    if dist:
+        tt = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    e2e_value = N * K / e2e_s
     e2e_h2d = (4 + 1) * N / K
-    e2e_d2h = ((4 + 1) * N + 16 * K) / K
-    assert len(series) == K
+    e2e_d2h = ((5 * N if world == 1 else 0) + 8 * K * world) / K  # final state + Σv series
+    assert len(mean_v) == K
     eng2.close()
 
     # ---- roofline --------------------------------------------------------
@@ -248,6 +282,7 @@ def run_ours(args, rank, world, local_rank):
     # N * spl car-updates.  The engine actually moves 10 B per car per launch
     # (u8 velocities) and, temporally blocked, once per spl steps.
     peak, peak_src = peaks()
+    peak *= world  # aggregate over the ranks' HBM
     launch_ms = step_ms * spl
     achieved = SURVEY_BYTES_PER_UPDATE * N * spl / (launch_ms / 1000.0) / 1e9
     traffic = ncu_traffic()
@@ -301,13 +336,6 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
-        return
-    if world > 1:
-        # The single ring is not sharded across ranks yet (DESIGN.md
-        # "Multi-GPU"); refuse rather than report replicas as scaling.
-        if rank == 0:
-            print(json.dumps({"metric": "car-updates/s", "value": None, "n_gpus": world,
-                              "unavailable": "segmented multi-GPU ring not built yet"}), flush=True)
         return
     run_ours(args, rank, world, local_rank)
 

@@ -179,6 +179,25 @@ const char* nasch_b200_version(void);
  * (src/model.cpp:51). */
 uint32_t nasch_b200_draw_threshold(double p);
 
+/* ---- one ring over several GPUs (extension) ------------------------------
+ * nasch_sim_new_kind(params, G, NASCH_ENGINE_CUDA, &sim) with G > 1 splits
+ * the ring into G contiguous car segments (the reference's block formula,
+ * engine.cpp:31-42) over the visible GPUs of this process; the trajectory is
+ * bit-identical for every G.  One process per GPU instead: rank 0 calls
+ * nasch_nccl_unique_id, the launcher broadcasts the 128 bytes, and every rank
+ * calls nasch_sim_new_distributed.  A distributed sim advances, times and
+ * reports its own segment: sumv/mean-velocity series are this rank's
+ * partial sums (the whole-ring series is their sum over ranks), the wrap
+ * series is the whole ring's, and whole-ring calls (state, observables,
+ * checksum, frames) return NASCH_ERR_INVALID. */
+nasch_status nasch_nccl_unique_id(void* out128);
+nasch_status nasch_sim_new_distributed(const nasch_params* params, unsigned rank,
+                                       unsigned world, const void* nccl_id,
+                                       nasch_sim** out);
+/* Global car ids this process holds: [first, first + count). */
+nasch_status nasch_sim_shard_range(const nasch_sim* sim, uint64_t* first,
+                                   uint64_t* count);
+
 /* ---- ensembles of independent rings (extension) ------------------------
  * One handle advances many independent simulations at once -- BASELINE
  * config 4's fundamental-diagram sweep.  Each ring is exactly the

@@ -80,6 +80,10 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_fill_uniform_state": (C.c_int, [_u64, _u64, _u64, _u64, _u32p, _u32p]),
     "nasch_b200_version": (C.c_char_p, []),
     "nasch_b200_draw_threshold": (C.c_uint32, [C.c_double]),
+    # multi-GPU ring
+    "nasch_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "nasch_sim_new_distributed": (C.c_int, [_P, C.c_uint, C.c_uint, C.c_void_p, C.POINTER(_P)]),
+    "nasch_sim_shard_range": (C.c_int, [_P, _u64p, _u64p]),
     # ensembles
     "nasch_ensemble_new": (C.c_int, [C.POINTER(_P), C.c_size_t, C.POINTER(_P)]),
     "nasch_ensemble_free": (None, [_P]),

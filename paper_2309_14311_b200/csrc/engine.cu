@@ -472,6 +472,10 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   a.a1 = powmod(kA, (1 + kOrder - (d.n % kOrder)) % kOrder);
   a.g = powmod(kA, uint64_t(d.grid) * tile);
   a.kplan = d.tb ? d.K : 0;
+  a.nl = d.n;
+  a.gofs = 0;
+  a.agofs = 1;
+  a.sharded = 0;
   a.blkpow = d.blkpow;
   a.thrpow = d.thrpow;
   a.ctl = d.ctl;
@@ -545,7 +549,6 @@ void GpuRing::synchronize() {
 
 uint64_t GpuRing::steps_done() const { return impl_->steps_done; }
 uint64_t GpuRing::checksum() const { return impl_->hash; }
-uint64_t GpuRing::draws() const { return impl_->steps_done * impl_->params.car_count; }
 const std::vector<Frame>& GpuRing::frames() const { return impl_->frames; }
 const SimParams& GpuRing::params() const { return impl_->params; }
 
@@ -599,6 +602,10 @@ void* GpuRing::cuda_stream() const { return impl_->stream; }
 uint64_t GpuRing::kernel_launches() const { return impl_->launches; }
 int GpuRing::velocity_bytes() const { return impl_->vbytes; }
 int GpuRing::steps_per_launch() const { return static_cast<int>(impl_->steps_per_launch()); }
+void GpuRing::shard_range(uint64_t* first, uint64_t* count) const {
+  if (first) *first = 0;
+  if (count) *count = impl_->params.car_count;
+}
 
 // Selection sampling (Knuth Vol. 2, Algorithm S): cell c is chosen with
 // probability need/(L - c), which yields every N-subset of [0, L) with

@@ -1,10 +1,16 @@
-// engine.hpp -- the B200 ring engine behind the C ABI (CUDA-free header).
+// engine.hpp -- the B200 ring engines behind the C ABI (CUDA-free header).
 //
-// Replaces the reference's stateful stepper nasch::Engine
+// Replace the reference's stateful stepper nasch::Engine
 // (src/engine.hpp:84-126, src/engine.cpp:44-200) for the agent kind.  The
-// state lives on one GPU in ID order (never rotated); see DESIGN.md
-// "Data layout" for the rank <-> id map that reproduces the reference's
-// rank-ordered draws bit for bit.
+// state lives in ID order (never rotated); see DESIGN.md section 2 for the
+// rank <-> id map that reproduces the reference's rank-ordered draws bit
+// for bit.
+//
+//   GpuRing      the whole ring on the current GPU
+//   ShardedRing  contiguous car segments on several GPUs (or several
+//                segments on one GPU), exchanging a halo + the origin-cone
+//                window once per launch: in-process peer copies, or NCCL with
+//                one process per GPU (sharded.cu)
 #pragma once
 #include <cstddef>
 #include <cstdint>
@@ -15,55 +21,119 @@
 
 namespace nb200 {
 
-class GpuRing {
+class RingEngine {
  public:
-  // src/engine.cpp:44-79: validates, places cars with init_state
-  // (model.cpp:30-40) and records frame 0 when output is on.
-  explicit GpuRing(const SimParams& params);
-  ~GpuRing();
-  GpuRing(const GpuRing&) = delete;
-  GpuRing& operator=(const GpuRing&) = delete;
+  virtual ~RingEngine() = default;
 
   // Extension: replace the current state by a rank-ordered one (strictly
   // ascending positions < L, velocities <= vmax).  Keeps steps_done,
   // draws and checksum, so it also serves as checkpoint restore.
-  void set_state(const uint64_t* x, const uint64_t* v, size_t n);
-  void set_state32(const uint32_t* x, const uint32_t* v, size_t n);
+  virtual void set_state(const uint64_t* x, const uint64_t* v, size_t n) = 0;
+  virtual void set_state32(const uint32_t* x, const uint32_t* v, size_t n) = 0;
 
   // src/engine.cpp:88-99: clamps at params.steps; synchronous.
-  void advance(uint64_t steps);
+  virtual void advance(uint64_t steps) = 0;
   // Extension: asynchronous advance on the engine's stream (no host sync
   // unless a checksum or frame is due); synchronize() completes it.
-  void enqueue(uint64_t steps);
-  void synchronize();
+  virtual void enqueue(uint64_t steps) = 0;
+  virtual void synchronize() = 0;
 
-  uint64_t steps_done() const;
-  uint64_t checksum() const;
-  uint64_t draws() const;
-  const std::vector<Frame>& frames() const;
-  const SimParams& params() const;
+  virtual uint64_t steps_done() const = 0;
+  virtual uint64_t checksum() const = 0;
+  uint64_t draws() const { return steps_done() * params().car_count; }
+  virtual const std::vector<Frame>& frames() const = 0;
+  virtual const SimParams& params() const = 0;
 
   // src/model.cpp:131-142 formula on the device's exact velocity sum.
-  void observables(double* density, double* mean_velocity, double* flow);
+  virtual void observables(double* density, double* mean_velocity, double* flow) = 0;
   // Rank (increasing position) order, widened to u64; either may be null.
-  void state(uint64_t* positions, uint64_t* velocities);
-  // Extension: exact velocity sum after each completed step 1..steps_done.
-  size_t sumv_series(uint64_t* out, size_t cap);
-  size_t wrap_series(uint64_t* out, size_t cap);
+  virtual void state(uint64_t* positions, uint64_t* velocities) = 0;
+  // Extension: exact velocity sum / wrap count after each completed step.
+  virtual size_t sumv_series(uint64_t* out, size_t cap) = 0;
+  virtual size_t wrap_series(uint64_t* out, size_t cap) = 0;
 
-  void set_checksum(bool enabled);
-  bool checksum_enabled() const;
-  void* cuda_stream() const;
-  uint64_t kernel_launches() const;
-  int velocity_bytes() const;
+  virtual void set_checksum(bool enabled) = 0;
+  virtual void* cuda_stream() const = 0;
+  virtual uint64_t kernel_launches() const = 0;
   // Steps advanced per step-kernel launch: K in temporal-blocked mode, 1
   // in single-step mode (small rings).
-  int steps_per_launch() const;
+  virtual int steps_per_launch() const = 0;
+  // Global ids held by this process: [first, first + count).
+  virtual void shard_range(uint64_t* first, uint64_t* count) const = 0;
+};
+
+class GpuRing : public RingEngine {
+ public:
+  // src/engine.cpp:44-79: validates, places cars with init_state
+  // (model.cpp:30-40) and records frame 0 when output is on.
+  explicit GpuRing(const SimParams& params);
+  ~GpuRing() override;
+  GpuRing(const GpuRing&) = delete;
+  GpuRing& operator=(const GpuRing&) = delete;
+
+  void set_state(const uint64_t* x, const uint64_t* v, size_t n) override;
+  void set_state32(const uint32_t* x, const uint32_t* v, size_t n) override;
+  void advance(uint64_t steps) override;
+  void enqueue(uint64_t steps) override;
+  void synchronize() override;
+  uint64_t steps_done() const override;
+  uint64_t checksum() const override;
+  const std::vector<Frame>& frames() const override;
+  const SimParams& params() const override;
+  void observables(double* density, double* mean_velocity, double* flow) override;
+  void state(uint64_t* positions, uint64_t* velocities) override;
+  size_t sumv_series(uint64_t* out, size_t cap) override;
+  size_t wrap_series(uint64_t* out, size_t cap) override;
+  void set_checksum(bool enabled) override;
+  void* cuda_stream() const override;
+  uint64_t kernel_launches() const override;
+  int steps_per_launch() const override;
+  void shard_range(uint64_t* first, uint64_t* count) const override;
+  bool checksum_enabled() const;
+  int velocity_bytes() const;
 
  private:
   struct Impl;
   std::unique_ptr<Impl> impl_;
 };
+
+class ShardedRing : public RingEngine {
+ public:
+  // In-process: `shards` segments spread round-robin over the visible GPUs,
+  // exchanging through peer copies.
+  ShardedRing(const SimParams& params, unsigned shards);
+  // One process per GPU: this process holds segment `rank` of `world`,
+  // exchanging through NCCL (unique id from nccl_unique_id()).
+  ShardedRing(const SimParams& params, unsigned rank, unsigned world, const void* nccl_id);
+  ~ShardedRing() override;
+
+  void set_state(const uint64_t* x, const uint64_t* v, size_t n) override;
+  void set_state32(const uint32_t* x, const uint32_t* v, size_t n) override;
+  void advance(uint64_t steps) override;
+  void enqueue(uint64_t steps) override;
+  void synchronize() override;
+  uint64_t steps_done() const override;
+  uint64_t checksum() const override;
+  const std::vector<Frame>& frames() const override;
+  const SimParams& params() const override;
+  void observables(double* density, double* mean_velocity, double* flow) override;
+  void state(uint64_t* positions, uint64_t* velocities) override;
+  size_t sumv_series(uint64_t* out, size_t cap) override;
+  size_t wrap_series(uint64_t* out, size_t cap) override;
+  void set_checksum(bool enabled) override;
+  void* cuda_stream() const override;
+  uint64_t kernel_launches() const override;
+  int steps_per_launch() const override;
+  void shard_range(uint64_t* first, uint64_t* count) const override;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
+// NCCL unique id (128 bytes) for ShardedRing's distributed constructor;
+// rank 0 creates it and the launcher broadcasts it.
+void nccl_unique_id(void* out128);
 
 // Extension: seeded uniform distinct sorted positions (selection sampling)
 // and velocities uniform in [0, vmax_init] -- the BASELINE.json inputs.

@@ -59,9 +59,11 @@ struct Ctl {
 };
 
 struct StepRec {
-  unsigned long long sumv;  // exact sum of velocities after the step
-  unsigned int c;           // cars that crossed the origin in the step
+  unsigned long long sumv;  // exact sum of velocities after the step (this shard's cars)
+  unsigned int c;           // cars (of this shard) that crossed the origin in the step
   unsigned int W;           // rank offset the step was drawn with
+  unsigned int cplan;       // crossings the origin-cone plan predicted (whole ring)
+  unsigned int pad;
 };
 
 constexpr uint32_t kRecCap = 1u << 16;  // device ring of per-step records
@@ -79,6 +81,10 @@ struct RingArgs {
   uint32_t a1;      // a^(1-N) mod m (step across the rank seam)
   uint32_t g;       // a^(gridDim.x * tile stride) mod m (grid-stride advance)
   uint32_t kplan;   // temporal-blocking plan length (0: single-step mode)
+  uint32_t nl;      // cars stored in this buffer (= n on one GPU; a shard's count otherwise)
+  uint32_t gofs;    // global id of local car 0 (0 on one GPU)
+  uint32_t agofs;   // a^gofs mod m
+  uint32_t sharded; // 1: the halo sits inline after nl and the plan comes from the exchange
   const uint32_t* blkpow;  // a^(blockIdx.x * tile stride)
   const uint32_t* thrpow;  // a^(threadIdx.x * cars per thread)
   Ctl* ctl;
@@ -263,20 +269,24 @@ __device__ __forceinline__ bool last_block_done(Ctl* ctl) {
 //   i in [M, M + kk) : ranks 0..kk-1, the leaders those cars need;
 // for kk steps with exact draws, and writes W, E, E2 and the crossing count
 // of each step into the plan.  Requires L > kk*vmax and N >= M + kk.
-template <typename VT, int TPB>
-__device__ void cone_plan(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t,
-                          uint32_t W, uint32_t kk, Ctl* ctl) {
+// Global id of cone slot i (slots [0, kk*vmax) trail the rank-0 car, the
+// next kk lead it).
+__device__ __forceinline__ uint32_t cone_slot_id(uint32_t N, uint32_t W, uint32_t M, uint32_t i) {
+  const uint32_t h = W == 0 ? 0u : N - W;
+  return static_cast<uint32_t>((uint64_t(h) + (N - M) + i) % N);
+}
+
+// The cone simulation proper; thread i holds cone slot i's car (x, v).
+template <int TPB>
+__device__ void cone_simulate(const RingArgs& ra, uint32_t x, uint32_t v, uint64_t t, uint32_t W,
+                              uint32_t kk, Ctl* ctl) {
   __shared__ uint32_t s_x[TPB];
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax;
   const uint32_t M = kk * vmax;
   const uint32_t C = M + kk;
   const uint32_t i = threadIdx.x;
   const bool act = i < C;
-  const uint32_t h = W == 0 ? 0u : N - W;
-  const uint32_t id = static_cast<uint32_t>((uint64_t(h) + (N - M) + i) % N);
-  // .cg loads: the state was just written by other blocks of this launch
-  uint32_t x = act ? __ldcg(X + id) : 0u;
-  uint32_t v = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+  const uint32_t id = cone_slot_id(N, W, M, i);
   const uint32_t apw = act ? powmod(kA, id) : 1u;
   uint32_t E = mulmod(ra.s0, powmod(kA, draw_exponent(t, N, W)));
   uint32_t Wj = W;
@@ -309,6 +319,20 @@ __device__ void cone_plan(const RingArgs& ra, const uint32_t* X, const VT* V, ui
     ctl->E = ctl->Ek[0];
     ctl->E2 = ctl->E2k[0];
   }
+}
+
+// Plan from the whole ring held by one GPU: cone cars read straight from
+// (X, V) with global ids.
+template <typename VT, int TPB>
+__device__ void cone_plan(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t,
+                          uint32_t W, uint32_t kk, Ctl* ctl) {
+  const uint32_t M = kk * ra.vmax;
+  const bool act = threadIdx.x < M + kk;
+  const uint32_t id = cone_slot_id(ra.n, W, M, threadIdx.x);
+  // .cg loads: the state was just written by other blocks of this launch
+  const uint32_t x = act ? __ldcg(X + id) : 0u;
+  const uint32_t v = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+  cone_simulate<TPB>(ra, x, v, t, W, kk, ctl);
 }
 
 // Plan for the current state (after set_state / construction).

@@ -56,25 +56,31 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
   const uint32_t i0 = threadIdx.x * CPT;  // first car of this thread within the tile
   const uint32_t reach = k * vmax;        // farthest any car moves in this launch (< L)
 
-  uint32_t P = mulmod_d(__ldg(ra.blkpow + blockIdx.x), __ldg(ra.thrpow + threadIdx.x));
+  // P = a^(global id of this thread's first car in its first tile)
+  uint32_t P = mulmod_d(mulmod_d(ra.agofs, __ldg(ra.blkpow + blockIdx.x)), __ldg(ra.thrpow + threadIdx.x));
   uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
-  const uint32_t ntiles = (N + STORE - 1) / STORE;
+  const uint32_t nl = ra.nl;  // cars stored here (a shard's segment, or the ring)
+  const uint32_t ntiles = (nl + STORE - 1) / STORE;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t a0 = tile * STORE;
-    const uint32_t base = a0 + i0;     // id of car 0 (may exceed N in the wrap tile)
-    const bool fast = a0 + LOAD <= N;  // block-uniform: no id wraps in this tile
+    const uint32_t a0 = tile * STORE;          // local index of the tile
+    const uint32_t bl = a0 + i0;               // local index of car 0
+    const uint32_t base = ra.gofs + bl;        // global id of car 0 (may exceed N at the wrap)
+    const bool nowrap = ra.gofs + a0 + LOAD <= N;  // block-uniform: ids do not wrap
+    // Contiguous in memory: always for a shard (its halo sits inline after
+    // nl); on one GPU unless the tile wraps past id N-1.
+    const bool fast = ra.sharded || nowrap;
     uint32_t x[CPT], v[CPT], ap[CPT];
     if (fast) {
 #pragma unroll
       for (int q = 0; q < CPT / 4; ++q) {
-        const uint4 r = ld_nc_v4(X + base + 4 * q);
+        const uint4 r = ld_nc_v4(X + bl + 4 * q);
         x[4 * q] = r.x;
         x[4 * q + 1] = r.y;
         x[4 * q + 2] = r.z;
         x[4 * q + 3] = r.w;
       }
-      VLanes<VT, CPT>::load(V + base, v);
-    } else {
+      VLanes<VT, CPT>::load(V + bl, v);
+    } else {  // one GPU, wrap tile: ids past N-1 continue at 0
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         uint32_t id = base + c;
@@ -93,12 +99,12 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
     P = mulmod_d(P, ra.g);
     uint32_t own = 0;  // bit c: car c is stored by this tile
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) own |= (i0 + c < STORE && base + c < N) ? (1u << c) : 0u;
+    for (int c = 0; c < CPT; ++c) own |= (i0 + c < STORE && bl + c < nl) ? (1u << c) : 0u;
     const bool own_all = own == (1u << CPT) - 1u;
     uint32_t xmax = x[0];
 #pragma unroll
     for (int c = 1; c < CPT; ++c) xmax = max(xmax, x[c]);
-    const bool plain = fast && xmax < L - reach;
+    const bool plain = nowrap && xmax < L - reach;
 
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t E = s_E[j], E2 = s_E2[j];
@@ -121,7 +127,14 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
           v[c] = vc;
           x[c] += vc;
         }
-        if (own_all) s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+        if (own_all) {
+          s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+        } else if (own) {  // a shard's last, partial tile
+          Acc sum = 0;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
+          s_acc[j][threadIdx.x] += sum;
+        }
       } else {
         Acc sum = 0;
         uint32_t crs = 0;
@@ -142,19 +155,21 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
       }
     }
     if (fast) {
+      // A shard's last tile may spill past nl into its halo/padding region,
+      // which the plan kernel rewrites before the next launch reads it.
       if (i0 + CPT <= STORE) {
 #pragma unroll
         for (int q = 0; q < CPT / 4; ++q)
-          *reinterpret_cast<uint4*>(Xo + base + 4 * q) =
+          *reinterpret_cast<uint4*>(Xo + bl + 4 * q) =
               make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
-        VLanes<VT, CPT>::store(Vo + base, v);
+        VLanes<VT, CPT>::store(Vo + bl, v);
       }
     } else {
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         if ((own >> c) & 1u) {
-          Xo[base + c] = x[c];
-          Vo[base + c] = static_cast<VT>(v[c]);
+          Xo[bl + c] = x[c];
+          Vo[bl + c] = static_cast<VT>(v[c]);
         }
       }
     }
@@ -178,7 +193,9 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
       StepRec* r = ra.rec + ((t + j) % kRecCap);
       const uint32_t c = atomicAdd(&r->c, 0u);
       r->W = ctl->Wk[j];
-      if (c != ctl->ck[j] && !ctl->err) {
+      r->cplan = ctl->ck[j];
+      // A shard sees only its own crossings; the host checks their sum.
+      if (!ra.sharded && c != ctl->ck[j] && !ctl->err) {
         ctl->err = 1;
         ctl->err_step = static_cast<unsigned int>(t + j);
       }
@@ -189,6 +206,17 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
   }
   __syncthreads();
   const uint32_t Wn = s_Wnext;
+  if (ra.sharded) {
+    // The next plan needs cars of other shards: the exchange + plan kernel
+    // (shard_kernels.cuh) produce it.
+    if (threadIdx.x == 0) {
+      ctl->W = Wn;
+      ctl->t = t + k;
+      ctl->buf = static_cast<unsigned int>(b ^ 1);
+      ctl->ticket = 0;
+    }
+    return;
+  }
   cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
   for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
     StepRec* r = ra.rec + ((t + k + j) % kRecCap);

@@ -122,12 +122,30 @@ class Engine:
 
     AGENT, GRID_REFERENCE, CUDA = 0, 1, 2
 
-    def __init__(self, params: SimParams, workers: int = 1, kind: int = 0):
-        h = C.c_void_p()
-        _check(_lib().nasch_sim_new_kind(params._h, workers, kind, C.byref(h)))
+    def __init__(self, params: SimParams, workers: int = 1, kind: int = 0, *, _handle=None):
+        if _handle is None:
+            h = C.c_void_p()
+            _check(_lib().nasch_sim_new_kind(params._h, workers, kind, C.byref(h)))
+        else:
+            h = _handle
         self._h = h
         self.ncars = params.ncars
         self.length = params.length
+
+    @classmethod
+    def distributed(cls, params: SimParams, rank: int, world: int, nccl_id: bytes) -> "Engine":
+        """One segment of a ring split over `world` processes (one GPU each),
+        exchanging through NCCL; `nccl_id` comes from nccl_unique_id() on
+        rank 0."""
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        h = C.c_void_p()
+        _check(_lib().nasch_sim_new_distributed(params._h, rank, world, buf, C.byref(h)))
+        return cls(params, _handle=h)
+
+    def shard_range(self) -> tuple[int, int]:
+        first, count = C.c_uint64(), C.c_uint64()
+        _check(_lib().nasch_sim_shard_range(self._h, C.byref(first), C.byref(count)))
+        return first.value, count.value
 
     # -- stepping ------------------------------------------------------
     def advance(self, steps: int) -> None:
@@ -314,6 +332,12 @@ def fill_uniform_state(length: int, ncars: int, vmax_init: int, seed: int):
     v = np.empty(ncars, np.uint32)
     _check(_lib().nasch_fill_uniform_state(length, ncars, vmax_init, seed, _u32p(x), _u32p(v)))
     return x, v
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib().nasch_nccl_unique_id(buf))
+    return buf.raw
 
 
 def physical_cores() -> int:

@@ -1,0 +1,117 @@
+"""GPU parity of the segmented ring (ShardedRing): G contiguous car segments
+exchanging a halo and the origin-cone window once per launch must give the
+single-ring trajectory bit for bit, for every G -- the B200 form of the
+reference's worker-count invariance (test_engine.cpp:136-152,
+test_capi.cpp:121-136).  Several shards share one GPU here (in-process
+peer-copy exchange); the NCCL exchange moves the same records."""
+import os
+
+import numpy as np
+import pytest
+
+from paper_2309_14311_b200 import nasch
+
+pytestmark = pytest.mark.gpu
+
+CUDA = nasch.Engine.CUDA
+
+
+def mk(L, N, vmax, p, steps, seed, output="none", stride=1):
+    return nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=steps, seed=seed,
+                           output=output, stride=stride)
+
+
+@pytest.fixture
+def k_env():
+    old = os.environ.get("NASCH_B200_K")
+    yield
+    if old is None:
+        os.environ.pop("NASCH_B200_K", None)
+    else:
+        os.environ["NASCH_B200_K"] = old
+
+
+def run_engine(params, workers, kind, x0=None, v0=None, steps=None, checksum=False, chunks=None):
+    e = nasch.Engine(params, workers, kind)
+    e.set_checksum(checksum)
+    if x0 is not None:
+        e.set_state(x0, v0)
+    for c in (chunks or [steps if steps is not None else params.steps]):
+        e.advance(c)
+    x, v = e.snapshot()
+    out = dict(x=x, v=v, sumv=e.sumv_series(), wraps=e.wrap_series(), checksum=e.checksum,
+               obs=e.observables(), spl=e.steps_per_launch)
+    e.close()
+    return out
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 7])
+def test_shards_match_oracle(port, G):
+    rng = np.random.default_rng(G)
+    for trial, (L, N, vmax, p) in enumerate([(40000, 6000, 5, 0.13), (9000, 8000, 5, 0.5),
+                                             (3 * 10**5, 25000, 12, 0.3), (20000, 2000, 3, 0.9)]):
+        x0 = np.sort(rng.choice(L, N, replace=False)).astype(np.uint64)
+        v0 = rng.integers(0, min(vmax, L - 1) + 1, N).astype(np.uint64)
+        T = 70
+        o = port.run(L, vmax, p, 5 + trial, T, x0, v0, want_checksum=False)
+        g = run_engine(mk(L, N, vmax, p, T, 5 + trial), G, CUDA, x0, v0, chunks=[13, 57])
+        assert (g["x"] == o["x"]).all() and (g["v"] == o["v"]).all(), (G, trial)
+        assert (g["sumv"] == o["sumv"]).all()
+        assert (g["wraps"] == o["wraps"]).all()
+
+
+@pytest.mark.parametrize("K", [2, 5, 16])
+def test_shard_depths_and_checksum(port, k_env, K):
+    os.environ["NASCH_B200_K"] = str(K)
+    L, N, vmax, p, T = 12000, 5000, 5, 0.35, 45
+    x0, v0 = port.init_state(L, N)
+    o = port.run(L, vmax, p, 21, T, x0, v0)
+    g = run_engine(mk(L, N, vmax, p, T, 21), 3, CUDA, checksum=True)
+    assert g["spl"] == K
+    assert g["checksum"] == o["checksum"]
+    assert (g["x"] == o["x"]).all() and (g["sumv"] == o["sumv"]).all()
+
+
+def test_shards_equal_single_gpu_engine_long_run():
+    L, N = 2 * 10**6, 4 * 10**5
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 4)
+    ref = run_engine(mk(L, N, 5, 0.25, 600, 8), 1, 0, x0, v0)
+    for G in (2, 5):
+        g = run_engine(mk(L, N, 5, 0.25, 600, 8), G, CUDA, x0, v0)
+        assert (g["x"] == ref["x"]).all() and (g["v"] == ref["v"]).all()
+        assert (g["sumv"] == ref["sumv"]).all() and g["obs"] == ref["obs"]
+
+
+def test_shard_frames_match_single(tmp_path):
+    p = mk(5000, 800, 5, 0.3, 40, 3, output="ascii", stride=7)
+    a = nasch.Engine(p, 1, 0)
+    a.set_checksum(False)
+    a.run()
+    b = nasch.Engine(p, 4, CUDA)
+    b.set_checksum(False)
+    b.run()
+    assert a.frame_count == b.frame_count == 6
+    a.write_ascii(str(tmp_path / "a.txt"))
+    b.write_ascii(str(tmp_path / "b.txt"))
+    assert open(tmp_path / "a.txt").read() == open(tmp_path / "b.txt").read()
+
+
+def test_nccl_distributed_path_single_rank(port):
+    """The one-process-per-GPU constructor with a 1-rank NCCL communicator:
+    exercises libnccl loading, communicator setup and the ncclAllGather
+    exchange on the real device."""
+    L, N, vmax, p, T = 30000, 9000, 5, 0.2, 48
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 12)
+    o = port.run(L, vmax, p, 4, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    e = nasch.Engine.distributed(mk(L, N, vmax, p, T, 4), 0, 1, nasch.nccl_unique_id())
+    assert e.shard_range() == (0, N)
+    e.set_state(x0, v0)
+    e.advance(T)
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all()
+
+
+def test_too_small_to_shard():
+    with pytest.raises(nasch.NaschError, match="too small"):
+        nasch.Engine(mk(1000, 100, 5, 0.3, 10, 1), 4, CUDA)
