@@ -44,6 +44,18 @@ __device__ __forceinline__ uint32_t mulmod_d(uint32_t x, uint32_t y) {
   const uint32_t r = static_cast<uint32_t>(p & kM) + static_cast<uint32_t>(p >> 31);
   return min(r, r - kM);
 }
+
+// Same product with the multiplier given doubled (x2 = 2x < 2^32): the fold
+// term p >> 31 is then the high word of x2*y, one IMAD.HI on the FMA pipe
+// instead of a 64-bit funnel shift on the ALU pipe.
+__device__ __forceinline__ uint32_t mulmod_x2(uint32_t x2, uint32_t y) {
+  uint32_t lo, hi;
+  asm("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(x2), "r"(y));
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(x2), "r"(y));
+  // x2*y = 2p: lo holds bits 1..31 of p shifted up one; p & m = lo >> 1
+  const uint32_t r = (lo >> 1) + hi;
+  return min(r, r - kM);
+}
 #endif
 
 // a^e mod m by square-and-multiply (host side / one-off device use).

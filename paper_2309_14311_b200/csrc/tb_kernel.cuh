@@ -89,12 +89,13 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
         v[c] = V[id];
       }
     }
-    // a^id for this thread's cars (an id wrapped past N multiplies by a^-N)
+    // 2 * a^id for this thread's cars (an id wrapped past N multiplies by
+    // a^-N); doubled for mulmod_x2
     uint32_t u = P;
 #pragma unroll
     for (int c = 0; c < CPT; ++c) {
       if (c) u = mulmod_d(u, kA);
-      ap[c] = (base + c >= N) ? mulmod_d(u, ra.an_inv) : u;
+      ap[c] = ((base + c >= N) ? mulmod_d(u, ra.an_inv) : u) << 1;
     }
     P = mulmod_d(P, ra.g);
     uint32_t own = 0;  // bit c: car c is stored by this tile
@@ -120,12 +121,18 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
         const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          const uint32_t s = mulmod_d(ap[c], Es);
+          // Balanced between the FMA and ALU pipes: draw via mulmod_x2
+          // (2 IMAD + 2 ALU), headway via IMAD, deceleration flag as the
+          // sign of s - tp from IMAD.HI.
+          const uint32_t s = mulmod_x2(ap[c], Es);
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t vc = min(min(v[c] + 1, vmax), xl - x[c] - 1);
-          if (s < tp) vc = static_cast<uint32_t>(max(static_cast<int>(vc) - 1, 0));
-          v[c] = vc;
-          x[c] += vc;
+          uint32_t d;
+          asm("mad.lo.u32 %0, %1, 0xffffffff, %2;" : "=r"(d) : "r"(x[c]), "r"(xl));
+          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+          int dec;
+          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+          v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+          x[c] += v[c];
         }
         if (own_all) {
           s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
@@ -142,7 +149,7 @@ __global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const 
         for (int c = 0; c < CPT; ++c) {
           uint32_t id = base + c;
           if (id >= N) id -= N;
-          const uint32_t s = mulmod_d(ap[c], id < bound ? E : E2);
+          const uint32_t s = mulmod_x2(ap[c], id < bound ? E : E2);
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
           uint32_t cr = 0;
           v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);

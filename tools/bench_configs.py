@@ -1,0 +1,179 @@
+"""Throughput on every BASELINE.json configuration (1 GPU), next to the
+reference's own OpenMP Engine on a bounded sample of the same workload.
+
+  python tools/bench_configs.py [--only C1,C4] [--out profiles/r01_configs.json]
+
+C1  L=1e3,  N=200,   p=0.13, 1000 steps, 200 uniform sites from seed 42, v=0
+C2  L=1e6,  N=2e5,   p=0.25, 1e4 steps, v uniform in [0,5]
+C3  L=1e9,  N=2e8,   p=0.13, 1000 steps (bench.py's headline workload)
+C4  4096 rings L=1e5, N_j = 5000 + floor(45000 j/63), p in {0,..,0.7}, 8 seeds,
+    5000 steps; time-averaged flux per ring
+C5  L=1e8,  N=6e7,   p=0.5, 2e4 steps, full snapshot every 1000 steps
+
+GPU times are CUDA-event times on the engine stream with the state resident
+(snapshots included for C5); checksum off.  Every run also checks a
+size-independent invariant (sorted positions, exact velocity-sum identity).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import torch  # noqa: E402
+
+from paper_2309_14311_b200 import nasch  # noqa: E402
+
+
+def ev_time(stream, fn):
+    s = torch.cuda.ExternalStream(stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(s)
+    fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3
+
+
+def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None, cores=1):
+    x, v = nasch.fill_uniform_state(L, N, vinit, seed)
+    prm = nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T + 8, seed=seed)
+    e = nasch.Engine(prm)
+    e.set_checksum(False)
+    e.set_state(x, v)
+    e.advance(8)  # warm-up
+    snaps = []
+    if snapshot_every:
+        sx = np.empty(N, np.uint64)
+        sv = np.empty(N, np.uint64)
+
+        def body():
+            done = 0
+            while done < T:
+                k = min(snapshot_every, T - done)
+                e.advance(k)
+                e.snapshot(out_x=sx, out_v=sv)
+                snaps.append(int(sx[-1]))
+                done += k
+    else:
+        def body():
+            e.enqueue(T)
+            e.synchronize()
+    secs = ev_time(e.cuda_stream, body)
+    xs, vs = e.snapshot()
+    s = e.sumv_series()
+    ok = bool((np.diff(xs.astype(np.int64)) > 0).all() and int(vs.sum()) == int(s[-1]))
+    out = {"config": name, "L": L, "N": N, "p": p, "steps": T, "gpu_seconds": secs,
+           "gpu_car_updates_per_s": N * T / secs, "steps_per_launch": e.steps_per_launch,
+           "mean_velocity_last": float(s[-1]) / N, "invariants_ok": ok,
+           "snapshots": len(snaps)}
+    e.close()
+    if ref is not None and cpu_steps:
+        r = ref.run(L, N, 5, p, seed, cpu_steps, workers=cores, x0=x.astype(np.uint64),
+                    v0=v.astype(np.uint64), per_step=False, want_state=False)
+        out["cpu_reference"] = {"steps": cpu_steps, "workers": cores, "seconds": r["seconds"],
+                                "car_updates_per_s": N * cpu_steps / r["seconds"]}
+        out["speedup_vs_cpu_reference"] = out["gpu_car_updates_per_s"] / out["cpu_reference"]["car_updates_per_s"]
+    return out
+
+
+def c4(ref=None, cores=1, T=5000):
+    L = 10**5
+    dens = [5000 + (45000 * j) // 63 for j in range(64)]
+    ps = [0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7]
+    specs = []
+    for rep in range(8):
+        for pi, p in enumerate(ps):
+            for j, N in enumerate(dens):
+                specs.append((N, p, 1 + rep * 1000 + pi * 100 + j))
+    params = [nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T, seed=sd) for N, p, sd in specs]
+    t0 = time.time()
+    ens = nasch.Ensemble(params)
+    inits = []
+    for r, (N, p, sd) in enumerate(specs):
+        x, v = nasch.fill_uniform_state(L, N, 0, sd)
+        ens.set_state(r, x, v)
+        if r < 64:
+            inits.append((x, v))
+    setup = time.time() - t0
+    secs = ev_time(ens.cuda_stream, lambda: (ens.enqueue(T), ens.synchronize()))
+    tot = ens.sumv_totals().astype(np.float64)
+    flux = tot / (T * L)
+    cars = sum(N for N, _, _ in specs)
+    out = {"config": "C4", "rings": len(specs), "L": L, "total_cars": cars, "steps": T,
+           "gpu_seconds": secs, "gpu_car_updates_per_s": cars * T / secs, "setup_seconds": setup,
+           "flux_min": float(flux.min()), "flux_max": float(flux.max()),
+           "flux_p0_density_sweep": [float(f) for f in flux[:64:8]]}
+    if ref is not None:
+        # one slice: the 64 densities at p = 0.0, replica 0, 100 steps each,
+        # rings run one after another with all workers each
+        ts = 100
+        secs_ref = 0.0
+        for j in range(64):
+            N, p, sd = specs[j]
+            x, v = inits[j]
+            r = ref.run(L, N, 5, p, sd, ts, workers=cores, x0=x.astype(np.uint64),
+                        v0=v.astype(np.uint64), per_step=False, want_state=False)
+            secs_ref += r["seconds"]
+        slice_cars = sum(specs[j][0] for j in range(64))
+        out["cpu_reference"] = {"sample": "64 densities at p=0.0, replica 0, 100 steps each",
+                                "workers": cores, "seconds": secs_ref,
+                                "car_updates_per_s": slice_cars * ts / secs_ref}
+        out["speedup_vs_cpu_reference"] = out["gpu_car_updates_per_s"] / out["cpu_reference"]["car_updates_per_s"]
+    # parity spot check: ring 0 against the oracle port on a 200-step prefix
+    import oracle
+    port = oracle.Port()
+    N0, p0, sd0 = specs[0]
+    e1 = nasch.Ensemble([nasch.SimParams(length=L, ncars=N0, vmax=5, p=p0, steps=200, seed=sd0)])
+    e1.set_state(0, *inits[0])
+    e1.advance(200)
+    o = port.run(L, 5, p0, sd0, 200, inits[0][0].astype(np.uint64), inits[0][1].astype(np.uint64),
+                 want_checksum=False)
+    xs, vs = e1.snapshot(0)
+    out["parity_ring0_200_steps"] = bool((xs == o["x"]).all() and (vs == o["v"]).all()
+                                         and int(e1.sumv_totals()[0]) == int(o["sumv"].sum()))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.json"))
+    ap.add_argument("--no-cpu", action="store_true")
+    a = ap.parse_args()
+    torch.cuda.set_device(0)
+    ref = None
+    cores = 1
+    if not a.no_cpu:
+        import oracle
+        ref = oracle.Ref()
+        cores = ref.physical_cores() or 1
+    want = a.only.split(",")
+    res = []
+    if "C1" in want:
+        res.append(ring("C1", 1000, 200, 0.13, 1000, 42, 0, cpu_steps=1000, ref=ref, cores=1))
+    if "C2" in want:
+        res.append(ring("C2", 10**6, 2 * 10**5, 0.25, 10**4, 2, 5, cpu_steps=500, ref=ref, cores=cores))
+    if "C3" in want:
+        res.append(ring("C3", 10**9, 2 * 10**8, 0.13, 1000, 3, 0, cpu_steps=4, ref=ref, cores=cores))
+    if "C4" in want:
+        res.append(c4(ref, cores))
+    if "C5" in want:
+        res.append(ring("C5", 10**8, 6 * 10**7, 0.5, 20000, 5, 0, snapshot_every=1000,
+                        cpu_steps=10, ref=ref, cores=cores))
+    doc = {"gpu": torch.cuda.get_device_name(0), "cpu_physical_cores": cores, "results": res}
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(doc, f, indent=1)
+    print(json.dumps(doc, indent=1))
+
+
+if __name__ == "__main__":
+    main()
