@@ -22,6 +22,7 @@
 #include "minstd.hpp"
 #include "step_kernels.cuh"
 #include "tb_kernel.cuh"
+#include "resident_kernel.cuh"
 
 namespace nb200 {
 
@@ -44,6 +45,9 @@ constexpr int kHalo = 16;
 constexpr uint32_t kLoadTB = kTPB * kCPTB;       // 2048 cars loaded per tile
 constexpr uint32_t kStoreTB = kLoadTB - kHalo;   // 2032 cars owned per tile
 constexpr int kGraphLaunches = 16;
+// resident small-ring kernel
+constexpr int kResidentTPB = 1024;
+constexpr uint32_t kResidentChunk = kRecCap / 4;  // steps per resident launch
 
 // Runs f(lo, hi) over [0, n) in parallel host chunks (input validation and
 // u64 <-> u32 conversion at the ABI; large rings only).
@@ -91,6 +95,7 @@ struct GpuRing::Impl {
   uint32_t n = 0, L = 0, vmax_eff = 0, npad = 0;
   int vbytes = 1;   // 1 => u8 velocities, 4 => u32
   bool tb = false;  // temporal-blocked mode
+  bool resident = false;  // small ring: one CTA runs whole chunks of steps
   uint32_t K = 1;   // steps per TB launch
   uint32_t* x[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -128,10 +133,17 @@ struct GpuRing::Impl {
     nasch_tb_kernel<VT, kTPB, kCPTB, kHalo><<<grid, kTPB, 0, stream>>>(args, k);
   }
 
-  // One launch advancing k steps (k == 1 in single-step mode).
+  // One launch advancing k steps (k == 1 in single-step mode; any k in
+  // resident mode).
   void launch(uint32_t k) {
     if (tb) {
       if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
+    } else if (resident) {
+      if (vbytes == 1) {
+        ring_resident_kernel<uint8_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
+      } else {
+        ring_resident_kernel<uint32_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
+      }
     } else {
       if (vbytes == 1) {
         nasch_step_kernel<uint8_t, kTPB, kCPT1><<<grid, kTPB, 0, stream>>>(args);
@@ -142,7 +154,7 @@ struct GpuRing::Impl {
     ++launches;
   }
 
-  uint32_t steps_per_launch() const { return tb ? K : 1u; }
+  uint32_t steps_per_launch() const { return tb ? K : resident ? kResidentChunk : 1u; }
 
   void build_graph() {
     cudaGraph_t g;
@@ -275,6 +287,17 @@ struct GpuRing::Impl {
   // launch's last block zeroes the slots of the next plan).
   void enqueue_steps(uint64_t count) {
     const uint64_t per = steps_per_launch();
+    if (resident) {  // whole chunks in one launch; no graph needed
+      while (count > 0) {
+        const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(count, per));
+        if (steps_done - drained + k > kRecCap / 2) drain();
+        launch(k);
+        CK(cudaGetLastError());
+        steps_done += k;
+        count -= k;
+      }
+      return;
+    }
     const uint64_t chunk = per * kGraphLaunches;
     while (count > 0) {
       if (steps_done - drained + std::min(count, chunk) > kRecCap / 2) drain();
@@ -410,6 +433,9 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   K = std::min<uint32_t>(K, kTPB / (d.vmax_eff + 1));
   d.tb = K >= 2 && d.n >= 2 * kLoadTB && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
   d.K = d.tb ? K : 1;
+  // Small rings run whole chunks of steps in one shared-memory-resident CTA
+  // (NASCH_B200_RESIDENT=0 forces the one-step-per-launch kernel instead).
+  d.resident = !d.tb && d.n <= kResidentMaxCars && env_long("NASCH_B200_RESIDENT", 1) != 0;
   const uint32_t tile = d.tb ? kStoreTB : kTile1;
   const uint32_t cpt = d.tb ? kCPTB : kCPT1;
   const uint32_t ntiles = (d.n + tile - 1) / tile;

@@ -131,6 +131,37 @@ class ShardedRing : public RingEngine {
   std::unique_ptr<Impl> impl_;
 };
 
+// The reference's cell-array engine (NASCH_ENGINE_GRID_REFERENCE,
+// src/model.cpp:77-129, src/engine.cpp:186-196) on the GPU (grid.cu).
+class GpuGrid : public RingEngine {
+ public:
+  explicit GpuGrid(const SimParams& params);
+  ~GpuGrid() override;
+
+  void set_state(const uint64_t* x, const uint64_t* v, size_t n) override;
+  void set_state32(const uint32_t* x, const uint32_t* v, size_t n) override;
+  void advance(uint64_t steps) override;
+  void enqueue(uint64_t steps) override;
+  void synchronize() override;
+  uint64_t steps_done() const override;
+  uint64_t checksum() const override;
+  const std::vector<Frame>& frames() const override;
+  const SimParams& params() const override;
+  void observables(double* density, double* mean_velocity, double* flow) override;
+  void state(uint64_t* positions, uint64_t* velocities) override;
+  size_t sumv_series(uint64_t* out, size_t cap) override;
+  size_t wrap_series(uint64_t* out, size_t cap) override;
+  void set_checksum(bool enabled) override;
+  void* cuda_stream() const override;
+  uint64_t kernel_launches() const override;
+  int steps_per_launch() const override;
+  void shard_range(uint64_t* first, uint64_t* count) const override;
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> impl_;
+};
+
 // NCCL unique id (128 bytes) for ShardedRing's distributed constructor;
 // rank 0 creates it and the launcher broadcasts it.
 void nccl_unique_id(void* out128);

@@ -1,0 +1,412 @@
+// grid.cu -- GpuGrid: the reference's cell-array engine on the GPU
+// (NASCH_ENGINE_GRID_REFERENCE; src/model.cpp:77-129, src/engine.cpp:186-196).
+//
+// The reference keeps it as a serial equivalence oracle: cells[x] = velocity
+// of the occupant or -1; each step scans the occupied cells in ascending
+// order (= rank order, so draw #(t*N + rank + 1)), brakes to the distance to
+// the next occupied cell, and scatters every car to (x + v) mod L.
+// Here one step is four launches over L one-byte cells (0xff = empty):
+//   count   occupied cells per 4096-cell block
+//   scan    exclusive prefix over the block counts (rank of a block's first car)
+//   clear   the next cell array
+//   move    per occupied cell: in-block rank by warp ballots, gap by looking
+//           ahead at most min(vmax, L-1) cells, the counter-based draw, and
+//           the scatter; exact per-step velocity sum and wrap count.
+// Bit-identical to the agent engines (tests/test_gpu_grid.py).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "minstd.hpp"
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+namespace {
+
+void check_g(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+  }
+}
+#define CKG(call) check_g((call), #call)
+
+constexpr uint32_t kCellsPerBlock = 4096;
+constexpr int kGridTPB = 256;  // 16 cells per thread
+constexpr uint8_t kEmpty = 0xff;
+
+inline uint64_t fnv_u32g(uint64_t h, uint32_t value) {
+  constexpr uint64_t p4 = kFnvPrime * kFnvPrime * kFnvPrime * kFnvPrime;
+  h = (h ^ (value & 0xffu)) * kFnvPrime;
+  h = (h ^ ((value >> 8) & 0xffu)) * kFnvPrime;
+  h = (h ^ ((value >> 16) & 0xffu)) * kFnvPrime;
+  h = (h ^ (value >> 24)) * kFnvPrime;
+  return h * p4;
+}
+
+__global__ void grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L, uint32_t* counts) {
+  const uint32_t b = blockIdx.x;
+  const uint32_t lo = b * kCellsPerBlock;
+  uint32_t c = 0;
+  for (uint32_t i = lo + threadIdx.x; i < min(L, lo + kCellsPerBlock); i += blockDim.x)
+    c += cells[i] != kEmpty;
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ uint32_t s[kGridTPB / 32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x / 32] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kGridTPB / 32; ++w) t += s[w];
+    counts[b] = t;
+  }
+}
+
+// Single-block exclusive scan of nb block counts.
+__global__ void grid_scan_kernel(const uint32_t* counts, uint32_t nb, uint32_t* prefix) {
+  __shared__ uint32_t s_tot[1024];
+  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = threadIdx.x * per, hi = min(nb, lo + per);
+  uint32_t sum = 0;
+  for (uint32_t i = lo; i < hi; ++i) sum += counts[i];
+  s_tot[threadIdx.x] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (uint32_t t = 0; t < blockDim.x; ++t) {
+      const uint32_t v = s_tot[t];
+      s_tot[t] = run;
+      run += v;
+    }
+  }
+  __syncthreads();
+  uint32_t run = s_tot[threadIdx.x];
+  for (uint32_t i = lo; i < hi; ++i) {
+    prefix[i] = run;
+    run += counts[i];
+  }
+}
+
+struct GridArgs {
+  uint32_t L, N, vmax, tp, s0;
+  unsigned long long t;
+};
+
+// One thread per 16 consecutive cells of the block.
+__global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __restrict__ cells,
+                                                             uint8_t* __restrict__ next,
+                                                             const uint32_t* __restrict__ prefix,
+                                                             GridArgs g, StepRec* rec) {
+  constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
+  const uint32_t lo = blockIdx.x * kCellsPerBlock + threadIdx.x * CPT;
+  uint8_t c[CPT];
+  uint32_t occ = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < CPT; ++k) {
+    c[k] = (lo + k < g.L) ? cells[lo + k] : kEmpty;
+    occ += c[k] != kEmpty;
+  }
+  // in-block exclusive rank of this thread's first car
+  uint32_t incl = occ;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += n;
+  }
+  __shared__ uint32_t s_w[kGridTPB / 32];
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint32_t wbase = 0;
+  for (uint32_t w = 0; w < warp; ++w) wbase += s_w[w];
+  uint32_t rank = prefix[blockIdx.x] + wbase + incl - occ;
+  const uint32_t look = min(g.vmax, g.L - 1);
+  uint32_t sum = 0, wraps = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < CPT; ++k) {
+    if (c[k] == kEmpty) continue;
+    const uint32_t x = lo + k;
+    // distance to the next occupied cell, only needed below vmax
+    uint32_t gap = look;
+    for (uint32_t d = 1; d <= look; ++d) {
+      uint32_t y = x + d;
+      if (y >= g.L) y -= g.L;
+      const uint8_t cy = (k + d < CPT && x + d < g.L) ? c[k + d] : cells[y];
+      if (cy != kEmpty) {
+        gap = d - 1;
+        break;
+      }
+    }
+    uint32_t v = min(min(static_cast<uint32_t>(c[k]) + 1, g.vmax), gap);
+    const uint32_t s = mulmod(g.s0, powmod(kA, draw_exponent(g.t, g.N, rank)));
+    if (s < g.tp && v > 0) --v;
+    uint32_t nx = x + v;
+    if (nx >= g.L) {
+      nx -= g.L;
+      ++wraps;
+    }
+    next[nx] = static_cast<uint8_t>(v);
+    sum += v;
+    ++rank;
+  }
+  sum = __reduce_add_sync(0xffffffffu, sum);
+  wraps = __reduce_add_sync(0xffffffffu, wraps);
+  if (lane == 0) {
+    StepRec* r = rec + (g.t % kRecCap);
+    if (sum) atomicAdd(&r->sumv, static_cast<unsigned long long>(sum));
+    if (wraps) atomicAdd(&r->c, wraps);
+  }
+}
+
+__global__ void grid_compact_kernel(const uint8_t* __restrict__ cells, uint32_t L,
+                                    const uint32_t* __restrict__ prefix, uint32_t* xs, uint8_t* vs) {
+  constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
+  const uint32_t lo = blockIdx.x * kCellsPerBlock + threadIdx.x * CPT;
+  uint32_t occ = 0;
+  for (uint32_t k = 0; k < CPT; ++k) occ += (lo + k < L) && cells[lo + k] != kEmpty;
+  uint32_t incl = occ;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += n;
+  }
+  __shared__ uint32_t s_w[kGridTPB / 32];
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint32_t r = prefix[blockIdx.x] + incl - occ;
+  for (uint32_t w = 0; w < warp; ++w) r += s_w[w];
+  for (uint32_t k = 0; k < CPT; ++k) {
+    if (lo + k < L && cells[lo + k] != kEmpty) {
+      xs[r] = lo + k;
+      vs[r] = cells[lo + k];
+      ++r;
+    }
+  }
+}
+
+__global__ void grid_init_kernel(uint8_t* cells, uint32_t L, uint32_t N) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < N; i += (uint64_t)gridDim.x * blockDim.x)
+    cells[i * L / N] = 0;  // model.cpp:30-40 then agent_to_grid, model.cpp:77-85
+}
+
+}  // namespace
+
+struct GpuGrid::Impl {
+  SimParams params;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t L = 0, N = 0, vmax = 0, nb = 0;
+  uint8_t* cells[2] = {nullptr, nullptr};
+  int cur = 0;
+  uint32_t *counts = nullptr, *prefix = nullptr, *xs = nullptr;
+  uint8_t* vs = nullptr;
+  StepRec* rec = nullptr;
+  StepRec* hrec = nullptr;
+  uint32_t* hx = nullptr;
+  uint8_t* hv = nullptr;
+  uint64_t steps_done = 0, hash = kFnvBasis, launches = 0, sumv0 = 0;
+  bool checksum_on = true;
+  std::vector<uint64_t> sumv_host, wraps_host;
+  std::vector<Frame> frames;
+
+  void step() {
+    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), seeded(params.seed), steps_done};
+    CKG(cudaMemsetAsync(rec + (steps_done % kRecCap), 0, sizeof(StepRec), stream));
+    grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
+    CKG(cudaMemsetAsync(cells[cur ^ 1], kEmpty, L, stream));
+    grid_move_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], prefix, g, rec);
+    CKG(cudaGetLastError());
+    launches += 3;
+    cur ^= 1;
+    ++steps_done;
+    CKG(cudaMemcpyAsync(hrec, rec + ((steps_done - 1) % kRecCap), sizeof(StepRec), cudaMemcpyDeviceToHost, stream));
+    CKG(cudaStreamSynchronize(stream));
+    sumv_host.push_back(hrec->sumv);
+    wraps_host.push_back(hrec->c);
+  }
+
+  // grid_to_agent (model.cpp:87-97): occupied cells in ascending order.
+  void fetch() {
+    grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
+    grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, prefix, xs, vs);
+    CKG(cudaGetLastError());
+    launches += 3;
+    CKG(cudaMemcpyAsync(hx, xs, size_t(N) * 4, cudaMemcpyDeviceToHost, stream));
+    CKG(cudaMemcpyAsync(hv, vs, N, cudaMemcpyDeviceToHost, stream));
+    CKG(cudaStreamSynchronize(stream));
+  }
+
+  bool frame_due() const {
+    return params.output_mode != OutputMode::none && steps_done < params.steps &&
+           steps_done % params.output_stride == 0;
+  }
+
+  void record_frame() {
+    Frame f;
+    f.step = steps_done;
+    f.positions.assign(hx, hx + N);
+    f.velocities.assign(hv, hv + N);
+    frames.push_back(std::move(f));
+  }
+};
+
+GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
+  Impl& d = *impl_;
+  p.validate();
+  d.params = p;
+  if (p.road_length > 0xffffffffull - kCellsPerBlock)
+    throw std::invalid_argument("length too large for the grid engine");
+  if (std::min<uint64_t>(p.v_max, p.road_length - 1) > 254)
+    throw std::invalid_argument("the grid engine stores velocities in one byte (vmax <= 254)");
+  int ndev = 0;
+  const cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    throw std::runtime_error(std::string("no CUDA device available for the B200 engine (") +
+                             cudaGetErrorString(e) + ")");
+  CKG(cudaGetDevice(&d.device));
+  d.L = static_cast<uint32_t>(p.road_length);
+  d.N = static_cast<uint32_t>(p.car_count);
+  d.vmax = static_cast<uint32_t>(std::min<uint64_t>(p.v_max, p.road_length - 1));
+  d.nb = (d.L + kCellsPerBlock - 1) / kCellsPerBlock;
+  CKG(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) CKG(cudaMalloc(&d.cells[b], d.L));
+  CKG(cudaMalloc(&d.counts, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.prefix, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.xs, size_t(d.N) * 4));
+  CKG(cudaMalloc(&d.vs, d.N));
+  CKG(cudaMalloc(&d.rec, sizeof(StepRec) * kRecCap));
+  CKG(cudaMallocHost(&d.hrec, sizeof(StepRec)));
+  CKG(cudaMallocHost(&d.hx, size_t(d.N) * 4));
+  CKG(cudaMallocHost(&d.hv, d.N));
+  CKG(cudaMemsetAsync(d.cells[0], kEmpty, d.L, d.stream));
+  grid_init_kernel<<<std::max(1u, std::min(4096u, (d.N + 255) / 256)), 256, 0, d.stream>>>(d.cells[0], d.L, d.N);
+  CKG(cudaGetLastError());
+  CKG(cudaStreamSynchronize(d.stream));
+  if (d.frame_due()) {
+    d.fetch();
+    d.record_frame();
+  }
+}
+
+GpuGrid::~GpuGrid() {
+  Impl& d = *impl_;
+  if (d.stream) cudaStreamSynchronize(d.stream);
+  for (int b = 0; b < 2; ++b) cudaFree(d.cells[b]);
+  cudaFree(d.counts);
+  cudaFree(d.prefix);
+  cudaFree(d.xs);
+  cudaFree(d.vs);
+  cudaFree(d.rec);
+  cudaFreeHost(d.hrec);
+  cudaFreeHost(d.hx);
+  cudaFreeHost(d.hv);
+  if (d.stream) cudaStreamDestroy(d.stream);
+}
+
+void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
+  Impl& d = *impl_;
+  if (n != d.N) throw std::invalid_argument("state length must equal ncars");
+  std::vector<uint8_t> cells(d.L, kEmpty);
+  uint64_t s = 0;
+  for (size_t i = 0; i < n; ++i) {
+    if (x[i] >= d.L) throw std::invalid_argument("position out of range [0, length)");
+    if (i && x[i - 1] >= x[i]) throw std::invalid_argument("positions must be strictly increasing");
+    if (v[i] > d.params.v_max) throw std::invalid_argument("velocity above vmax");
+    if (v[i] > 254) throw std::invalid_argument("velocity above 254 (grid engine restriction)");
+    cells[x[i]] = static_cast<uint8_t>(v[i]);
+    s += v[i];
+  }
+  CKG(cudaMemcpy(d.cells[d.cur], cells.data(), d.L, cudaMemcpyHostToDevice));
+  d.sumv0 = s;
+  d.sumv_host.clear();
+  d.wraps_host.clear();
+  if (d.steps_done == 0) {
+    d.frames.clear();
+    if (d.frame_due()) {
+      d.fetch();
+      d.record_frame();
+    }
+  }
+}
+
+void GpuGrid::set_state32(const uint32_t* x, const uint32_t* v, size_t n) {
+  std::vector<uint64_t> x64(x, x + n), v64(v, v + n);
+  set_state(x64.data(), v64.data(), n);
+}
+
+void GpuGrid::advance(uint64_t steps) {
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  const uint64_t count = std::min(steps, d.params.steps - d.steps_done);
+  for (uint64_t k = 0; k < count; ++k) {  // engine.cpp:186-196
+    d.step();
+    const bool frame = d.frame_due();
+    if (d.checksum_on || frame) d.fetch();
+    if (d.checksum_on) {
+      uint64_t h = d.hash;
+      for (uint32_t i = 0; i < d.N; ++i) h = fnv_u32g(h, d.hx[i]);
+      for (uint32_t i = 0; i < d.N; ++i) h = fnv_u32g(h, d.hv[i]);
+      d.hash = h;
+    }
+    if (frame) d.record_frame();
+  }
+}
+
+void GpuGrid::enqueue(uint64_t steps) { advance(steps); }
+void GpuGrid::synchronize() { CKG(cudaStreamSynchronize(impl_->stream)); }
+uint64_t GpuGrid::steps_done() const { return impl_->steps_done; }
+uint64_t GpuGrid::checksum() const { return impl_->hash; }
+const std::vector<Frame>& GpuGrid::frames() const { return impl_->frames; }
+const SimParams& GpuGrid::params() const { return impl_->params; }
+
+void GpuGrid::observables(double* density, double* mean_velocity, double* flow) {
+  const Impl& d = *impl_;
+  const uint64_t total = d.sumv_host.empty() ? d.sumv0 : d.sumv_host.back();
+  const double n = static_cast<double>(d.params.car_count);
+  const double mean = static_cast<double>(total) / n;
+  const double dens = n / static_cast<double>(d.params.road_length);
+  if (density) *density = dens;
+  if (mean_velocity) *mean_velocity = mean;
+  if (flow) *flow = dens * mean;
+}
+
+void GpuGrid::state(uint64_t* positions, uint64_t* velocities) {
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  d.fetch();
+  for (uint32_t i = 0; i < d.N; ++i) {
+    if (positions) positions[i] = d.hx[i];
+    if (velocities) velocities[i] = d.hv[i];
+  }
+}
+
+size_t GpuGrid::sumv_series(uint64_t* out, size_t cap) {
+  const Impl& d = *impl_;
+  const size_t k = std::min(cap, d.sumv_host.size());
+  if (out) std::memcpy(out, d.sumv_host.data(), k * sizeof(uint64_t));
+  return d.sumv_host.size();
+}
+
+size_t GpuGrid::wrap_series(uint64_t* out, size_t cap) {
+  const Impl& d = *impl_;
+  const size_t k = std::min(cap, d.wraps_host.size());
+  if (out) std::memcpy(out, d.wraps_host.data(), k * sizeof(uint64_t));
+  return d.wraps_host.size();
+}
+
+void GpuGrid::set_checksum(bool enabled) { impl_->checksum_on = enabled; }
+void* GpuGrid::cuda_stream() const { return impl_->stream; }
+uint64_t GpuGrid::kernel_launches() const { return impl_->launches; }
+int GpuGrid::steps_per_launch() const { return 1; }
+void GpuGrid::shard_range(uint64_t* first, uint64_t* count) const {
+  if (first) *first = 0;
+  if (count) *count = impl_->N;
+}
+
+}  // namespace nb200

@@ -1,0 +1,108 @@
+// resident_kernel.cuh -- small rings (N <= 4096): the whole ring lives in
+// one CTA's shared memory for all the steps of a launch.
+//
+// Below the temporal-blocking threshold a per-step launch costs far more
+// than the step itself (BASELINE config 1: 200 cars).  One 1024-thread
+// block loads the ring once, runs `steps` steps with two barriers each --
+// exactly the rank/draw bookkeeping of step_kernels.cuh, folded per step by
+// every warp from per-warp crossing counts -- records every step's exact
+// velocity sum, crossing count and rank offset, and writes the ring back
+// in place.
+#pragma once
+#include <cstdint>
+
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+constexpr uint32_t kResidentMaxCars = 4096;
+
+template <typename VT, int TPB>
+__global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra, const uint32_t steps) {
+  __shared__ uint32_t sx[kResidentMaxCars];
+  __shared__ uint32_t sv[kResidentMaxCars];
+  __shared__ uint32_t apw[256];
+  __shared__ uint32_t slot_c[2][TPB / 32], slot_v[2][TPB / 32];
+  Ctl* ctl = ra.ctl;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint64_t t0 = ctl->t;
+  const int b = static_cast<int>(ctl->buf);
+  uint32_t* X = xbuf(ra, b);
+  VT* V = vbuf_w<VT>(ra, b);
+  if (tid < 256) apw[tid] = powmod(kA, tid);
+  for (uint32_t i = tid; i < N; i += TPB) {
+    sx[i] = X[i];
+    sv[i] = static_cast<uint32_t>(V[i]);
+  }
+  uint32_t cpt = (N + TPB - 1) / TPB;
+  cpt |= 1u;  // odd stride: conflict-free banks
+  const uint32_t first = tid * cpt;
+  const uint32_t cnt = first < N ? min(cpt, N - first) : 0u;
+  const uint32_t lead_idx = (first + cnt >= N) ? 0u : first + cnt;
+  const uint32_t ap0 = cnt ? powmod(kA, first) : 1u;
+  uint32_t W = ctl->W, E = ctl->E;
+  __syncthreads();
+  for (uint32_t st = 0; st <= steps; ++st) {
+    if (st > 0) {
+      const uint32_t p = (st - 1) & 1u;
+      const uint32_t c = __reduce_add_sync(0xffffffffu, lane < TPB / 32 ? slot_c[p][lane] : 0u);
+      const uint32_t sum = __reduce_add_sync(0xffffffffu, lane < TPB / 32 ? slot_v[p][lane] : 0u);
+      uint32_t Wn = W + c;
+      const bool wrap = Wn >= N;
+      if (wrap) Wn -= N;
+      if (tid == 0) {
+        StepRec* r = ra.rec + ((t0 + st - 1) % kRecCap);
+        r->sumv = sum;
+        r->c = c;
+        r->W = W;
+      }
+      const uint32_t ac = c < 256 ? apw[c] : powmod(kA, c);
+      E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
+      W = Wn;
+    }
+    if (st == steps) break;
+    const uint32_t E2 = mulmod_d(E, ra.an_inv);
+    const uint32_t bound = N - W;
+    const uint32_t lead = cnt ? sx[lead_idx] : 0u;
+    __syncthreads();
+    uint32_t crs = 0, sum = 0;
+    if (cnt) {
+      uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
+      uint32_t cx = sx[first];
+      for (uint32_t c = 0; c < cnt; ++c) {
+        const uint32_t id = first + c;
+        if (c) s = mulmod_d(s, id == bound ? ra.a1 : kA);
+        const uint32_t nx = (c + 1 < cnt) ? sx[id + 1] : lead;
+        uint32_t xn;
+        const uint32_t vn = car_any(cx, nx, sv[id], s, L, vmax, tp, xn, crs);
+        sx[id] = xn;
+        sv[id] = vn;
+        sum += vn;
+        cx = nx;
+      }
+    }
+    crs = __reduce_add_sync(0xffffffffu, crs);
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    if (lane == 0) {
+      slot_c[st & 1][warp] = crs;
+      slot_v[st & 1][warp] = sum;
+    }
+    __syncthreads();
+  }
+  for (uint32_t i = tid; i < N; i += TPB) {
+    X[i] = sx[i];
+    V[i] = static_cast<VT>(sv[i]);
+  }
+  if (tid == 0) {
+    StepRec* nrec = ra.rec + ((t0 + steps) % kRecCap);
+    nrec->sumv = 0;
+    nrec->c = 0;
+    ctl->t = t0 + steps;
+    ctl->W = W;
+    ctl->E = E;
+    ctl->E2 = mulmod_d(E, ra.an_inv);
+  }
+}
+
+}  // namespace nb200

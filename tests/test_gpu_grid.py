@@ -1,0 +1,63 @@
+"""GPU grid-representation engine (NASCH_ENGINE_GRID_REFERENCE) against the
+reference's golden values and against the agent engine, the way the
+reference pins its serial grid engine (test_capi.cpp:138-155,
+test_engine.cpp:224-236, acceptance.cpp:89-137)."""
+import random
+
+import numpy as np
+import pytest
+
+from paper_2309_14311_b200 import nasch
+
+pytestmark = pytest.mark.gpu
+
+GRID = nasch.Engine.GRID_REFERENCE
+BASE = "length = 50\nncars = 10\nvmax = 3\np = 0.5\nsteps = 20\nseed = 1\n"
+
+
+def test_grid_golden_checksum():
+    p, _ = nasch.SimParams.parse(BASE)
+    g = nasch.Engine(p, 1, GRID)
+    g.run()
+    assert g.checksum == 6917392272001519308
+    x, v = g.snapshot()
+    assert list(x) == [0, 8, 11, 17, 27, 29, 40, 43, 45, 48]
+    assert list(v) == [1, 2, 2, 2, 2, 1, 3, 1, 0, 1]
+    with pytest.raises(nasch.NaschError, match="serial only"):
+        nasch.Engine(p, 2, GRID)
+
+
+def test_grid_equals_agent_random_sweep():  # acceptance.cpp:89-137
+    rd = random.Random(20260823)
+    for trial in range(40):
+        L = 1 + rd.randrange(300)
+        N = 1 + rd.randrange(L)
+        vmax = 1 + rd.randrange(7)
+        p = rd.randrange(10001) / 10000.0
+        T = 1 + rd.randrange(150)
+        seed = rd.getrandbits(64)
+        prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=seed)
+        a = nasch.Engine(prm, 1, nasch.Engine.AGENT)
+        g = nasch.Engine(prm, 1, GRID)
+        a.run()
+        g.run()
+        assert a.checksum == g.checksum, trial  # folds every step's state
+        xa, va = a.snapshot()
+        xg, vg = g.snapshot()
+        assert (xa == xg).all() and (va == vg).all()
+        assert (a.sumv_series() == g.sumv_series()).all()
+        assert a.observables() == g.observables()
+
+
+def test_grid_large_ring_vs_oracle(port):
+    """Many 4096-cell blocks, injected state, crossings at the block seams."""
+    L, N, vmax, p, T = 300001, 60000, 9, 0.3, 60
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 5)
+    o = port.run(L, vmax, p, 9, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    g = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=9), 1, GRID)
+    g.set_checksum(False)
+    g.set_state(x0, v0)
+    g.run()
+    x, v = g.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()

@@ -357,8 +357,8 @@ def test_temporal_blocking_depths(port, k_env, K):
         e.set_checksum(False)
         e.set_state(x0, v0)
         kk = e.steps_per_launch
-        if K == 1:
-            assert kk == 1
+        if K == 1:  # single-step kernel, or the resident kernel for N <= 4096
+            assert kk == 1 or N <= 4096
         e.advance(17)
         e.advance(36)
         x, v = e.snapshot()
@@ -388,3 +388,31 @@ def test_temporal_blocking_long_run_vs_reference(ref, k_env):
     g = gpu_run(L, N, 5, 0.5, 8, 3000, x0, v0, checksum=False)
     assert (g["x"] == r["x"]).all() and (g["v"] == r["v"]).all()
     assert (g["sumv"] == r["sumv"]).all()
+
+
+@pytest.fixture
+def resident_env():
+    old = os.environ.get("NASCH_B200_RESIDENT")
+    yield
+    if old is None:
+        os.environ.pop("NASCH_B200_RESIDENT", None)
+    else:
+        os.environ["NASCH_B200_RESIDENT"] = old
+
+
+@pytest.mark.parametrize("resident", ["0", "1"])
+def test_small_ring_kernels(port, resident_env, resident):
+    """Rings below the temporal-blocking threshold: the one-CTA resident
+    kernel (default) and the one-step-per-launch kernel agree with the
+    oracle, including vmax > 255 (u32 velocity lanes) and long runs."""
+    os.environ["NASCH_B200_RESIDENT"] = resident
+    rng = np.random.default_rng(77)
+    for trial, (L, N, vmax, p, T) in enumerate([(1000, 200, 5, 0.13, 1000), (4096, 4000, 5, 0.3, 300),
+                                                (6000, 900, 300, 0.2, 200), (50, 49, 5, 0.5, 500),
+                                                (3, 1, 5, 0.5, 100)]):
+        x0 = np.sort(rng.choice(L, N, replace=False)).astype(np.uint64)
+        v0 = rng.integers(0, min(vmax, L - 1) + 1, N).astype(np.uint64)
+        o = port.run(L, vmax, p, 31 + trial, T, x0, v0)
+        g = gpu_run(L, N, vmax, p, 31 + trial, T, x0, v0, checksum=False, chunks=[T // 3, T])
+        assert (g["x"] == o["x"]).all() and (g["v"] == o["v"]).all(), trial
+        assert (g["sumv"] == o["sumv"]).all() and (g["wraps"] == o["wraps"]).all()
