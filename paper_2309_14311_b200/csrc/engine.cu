@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -23,6 +24,7 @@
 #include "step_kernels.cuh"
 #include "tb_kernel.cuh"
 #include "resident_kernel.cuh"
+#include "fnv_kernels.cuh"
 
 namespace nb200 {
 
@@ -73,17 +75,6 @@ long env_long(const char* name, long fallback) {
   const char* s = std::getenv(name);
   if (!s || !*s) return fallback;
   return std::strtol(s, nullptr, 10);
-}
-
-// FNV-1a-64 of one value given as 8 little-endian bytes; values < 2^32 take
-// the 4-byte fold plus four zero-byte multiplies (src/engine.hpp:15-36).
-inline uint64_t fnv_u32(uint64_t h, uint32_t value) {
-  constexpr uint64_t p4 = kFnvPrime * kFnvPrime * kFnvPrime * kFnvPrime;
-  h = (h ^ (value & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 8) & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 16) & 0xffu)) * kFnvPrime;
-  h = (h ^ (value >> 24)) * kFnvPrime;
-  return h * p4;
 }
 
 }  // namespace
@@ -253,13 +244,6 @@ struct GpuRing::Impl {
     return vbytes == 1 ? static_cast<const uint8_t*>(hv)[i] : static_cast<const uint32_t*>(hv)[i];
   }
 
-  void hash_staged() {
-    uint64_t h = hash;
-    for (uint32_t i = 0; i < n; ++i) h = fnv_u32(h, hx[i]);
-    for (uint32_t i = 0; i < n; ++i) h = fnv_u32(h, hvel(i));
-    hash = h;
-  }
-
   void record_frame_staged() {
     Frame f;
     f.step = steps_done;
@@ -342,21 +326,78 @@ struct GpuRing::Impl {
       if (sync) drain();
       return;
     }
-    // Checksum and frames need every step's rank-ordered state on the host
-    // (src/engine.cpp:173-181); the reference pays this serially too.
+    // The checksum folds every step's row (src/engine.cpp:173-181): one
+    // step per launch, each followed by the on-device FNV fold
+    // (fnv_kernels.cuh) -- no host round trip unless a frame is due.
     for (uint64_t k = 0; k < count; ++k) {
       launch(1);
       CK(cudaGetLastError());
       ++steps_done;
-      const bool frame = frame_due();
-      if (checksum_on || frame || steps_done - drained > kRecCap / 2) {
+      fnv_fold();
+      if (frame_due()) {
         drain();
-        if (checksum_on || frame) fetch_rank_order();
-        if (checksum_on) hash_staged();
-        if (frame) record_frame_staged();
+        fetch_rank_order();
+        record_frame_staged();
+      } else if (steps_done - drained > kRecCap / 2) {
+        drain();
       }
     }
     if (sync) drain();
+  }
+
+  // ---- on-device trajectory checksum ---------------------------------
+  unsigned long long* fnv_T[2] = {nullptr, nullptr};
+  unsigned long long* fnv_P[2] = {nullptr, nullptr};
+  unsigned long long* fnv_hash = nullptr;
+  uint32_t fnv_chunks = 0;
+  cudaGraphExec_t fnv_graph = nullptr;
+
+  void fnv_enqueue() {
+    const uint32_t nchunks = fnv_chunks;
+    if (vbytes == 1) {
+      fnv_chunk_kernel<uint8_t><<<nchunks, 256, 0, stream>>>(args, fnv_T[0], fnv_P[0]);
+    } else {
+      fnv_chunk_kernel<uint32_t><<<nchunks, 256, 0, stream>>>(args, fnv_T[0], fnv_P[0]);
+    }
+    int in = 0;
+    uint32_t n = nchunks;
+    while (n > 1) {
+      const uint32_t m = (n + 1) / 2;
+      fnv_compose_kernel<<<m, 256, 0, stream>>>(fnv_T[in], fnv_P[in], n, fnv_T[in ^ 1], fnv_P[in ^ 1]);
+      in ^= 1;
+      n = m;
+    }
+    fnv_apply_kernel<<<1, 1, 0, stream>>>(fnv_T[in], fnv_P[in], fnv_hash);
+  }
+
+  // Folds the current state's row into the device digest (one graph launch).
+  void fnv_fold() {
+    if (!fnv_hash) {
+      fnv_chunks = static_cast<uint32_t>((2ull * n + kFnvChunk - 1) / kFnvChunk);
+      for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&fnv_T[b], size_t(fnv_chunks) * 256 * 8));
+        CK(cudaMalloc(&fnv_P[b], size_t(fnv_chunks) * 8));
+      }
+      CK(cudaMalloc(&fnv_hash, 8));
+      const unsigned long long h = hash;
+      CK(cudaMemcpy(fnv_hash, &h, 8, cudaMemcpyHostToDevice));
+      cudaGraph_t g;
+      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      fnv_enqueue();
+      CK(cudaStreamEndCapture(stream, &g));
+      CK(cudaGraphInstantiate(&fnv_graph, g, 0));
+      CK(cudaGraphDestroy(g));
+    }
+    CK(cudaGraphLaunch(fnv_graph, stream));
+    launches += 2 + static_cast<uint64_t>(std::ceil(std::log2(std::max(1u, fnv_chunks))));
+  }
+
+  void pull_hash() {
+    if (!fnv_hash) return;
+    unsigned long long h = 0;
+    CK(cudaMemcpyAsync(&h, fnv_hash, 8, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    hash = h;
   }
 
   // Validates a rank-ordered state (strictly ascending positions < L,
@@ -541,6 +582,12 @@ GpuRing::~GpuRing() {
   cudaFreeHost(d.hv);
   cudaFreeHost(d.hrec);
   cudaFreeHost(d.hctl);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(d.fnv_T[b]);
+    cudaFree(d.fnv_P[b]);
+  }
+  cudaFree(d.fnv_hash);
+  if (d.fnv_graph) cudaGraphExecDestroy(d.fnv_graph);
   if (d.stream) cudaStreamDestroy(d.stream);
 }
 
@@ -574,7 +621,11 @@ void GpuRing::synchronize() {
 }
 
 uint64_t GpuRing::steps_done() const { return impl_->steps_done; }
-uint64_t GpuRing::checksum() const { return impl_->hash; }
+uint64_t GpuRing::checksum() const {
+  CK(cudaSetDevice(impl_->device));
+  impl_->pull_hash();
+  return impl_->hash;
+}
 const std::vector<Frame>& GpuRing::frames() const { return impl_->frames; }
 const SimParams& GpuRing::params() const { return impl_->params; }
 

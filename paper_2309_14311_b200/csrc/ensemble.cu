@@ -112,7 +112,26 @@ __global__ void __launch_bounds__(TPB, 1)
       const uint32_t lead = cnt ? (packed[lead_idx] & xmask) : 0u;
       __syncthreads();
       uint32_t crs = 0, sum = 0;
-      if (cnt) {
+      // Plain run: the rank seam is neither inside it nor at its last car's
+      // leader, and its farthest car cannot reach L this step -- positions
+      // increase along the run, no mod L, one draw base.
+      const bool plain = cnt && !(first < bound && bound <= first + cnt) &&
+                         (packed[first + cnt - 1] & xmask) + vmax < L;
+      if (plain) {
+        uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
+        uint32_t cur = packed[first];
+        for (uint32_t c = 0; c < cnt; ++c) {
+          const uint32_t id = first + c;
+          if (c) s = mulmod_d(s, kA);
+          const uint32_t nxt = (c + 1 < cnt) ? packed[id + 1] : lead;
+          const uint32_t x = cur & xmask;
+          uint32_t vn = min(min((cur >> bx) + 1, vmax), (nxt & xmask) - x - 1);
+          if (s < tp) vn = static_cast<uint32_t>(max(static_cast<int>(vn) - 1, 0));
+          packed[id] = (x + vn) | (vn << bx);
+          sum += vn;
+          cur = nxt;
+        }
+      } else if (cnt) {
         uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
         uint32_t cur = packed[first];
         for (uint32_t c = 0; c < cnt; ++c) {

@@ -67,7 +67,24 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
     const uint32_t lead = cnt ? sx[lead_idx] : 0u;
     __syncthreads();
     uint32_t crs = 0, sum = 0;
-    if (cnt) {
+    // plain run: no rank seam at or inside it, farthest car short of L
+    const bool plain = cnt && !(first < bound && bound <= first + cnt) &&
+                       sx[first + cnt - 1] + vmax < L;
+    if (plain) {
+      uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
+      uint32_t cx = sx[first];
+      for (uint32_t c = 0; c < cnt; ++c) {
+        const uint32_t id = first + c;
+        if (c) s = mulmod_d(s, kA);
+        const uint32_t nx = (c + 1 < cnt) ? sx[id + 1] : lead;
+        uint32_t vn = min(min(sv[id] + 1, vmax), nx - cx - 1);
+        if (s < tp) vn = static_cast<uint32_t>(max(static_cast<int>(vn) - 1, 0));
+        sx[id] = cx + vn;
+        sv[id] = vn;
+        sum += vn;
+        cx = nx;
+      }
+    } else if (cnt) {
       uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
       uint32_t cx = sx[first];
       for (uint32_t c = 0; c < cnt; ++c) {

@@ -390,6 +390,18 @@ def test_temporal_blocking_long_run_vs_reference(ref, k_env):
     assert (g["sumv"] == r["sumv"]).all()
 
 
+def test_device_checksum_many_chunks(port):
+    """The on-device FNV-1a fold (256-state chunk tables composed in a tree)
+    equals the reference's serial byte-at-a-time digest when a step's row
+    spans many 4096-value chunks and an odd chunk count."""
+    for (L, N, T) in [(10**6, 300001, 12), (9000, 2049, 30)]:
+        x0, v0 = nasch.fill_uniform_state(L, N, 5, 6)
+        o = port.run(L, 5, 0.3, 2, T, x0.astype(np.uint64), v0.astype(np.uint64))
+        g = gpu_run(L, N, 5, 0.3, 2, T, x0, v0, checksum=True)
+        assert g["checksum"] == o["checksum"], (L, N)
+        assert (g["x"] == o["x"]).all()
+
+
 @pytest.fixture
 def resident_env():
     old = os.environ.get("NASCH_B200_RESIDENT")
