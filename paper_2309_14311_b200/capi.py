@@ -111,10 +111,12 @@ def build(verbose: bool = False) -> None:
 
 
 def load(path: str = LIB_PATH):
-    """Load the library once and attach signatures.  Raises if absent."""
+    """Load the library once and attach signatures.  Raises if absent.
+    NASCH_B200_LIB overrides the path (kernel-geometry experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("NASCH_B200_LIB") or path
     if not os.path.exists(path):
         raise ImportError(
             f"{path} is missing: build it with `make -C {CSRC}` "

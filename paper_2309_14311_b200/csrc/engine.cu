@@ -22,6 +22,7 @@
 #include "engine.hpp"
 #include "minstd.hpp"
 #include "step_kernels.cuh"
+#include "tb_config.hpp"
 #include "tb_kernel.cuh"
 #include "resident_kernel.cuh"
 #include "fnv_kernels.cuh"
@@ -41,11 +42,7 @@ constexpr int kTPB = 256;
 // single-step kernel geometry
 constexpr int kCPT1 = 8;
 constexpr uint32_t kTile1 = kTPB * kCPT1;
-// temporal-blocked kernel geometry
-constexpr int kCPTB = 8;
-constexpr int kHalo = 16;
-constexpr uint32_t kLoadTB = kTPB * kCPTB;       // 2048 cars loaded per tile
-constexpr uint32_t kStoreTB = kLoadTB - kHalo;   // 2032 cars owned per tile
+// temporal-blocked kernel geometry: tb_config.hpp
 constexpr int kGraphLaunches = 16;
 // resident small-ring kernel
 constexpr int kResidentTPB = 1024;
@@ -87,6 +84,7 @@ struct GpuRing::Impl {
   int vbytes = 1;   // 1 => u8 velocities, 4 => u32
   bool tb = false;  // temporal-blocked mode
   bool resident = false;  // small ring: one CTA runs whole chunks of steps
+  bool medium = false;    // TB with 512-car tiles (medium rings)
   uint32_t K = 1;   // steps per TB launch
   uint32_t* x[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -121,7 +119,11 @@ struct GpuRing::Impl {
 
   template <typename VT>
   void launch_tb(uint32_t k) {
-    nasch_tb_kernel<VT, kTPB, kCPTB, kHalo><<<grid, kTPB, 0, stream>>>(args, k);
+    if (medium) {
+      nasch_tb_kernel<VT, kTbmTPB, kTbmCPT, kTbHalo><<<grid, kTbmTPB, 0, stream>>>(args, k);
+      return;
+    }
+    nasch_tb_kernel<VT, kTbTPB, kTbCPT, kTbHalo><<<grid, kTbTPB, 0, stream>>>(args, k);
   }
 
   // One launch advancing k steps (k == 1 in single-step mode; any k in
@@ -169,10 +171,13 @@ struct GpuRing::Impl {
     CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
     CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
     if (tb) {
+      // the cone runs on one block of the TB kernel's width (K*(vmax+1) <= TPB)
       if (vbytes == 1) {
-        cone_init_kernel<uint8_t, kTPB><<<1, kTPB, 0, stream>>>(args);
+        if (medium) cone_init_kernel<uint8_t, kTbmTPB><<<1, kTbmTPB, 0, stream>>>(args);
+        else cone_init_kernel<uint8_t, kTbTPB><<<1, kTbTPB, 0, stream>>>(args);
       } else {
-        cone_init_kernel<uint32_t, kTPB><<<1, kTPB, 0, stream>>>(args);
+        if (medium) cone_init_kernel<uint32_t, kTbmTPB><<<1, kTbmTPB, 0, stream>>>(args);
+        else cone_init_kernel<uint32_t, kTbTPB><<<1, kTbTPB, 0, stream>>>(args);
       }
       CK(cudaGetLastError());
     }
@@ -469,18 +474,29 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
 
   // Temporal blocking: K steps per launch when the origin cone fits one
   // block and the ring holds at least two full tiles.
+  int sms = 0, per_sm = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
+  // Medium rings (fewer than ~4 large tiles per SM) use 512-car tiles so
+  // every SM gets work; NASCH_B200_TILE=large|medium forces one.
+  const char* tile_env = std::getenv("NASCH_B200_TILE");
+  const uint32_t large_tiles = (d.n + kTbStore - 1) / kTbStore;
+  d.medium = tile_env ? std::string(tile_env) == "medium" : large_tiles < 4u * uint32_t(sms);
+  const int tb_tpb = d.medium ? kTbmTPB : kTbTPB;
+  const uint32_t tb_load = d.medium ? kTbmLoad : kTbLoad;
   const long kreq = env_long("NASCH_B200_K", kPlanMax);
   uint32_t K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
-  K = std::min<uint32_t>(K, kTPB / (d.vmax_eff + 1));
-  d.tb = K >= 2 && d.n >= 2 * kLoadTB && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
+  K = std::min<uint32_t>(K, tb_tpb / (d.vmax_eff + 1));
+  d.tb = K >= 2 && d.n >= std::max(4096u, 2 * tb_load) && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
   d.K = d.tb ? K : 1;
+  if (!d.tb) d.medium = false;
   // Small rings run whole chunks of steps in one shared-memory-resident CTA
   // (NASCH_B200_RESIDENT=0 forces the one-step-per-launch kernel instead).
   d.resident = !d.tb && d.n <= kResidentMaxCars && env_long("NASCH_B200_RESIDENT", 1) != 0;
-  const uint32_t tile = d.tb ? kStoreTB : kTile1;
-  const uint32_t cpt = d.tb ? kCPTB : kCPT1;
+  const uint32_t tile = d.tb ? (d.medium ? kTbmStore : kTbStore) : kTile1;
+  const uint32_t cpt = d.tb ? (d.medium ? kTbmCPT : kTbCPT) : kCPT1;
+  const int tpb = d.tb ? tb_tpb : kTPB;
   const uint32_t ntiles = (d.n + tile - 1) / tile;
-  d.npad = ntiles * tile + kLoadTB;  // vector loads of the last tile stay in bounds
+  d.npad = ntiles * tile + std::max(kTbLoad, kTile1);  // vector loads of the last tile stay in bounds
 
   CK(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
@@ -496,13 +512,17 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   CK(cudaMallocHost(&d.hctl, sizeof(Ctl)));
 
   // Persistent grid: resident blocks on every SM, never more than tiles.
-  int sms = 0, per_sm = 0;
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
-  if (d.tb) {
+  if (d.tb && d.medium) {
     if (d.vbytes == 1) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTPB, kCPTB, kHalo>, kTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbmTPB, kTbmCPT, kTbHalo>, kTbmTPB, 0));
     } else {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTPB, kCPTB, kHalo>, kTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbmTPB, kTbmCPT, kTbHalo>, kTbmTPB, 0));
+    }
+  } else if (d.tb) {
+    if (d.vbytes == 1) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbTPB, kTbCPT, kTbHalo>, kTbTPB, 0));
+    } else {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbTPB, kTbCPT, kTbHalo>, kTbTPB, 0));
     }
   } else if (d.vbytes == 1) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB, kCPT1>, kTPB, 0));
@@ -516,9 +536,9 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   if (gwant > 0) d.grid = static_cast<int>(std::min<long>(gwant, 1 << 20));
 
   // Geometry-dependent draw multipliers a^(first id of block / thread).
-  std::vector<uint32_t> blk(d.grid), thr(kTPB);
+  std::vector<uint32_t> blk(d.grid), thr(tpb);
   for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * tile);
-  for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, uint64_t(t) * cpt);
+  for (int t = 0; t < tpb; ++t) thr[t] = powmod(kA, uint64_t(t) * cpt);
   CK(cudaMalloc(&d.blkpow, blk.size() * 4));
   CK(cudaMalloc(&d.thrpow, thr.size() * 4));
   CK(cudaMemcpy(d.blkpow, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));

@@ -40,7 +40,8 @@ void check_e(cudaError_t e, const char* what) {
 #define CKE(call) check_e((call), #call)
 
 constexpr int kEnsTPB = 1024;
-constexpr int kEnsHeaderWords = 256 + 64 + 64 + 16;  // a^c table, slots, scalars
+// a^c table, crossing/velocity slots, scalars, lead slots [2][TPB]
+constexpr int kEnsHeaderWords = 256 + 64 + 64 + 16 + 2 * kEnsTPB;
 
 struct RingDesc {
   unsigned long long off;         // first car of the ring in X / V
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(TPB, 1)
   uint32_t* slot_c = sm + 256;      // [2][32] crossing counts per warp
   uint32_t* slot_v = slot_c + 64;   // [2][32] velocity sums per warp
   uint32_t* sc = slot_v + 64;       // scalars
+  uint32_t* leadslot = sc + 16;     // [2][TPB] first position of each thread's run
   uint32_t* packed = sm + kEnsHeaderWords;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   if (tid < 256) apw[tid] = powmod(kA, tid);
@@ -86,16 +88,23 @@ __global__ void __launch_bounds__(TPB, 1)
     cpt |= 1u;  // odd stride: conflict-free banks
     const uint32_t first = tid * cpt;
     const uint32_t cnt = first < N ? min(cpt, N - first) : 0u;
-    const uint32_t lead_idx = (first + cnt >= N) ? 0u : first + cnt;
+    // the car after this run is the first car of the next thread's run
+    const uint32_t next_tid = (first + cnt >= N) ? 0u : tid + 1;
     const uint32_t ap0 = cnt ? powmod(kA, first) : 1u;
     uint32_t W = d.W, E = d.E;
     unsigned long long total = 0;  // meaningful in warp 0 lane 0
     uint32_t last = d.last_sumv;
     __syncthreads();
+    // One barrier per step: each thread publishes its run's first position
+    // (state st) in a slot alternating with the step parity, so the thread
+    // behind reads its leader there and nobody reads a run being updated.
     for (unsigned long long st = 0; st <= todo; ++st) {
+      const uint32_t par = static_cast<uint32_t>(st & 1);
+      if (st < todo && cnt) leadslot[par * TPB + tid] = packed[first] & xmask;
+      __syncthreads();
       if (st > 0) {
         // fold the previous step's crossings into W and E (every warp)
-        const uint32_t p = static_cast<uint32_t>((st - 1) & 1);
+        const uint32_t p = par ^ 1u;
         const uint32_t c = warp_sum(slot_c[p * 32 + lane]);
         const uint32_t sv = warp_sum(slot_v[p * 32 + lane]);
         total += sv;
@@ -109,8 +118,7 @@ __global__ void __launch_bounds__(TPB, 1)
       if (st == todo) break;
       const uint32_t E2 = mulmod_d(E, d.an_inv);
       const uint32_t bound = N - W;
-      const uint32_t lead = cnt ? (packed[lead_idx] & xmask) : 0u;
-      __syncthreads();
+      const uint32_t lead = cnt ? leadslot[par * TPB + next_tid] : 0u;
       uint32_t crs = 0, sum = 0;
       // Plain run: the rank seam is neither inside it nor at its last car's
       // leader, and its farthest car cannot reach L this step -- positions
@@ -120,9 +128,10 @@ __global__ void __launch_bounds__(TPB, 1)
       if (plain) {
         uint32_t s = mulmod_d(ap0, first < bound ? E : E2);
         uint32_t cur = packed[first];
+#pragma unroll 2
         for (uint32_t c = 0; c < cnt; ++c) {
           const uint32_t id = first + c;
-          if (c) s = mulmod_d(s, kA);
+          if (c) s = mulmod_x2(2u * kA, s);
           const uint32_t nxt = (c + 1 < cnt) ? packed[id + 1] : lead;
           const uint32_t x = cur & xmask;
           uint32_t vn = min(min((cur >> bx) + 1, vmax), (nxt & xmask) - x - 1);
@@ -148,10 +157,9 @@ __global__ void __launch_bounds__(TPB, 1)
       crs = warp_sum(crs);
       sum = warp_sum(sum);
       if (lane == 0) {
-        slot_c[(st & 1) * 32 + warp] = crs;
-        slot_v[(st & 1) * 32 + warp] = sum;
+        slot_c[par * 32 + warp] = crs;
+        slot_v[par * 32 + warp] = sum;
       }
-      __syncthreads();
     }
     for (uint32_t i = tid; i < N; i += TPB) {
       const uint32_t w = packed[i];

@@ -23,6 +23,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
   __shared__ uint32_t sv[kResidentMaxCars];
   __shared__ uint32_t apw[256];
   __shared__ uint32_t slot_c[2][TPB / 32], slot_v[2][TPB / 32];
+  __shared__ uint32_t s_lead[2][TPB];
   Ctl* ctl = ra.ctl;
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
@@ -39,13 +40,18 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
   cpt |= 1u;  // odd stride: conflict-free banks
   const uint32_t first = tid * cpt;
   const uint32_t cnt = first < N ? min(cpt, N - first) : 0u;
-  const uint32_t lead_idx = (first + cnt >= N) ? 0u : first + cnt;
+  const uint32_t next_tid = (first + cnt >= N) ? 0u : tid + 1;  // owner of the run's leader
   const uint32_t ap0 = cnt ? powmod(kA, first) : 1u;
   uint32_t W = ctl->W, E = ctl->E;
   __syncthreads();
+  // One barrier per step (see ensemble.cu): runs publish their first
+  // position in a parity-alternating slot read by the thread behind.
   for (uint32_t st = 0; st <= steps; ++st) {
+    const uint32_t par = st & 1u;
+    if (st < steps && cnt) s_lead[par][tid] = sx[first];
+    __syncthreads();
     if (st > 0) {
-      const uint32_t p = (st - 1) & 1u;
+      const uint32_t p = par ^ 1u;
       const uint32_t c = __reduce_add_sync(0xffffffffu, lane < TPB / 32 ? slot_c[p][lane] : 0u);
       const uint32_t sum = __reduce_add_sync(0xffffffffu, lane < TPB / 32 ? slot_v[p][lane] : 0u);
       uint32_t Wn = W + c;
@@ -64,8 +70,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
     if (st == steps) break;
     const uint32_t E2 = mulmod_d(E, ra.an_inv);
     const uint32_t bound = N - W;
-    const uint32_t lead = cnt ? sx[lead_idx] : 0u;
-    __syncthreads();
+    const uint32_t lead = cnt ? s_lead[par][next_tid] : 0u;
     uint32_t crs = 0, sum = 0;
     // plain run: no rank seam at or inside it, farthest car short of L
     const bool plain = cnt && !(first < bound && bound <= first + cnt) &&
@@ -102,10 +107,9 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
     crs = __reduce_add_sync(0xffffffffu, crs);
     sum = __reduce_add_sync(0xffffffffu, sum);
     if (lane == 0) {
-      slot_c[st & 1][warp] = crs;
-      slot_v[st & 1][warp] = sum;
+      slot_c[par][warp] = crs;
+      slot_v[par][warp] = sum;
     }
-    __syncthreads();
   }
   for (uint32_t i = tid; i < N; i += TPB) {
     X[i] = sx[i];

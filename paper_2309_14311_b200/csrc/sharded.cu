@@ -29,6 +29,7 @@
 #include "minstd.hpp"
 #include "shard_kernels.cuh"
 #include "step_kernels.cuh"
+#include "tb_config.hpp"
 #include "tb_kernel.cuh"
 
 namespace nb200 {
@@ -42,11 +43,11 @@ void check_s(cudaError_t e, const char* what) {
 }
 #define CKS(call) check_s((call), #call)
 
-constexpr int kTPB = 256;
-constexpr int kCPT = 8;
-constexpr int kHalo = 16;
-constexpr uint32_t kLoad = kTPB * kCPT;
-constexpr uint32_t kStore = kLoad - kHalo;
+constexpr int kTPB = kTbTPB;
+constexpr int kCPT = kTbCPT;
+constexpr int kHalo = kTbHalo;
+constexpr uint32_t kLoad = kTbLoad;
+constexpr uint32_t kStore = kTbStore;
 
 // NCCL entry points, resolved from libnccl.so.2 at first use (no link-time
 // dependency: the library loads on machines without NCCL).

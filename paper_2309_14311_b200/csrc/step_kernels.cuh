@@ -148,6 +148,25 @@ struct VLanes<uint8_t, 8> {
     *reinterpret_cast<uint2*>(p) = pack(v);
   }
 };
+template <>
+struct VLanes<uint8_t, 16> {
+  static __device__ __forceinline__ void load(const uint8_t* p, uint32_t* v) {
+    const uint4 r = ld_nc_v4(p);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      v[j] = __byte_perm(r.x, 0u, 0x4440u | j);
+      v[4 + j] = __byte_perm(r.y, 0u, 0x4440u | j);
+      v[8 + j] = __byte_perm(r.z, 0u, 0x4440u | j);
+      v[12 + j] = __byte_perm(r.w, 0u, 0x4440u | j);
+    }
+  }
+  static __device__ __forceinline__ uint32_t pack4(const uint32_t* v) {
+    return __byte_perm(__byte_perm(v[0], v[1], 0x0040u), __byte_perm(v[2], v[3], 0x0040u), 0x5410u);
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(pack4(v), pack4(v + 4), pack4(v + 8), pack4(v + 12));
+  }
+};
 template <int CPT>
 struct VLanes<uint32_t, CPT> {
   static __device__ __forceinline__ void load(const uint32_t* p, uint32_t* v) {

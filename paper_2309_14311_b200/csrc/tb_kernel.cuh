@@ -22,11 +22,12 @@
 #include <type_traits>
 
 #include "step_kernels.cuh"
+#include "tb_config.hpp"
 
 namespace nb200 {
 
 template <typename VT, int TPB, int CPT, int HALO>
-__global__ void __launch_bounds__(TPB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
+__global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
   constexpr uint32_t LOAD = TPB * CPT;     // cars loaded per tile
   constexpr uint32_t STORE = LOAD - HALO;  // cars owned (stored) per tile
   constexpr int NW = TPB / 32;

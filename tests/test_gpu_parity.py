@@ -331,20 +331,24 @@ def test_config3_prefix_vs_oracle(port):
 
 @pytest.fixture
 def k_env():
-    old = os.environ.get("NASCH_B200_K")
+    old = {k: os.environ.get(k) for k in ("NASCH_B200_K", "NASCH_B200_TILE")}
     yield
-    if old is None:
-        os.environ.pop("NASCH_B200_K", None)
-    else:
-        os.environ["NASCH_B200_K"] = old
+    for k, v in old.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
 
 
+@pytest.mark.parametrize("tile", ["large", "medium"])
 @pytest.mark.parametrize("K", [1, 2, 3, 8, 16])
-def test_temporal_blocking_depths(port, k_env, K):
+def test_temporal_blocking_depths(port, k_env, K, tile):
     """Rings long enough for the temporal-blocked kernel: every depth K
-    (and the single-step kernel, K=1) is bit-exact with the oracle,
-    including K not dividing the step count and chunked advances."""
+    (and the single-step kernel, K=1) and both tile geometries are
+    bit-exact with the oracle, including K not dividing the step count and
+    chunked advances."""
     os.environ["NASCH_B200_K"] = str(K)
+    os.environ["NASCH_B200_TILE"] = tile
     rng = np.random.default_rng(100 + K)
     cases = [(20000, 4096, 5, 0.13), (5000, 4100, 5, 0.5), (4096, 4096, 5, 0.3),
              (300000, 9000, 20, 0.2), (70000, 12000, 40, 0.35), (1 << 20, 70001, 5, 0.7)]
