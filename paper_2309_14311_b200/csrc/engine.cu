@@ -85,6 +85,7 @@ struct GpuRing::Impl {
   bool tb = false;  // temporal-blocked mode
   bool resident = false;  // small ring: one CTA runs whole chunks of steps
   bool medium = false;    // TB with 512-car tiles (medium rings)
+  ~Impl();
   uint32_t K = 1;   // steps per TB launch
   uint32_t* x[2] = {nullptr, nullptr};
   void* v[2] = {nullptr, nullptr};
@@ -585,31 +586,33 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   d.record_frame_if_due();
 }
 
-GpuRing::~GpuRing() {
-  Impl& d = *impl_;
-  if (d.stream) cudaStreamSynchronize(d.stream);
-  if (d.graph) cudaGraphExecDestroy(d.graph);
+// Resources are released by Impl's destructor, so a constructor that throws
+// half way (e.g. out of device memory) leaks nothing.
+GpuRing::Impl::~Impl() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (graph) cudaGraphExecDestroy(graph);
+  if (fnv_graph) cudaGraphExecDestroy(fnv_graph);
   for (int b = 0; b < 2; ++b) {
-    cudaFree(d.x[b]);
-    cudaFree(d.v[b]);
+    cudaFree(x[b]);
+    cudaFree(v[b]);
+    cudaFree(fnv_T[b]);
+    cudaFree(fnv_P[b]);
   }
-  cudaFree(d.ctl);
-  cudaFree(d.rec);
-  cudaFree(d.dsum);
-  cudaFree(d.blkpow);
-  cudaFree(d.thrpow);
-  cudaFreeHost(d.hx);
-  cudaFreeHost(d.hv);
-  cudaFreeHost(d.hrec);
-  cudaFreeHost(d.hctl);
-  for (int b = 0; b < 2; ++b) {
-    cudaFree(d.fnv_T[b]);
-    cudaFree(d.fnv_P[b]);
-  }
-  cudaFree(d.fnv_hash);
-  if (d.fnv_graph) cudaGraphExecDestroy(d.fnv_graph);
-  if (d.stream) cudaStreamDestroy(d.stream);
+  cudaFree(fnv_hash);
+  cudaFree(ctl);
+  cudaFree(rec);
+  cudaFree(dsum);
+  cudaFree(blkpow);
+  cudaFree(thrpow);
+  cudaFreeHost(hx);
+  cudaFreeHost(hv);
+  cudaFreeHost(hrec);
+  cudaFreeHost(hctl);
+  if (stream) cudaStreamDestroy(stream);
 }
+
+GpuRing::~GpuRing() = default;
 
 void GpuRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   Impl& d = *impl_;

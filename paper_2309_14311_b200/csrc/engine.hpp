@@ -106,6 +106,9 @@ class ShardedRing : public RingEngine {
   // exchanging through NCCL (unique id from nccl_unique_id()).
   ShardedRing(const SimParams& params, unsigned rank, unsigned world, const void* nccl_id);
   ~ShardedRing() override;
+  // Whether the ring is long enough to split into `shards` segments
+  // (>= 64 cars each, temporal blocking eligible).
+  static bool can_shard(const SimParams& params, unsigned shards);
 
   void set_state(const uint64_t* x, const uint64_t* v, size_t n) override;
   void set_state32(const uint32_t* x, const uint32_t* v, size_t n) override;

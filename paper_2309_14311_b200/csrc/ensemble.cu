@@ -215,6 +215,7 @@ struct GpuEnsemble::Impl {
   size_t cap_cars = 0;
   uint64_t launches = 0;
   bool dirty = false;  // device descriptors newer than host mirror
+  ~Impl();
 
   void pull() {
     if (!dirty || desc.empty()) return;
@@ -329,17 +330,20 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
   }
 }
 
-GpuEnsemble::~GpuEnsemble() {
-  Impl& d = *impl_;
-  if (d.stream) cudaStreamSynchronize(d.stream);
-  cudaFree(d.X);
-  cudaFree(d.V);
-  cudaFree(d.d_desc);
-  cudaFree(d.d_order);
-  cudaFree(d.d_counter);
-  cudaFreeHost(d.h_desc);
-  if (d.stream) cudaStreamDestroy(d.stream);
+// Released by Impl's destructor: nothing leaks if construction throws.
+GpuEnsemble::Impl::~Impl() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  cudaFree(X);
+  cudaFree(V);
+  cudaFree(d_desc);
+  cudaFree(d_order);
+  cudaFree(d_counter);
+  cudaFreeHost(h_desc);
+  if (stream) cudaStreamDestroy(stream);
 }
+
+GpuEnsemble::~GpuEnsemble() = default;
 
 size_t GpuEnsemble::size() const { return impl_->params.size(); }
 size_t GpuEnsemble::resident_capacity_cars() const { return impl_->cap_cars; }

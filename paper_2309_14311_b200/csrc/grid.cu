@@ -212,6 +212,7 @@ struct GpuGrid::Impl {
   bool checksum_on = true;
   std::vector<uint64_t> sumv_host, wraps_host;
   std::vector<Frame> frames;
+  ~Impl();
 
   void step() {
     const GridArgs g{L, N, vmax, deceleration_threshold(params.p), seeded(params.seed), steps_done};
@@ -294,20 +295,23 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   }
 }
 
-GpuGrid::~GpuGrid() {
-  Impl& d = *impl_;
-  if (d.stream) cudaStreamSynchronize(d.stream);
-  for (int b = 0; b < 2; ++b) cudaFree(d.cells[b]);
-  cudaFree(d.counts);
-  cudaFree(d.prefix);
-  cudaFree(d.xs);
-  cudaFree(d.vs);
-  cudaFree(d.rec);
-  cudaFreeHost(d.hrec);
-  cudaFreeHost(d.hx);
-  cudaFreeHost(d.hv);
-  if (d.stream) cudaStreamDestroy(d.stream);
+// Released by Impl's destructor: nothing leaks if construction throws.
+GpuGrid::Impl::~Impl() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  for (int b = 0; b < 2; ++b) cudaFree(cells[b]);
+  cudaFree(counts);
+  cudaFree(prefix);
+  cudaFree(xs);
+  cudaFree(vs);
+  cudaFree(rec);
+  cudaFreeHost(hrec);
+  cudaFreeHost(hx);
+  cudaFreeHost(hv);
+  if (stream) cudaStreamDestroy(stream);
 }
+
+GpuGrid::~GpuGrid() = default;
 
 void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   Impl& d = *impl_;

@@ -110,6 +110,22 @@ void par_chunks(size_t n, F&& f) {
 
 }  // namespace
 
+bool ShardedRing::can_shard(const SimParams& p, unsigned shards) {
+  try {
+    p.validate();
+  } catch (...) {
+    return false;
+  }
+  if (shards < 2 || p.road_length > 2147483647ull) return false;
+  const uint64_t vmax_eff = std::min<uint64_t>(p.v_max, p.road_length - 1);
+  const char* ks = std::getenv("NASCH_B200_K");
+  const long kreq = ks && *ks ? std::strtol(ks, nullptr, 10) : kPlanMax;
+  uint64_t K = static_cast<uint64_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
+  K = std::min<uint64_t>(K, kConeMax / (vmax_eff + 1));
+  const uint64_t min_seg = p.car_count / shards;  // floor partition: smallest segment
+  return K >= 2 && p.road_length > K * vmax_eff && p.car_count >= K * (vmax_eff + 1) && min_seg >= 64;
+}
+
 void nccl_unique_id(void* out128) {
   NcclApi& api = NcclApi::get();
   ncclUniqueId id;
@@ -148,6 +164,7 @@ struct ShardedRing::Impl {
   ncclComm_t comm = nullptr;
   std::vector<Shard> sh;  // shards held by this process
   bool exchanged_once = false;
+  ~Impl();
 
   uint64_t steps_done = 0, drained = 0, series_base = 0;
   uint64_t hash = kFnvBasis;
@@ -197,7 +214,8 @@ struct ShardedRing::Impl {
   }
 
   void make_shard(uint32_t g, int device) {
-    Shard s;
+    sh.emplace_back();  // registered first: ~Impl frees whatever gets allocated
+    Shard& s = sh.back();
     s.g = g;
     s.device = device;
     CKS(cudaSetDevice(device));
@@ -262,7 +280,6 @@ struct ShardedRing::Impl {
         shard_init_kernel<uint32_t><<<ib, kTPB, 0, s.stream>>>(s.x[b], static_cast<uint32_t*>(s.v[b]), s.nl, s.npad, s.gofs, n, L);
     }
     CKS(cudaGetLastError());
-    sh.push_back(s);
   }
 
   // ---- the per-launch pipeline ---------------------------------------
@@ -600,8 +617,12 @@ ShardedRing::ShardedRing(const SimParams& params, unsigned rank, unsigned world,
   d.finish_construction();
 }
 
-ShardedRing::~ShardedRing() {
-  Impl& d = *impl_;
+// Released by Impl's destructor (shards are registered before their
+// allocations), so nothing leaks if construction throws.
+ShardedRing::~ShardedRing() = default;
+
+ShardedRing::Impl::~Impl() {
+  Impl& d = *this;
   for (auto& s : d.sh) {
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);

@@ -112,6 +112,13 @@ def test_nccl_distributed_path_single_rank(port):
     assert (e.sumv_series() == o["sumv"]).all()
 
 
-def test_too_small_to_shard():
-    with pytest.raises(nasch.NaschError, match="too small"):
-        nasch.Engine(mk(1000, 100, 5, 0.3, 10, 1), 4, CUDA)
+def test_too_small_to_shard_runs_on_one_gpu(port):
+    """A ring too small to split still runs (on one GPU) with the same
+    trajectory, as the reference accepts any worker count."""
+    e = nasch.Engine(mk(1000, 100, 5, 0.3, 10, 1), 4, CUDA)
+    e.run()
+    x, v = port.init_state(1000, 100)
+    o = port.run(1000, 5, 0.3, 1, 10, x, v)
+    assert e.checksum == o["checksum"]
+    with pytest.raises(nasch.NaschError, match="too small"):  # explicit distributed use
+        nasch.Engine.distributed(mk(1000, 100, 5, 0.3, 10, 1), 0, 4, nasch.nccl_unique_id())
