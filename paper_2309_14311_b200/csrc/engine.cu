@@ -410,27 +410,42 @@ struct GpuRing::Impl {
   // velocities <= vmax -- the invariants of acceptance.cpp:118-123 -- and
   // <= L-1) while narrowing it into the pinned staging buffers, in parallel
   // host chunks, then uploads it.
+  //
+  // Pipelined: 16M-car chunks are converted on all host cores while the
+  // previous chunk is in flight to the device.  The upload goes to the idle
+  // ping-pong buffer, which becomes current only once every chunk
+  // validated, so a rejected state leaves the simulation untouched.
   template <typename T>
   void load_state(const T* hx_in, const T* hv_in) {
+    drain();
     std::atomic<int> err{0};
     const uint64_t vlim = std::min<uint64_t>(params.v_max, vmax_eff);
-    parallel_chunks(n, [&](size_t lo, size_t hi) {
-      int e = 0;
-      for (size_t i = lo; i < hi && !e; ++i) {
-        const uint64_t xi = hx_in[i], vi = hv_in[i];
-        if (xi >= L) e = 1;
-        else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
-        else if (vi > params.v_max) e = 3;
-        else if (vi > vlim) e = 4;
-        hx[i] = static_cast<uint32_t>(xi);
-        if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
-        else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
-      }
-      if (e) {
-        int expected = 0;
-        err.compare_exchange_strong(expected, e);
-      }
-    });
+    const int dst = static_cast<int>(buf_host ^ 1u);
+    constexpr size_t kChunk = size_t(1) << 24;
+    for (size_t c0 = 0; c0 < n && !err.load(); c0 += kChunk) {
+      const size_t c1 = std::min<size_t>(n, c0 + kChunk);
+      parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
+        int e = 0;
+        for (size_t i = c0 + a; i < c0 + b && !e; ++i) {
+          const uint64_t xi = hx_in[i], vi = hv_in[i];
+          if (xi >= L) e = 1;
+          else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
+          else if (vi > params.v_max) e = 3;
+          else if (vi > vlim) e = 4;
+          hx[i] = static_cast<uint32_t>(xi);
+          if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
+          else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
+        }
+        if (e) {
+          int expected = 0;
+          err.compare_exchange_strong(expected, e);
+        }
+      });
+      CK(cudaMemcpyAsync(x[dst] + c0, hx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(static_cast<char*>(v[dst]) + c0 * vbytes, static_cast<char*>(hv) + c0 * vbytes,
+                         (c1 - c0) * vbytes, cudaMemcpyHostToDevice, stream));
+    }
+    CK(cudaStreamSynchronize(stream));
     switch (err.load()) {
       case 1: throw std::invalid_argument("position out of range [0, length)");
       case 2: throw std::invalid_argument("positions must be strictly increasing");
@@ -438,10 +453,7 @@ struct GpuRing::Impl {
       case 4: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
       default: break;
     }
-    drain();
-    const int cur = static_cast<int>(buf_host);
-    CK(cudaMemcpyAsync(x[cur], hx, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
-    CK(cudaMemcpyAsync(v[cur], hv, size_t(n) * vbytes, cudaMemcpyHostToDevice, stream));
+    buf_host ^= 1u;
     reset_ctl();
     compute_sumv0();
     series_base = steps_done;
@@ -669,13 +681,45 @@ void GpuRing::state(uint64_t* positions, uint64_t* velocities) {
   Impl& d = *impl_;
   CK(cudaSetDevice(d.device));
   d.drain();
-  d.fetch_rank_order();
-  parallel_chunks(d.n, [&](size_t lo, size_t hi) {
-    if (positions)
-      for (size_t i = lo; i < hi; ++i) positions[i] = d.hx[i];
+  // Pipelined: rank-order chunks are copied to pinned staging one after the
+  // other and each is widened to u64 on all host cores as soon as its copy
+  // lands, while the next is in flight.
+  constexpr uint32_t kChunk = 1u << 24;
+  const int cur = static_cast<int>(d.buf_host);
+  const uint32_t head = (d.n - d.W_host) % d.n;  // id of the rank-0 car
+  struct Piece { uint32_t r0, r1; cudaEvent_t ev; };
+  std::vector<Piece> pieces;
+  for (uint32_t r0 = 0; r0 < d.n;) {
+    const uint32_t id0 = head + r0 < d.n ? head + r0 : head + r0 - d.n;
+    const uint32_t r1 = std::min<uint32_t>({d.n, r0 + kChunk, r0 + (d.n - id0)});
+    Piece p{r0, r1, nullptr};
+    CK(cudaEventCreateWithFlags(&p.ev, cudaEventDisableTiming));
+    const size_t m = r1 - r0;
+    if (positions) CK(cudaMemcpyAsync(d.hx + r0, d.x[cur] + id0, m * 4, cudaMemcpyDeviceToHost, d.stream));
     if (velocities)
-      for (size_t i = lo; i < hi; ++i) velocities[i] = d.hvel(i);
-  });
+      CK(cudaMemcpyAsync(static_cast<char*>(d.hv) + size_t(r0) * d.vbytes,
+                         static_cast<const char*>(d.v[cur]) + size_t(id0) * d.vbytes, m * d.vbytes,
+                         cudaMemcpyDeviceToHost, d.stream));
+    CK(cudaEventRecord(p.ev, d.stream));
+    pieces.push_back(p);
+    r0 = r1;
+  }
+  cudaError_t err = cudaSuccess;
+  for (const Piece& p : pieces) {
+    if (err == cudaSuccess) err = cudaEventSynchronize(p.ev);
+    if (err == cudaSuccess) {
+      parallel_chunks(p.r1 - p.r0, [&](size_t lo, size_t hi) {
+        lo += p.r0;
+        hi += p.r0;
+        if (positions)
+          for (size_t i = lo; i < hi; ++i) positions[i] = d.hx[i];
+        if (velocities)
+          for (size_t i = lo; i < hi; ++i) velocities[i] = d.hvel(i);
+      });
+    }
+    cudaEventDestroy(p.ev);
+  }
+  CK(err);
 }
 
 size_t GpuRing::sumv_series(uint64_t* out, size_t cap) {
