@@ -299,15 +299,27 @@ __device__ __forceinline__ uint32_t cone_slot_id(uint32_t N, uint32_t W, uint32_
 template <int TPB>
 __device__ void cone_simulate(const RingArgs& ra, uint32_t x, uint32_t v, uint64_t t, uint32_t W,
                               uint32_t kk, Ctl* ctl) {
+  static_assert(TPB >= 64 && TPB <= 256, "cone block: two warps of setup, slots < 256");
   __shared__ uint32_t s_x[TPB];
+  __shared__ uint32_t s_pow[2];
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax;
   const uint32_t M = kk * vmax;
   const uint32_t C = M + kk;
   const uint32_t i = threadIdx.x;
   const bool act = i < C;
+  const uint32_t id0 = cone_slot_id(N, W, M, 0);
   const uint32_t id = cone_slot_id(N, W, M, i);
-  const uint32_t apw = act ? powmod(kA, id) : 1u;
-  uint32_t E = mulmod(ra.s0, powmod(kA, draw_exponent(t, N, W)));
+  // Warp 0: a^id0; warp 1: a^(t*N + 1 + W).  Slot ids run consecutively
+  // from id0 (wrapping past N - 1), so a^id = a^id0 * a^i [* a^-N].
+  if (i < 64) {
+    const uint32_t r = i < 32 ? powmod_warp(id0) : powmod_warp(draw_exponent(t, N, W));
+    if ((i & 31u) == 0) s_pow[i >> 5] = r;
+  }
+  __syncthreads();
+  uint32_t apw = mulmod(s_pow[0], c_pow.lin[i]);
+  if (id < id0) apw = mulmod(apw, ra.an_inv);
+  if (!act) apw = 1u;
+  uint32_t E = mulmod(ra.s0, s_pow[1]);
   uint32_t Wj = W;
   for (uint32_t j = 0; j < kk; ++j) {
     s_x[i] = x;
@@ -329,7 +341,7 @@ __device__ void cone_simulate(const RingArgs& ra, uint32_t x, uint32_t v, uint64
     const bool wrap = Wn >= N;
     if (wrap) Wn -= N;
     // E_{t+j+1} = E_{t+j} * a^(N + W_{j+1} - W_j)
-    const uint32_t ac = powmod(kA, c);
+    const uint32_t ac = c_pow.lin[c];  // c <= M < 256
     E = mulmod(E, wrap ? ac : mulmod(ra.an, ac));
     Wj = Wn;
   }
@@ -478,8 +490,11 @@ __global__ void __launch_bounds__(TPB) nasch_step_kernel(const RingArgs ra) {
     // offset and draw base (the rotation, model.cpp:70-73).
     const uint32_t c = atomicAdd(&rec->c, 0u);
     uint32_t Wn = W + c;  // W < N, c <= N
-    if (Wn >= N) Wn -= N;
-    const uint32_t En = mulmod(ra.s0, powmod(kA, draw_exponent(t + 1, N, Wn)));
+    const bool wrap = Wn >= N;
+    if (wrap) Wn -= N;
+    // exponent t*N + 1 + W grows by N + c (- N when W wraps)
+    const uint32_t ac = c < 256 ? c_pow.lin[c] : powmod(kA, c);
+    const uint32_t En = mulmod(E, wrap ? ac : mulmod(ra.an, ac));
     rec->W = W;
     StepRec* nrec = ra.rec + ((t + 1) % kRecCap);
     nrec->sumv = 0;

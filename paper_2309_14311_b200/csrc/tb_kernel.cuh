@@ -195,18 +195,24 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
   if (!last_block_done(ctl)) return;
 
   // Last block: check the plan, advance the control block, plan the next k.
-  __shared__ uint32_t s_Wnext;
+  // One thread per step (k <= kPlanMax <= TPB), earliest mismatch wins.
+  __shared__ uint32_t s_Wnext, s_bad;
+  if (threadIdx.x == 0) s_bad = ~0u;
+  __syncthreads();
+  if (threadIdx.x < k) {
+    const uint32_t j = threadIdx.x;
+    StepRec* r = ra.rec + ((t + j) % kRecCap);
+    const uint32_t c = __ldcg(&r->c);  // other blocks' atomics live in L2
+    r->W = ctl->Wk[j];
+    r->cplan = ctl->ck[j];
+    // A shard sees only its own crossings; the host checks their sum.
+    if (!ra.sharded && c != ctl->ck[j]) atomicMin(&s_bad, j);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    for (uint32_t j = 0; j < k; ++j) {
-      StepRec* r = ra.rec + ((t + j) % kRecCap);
-      const uint32_t c = atomicAdd(&r->c, 0u);
-      r->W = ctl->Wk[j];
-      r->cplan = ctl->ck[j];
-      // A shard sees only its own crossings; the host checks their sum.
-      if (!ra.sharded && c != ctl->ck[j] && !ctl->err) {
-        ctl->err = 1;
-        ctl->err_step = static_cast<unsigned int>(t + j);
-      }
+    if (s_bad != ~0u && !ctl->err) {
+      ctl->err = 1;
+      ctl->err_step = static_cast<unsigned int>(t + s_bad);
     }
     uint32_t Wn = ctl->Wk[k - 1] + ctl->ck[k - 1];
     if (Wn >= N) Wn -= N;
