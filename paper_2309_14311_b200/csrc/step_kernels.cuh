@@ -89,6 +89,9 @@ struct RingArgs {
   const uint32_t* thrpow;  // a^(threadIdx.x * cars per thread)
   Ctl* ctl;
   StepRec* rec;     // kRecCap ring indexed by t mod kRecCap
+  // -1 as a launch parameter: ptxas cannot fold it, so x * neg1 + xl stays
+  // one IMAD on the FMA pipe instead of an IADD3 on the (busier) ALU pipe.
+  uint32_t neg1 = 0xffffffffu;
 };
 
 // ---- vector access helpers ----------------------------------------------

@@ -122,13 +122,14 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
         const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          // Balanced between the FMA and ALU pipes: draw via mulmod_x2
-          // (2 IMAD + 2 ALU), headway via IMAD, deceleration flag as the
-          // sign of s - tp from IMAD.HI.
+          // Balanced between the FMA and ALU pipes (both issue a warp
+          // instruction every 2 cycles per SMSP): draw via mulmod_x2 (2 IMAD
+          // + 2 ALU), headway x*(-1) + leader as one IMAD (neg1 is a launch
+          // parameter, so ptxas cannot turn it into an ALU IADD3; measured
+          // +10 % on C3), deceleration flag as the sign of s - tp.
           const uint32_t s = mulmod_x2(ap[c], Es);
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t d;
-          asm("mad.lo.u32 %0, %1, 0xffffffff, %2;" : "=r"(d) : "r"(x[c]), "r"(xl));
+          const uint32_t d = x[c] * ra.neg1 + xl;
           const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
           int dec;
           asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
