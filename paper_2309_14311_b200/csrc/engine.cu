@@ -121,10 +121,10 @@ struct GpuRing::Impl {
   template <typename VT>
   void launch_tb(uint32_t k) {
     if (medium) {
-      nasch_tb_kernel<VT, kTbmTPB, kTbmCPT, kTbHalo><<<grid, kTbmTPB, 0, stream>>>(args, k);
+      nasch_tb_kernel<VT, kTbmTPB, kTbmCPT, kTbHalo, false><<<grid, kTbmTPB, 0, stream>>>(args, k);
       return;
     }
-    nasch_tb_kernel<VT, kTbTPB, kTbCPT, kTbHalo><<<grid, kTbTPB, 0, stream>>>(args, k);
+    nasch_tb_kernel<VT, kTbTPB, kTbCPT, kTbHalo, kTbWT><<<grid, kTbTPB, 0, stream>>>(args, k);
   }
 
   // One launch advancing k steps (k == 1 in single-step mode; any k in
@@ -527,15 +527,15 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // Persistent grid: resident blocks on every SM, never more than tiles.
   if (d.tb && d.medium) {
     if (d.vbytes == 1) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbmTPB, kTbmCPT, kTbHalo>, kTbmTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbmTPB, kTbmCPT, kTbHalo, false>, kTbmTPB, 0));
     } else {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbmTPB, kTbmCPT, kTbHalo>, kTbmTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbmTPB, kTbmCPT, kTbHalo, false>, kTbmTPB, 0));
     }
   } else if (d.tb) {
     if (d.vbytes == 1) {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbTPB, kTbCPT, kTbHalo>, kTbTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint8_t, kTbTPB, kTbCPT, kTbHalo, kTbWT>, kTbTPB, 0));
     } else {
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbTPB, kTbCPT, kTbHalo>, kTbTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_tb_kernel<uint32_t, kTbTPB, kTbCPT, kTbHalo, kTbWT>, kTbTPB, 0));
     }
   } else if (d.vbytes == 1) {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint8_t, kTPB, kCPT1>, kTPB, 0));
@@ -551,7 +551,10 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // Geometry-dependent draw multipliers a^(first id of block / thread).
   std::vector<uint32_t> blk(d.grid), thr(tpb);
   for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * tile);
-  for (int t = 0; t < tpb; ++t) thr[t] = powmod(kA, uint64_t(t) * cpt);
+  for (int t = 0; t < tpb; ++t) {
+    const uint32_t ofs = !d.tb ? t * cpt : d.medium ? TbMedium::offset(t) : TbLarge::offset(t);
+    thr[t] = powmod(kA, ofs);
+  }
   CK(cudaMalloc(&d.blkpow, blk.size() * 4));
   CK(cudaMalloc(&d.thrpow, thr.size() * 4));
   CK(cudaMemcpy(d.blkpow, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));

@@ -209,7 +209,7 @@ struct ShardedRing::Impl {
 
   template <typename VT>
   void occupancy(int* per_sm) {
-    CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, nasch_tb_kernel<VT, kTPB, kCPT, kHalo>,
+    CKS(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, nasch_tb_kernel<VT, kTPB, kCPT, kHalo, kTbWT>,
                                                       kTPB, 0));
   }
 
@@ -244,7 +244,7 @@ struct ShardedRing::Impl {
     s.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
     std::vector<uint32_t> blk(s.grid), thr(kTPB);
     for (int b = 0; b < s.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * kStore);
-    for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, uint64_t(t) * kCPT);
+    for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, TbLarge::offset(t));
     CKS(cudaMalloc(&s.blkpow, blk.size() * 4));
     CKS(cudaMalloc(&s.thrpow, thr.size() * 4));
     CKS(cudaMemcpy(s.blkpow, blk.data(), blk.size() * 4, cudaMemcpyHostToDevice));
@@ -339,8 +339,8 @@ struct ShardedRing::Impl {
   void launch(uint32_t k) {
     for (Shard& s : sh) {
       CKS(cudaSetDevice(s.device));
-      if (vbytes == 1) nasch_tb_kernel<uint8_t, kTPB, kCPT, kHalo><<<s.grid, kTPB, 0, s.stream>>>(s.args, k);
-      else nasch_tb_kernel<uint32_t, kTPB, kCPT, kHalo><<<s.grid, kTPB, 0, s.stream>>>(s.args, k);
+      if (vbytes == 1) nasch_tb_kernel<uint8_t, kTPB, kCPT, kHalo, kTbWT><<<s.grid, kTPB, 0, s.stream>>>(s.args, k);
+      else nasch_tb_kernel<uint32_t, kTPB, kCPT, kHalo, kTbWT><<<s.grid, kTPB, 0, s.stream>>>(s.args, k);
       CKS(cudaGetLastError());
       ++launches;
     }

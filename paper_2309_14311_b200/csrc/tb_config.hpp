@@ -3,6 +3,8 @@
 #pragma once
 #include <cstdint>
 
+#include "minstd.hpp"  // NB_HD
+
 namespace nb200 {
 
 // Measured on C3 (tools/variants, round 1): 128 threads x 16 cars with
@@ -18,16 +20,39 @@ namespace nb200 {
 #define NB_TB_MINB 5
 #endif
 
+#ifndef NB_TB_WT
+#define NB_TB_WT 1
+#endif
+
+// Tile geometry.  Block tiles (WT = false): the block's TPB*CPT cars share
+// one 16-car halo and hand leaders across warps through shared memory (one
+// barrier per step).  Warp tiles (WT = true): each warp owns 32*CPT - 16
+// cars with its own halo and never synchronises with the other warps.
+template <int TPB, int CPT, int HALO, bool WT>
+struct TbGeom {
+  static constexpr uint32_t kWarpLoad = WT ? 32u * CPT : uint32_t(TPB) * CPT;  // one halo per ...
+  static constexpr uint32_t kWarpStore = kWarpLoad - HALO;                     // ... this many owned
+  static constexpr uint32_t kStore = WT ? (TPB / 32) * kWarpStore : kWarpStore;  // owned per block tile
+  static constexpr uint32_t kLoad = kStore + HALO;                              // block tile's extent
+  // First car of thread t within its block tile.
+  static constexpr NB_HD uint32_t offset(uint32_t t) {
+    return WT ? (t / 32) * kWarpStore + (t % 32) * CPT : t * CPT;
+  }
+};
+
 constexpr int kTbTPB = NB_TB_TPB;                   // threads per tile
 constexpr int kTbCPT = NB_TB_CPT;                   // consecutive cars per thread
 constexpr int kTbHalo = 16;                         // cars ahead re-read per tile (>= K)
-constexpr uint32_t kTbLoad = kTbTPB * kTbCPT;       // cars loaded per tile
-constexpr uint32_t kTbStore = kTbLoad - kTbHalo;    // cars owned per tile
+constexpr bool kTbWT = NB_TB_WT != 0;
+using TbLarge = TbGeom<kTbTPB, kTbCPT, kTbHalo, kTbWT>;
+constexpr uint32_t kTbLoad = TbLarge::kLoad;        // cars spanned per tile
+constexpr uint32_t kTbStore = TbLarge::kStore;      // cars owned per tile
 
 // Medium rings: narrower tiles so every SM gets work.
 constexpr int kTbmTPB = 128;
 constexpr int kTbmCPT = 4;
-constexpr uint32_t kTbmLoad = kTbmTPB * kTbmCPT;    // 512
-constexpr uint32_t kTbmStore = kTbmLoad - kTbHalo;  // 496
+using TbMedium = TbGeom<kTbmTPB, kTbmCPT, kTbHalo, false>;
+constexpr uint32_t kTbmLoad = TbMedium::kLoad;      // 512
+constexpr uint32_t kTbmStore = TbMedium::kStore;    // 496
 
 }  // namespace nb200

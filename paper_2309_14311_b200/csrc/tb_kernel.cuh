@@ -26,10 +26,12 @@
 
 namespace nb200 {
 
-template <typename VT, int TPB, int CPT, int HALO>
+template <typename VT, int TPB, int CPT, int HALO, bool WT>
 __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
-  constexpr uint32_t LOAD = TPB * CPT;     // cars loaded per tile
-  constexpr uint32_t STORE = LOAD - HALO;  // cars owned (stored) per tile
+  using G = TbGeom<TPB, CPT, HALO, WT>;
+  constexpr uint32_t LOAD = G::kLoad;     // cars spanned per block tile
+  constexpr uint32_t STORE = G::kStore;   // cars owned (stored) per block tile
+  constexpr uint32_t WSTORE = G::kWarpStore;  // owned per halo unit (warp or block)
   constexpr int NW = TPB / 32;
   static_assert(HALO >= kPlanMax && HALO % 16 == 0, "halo must cover the plan");
   using Acc = typename std::conditional<sizeof(VT) == 1, uint32_t, unsigned long long>::type;
@@ -54,7 +56,9 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
   uint32_t* __restrict__ Xo = xbuf(ra, b ^ 1);
   VT* __restrict__ Vo = vbuf_w<VT>(ra, b ^ 1);
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t i0 = threadIdx.x * CPT;  // first car of this thread within the tile
+  const uint32_t i0 = G::offset(threadIdx.x);  // first car of this thread within the tile
+  // index of car 0 within its halo unit (the warp's tile, or the block's)
+  const uint32_t u0 = WT ? lane * CPT : i0;
   const uint32_t reach = k * vmax;        // farthest any car moves in this launch (< L)
 
   // P = a^(global id of this thread's first car in its first tile)
@@ -101,7 +105,7 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
     P = mulmod_d(P, ra.g);
     uint32_t own = 0;  // bit c: car c is stored by this tile
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) own |= (i0 + c < STORE && bl + c < nl) ? (1u << c) : 0u;
+    for (int c = 0; c < CPT; ++c) own |= (u0 + c < WSTORE && bl + c < nl) ? (1u << c) : 0u;
     const bool own_all = own == (1u << CPT) - 1u;
     uint32_t xmax = x[0];
 #pragma unroll
@@ -113,11 +117,19 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
       const uint32_t bound = N - s_W[j];  // id of the rank-0 car (N when W = 0)
       // Slots alternate with the running step count, so one barrier per step
       // suffices (a slot is rewritten only after the next barrier).
-      const uint32_t slot = phase++ & 1u;
-      if (lane == 0) s_lead[slot][warp] = x[0];
-      __syncthreads();
-      uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
-      if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
+      uint32_t xn;
+      if (WT) {
+        xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+        // warp tiles: the front car of the warp's halo has no leader (its
+        // error reaches at most k <= HALO cars back by the launch's end)
+        if (lane == 31) xn = x[CPT - 1];
+      } else {
+        const uint32_t slot = phase++ & 1u;
+        if (lane == 0) s_lead[slot][warp] = x[0];
+        __syncthreads();
+        xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+        if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
+      }
       if (plain && !(base < bound && bound <= base + CPT)) {
         const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
@@ -166,7 +178,7 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
     if (fast) {
       // A shard's last tile may spill past nl into its halo/padding region,
       // which the plan kernel rewrites before the next launch reads it.
-      if (i0 + CPT <= STORE) {
+      if (u0 + CPT <= WSTORE) {
 #pragma unroll
         for (int q = 0; q < CPT / 4; ++q)
           *reinterpret_cast<uint4*>(Xo + bl + 4 * q) =
