@@ -94,19 +94,27 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
         v[c] = V[id];
       }
     }
-    // 2 * a^id for this thread's cars (an id wrapped past N multiplies by
-    // a^-N); doubled for mulmod_x2
-    uint32_t u = P;
+    // 2 * a^id for this thread's cars (doubled for mulmod_x2): a^(first
+    // id) times a^c from the constant table -- independent products, no
+    // dependent chain.  Ids wrapped past N (only in the tile straddling id
+    // N-1) also multiply by a^-N.
+    ap[0] = P << 1;
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if (c) u = mulmod_d(u, kA);
-      ap[c] = ((base + c >= N) ? mulmod_d(u, ra.an_inv) : u) << 1;
+    for (int c = 1; c < CPT; ++c) ap[c] = mulmod_d(P, c_pow.lin[c]) << 1;
+    if (!nowrap) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+        if (base + c >= N) ap[c] = mulmod_d(ap[c] >> 1, ra.an_inv) << 1;
     }
     P = mulmod_d(P, ra.g);
-    uint32_t own = 0;  // bit c: car c is stored by this tile
+    // bit c: car c is stored by this tile (all of them but in the halo and
+    // at a shard's end)
+    const bool own_all = u0 + CPT <= WSTORE && bl + CPT <= nl;
+    uint32_t own = own_all ? (1u << CPT) - 1u : 0u;
+    if (!own_all) {
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) own |= (u0 + c < WSTORE && bl + c < nl) ? (1u << c) : 0u;
-    const bool own_all = own == (1u << CPT) - 1u;
+      for (int c = 0; c < CPT; ++c) own |= (u0 + c < WSTORE && bl + c < nl) ? (1u << c) : 0u;
+    }
     uint32_t xmax = x[0];
 #pragma unroll
     for (int c = 1; c < CPT; ++c) xmax = max(xmax, x[c]);
