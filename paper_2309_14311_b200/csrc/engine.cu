@@ -25,6 +25,7 @@
 #include "tb_config.hpp"
 #include "tb_kernel.cuh"
 #include "resident_kernel.cuh"
+#include "dr_kernel.cuh"
 #include "fnv_kernels.cuh"
 
 namespace nb200 {
@@ -85,6 +86,11 @@ struct GpuRing::Impl {
   bool tb = false;  // temporal-blocked mode
   bool resident = false;  // small ring: one CTA runs whole chunks of steps
   bool medium = false;    // TB with 512-car tiles (medium rings)
+  bool dr = false;        // distributed-resident medium ring (dr_kernel.cuh)
+  uint32_t dr_G = 0, dr_cpt = 0;
+  Ctl* dplans = nullptr;
+  DrSync* dsync = nullptr;
+  uint32_t* dseg = nullptr;
   ~Impl();
   uint32_t K = 1;   // steps per TB launch
   uint32_t* x[2] = {nullptr, nullptr};
@@ -118,6 +124,21 @@ struct GpuRing::Impl {
   StepRec* hrec = nullptr;
   Ctl* hctl = nullptr;
 
+  template <typename VT, int CPT>
+  void launch_dr_cpt(uint32_t k) {
+    DrArgs da{dplans, dsync, dseg, dr_G, K};
+    void* kargs[] = {&args, &da, &k};
+    CK(cudaMemsetAsync(dsync, 0, sizeof(DrSync), stream));
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, kDrTPB, CPT>),
+                                   dim3(dr_G + 1), dim3(kDrTPB), kargs, 0, stream));
+  }
+  template <typename VT>
+  void launch_dr(uint32_t k) {
+    if (dr_cpt == 4) launch_dr_cpt<VT, 4>(k);
+    else if (dr_cpt == 8) launch_dr_cpt<VT, 8>(k);
+    else launch_dr_cpt<VT, 16>(k);
+  }
+
   template <typename VT>
   void launch_tb(uint32_t k) {
     if (medium) {
@@ -130,7 +151,9 @@ struct GpuRing::Impl {
   // One launch advancing k steps (k == 1 in single-step mode; any k in
   // resident mode).
   void launch(uint32_t k) {
-    if (tb) {
+    if (dr) {
+      if (vbytes == 1) launch_dr<uint8_t>(k); else launch_dr<uint32_t>(k);
+    } else if (tb) {
       if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
     } else if (resident) {
       if (vbytes == 1) {
@@ -148,7 +171,7 @@ struct GpuRing::Impl {
     ++launches;
   }
 
-  uint32_t steps_per_launch() const { return tb ? K : resident ? kResidentChunk : 1u; }
+  uint32_t steps_per_launch() const { return (resident || dr) ? kResidentChunk : tb ? K : 1u; }
 
   void build_graph() {
     cudaGraph_t g;
@@ -171,7 +194,11 @@ struct GpuRing::Impl {
     *hctl = c;
     CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
     CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
-    if (tb) {
+    if (dr) {  // the DR planner's width
+      if (vbytes == 1) cone_init_kernel<uint8_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
+      else cone_init_kernel<uint32_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
+      CK(cudaGetLastError());
+    } else if (tb) {
       // the cone runs on one block of the TB kernel's width (K*(vmax+1) <= TPB)
       if (vbytes == 1) {
         if (medium) cone_init_kernel<uint8_t, kTbmTPB><<<1, kTbmTPB, 0, stream>>>(args);
@@ -277,7 +304,7 @@ struct GpuRing::Impl {
   // launch's last block zeroes the slots of the next plan).
   void enqueue_steps(uint64_t count) {
     const uint64_t per = steps_per_launch();
-    if (resident) {  // whole chunks in one launch; no graph needed
+    if (resident || dr) {  // whole chunks in one launch; no graph needed
       while (count > 0) {
         const uint32_t k = static_cast<uint32_t>(std::min<uint64_t>(count, per));
         if (steps_done - drained + k > kRecCap / 2) drain();
@@ -505,6 +532,45 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // Small rings run whole chunks of steps in one shared-memory-resident CTA
   // (NASCH_B200_RESIDENT=0 forces the one-step-per-launch kernel instead).
   d.resident = !d.tb && d.n <= kResidentMaxCars && env_long("NASCH_B200_RESIDENT", 1) != 0;
+  // Medium rings: the distributed-resident kernel (dr_kernel.cuh) keeps the
+  // ring in registers on every SM for whole chunks of steps
+  // (NASCH_B200_DR=0 disables it).
+  std::vector<uint32_t> dr_seg;
+  if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 0) != 0) {
+    uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
+    Kd = std::min<uint32_t>(Kd, kDrTPB / (d.vmax_eff + 1));
+    int coop = 0;
+    CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, d.device));
+    const uint32_t Gw = std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(sms) - 1, (d.n + 255) / 256));
+    const uint32_t segsz = ((d.n + Gw - 1) / Gw + 15) / 16 * 16;  // 16-aligned segments
+    uint32_t cptd = 0;
+    for (uint32_t c : {4u, 8u, 16u})
+      if (!cptd && segsz + kDrHalo <= uint32_t(kDrTPB) * c) cptd = c;
+    if (coop && sms >= 2 && cptd && Kd >= 2 && uint64_t(d.L) > uint64_t(Kd) * d.vmax_eff) {
+      int occ = 0;
+      const void* fn = nullptr;
+      if (d.vbytes == 1) {
+        fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)
+           : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)
+                       : reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>);
+      } else {
+        fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 4>)
+           : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 8>)
+                       : reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 16>);
+      }
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kDrTPB, 0));
+      const uint32_t G = (d.n + segsz - 1) / segsz;
+      if (occ >= 1 && G + 1 <= uint32_t(sms) * uint32_t(occ)) {
+        d.dr = true;
+        d.tb = d.medium = d.resident = false;
+        d.K = Kd;
+        d.dr_G = G;
+        d.dr_cpt = cptd;
+        for (uint32_t g = 0; g < G; ++g) dr_seg.push_back(g * segsz);
+        dr_seg.push_back(d.n);
+      }
+    }
+  }
   const uint32_t tile = d.tb ? (d.medium ? kTbmStore : kTbStore) : kTile1;
   const uint32_t cpt = d.tb ? (d.medium ? kTbmCPT : kTbCPT) : kCPT1;
   const int tpb = d.tb ? tb_tpb : kTPB;
@@ -574,7 +640,7 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   a.an_inv = powmod(kA, kOrder - (d.n % kOrder));
   a.a1 = powmod(kA, (1 + kOrder - (d.n % kOrder)) % kOrder);
   a.g = powmod(kA, uint64_t(d.grid) * tile);
-  a.kplan = d.tb ? d.K : 0;
+  a.kplan = (d.tb || d.dr) ? d.K : 0;
   a.nl = d.n;
   a.gofs = 0;
   a.agofs = 1;
@@ -583,6 +649,13 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   a.thrpow = d.thrpow;
   a.ctl = d.ctl;
   a.rec = d.rec;
+
+  if (d.dr) {
+    CK(cudaMalloc(&d.dplans, 2 * sizeof(Ctl)));
+    CK(cudaMalloc(&d.dsync, sizeof(DrSync)));
+    CK(cudaMalloc(&d.dseg, dr_seg.size() * 4));
+    CK(cudaMemcpy(d.dseg, dr_seg.data(), dr_seg.size() * 4, cudaMemcpyHostToDevice));
+  }
 
   // init_state (model.cpp:30-40) on the device.
   const int ib = std::max(1, std::min<int>((d.npad + kTPB - 1) / kTPB, 4096));
@@ -620,6 +693,9 @@ GpuRing::Impl::~Impl() {
   cudaFree(dsum);
   cudaFree(blkpow);
   cudaFree(thrpow);
+  cudaFree(dplans);
+  cudaFree(dsync);
+  cudaFree(dseg);
   cudaFreeHost(hx);
   cudaFreeHost(hv);
   cudaFreeHost(hrec);
@@ -790,3 +866,9 @@ void fill_uniform_state(uint64_t L, uint64_t N, uint64_t vmax_init, uint64_t see
 }
 
 }  // namespace nb200
+
+#ifdef NB_DR_TRACE
+extern "C" int nasch_b200_dr_trace(unsigned long long* out, size_t n) {
+  return cudaMemcpyFromSymbol(out, nb200::g_dr_trace, std::min<size_t>(n, 256 * 8) * 8) == cudaSuccess ? 0 : 1;
+}
+#endif

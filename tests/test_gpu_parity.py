@@ -331,7 +331,7 @@ def test_config3_prefix_vs_oracle(port):
 
 @pytest.fixture
 def k_env():
-    old = {k: os.environ.get(k) for k in ("NASCH_B200_K", "NASCH_B200_TILE")}
+    old = {k: os.environ.get(k) for k in ("NASCH_B200_K", "NASCH_B200_TILE", "NASCH_B200_DR")}
     yield
     for k, v in old.items():
         if v is None:
@@ -340,15 +340,16 @@ def k_env():
             os.environ[k] = v
 
 
-@pytest.mark.parametrize("tile", ["large", "medium"])
+@pytest.mark.parametrize("tile", ["large", "medium", "dr"])
 @pytest.mark.parametrize("K", [1, 2, 3, 8, 16])
 def test_temporal_blocking_depths(port, k_env, K, tile):
-    """Rings long enough for the temporal-blocked kernel: every depth K
-    (and the single-step kernel, K=1) and both tile geometries are
-    bit-exact with the oracle, including K not dividing the step count and
-    chunked advances."""
+    """Rings long enough for the temporal-blocked kernels: every depth K
+    (and the single-step kernel, K=1), both TB tile geometries and the
+    distributed-resident kernel (medium rings) are bit-exact with the
+    oracle, including K not dividing the step count and chunked advances."""
     os.environ["NASCH_B200_K"] = str(K)
-    os.environ["NASCH_B200_TILE"] = tile
+    os.environ["NASCH_B200_TILE"] = "large" if tile == "dr" else tile
+    os.environ["NASCH_B200_DR"] = "1" if tile == "dr" else "0"
     rng = np.random.default_rng(100 + K)
     cases = [(20000, 4096, 5, 0.13), (5000, 4100, 5, 0.5), (4096, 4096, 5, 0.3),
              (300000, 9000, 20, 0.2), (70000, 12000, 40, 0.35), (1 << 20, 70001, 5, 0.7)]
@@ -372,9 +373,11 @@ def test_temporal_blocking_depths(port, k_env, K, tile):
         e.close()
 
 
-def test_temporal_blocking_checksum_mode(port, k_env):
-    """Checksum mode steps one at a time through the TB kernel."""
+@pytest.mark.parametrize("dr", ["0", "1"])
+def test_temporal_blocking_checksum_mode(port, k_env, dr):
+    """Checksum mode steps one at a time through the TB / DR kernels."""
     os.environ["NASCH_B200_K"] = "8"
+    os.environ["NASCH_B200_DR"] = dr
     L, N = 40000, 6000
     x0, v0 = nasch.fill_uniform_state(L, N, 5, 1)
     o = port.run(L, 5, 0.25, 1, 40, x0.astype(np.uint64), v0.astype(np.uint64))
@@ -382,16 +385,44 @@ def test_temporal_blocking_checksum_mode(port, k_env):
     assert_same(g, o)
 
 
-def test_temporal_blocking_long_run_vs_reference(ref, k_env):
+@pytest.mark.parametrize("dr", ["0", "1"])
+def test_temporal_blocking_long_run_vs_reference(ref, k_env, dr):
     """Thousands of steps of a dense jammed ring (many crossings per plan)
     against the reference Engine."""
     os.environ["NASCH_B200_K"] = "16"
+    os.environ["NASCH_B200_DR"] = dr
     L, N = 12000, 7000
     x0, v0 = nasch.fill_uniform_state(L, N, 5, 8)
     r = ref.run(L, N, 5, 0.5, 8, 3000, x0=x0, v0=v0, workers=4)
     g = gpu_run(L, N, 5, 0.5, 8, 3000, x0, v0, checksum=False)
     assert (g["x"] == r["x"]).all() and (g["v"] == r["v"]).all()
     assert (g["sumv"] == r["sumv"]).all()
+
+
+def test_distributed_resident_geometries(port, k_env):
+    """The distributed-resident kernel across its register geometries (4, 8
+    and 16 cars per thread), a vmax that shortens the epoch (K = 6), a
+    jammed ring, and a run longer than one launch (16384 steps)."""
+    os.environ.pop("NASCH_B200_K", None)
+    os.environ["NASCH_B200_DR"] = "1"
+    rng = np.random.default_rng(2024)
+    cases = [(60000, 20000, 5, 0.13, 77), (1 << 20, 200001, 5, 0.25, 41), (2_000_000, 500_000, 5, 0.3, 23),
+             (70000, 12000, 40, 0.35, 50), (9000, 8191, 5, 0.5, 90), (5000, 4100, 5, 0.5, 20000)]
+    for trial, (L, N, vmax, p, T) in enumerate(cases):
+        x0 = np.sort(rng.choice(L, N, replace=False)).astype(np.uint64)
+        v0 = rng.integers(0, vmax + 1, N).astype(np.uint64)
+        o = port.run(L, vmax, p, 3 + trial, T, x0, v0)
+        e = nasch.Engine(params(L, N, vmax, p, T, 3 + trial))
+        e.set_checksum(False)
+        e.set_state(x0, v0)
+        assert e.steps_per_launch > 16, "distributed-resident mode expected"
+        e.advance(T // 3)
+        e.advance(T)
+        x, v = e.snapshot()
+        assert (x == o["x"]).all() and (v == o["v"]).all(), trial
+        assert (e.sumv_series() == o["sumv"]).all(), trial
+        assert (e.wrap_series() == o["wraps"]).all(), trial
+        e.close()
 
 
 def test_device_checksum_many_chunks(port):
