@@ -1,0 +1,144 @@
+// cone_warp.cuh -- the origin-cone planner (step_kernels.cuh, cone_simulate)
+// run by ONE warp with no block barriers: cone slot i = lane * CPW + c lives
+// in lane `lane`'s registers, leaders cross lanes by shuffle and the
+// per-step crossing count is a warp reduction.  Used by the distributed-
+// resident planner (dr_kernel.cuh), whose epochs wait on it.
+//
+// Slots, draws and outputs are exactly those of cone_simulate: slot i holds
+// the car of id (h + N - M + i) mod N with h the rank-0 id, M = kk * vmax
+// rear cars (every car that can reach the origin within kk steps) and kk
+// leaders ahead; the front slot's missing leader corrupts at most kk slots
+// from the front, never the counted rear ones.
+#pragma once
+#include <cstdint>
+
+#include "step_kernels.cuh"
+
+namespace nb200 {
+
+// Shared-memory power tables of the planner: lin[i] = a^i, step2[c] =
+// 2 a^c and step2[256 + c] = 2 a^(c + N) (the per-step draw-base update
+// E' = E a^c [a^N unless W wraps], doubled for mulmod_x2).
+struct ConeTab {
+  uint32_t lin[256];
+  uint32_t step2[512];
+};
+
+__device__ __forceinline__ void cone_tab_fill(ConeTab& tab, const RingArgs& ra) {
+  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+    const uint32_t a = c_pow.lin[i];
+    tab.lin[i] = a;
+    tab.step2[i] = a << 1;
+    tab.step2[256 + i] = mulmod(a, ra.an) << 1;
+  }
+}
+
+// Simulates kk <= 32 steps of the cone (M rear cars + kk leaders) from step
+// t with rank offset W over (X, V); writes plan steps [ofs, ofs + kout) --
+// W, E, E2 and the crossing count of each -- into out->Wk/Ek/E2k/ck, plus
+// out->kplan/E/E2.  Returns (in every lane) W after ofs steps, the first
+// planned step's.  Requires M + kk <= 32 * CPW and ofs + kout <= kk.
+//
+// The serial chain of a step is crossing count -> E_{j+1} -> draws ->
+// velocities -> crossings: one table lookup and two mulmod_x2; each car's
+// multiplier for either side of the rank seam (a^id, a^(id-N)) is
+// precomputed, so the seam test selects a register, not a product.
+template <typename VT, int CPW>
+__device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
+                                  uint32_t kk, uint32_t M, uint32_t ofs, uint32_t kout, Ctl* out,
+                                  const ConeTab& tab) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint32_t C = M + kk;
+  const uint32_t id0 = cone_slot_id(N, W, M, 0);
+  const uint32_t aid0 = powmod_warp(id0);
+  uint32_t E = mulmod(ra.s0, powmod_warp(draw_exponent(t, N, W)));
+  uint32_t x[CPW], v[CPW], apA[CPW], apB[CPW], idv[CPW];
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const uint32_t i = lane * CPW + c;
+    const bool act = i < C;
+    uint32_t id = id0 + (act ? i : 0u);  // < 2^32: id0 < N < 2^31, i < 256
+    const bool wrapped = id >= N;
+    if (wrapped) id -= N;
+    idv[c] = id;
+    x[c] = act ? __ldcg(X + id) : 0u;
+    v[c] = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+    uint32_t a = mulmod(aid0, tab.lin[act ? i : 0u]);
+    if (wrapped) a = mulmod(a, ra.an_inv);
+    apA[c] = a << 1;                         // ids below the seam: E a^id
+    apB[c] = mulmod(a, ra.an_inv) << 1;      // at or past it: E a^(id-N)
+  }
+  const uint32_t an_inv2 = ra.an_inv << 1;
+  uint32_t Wj = W, Wofs = W;
+  uint32_t rW = 0, rE = 0, rE2 = 0, rc = 0;  // lane j keeps plan step ofs + j
+  for (uint32_t j = 0; j < kk; ++j) {
+    const uint32_t bound = N - Wj;
+    uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+    if (lane == 31) xn = x[CPW - 1];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      const uint32_t i = lane * CPW + c;
+      const uint32_t s = mulmod_x2(idv[c] < bound ? apA[c] : apB[c], E);
+      const uint32_t xl = (c + 1 < CPW) ? x[c + 1] : xn;
+      uint32_t xnew, cr;
+      v[c] = car_rule(x[c], xl, v[c], s, L, vmax, tp, xnew, cr);
+      x[c] = xnew;
+      cnt += (i < M && cr) ? 1u : 0u;
+    }
+    const uint32_t cj = __reduce_add_sync(0xffffffffu, cnt);
+    if (j == ofs) Wofs = Wj;
+    if (j >= ofs && lane == j - ofs) {
+      rW = Wj;
+      rE = E;
+      rE2 = mulmod_x2(an_inv2, E);
+      rc = cj;
+    }
+    uint32_t Wn = Wj + cj;
+    const bool wrap = Wn >= N;
+    if (wrap) Wn -= N;
+    E = mulmod_x2(tab.step2[cj + (wrap ? 0u : 256u)], E);  // cj <= M < 256
+    Wj = Wn;
+    if (j + 1 == ofs + kout) break;
+  }
+  if (lane < kout) {
+    out->Wk[lane] = rW;
+    out->Ek[lane] = rE;
+    out->E2k[lane] = rE2;
+    out->ck[lane] = rc;
+  }
+  if (lane == 0) {
+    out->kplan = kout;
+    out->E = rE;
+    out->E2 = rE2;
+  }
+  return Wofs;
+}
+
+// The rear slots need only the cars that can reach the origin within kk
+// steps: of the last kk*vmax ranks, the suffix with x >= L - kk*vmax (cars
+// behind them cannot cross and never influence them -- influence runs from
+// leader to follower).  At moderate density that is a fraction of kk*vmax,
+// and the per-lane work shrinks with it.  Requires L > kk*vmax.
+template <typename VT>
+__device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
+                              uint32_t kk, uint32_t ofs, uint32_t kout, Ctl* out, const ConeTab& tab) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t N = ra.n, L = ra.L;
+  const uint32_t Mmax = kk * ra.vmax;
+  const uint32_t id0 = cone_slot_id(N, W, Mmax, 0);
+  uint32_t cnt = 0;
+  for (uint32_t i = lane; i < Mmax; i += 32) {
+    uint32_t id = id0 + i;
+    if (id >= N) id -= N;
+    cnt += __ldcg(X + id) >= L - Mmax ? 1u : 0u;
+  }
+  const uint32_t M = __reduce_add_sync(0xffffffffu, cnt);
+  const uint32_t C = M + kk;
+  if (C <= 64) return cone_warp_run<VT, 2>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 128) return cone_warp_run<VT, 4>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  return cone_warp_run<VT, 8>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+}
+
+}  // namespace nb200

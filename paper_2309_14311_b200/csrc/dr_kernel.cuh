@@ -1,34 +1,38 @@
 // dr_kernel.cuh -- distributed-resident step kernel for medium rings
 // (4096 < N <= ~600k cars): the whole ring stays in the registers of G
 // worker CTAs (one per SM, cooperative launch) for every step of a launch,
-// and one planner CTA produces each epoch's origin-cone plan.
+// and one planner CTA produces the origin-cone plan of each epoch one epoch
+// ahead, off the workers' critical path.
 //
 // A launch runs `steps` steps as epochs of k <= K steps (temporal blocking,
 // as nasch_tb_kernel).  Worker g owns the car-id
-// segment [seg[g], seg[g+1]) (16-aligned floor partition) plus a 16-car
-// halo: the first cars of segment g+1, re-read at every epoch start.  Its
-// cars never leave registers between epochs; per epoch it
-//   1. waits for plan(e) (epoch 0: the plan in Ctl from the previous launch),
-//   2. reloads the halo from the state buffer of epoch e,
-//   3. runs k steps (block-wide leader hand-off, one barrier per step),
-//   4. stores its owned cars into the buffer of epoch e+1, adds its per-step
-//      velocity sums / crossing counts into the step records and signals.
-// The planner waits for all G signals of epoch e, checks the counted
-// crossings against plan(e), simulates the origin cone from the stored
-// state for the next K steps (cone_plan, step_kernels.cuh) and publishes
-// plan(e+1).  After the last epoch it plans the next launch into Ctl.
+// segment [seg[g], seg[g+1]) (16-aligned) plus a 16-car halo: the first
+// cars of the next segment, re-read at every epoch start.  Its own cars
+// never leave registers; per epoch e it
+//   1. waits for plan(e) (epoch 0: the plan in Ctl) and for worker g+1 to
+//      have published the state S_e (its flag >= e),
+//   2. reloads the halo from S_e's buffer, runs k steps (block-wide leader
+//      hand-off, one barrier per step),
+//   3. waits until worker g-1 finished epoch e-1 (it has read its halo from
+//      the buffer about to be overwritten), stores its cars as S_{e+1}, adds
+//      its per-step velocity sums / crossing counts into the step records
+//      and raises its flag to e+1.
+// The planner, at epoch e, waits until every worker published S_e, checks
+// epoch e-1's counted crossings against plan(e-1), simulates the origin cone
+// from S_e for k_e + K steps in one warp (cone_warp.cuh) and publishes the
+// last K of them as plan(e+1) -- while the workers run epoch e.  After the
+// last epoch it installs the next launch's plan in Ctl.
 //
-// Compared with one TB launch per 16 steps this removes the launch gap, the
-// state reload and the end-of-launch ticket per epoch (BASELINE config 2:
-// 2e5 cars, where a TB launch is ~10x longer than its arithmetic).
-//
-// Every wait is bounded: a CTA that waits for more than ~2 s raises
-// `abort` and flags Ctl::err = 3, and every other waiter leaves on `abort`,
-// so a fault cannot hang the GPU.
+// No worker can run more than two epochs ahead of any other (plan(e) needs
+// every worker past e-2), which is what makes two plan slots and two state
+// buffers enough.  Every wait is bounded: a CTA waiting more than ~2 s
+// raises `abort` and Ctl::err = 3, and every other waiter leaves on
+// `abort`, so a fault cannot hang the GPU.
 #pragma once
 #include <cstdint>
 #include <type_traits>
 
+#include "cone_warp.cuh"
 #include "step_kernels.cuh"
 
 namespace nb200 {
@@ -36,6 +40,7 @@ namespace nb200 {
 #ifdef NB_DR_TRACE
 // Diagnostic build only: per-epoch %globaltimer stamps (tools/dr_trace.py).
 __device__ unsigned long long g_dr_trace[256 * 8];
+__device__ unsigned long long g_dr_wtrace[64 * 160 * 4];  // [epoch][worker][ready, steps, checked, signalled]
 #define DR_TRACE(e, slot)                                                   \
   do {                                                                      \
     if ((e) < 256) {                                                        \
@@ -44,7 +49,18 @@ __device__ unsigned long long g_dr_trace[256 * 8];
       g_dr_trace[(e) * 8 + (slot)] = tt;                                    \
     }                                                                       \
   } while (0)
+#define DR_WTRACE(e, g, slot)                                              \
+  do {                                                                      \
+    if ((e) < 64 && (g) < 160) {                                            \
+      unsigned long long tt;                                                \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                \
+      g_dr_wtrace[((e) * 160 + (g)) * 4 + (slot)] = tt;                     \
+    }                                                                       \
+  } while (0)
 #else
+#define DR_WTRACE(e, g, slot) \
+  do {                        \
+  } while (0)
 #define DR_TRACE(e, slot) \
   do {                    \
   } while (0)
@@ -54,14 +70,15 @@ constexpr int kDrTPB = 256;
 constexpr uint32_t kDrHalo = 16;
 
 struct DrSync {
-  unsigned int done[2];     // workers finished with epoch e (slot e & 1)
   unsigned int plan_epoch;  // plan(e) is published for e <= plan_epoch
   unsigned int abort;
+  unsigned int flags[1];    // [G]: epochs worker g has finished (S_flag published)
 };
 
 struct DrArgs {
   Ctl* plans;              // [2]: plan of epoch e in plans[e & 1] (e >= 1)
-  DrSync* sync;            // zeroed before every launch
+  uint32_t* mbox;          // [3][G][2 * kDrHalo]: worker g's first cars (x, v) of S_e in slot e % 3
+  DrSync* sync;            // zeroed before every launch (2 + G words)
   const uint32_t* seg;     // [G + 1] segment starts, seg[G] = N
   uint32_t G;              // worker CTAs; block G is the planner
   uint32_t K;              // steps per epoch (the cone plan length)
@@ -95,6 +112,36 @@ __device__ __noinline__ bool dr_wait_geq(const unsigned int* p, unsigned int tar
   }
 }
 
+// Publish a flag after this CTA's writes (ordered by the caller's
+// __syncthreads): gpu-scope fence, then a plain relaxed store -- no atomic
+// round trip.
+__device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
+  __threadfence();
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+
+// Thread-0 spin until *p >= a and *q >= b (one acquire fence at the end).
+__device__ __noinline__ bool dr_wait2(const unsigned int* p, unsigned int a, const unsigned int* q, unsigned int b,
+                                      DrSync* sync, Ctl* ctl) {
+  const long long start = clock64();
+  for (uint32_t i = 0;; ++i) {
+    const unsigned int vp = ld_relaxed_u32(p), vq = ld_relaxed_u32(q);
+    if (vp >= a && vq >= b) {
+      __threadfence();
+      return true;
+    }
+    if ((i & 63u) == 63u) {
+      if (ld_relaxed_u32(&sync->abort)) return false;
+      if (clock64() - start > 4000000000ll) {
+        atomicExch(&sync->abort, 1u);
+        atomicCAS(&ctl->err, 0u, 3u);
+        return false;
+      }
+      if (i > 4096) __nanosleep(64);
+    }
+  }
+}
+
 // Block-wide: thread 0 waits, everyone learns the outcome.
 __device__ __forceinline__ bool dr_block_wait(const unsigned int* p, unsigned int target, DrSync* sync,
                                               Ctl* ctl) {
@@ -104,70 +151,107 @@ __device__ __forceinline__ bool dr_block_wait(const unsigned int* p, unsigned in
   return s_ok != 0;
 }
 
+// Block-wide: until every worker's flag is >= target.
+__device__ __noinline__ bool dr_wait_all(const DrSync* sync, uint32_t G, unsigned int target, Ctl* ctl) {
+  const long long start = clock64();
+  for (uint32_t i = 0;; ++i) {
+    bool ok = true;
+    for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) ok = ok && ld_relaxed_u32(&sync->flags[g]) >= target;
+    if (__syncthreads_and(ok)) break;
+    if ((i & 63u) == 63u) {
+      int bad = 0;
+      if (threadIdx.x == 0) {
+        bad = ld_relaxed_u32(&sync->abort) != 0;
+        if (!bad && clock64() - start > 4000000000ll) {
+          atomicExch(const_cast<unsigned int*>(&sync->abort), 1u);
+          atomicCAS(&ctl->err, 0u, 3u);
+          bad = 1;
+        }
+      }
+      if (__syncthreads_or(bad)) return false;
+    }
+  }
+  __threadfence();
+  return true;
+}
+
+// Crossing counts of the k steps from te (all workers done) against plan pl.
+__device__ __forceinline__ void dr_verify(const RingArgs& ra, const Ctl* pl, uint64_t te, uint32_t k, Ctl* ctl) {
+  if (threadIdx.x < k) {
+    const uint32_t j = threadIdx.x;
+    StepRec* r = ra.rec + ((te + j) % kRecCap);
+    const uint32_t c = __ldcg(&r->c);
+    const uint32_t ck = __ldcg(&pl->ck[j]);
+    r->W = __ldcg(&pl->Wk[j]);
+    r->cplan = ck;
+    if (c != ck && atomicCAS(&ctl->err, 0u, 1u) == 0u) ctl->err_step = static_cast<unsigned int>(te + j);
+  }
+}
+
 template <typename VT, int TPB>
 __device__ void dr_planner(const RingArgs& ra, const DrArgs& da, const uint32_t steps) {
+  __shared__ ConeTab s_tab;
   Ctl* ctl = ra.ctl;
   DrSync* sync = da.sync;
-  const uint32_t N = ra.n;
   const uint64_t t0 = ctl->t;
   const int b0 = static_cast<int>(ctl->buf);
-  const uint32_t nE = (steps + da.K - 1) / da.K;
-  __shared__ uint32_t s_bad, s_Wn;
+  const uint32_t K = da.K;
+  const uint32_t nE = (steps + K - 1) / K;
+  cone_tab_fill(s_tab, ra);
+  __shared__ uint32_t s_W;
+  if (threadIdx.x == 0) s_W = ctl->W;
+  __syncthreads();
+  uint32_t We = s_W;  // rank offset at the start of epoch e
   for (uint32_t e = 0; e < nE; ++e) {
-    const uint32_t k = min(da.K, steps - e * da.K);
-    const uint64_t te = t0 + uint64_t(e) * da.K;
-    Ctl* pl = e == 0 ? ctl : da.plans + (e & 1u);
-    if (!dr_block_wait(&sync->done[e & 1u], da.G, sync, ctl)) return;
+    const uint32_t k = min(K, steps - e * K);
+    const uint64_t te = t0 + uint64_t(e) * K;
+    // S_e complete, hence every worker is past epoch e-1 and done reading
+    // plan(e-1), whose slot receives plan(e+1).
+    if (e > 0 && !dr_wait_all(sync, da.G, e, ctl)) return;
     if (threadIdx.x == 0) DR_TRACE(e, 4);
-    if (threadIdx.x == 0) {
-      sync->done[e & 1u] = 0;  // reused by epoch e + 2, which waits for plan(e + 2)
-      s_bad = ~0u;
-    }
+    if (e > 0) dr_verify(ra, e == 1 ? ctl : da.plans + ((e - 1) & 1u), te - K, K, ctl);
     __syncthreads();
-    // Check the workers' crossing counts against the plan.
-    if (threadIdx.x < k) {
-      const uint32_t j = threadIdx.x;
-      StepRec* r = ra.rec + ((te + j) % kRecCap);
-      const uint32_t c = __ldcg(&r->c);
-      const uint32_t ck = __ldcg(&pl->ck[j]);
-      r->W = __ldcg(&pl->Wk[j]);
-      r->cplan = ck;
-      if (c != ck) atomicMin(&s_bad, j);
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      if (s_bad != ~0u && atomicCAS(&ctl->err, 0u, 1u) == 0u) ctl->err_step = static_cast<unsigned int>(te + s_bad);
-      uint32_t Wn = __ldcg(&pl->Wk[k - 1]) + __ldcg(&pl->ck[k - 1]);
-      if (Wn >= N) Wn -= N;
-      s_Wn = Wn;
-    }
-    __syncthreads();
-    const uint32_t Wn = s_Wn;
+    const int be = (b0 + static_cast<int>(e)) & 1;
+    Ctl* dst = da.plans + ((e + 1) & 1u);
+    uint32_t Wn = 0;
+    if (threadIdx.x < 32)
+      Wn = cone_warp<VT>(ra, xbuf(ra, be), vbuf<VT>(ra, be), te, We, k + K, k, K, dst, s_tab);
     const uint64_t tn = te + k;
-    const int bn = (b0 + static_cast<int>(e) + 1) & 1;
-    const bool last = e + 1 == nE;
-    Ctl* dst = last ? ctl : da.plans + ((e + 1) & 1u);
-    const uint32_t kk = last ? ra.kplan : da.K;
-    if (threadIdx.x == 0) DR_TRACE(e, 5);
-    cone_plan<VT, TPB>(ra, xbuf(ra, bn), vbuf<VT>(ra, bn), tn, Wn, kk, dst);
-    if (threadIdx.x == 0) DR_TRACE(e, 6);
-    for (uint32_t j = threadIdx.x; j < kk; j += TPB) {
+    for (uint32_t j = threadIdx.x; j < K; j += TPB) {
       StepRec* r = ra.rec + ((tn + j) % kRecCap);
       r->sumv = 0;
       r->c = 0;
     }
-    __syncthreads();
     if (threadIdx.x == 0) {
-      if (last) {
-        ctl->W = Wn;
-        ctl->t = tn;
-        ctl->buf = static_cast<unsigned int>(bn);
-      } else {
-        __threadfence();
-        atomicExch(&sync->plan_epoch, e + 1);
-        DR_TRACE(e, 7);
-      }
+      s_W = Wn;
+      DR_TRACE(e, 5);
     }
+    __syncthreads();
+    We = s_W;
+    if (threadIdx.x == 0 && e + 1 < nE) {
+      st_release_u32(&sync->plan_epoch, e + 1);
+      DR_TRACE(e, 7);
+    }
+  }
+  // Last epoch done everywhere: check it, install the next launch's plan.
+  if (!dr_wait_all(sync, da.G, nE, ctl)) return;
+  const uint32_t kl = steps - (nE - 1) * K;
+  dr_verify(ra, nE == 1 ? ctl : da.plans + ((nE - 1) & 1u), t0 + uint64_t(nE - 1) * K, kl, ctl);
+  __syncthreads();
+  const Ctl* np = da.plans + (nE & 1u);
+  if (threadIdx.x < K) {
+    ctl->Wk[threadIdx.x] = __ldcg(&np->Wk[threadIdx.x]);
+    ctl->Ek[threadIdx.x] = __ldcg(&np->Ek[threadIdx.x]);
+    ctl->E2k[threadIdx.x] = __ldcg(&np->E2k[threadIdx.x]);
+    ctl->ck[threadIdx.x] = __ldcg(&np->ck[threadIdx.x]);
+  }
+  if (threadIdx.x == 0) {
+    ctl->kplan = K;
+    ctl->E = __ldcg(&np->E);
+    ctl->E2 = __ldcg(&np->E2);
+    ctl->W = We;
+    ctl->t = t0 + steps;
+    ctl->buf = static_cast<unsigned int>((b0 + static_cast<int>(nE)) & 1);
   }
 }
 
@@ -179,7 +263,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
     dr_planner<VT, TPB>(ra, da, steps);
     return;
   }
-  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax];
+  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax], s_ck[kPlanMax];
   __shared__ uint32_t s_lead[2][NW];
   __shared__ Acc s_acc[kPlanMax][TPB];
   Ctl* ctl = ra.ctl;
@@ -195,7 +279,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
   const uint32_t base = lo + i0;  // id of car 0 (>= N past the ring's end)
   // Car c of this thread holds local index min(i0 + c, span - 1): slots past
   // the halo replicate its front car (their results are never used).
-  uint32_t idc[CPT], ap[CPT], x[CPT], v[CPT];
+  uint32_t idc[CPT], ap[CPT], apB[CPT], x[CPT], v[CPT];
   uint32_t own = 0;
 #pragma unroll
   for (int c = 0; c < CPT; ++c) {
@@ -205,7 +289,8 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
     if (wrapped) id -= N;
     idc[c] = id;
     uint32_t a = powmod(kA, id);  // once per launch
-    ap[c] = a << 1;
+    ap[c] = a << 1;                              // ids below the rank seam
+    apB[c] = mulmod(a, ra.an_inv) << 1;          // at or past it
     own |= (i0 + c < S) ? (1u << c) : 0u;
   }
   const bool own_all = own == (1u << CPT) - 1u;
@@ -220,21 +305,37 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
     const uint64_t te = t0 + uint64_t(e) * da.K;
     const int bi = (b0 + static_cast<int>(e)) & 1;
     const Ctl* pl = e == 0 ? ctl : da.plans + (e & 1u);
-    if (e > 0 && !dr_block_wait(&sync->plan_epoch, e, sync, ctl)) return;
+    // plan(e) published, and the halo's owner has published S_e
+    __shared__ int s_ok;
+    if (threadIdx.x == 0)
+      s_ok = e == 0 || dr_wait2(&sync->plan_epoch, e, &sync->flags[g + 1 == da.G ? 0 : g + 1], e, sync, ctl);
+    __syncthreads();
+    if (!s_ok) return;
     if (g == 0 && threadIdx.x == 0) DR_TRACE(e, 0);
+    if (threadIdx.x == 0) DR_WTRACE(e, g, 0);
     if (threadIdx.x < k) {
       s_W[threadIdx.x] = __ldcg(&pl->Wk[threadIdx.x]);
       s_E[threadIdx.x] = __ldcg(&pl->Ek[threadIdx.x]);
       s_E2[threadIdx.x] = __ldcg(&pl->E2k[threadIdx.x]);
+      s_ck[threadIdx.x] = __ldcg(&pl->ck[threadIdx.x]);
     }
-    // (Re)load: everything at the first epoch, the halo afterwards.
-    const uint32_t* X = xbuf(ra, bi);
-    const VT* V = vbuf<VT>(ra, bi);
+    if (e == 0) {  // the whole segment and halo from the state buffer
+      const uint32_t* X = xbuf(ra, bi);
+      const VT* V = vbuf<VT>(ra, bi);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if (e == 0 || !((own >> c) & 1u)) {
+      for (int c = 0; c < CPT; ++c) {
         x[c] = __ldcg(X + idc[c]);
         v[c] = static_cast<uint32_t>(__ldcg(V + idc[c]));
+      }
+    } else {  // the halo from worker g+1's mailbox
+      const uint32_t* mb = da.mbox + ((e % 3u) * da.G + (g + 1 == da.G ? 0 : g + 1)) * (2 * kDrHalo);
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if (!((own >> c) & 1u)) {
+          const uint32_t h = min(i0 + c, span - 1) - S;  // halo index
+          x[c] = __ldcg(mb + h);
+          v[c] = __ldcg(mb + kDrHalo + h);
+        }
       }
     }
     __syncthreads();
@@ -251,7 +352,11 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
       uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
       if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
       if (!active) continue;
-      if (plain && !(base < bound && bound <= base + CPT)) {
+      // Warp-uniform path choice: one lane near the origin or on the rank
+      // seam sends its whole warp down the general path, which costs a few
+      // instructions more per car -- instead of the warp running both.
+      const bool tplain = plain && !(base < bound && bound <= base + CPT);
+      if (__all_sync(__activemask(), tplain)) {
         const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
@@ -273,31 +378,66 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
           s_acc[j][threadIdx.x] += sum;
         }
       } else {
+        // Any car: seam side per car (precomputed multipliers), headway and
+        // position modulo L as unsigned min's (L < 2^31).
         Acc sum = 0;
         uint32_t crs = 0;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          const uint32_t s = mulmod_x2(ap[c], idc[c] < bound ? E : E2);
+          const uint32_t s = mulmod_x2(idc[c] < bound ? ap[c] : apB[c], E);
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t cr = 0;
-          v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);
+          uint32_t d = x[c] * ra.neg1 + xl;
+          d = min(d, d + L);  // leader past the origin: + L
+          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+          int dec;
+          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+          v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+          const uint32_t xs = x[c] + v[c];
+          x[c] = min(xs, xs - L);
           const bool mine = (own >> c) & 1u;
           sum += mine ? v[c] : 0u;
-          crs += mine ? cr : 0u;
+          crs += (mine && xs >= L) ? 1u : 0u;
         }
         s_acc[j][threadIdx.x] += sum;
         if (crs) atomicAdd(&ra.rec[(te + j) % kRecCap].c, crs);
       }
     }
     if (g == 0 && threadIdx.x == 0) DR_TRACE(e, 1);
-    // Owned cars into the next epoch's buffer.
-    uint32_t* Xo = xbuf(ra, bi ^ 1);
-    VT* Vo = vbuf_w<VT>(ra, bi ^ 1);
+    if (threadIdx.x == 0) DR_WTRACE(e, g, 1);
+    if (threadIdx.x == 0) DR_WTRACE(e, g, 2);
+    // S_{e+1}: the first cars into mailbox slot (e+1) % 3 (last read as the
+    // halo of epoch e-2, which every worker has finished: we hold plan(e)).
+    {
+      uint32_t* mb = da.mbox + (((e + 1) % 3u) * da.G + g) * (2 * kDrHalo);
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) {
-      if ((own >> c) & 1u) {
-        Xo[idc[c]] = x[c];
-        Vo[idc[c]] = static_cast<VT>(v[c]);
+      for (int c = 0; c < CPT; ++c) {
+        if (i0 + c < kDrHalo && i0 + c < S) {
+          mb[i0 + c] = x[c];
+          mb[kDrHalo + i0 + c] = v[c];
+        }
+      }
+    }
+    // The whole segment into the state buffer only where the planner will
+    // read it (the origin cone of S_{e+1}) and at the end of the launch.
+    // Readers of that buffer's previous contents (S_{e-1}: the planner's
+    // cone at epoch e-1) are done -- plan(e) is out.
+    {
+      uint32_t Wn = s_W[k - 1] + s_ck[k - 1];
+      if (Wn >= N) Wn -= N;
+      const uint32_t span_c = 2u * da.K * (vmax + 1);        // cone slots, upper bound
+      const uint32_t c0 = cone_slot_id(N, Wn, 2u * da.K * vmax, 0);  // first cone id
+      const uint32_t rel = lo >= c0 ? lo - c0 : lo + N - c0;        // segment start past c0
+      const bool cone = rel < span_c || rel + S > N;               // ranges intersect (mod N)
+      if (e + 1 == nE || cone) {
+        uint32_t* Xo = xbuf(ra, bi ^ 1);
+        VT* Vo = vbuf_w<VT>(ra, bi ^ 1);
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+          if ((own >> c) & 1u) {
+            Xo[idc[c]] = x[c];
+            Vo[idc[c]] = static_cast<VT>(v[c]);
+          }
+        }
       }
     }
     __syncthreads();
@@ -313,9 +453,9 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
 #pragma unroll
     for (int j = 0; j < kPlanMax; ++j) s_acc[j][threadIdx.x] = 0;
     if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(&sync->done[e & 1u], 1u);
+      st_release_u32(&sync->flags[g], e + 1);
       if (g == 0) DR_TRACE(e, 2);
+      DR_WTRACE(e, g, 3);
       if (g + 1 == da.G) DR_TRACE(e, 3);
     }
   }

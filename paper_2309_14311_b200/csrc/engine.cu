@@ -90,6 +90,7 @@ struct GpuRing::Impl {
   uint32_t dr_G = 0, dr_cpt = 0;
   Ctl* dplans = nullptr;
   DrSync* dsync = nullptr;
+  uint32_t* dmbox = nullptr;
   uint32_t* dseg = nullptr;
   ~Impl();
   uint32_t K = 1;   // steps per TB launch
@@ -126,9 +127,9 @@ struct GpuRing::Impl {
 
   template <typename VT, int CPT>
   void launch_dr_cpt(uint32_t k) {
-    DrArgs da{dplans, dsync, dseg, dr_G, K};
+    DrArgs da{dplans, dmbox, dsync, dseg, dr_G, K};
     void* kargs[] = {&args, &da, &k};
-    CK(cudaMemsetAsync(dsync, 0, sizeof(DrSync), stream));
+    CK(cudaMemsetAsync(dsync, 0, (2 + dr_G) * sizeof(unsigned int), stream));
     CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, kDrTPB, CPT>),
                                    dim3(dr_G + 1), dim3(kDrTPB), kargs, 0, stream));
   }
@@ -536,17 +537,19 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // ring in registers on every SM for whole chunks of steps
   // (NASCH_B200_DR=0 disables it).
   std::vector<uint32_t> dr_seg;
-  if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 0) != 0) {
+  if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 1) != 0) {
     uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
-    Kd = std::min<uint32_t>(Kd, kDrTPB / (d.vmax_eff + 1));
+    // the planner simulates 2K-step cones of 2K*(vmax+1) <= 256 cars
+    Kd = std::min<uint32_t>(Kd, 128 / (d.vmax_eff + 1));
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, d.device));
     const uint32_t Gw = std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(sms) - 1, (d.n + 255) / 256));
-    const uint32_t segsz = ((d.n + Gw - 1) / Gw + 15) / 16 * 16;  // 16-aligned segments
+    // balanced, 16-aligned segments of at least kDrHalo cars (N >= 256 G)
+    const uint32_t segsz = (d.n + Gw - 1) / Gw + 16;  // largest segment
     uint32_t cptd = 0;
     for (uint32_t c : {4u, 8u, 16u})
       if (!cptd && segsz + kDrHalo <= uint32_t(kDrTPB) * c) cptd = c;
-    if (coop && sms >= 2 && cptd && Kd >= 2 && uint64_t(d.L) > uint64_t(Kd) * d.vmax_eff) {
+    if (coop && sms >= 2 && cptd && Kd >= 2 && uint64_t(d.L) > 2ull * Kd * d.vmax_eff) {
       int occ = 0;
       const void* fn = nullptr;
       if (d.vbytes == 1) {
@@ -559,14 +562,14 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
                        : reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 16>);
       }
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kDrTPB, 0));
-      const uint32_t G = (d.n + segsz - 1) / segsz;
+      const uint32_t G = Gw;
       if (occ >= 1 && G + 1 <= uint32_t(sms) * uint32_t(occ)) {
         d.dr = true;
         d.tb = d.medium = d.resident = false;
         d.K = Kd;
         d.dr_G = G;
         d.dr_cpt = cptd;
-        for (uint32_t g = 0; g < G; ++g) dr_seg.push_back(g * segsz);
+        for (uint32_t g = 0; g < G; ++g) dr_seg.push_back(static_cast<uint32_t>(uint64_t(g) * d.n / G) & ~15u);
         dr_seg.push_back(d.n);
       }
     }
@@ -652,7 +655,8 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
 
   if (d.dr) {
     CK(cudaMalloc(&d.dplans, 2 * sizeof(Ctl)));
-    CK(cudaMalloc(&d.dsync, sizeof(DrSync)));
+    CK(cudaMalloc(&d.dsync, (2 + d.dr_G) * sizeof(unsigned int)));
+    CK(cudaMalloc(&d.dmbox, size_t(3) * d.dr_G * 2 * kDrHalo * sizeof(uint32_t)));
     CK(cudaMalloc(&d.dseg, dr_seg.size() * 4));
     CK(cudaMemcpy(d.dseg, dr_seg.data(), dr_seg.size() * 4, cudaMemcpyHostToDevice));
   }
@@ -695,6 +699,7 @@ GpuRing::Impl::~Impl() {
   cudaFree(thrpow);
   cudaFree(dplans);
   cudaFree(dsync);
+  cudaFree(dmbox);
   cudaFree(dseg);
   cudaFreeHost(hx);
   cudaFreeHost(hv);
@@ -870,5 +875,8 @@ void fill_uniform_state(uint64_t L, uint64_t N, uint64_t vmax_init, uint64_t see
 #ifdef NB_DR_TRACE
 extern "C" int nasch_b200_dr_trace(unsigned long long* out, size_t n) {
   return cudaMemcpyFromSymbol(out, nb200::g_dr_trace, std::min<size_t>(n, 256 * 8) * 8) == cudaSuccess ? 0 : 1;
+}
+extern "C" int nasch_b200_dr_wtrace(unsigned long long* out, size_t n) {
+  return cudaMemcpyFromSymbol(out, nb200::g_dr_wtrace, std::min<size_t>(n, 64 * 160 * 4) * 8) == cudaSuccess ? 0 : 1;
 }
 #endif
