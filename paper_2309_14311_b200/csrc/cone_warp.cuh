@@ -17,27 +17,29 @@
 namespace nb200 {
 
 // Shared-memory power tables of the planner: lin[i] = a^i, step2[c] =
-// 2 a^c and step2[256 + c] = 2 a^(c + N) (the per-step draw-base update
-// E' = E a^c [a^N unless W wraps], doubled for mulmod_x2).
+// 2 a^c and step2[kConeSlots + c] = 2 a^(c + N) (the per-step draw-base
+// update E' = E a^c [a^N unless W wraps], doubled for mulmod_x2).
+constexpr uint32_t kConeSlots = 512;  // 32 lanes x up to 16 cars
 struct ConeTab {
-  uint32_t lin[256];
-  uint32_t step2[512];
+  uint32_t lin[kConeSlots];
+  uint32_t step2[2 * kConeSlots];
 };
 
 __device__ __forceinline__ void cone_tab_fill(ConeTab& tab, const RingArgs& ra) {
-  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
-    const uint32_t a = c_pow.lin[i];
+  const uint32_t a256 = mulmod(c_pow.lin[255], kA);
+  for (uint32_t i = threadIdx.x; i < kConeSlots; i += blockDim.x) {
+    const uint32_t a = i < 256 ? c_pow.lin[i] : mulmod(c_pow.lin[i - 256], a256);
     tab.lin[i] = a;
     tab.step2[i] = a << 1;
-    tab.step2[256 + i] = mulmod(a, ra.an) << 1;
+    tab.step2[kConeSlots + i] = mulmod(a, ra.an) << 1;
   }
 }
 
-// Simulates kk <= 32 steps of the cone (M rear cars + kk leaders) from step
+// Simulates kk <= 64 steps of the cone (M rear cars + kk leaders) from step
 // t with rank offset W over (X, V); writes plan steps [ofs, ofs + kout) --
 // W, E, E2 and the crossing count of each -- into out->Wk/Ek/E2k/ck, plus
 // out->kplan/E/E2.  Returns (in every lane) W after ofs steps, the first
-// planned step's.  Requires M + kk <= 32 * CPW and ofs + kout <= kk.
+// planned step's.  Requires M + kk <= 32 * CPW, kout <= 32 and ofs + kout <= kk.
 //
 // The serial chain of a step is crossing count -> E_{j+1} -> draws ->
 // velocities -> crossings: one table lookup and two mulmod_x2; each car's
@@ -98,7 +100,7 @@ __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const V
     uint32_t Wn = Wj + cj;
     const bool wrap = Wn >= N;
     if (wrap) Wn -= N;
-    E = mulmod_x2(tab.step2[cj + (wrap ? 0u : 256u)], E);  // cj <= M < 256
+    E = mulmod_x2(tab.step2[cj + (wrap ? 0u : kConeSlots)], E);  // cj <= M < kConeSlots
     Wj = Wn;
     if (j + 1 == ofs + kout) break;
   }
@@ -138,7 +140,8 @@ __device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V
   const uint32_t C = M + kk;
   if (C <= 64) return cone_warp_run<VT, 2>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
   if (C <= 128) return cone_warp_run<VT, 4>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  return cone_warp_run<VT, 8>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 256) return cone_warp_run<VT, 8>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  return cone_warp_run<VT, 16>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
 }
 
 }  // namespace nb200

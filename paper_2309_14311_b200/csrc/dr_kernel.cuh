@@ -67,7 +67,8 @@ __device__ unsigned long long g_dr_wtrace[64 * 160 * 4];  // [epoch][worker][rea
 #endif
 
 constexpr int kDrTPB = 256;
-constexpr uint32_t kDrHalo = 16;
+constexpr uint32_t kDrHalo = 32;  // >= K (epochs of up to 32 steps)
+constexpr uint32_t kDrKMax = 32;
 
 struct DrSync {
   unsigned int plan_epoch;  // plan(e) is published for e <= plan_epoch
@@ -255,17 +256,25 @@ __device__ void dr_planner(const RingArgs& ra, const DrArgs& da, const uint32_t 
   }
 }
 
+// Cars a worker CTA can hold: NW warp tiles of 32*CPT cars, each with its
+// own 16-car halo (the next warp's first cars, or the next segment's).
+template <int TPB, int CPT>
+constexpr uint32_t dr_capacity() {
+  return (TPB / 32) * (32u * CPT - kDrHalo);
+}
+
 template <typename VT, int TPB, int CPT>
 __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, const DrArgs da, const uint32_t steps) {
   using Acc = typename std::conditional<sizeof(VT) == 1, uint32_t, unsigned long long>::type;
   constexpr int NW = TPB / 32;
+  constexpr uint32_t OW = 32u * CPT - kDrHalo;  // cars owned per warp tile
   if (blockIdx.x == da.G) {
     dr_planner<VT, TPB>(ra, da, steps);
     return;
   }
-  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax], s_ck[kPlanMax];
-  __shared__ uint32_t s_lead[2][NW];
-  __shared__ Acc s_acc[kPlanMax][TPB];
+  __shared__ uint32_t s_W[kPlanCap], s_E[kPlanCap], s_E2[kPlanCap], s_ck[kPlanCap];
+  __shared__ uint32_t s_head[NW][2 * kDrHalo];  // each warp tile's first cars, for the warp behind
+  __shared__ Acc s_acc[kDrKMax][TPB];
   Ctl* ctl = ra.ctl;
   DrSync* sync = da.sync;
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
@@ -274,11 +283,14 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
   const int b0 = static_cast<int>(ctl->buf);
   const uint32_t g = blockIdx.x;
   const uint32_t lo = da.seg[g], S = da.seg[g + 1] - lo;  // owned cars
-  const uint32_t span = S + kDrHalo;                     // cars held (owned + halo)
-  const uint32_t i0 = threadIdx.x * CPT;
-  const uint32_t base = lo + i0;  // id of car 0 (>= N past the ring's end)
-  // Car c of this thread holds local index min(i0 + c, span - 1): slots past
-  // the halo replicate its front car (their results are never used).
+  const uint32_t wbase = warp * OW;                      // first car of this warp tile
+  const bool wactive = wbase < S;                        // warp-uniform
+  const uint32_t u0 = lane * CPT;                        // first car within the warp tile
+  const uint32_t i0 = wbase + u0;                        // ... within the segment
+  const uint32_t base = lo + i0;                         // its id (>= N past the ring's end)
+  // Cars past S are the halo (the next segment's first cars; slots past
+  // those replicate the last one and are never used).
+  const uint32_t span = S + kDrHalo;
   uint32_t idc[CPT], ap[CPT], apB[CPT], x[CPT], v[CPT];
   uint32_t own = 0;
 #pragma unroll
@@ -288,18 +300,16 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
     const bool wrapped = id >= N;
     if (wrapped) id -= N;
     idc[c] = id;
-    uint32_t a = powmod(kA, id);  // once per launch
+    uint32_t a = wactive ? powmod(kA, id) : 1u;  // once per launch
     ap[c] = a << 1;                              // ids below the rank seam
     apB[c] = mulmod(a, ra.an_inv) << 1;          // at or past it
-    own |= (i0 + c < S) ? (1u << c) : 0u;
+    own |= (u0 + c < OW && i0 + c < S) ? (1u << c) : 0u;
   }
   const bool own_all = own == (1u << CPT) - 1u;
   const bool nowrap = base + CPT <= N;  // ids of this thread's cars run consecutively
-  const bool active = i0 < span;
   const uint32_t nE = (steps + da.K - 1) / da.K;
-  uint32_t phase = 0;
 #pragma unroll
-  for (int j = 0; j < kPlanMax; ++j) s_acc[j][threadIdx.x] = 0;
+  for (int j = 0; j < int(kDrKMax); ++j) s_acc[j][threadIdx.x] = 0;
   for (uint32_t e = 0; e < nE; ++e) {
     const uint32_t k = min(da.K, steps - e * da.K);
     const uint64_t te = t0 + uint64_t(e) * da.K;
@@ -327,14 +337,23 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
         x[c] = __ldcg(X + idc[c]);
         v[c] = static_cast<uint32_t>(__ldcg(V + idc[c]));
       }
-    } else {  // the halo from worker g+1's mailbox
+    } else {
+      // Halo slots: the next warp's first cars (shared memory, written at
+      // the end of the previous epoch) or worker g+1's mailbox.
       const uint32_t* mb = da.mbox + ((e % 3u) * da.G + (g + 1 == da.G ? 0 : g + 1)) * (2 * kDrHalo);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
         if (!((own >> c) & 1u)) {
-          const uint32_t h = min(i0 + c, span - 1) - S;  // halo index
-          x[c] = __ldcg(mb + h);
-          v[c] = __ldcg(mb + kDrHalo + h);
+          const uint32_t li = min(i0 + c, span - 1);
+          if (li < S) {
+            const uint32_t h = li - (wbase + OW);  // < kDrHalo: in warp + 1's head
+            x[c] = s_head[warp + 1][h];
+            v[c] = s_head[warp + 1][kDrHalo + h];
+          } else {
+            const uint32_t h = li - S;
+            x[c] = __ldcg(mb + h);
+            v[c] = __ldcg(mb + kDrHalo + h);
+          }
         }
       }
     }
@@ -343,80 +362,86 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
 #pragma unroll
     for (int c = 1; c < CPT; ++c) xmax = max(xmax, x[c]);
     const bool plain = nowrap && xmax < L - k * vmax;
-    for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t E = s_E[j], E2 = s_E2[j];
-      const uint32_t bound = N - s_W[j];
-      const uint32_t slot = phase++ & 1u;
-      if (lane == 0) s_lead[slot][warp] = x[0];
-      __syncthreads();
-      uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
-      if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
-      if (!active) continue;
-      // Warp-uniform path choice: one lane near the origin or on the rank
-      // seam sends its whole warp down the general path, which costs a few
-      // instructions more per car -- instead of the warp running both.
-      const bool tplain = plain && !(base < bound && bound <= base + CPT);
-      if (__all_sync(__activemask(), tplain)) {
-        const uint32_t Es = base < bound ? E : E2;
+    if (wactive) {
+      // Warp tiles: no block barrier inside the epoch.
+      for (uint32_t j = 0; j < k; ++j) {
+        const uint32_t E = s_E[j], E2 = s_E2[j];
+        const uint32_t bound = N - s_W[j];
+        uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+        if (lane == 31) xn = x[CPT - 1];  // the tile front's leader is unknown: k <= halo
+        // Warp-uniform path choice: a lane near the origin or on the rank
+        // seam sends the whole warp down the general path (a few more
+        // instructions per car) instead of the warp running both.
+        const bool tplain = plain && !(base < bound && bound <= base + CPT);
+        if (__all_sync(0xffffffffu, tplain)) {
+          const uint32_t Es = base < bound ? E : E2;
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          const uint32_t s = mulmod_x2(ap[c], Es);
-          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          const uint32_t d = x[c] * ra.neg1 + xl;
-          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
-          int dec;
-          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
-          v[c] = static_cast<uint32_t>(max(vc + dec, 0));
-          x[c] += v[c];
-        }
-        if (own_all) {
-          s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
-        } else if (own) {
+          for (int c = 0; c < CPT; ++c) {
+            const uint32_t s = mulmod_x2(ap[c], Es);
+            const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+            const uint32_t d = x[c] * ra.neg1 + xl;
+            const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+            int dec;
+            asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+            v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+            x[c] += v[c];
+          }
+          if (own_all) {
+            s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+          } else if (own) {
+            Acc sum = 0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
+            s_acc[j][threadIdx.x] += sum;
+          }
+        } else {
+          // Any car: seam side per car (precomputed multipliers), headway
+          // and position modulo L as unsigned min's (L < 2^31).
           Acc sum = 0;
+          uint32_t crs = 0;
 #pragma unroll
-          for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
+          for (int c = 0; c < CPT; ++c) {
+            const uint32_t s = mulmod_x2(idc[c] < bound ? ap[c] : apB[c], E);
+            const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+            uint32_t d = x[c] * ra.neg1 + xl;
+            d = min(d, d + L);  // leader past the origin: + L
+            const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+            int dec;
+            asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+            v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+            const uint32_t xs = x[c] + v[c];
+            x[c] = min(xs, xs - L);
+            const bool mine = (own >> c) & 1u;
+            sum += mine ? v[c] : 0u;
+            crs += (mine && xs >= L) ? 1u : 0u;
+          }
           s_acc[j][threadIdx.x] += sum;
+          crs = __reduce_add_sync(0xffffffffu, crs);
+          if (lane == 0 && crs) atomicAdd(&ra.rec[(te + j) % kRecCap].c, crs);
         }
-      } else {
-        // Any car: seam side per car (precomputed multipliers), headway and
-        // position modulo L as unsigned min's (L < 2^31).
-        Acc sum = 0;
-        uint32_t crs = 0;
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-          const uint32_t s = mulmod_x2(idc[c] < bound ? ap[c] : apB[c], E);
-          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t d = x[c] * ra.neg1 + xl;
-          d = min(d, d + L);  // leader past the origin: + L
-          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
-          int dec;
-          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
-          v[c] = static_cast<uint32_t>(max(vc + dec, 0));
-          const uint32_t xs = x[c] + v[c];
-          x[c] = min(xs, xs - L);
-          const bool mine = (own >> c) & 1u;
-          sum += mine ? v[c] : 0u;
-          crs += (mine && xs >= L) ? 1u : 0u;
-        }
-        s_acc[j][threadIdx.x] += sum;
-        if (crs) atomicAdd(&ra.rec[(te + j) % kRecCap].c, crs);
       }
     }
     if (g == 0 && threadIdx.x == 0) DR_TRACE(e, 1);
     if (threadIdx.x == 0) DR_WTRACE(e, g, 1);
-    if (threadIdx.x == 0) DR_WTRACE(e, g, 2);
-    // S_{e+1}: the first cars into mailbox slot (e+1) % 3 (last read as the
-    // halo of epoch e-2, which every worker has finished: we hold plan(e)).
+    // S_{e+1}: each warp tile's first cars to shared memory (the halo of the
+    // warp behind); the segment's first cars also into mailbox slot
+    // (e+1) % 3 (last read as the halo of epoch e-2, which every worker has
+    // finished: we hold plan(e)).
     {
       uint32_t* mb = da.mbox + (((e + 1) % 3u) * da.G + g) * (2 * kDrHalo);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        if (i0 + c < kDrHalo && i0 + c < S) {
-          mb[i0 + c] = x[c];
-          mb[kDrHalo + i0 + c] = v[c];
+        if (u0 + c < kDrHalo && i0 + c < S) {
+          s_head[warp][u0 + c] = x[c];
+          s_head[warp][kDrHalo + u0 + c] = v[c];
+          if (warp == 0) {
+            mb[u0 + c] = x[c];
+            mb[kDrHalo + u0 + c] = v[c];
+          }
         }
       }
     }
+    if (threadIdx.x == 0) DR_WTRACE(e, g, 2);
     // The whole segment into the state buffer only where the planner will
     // read it (the origin cone of S_{e+1}) and at the end of the launch.
     // Readers of that buffer's previous contents (S_{e-1}: the planner's
@@ -451,7 +476,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kPlanMax; ++j) s_acc[j][threadIdx.x] = 0;
+    for (int j = 0; j < int(kDrKMax); ++j) s_acc[j][threadIdx.x] = 0;
     if (threadIdx.x == 0) {
       st_release_u32(&sync->flags[g], e + 1);
       if (g == 0) DR_TRACE(e, 2);

@@ -153,7 +153,7 @@ struct GpuRing::Impl {
   // resident mode).
   void launch(uint32_t k) {
     if (dr) {
-      if (vbytes == 1) launch_dr<uint8_t>(k); else launch_dr<uint32_t>(k);
+      launch_dr<uint8_t>(k);  // DR needs K(vmax+1) <= 256: u8 velocities
     } else if (tb) {
       if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
     } else if (resident) {
@@ -196,8 +196,7 @@ struct GpuRing::Impl {
     CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
     CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
     if (dr) {  // the DR planner's width
-      if (vbytes == 1) cone_init_kernel<uint8_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
-      else cone_init_kernel<uint32_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
+      cone_init_kernel<uint8_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
       CK(cudaGetLastError());
     } else if (tb) {
       // the cone runs on one block of the TB kernel's width (K*(vmax+1) <= TPB)
@@ -538,29 +537,26 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // (NASCH_B200_DR=0 disables it).
   std::vector<uint32_t> dr_seg;
   if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 1) != 0) {
-    uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
-    // the planner simulates 2K-step cones of 2K*(vmax+1) <= 256 cars
-    Kd = std::min<uint32_t>(Kd, 128 / (d.vmax_eff + 1));
+    // 16-step epochs: at 32 the 64-step pipelined cone outlasts an epoch
+    const long kreq_dr = env_long("NASCH_B200_K", 16);
+    uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq_dr, kDrKMax)));
+    // the planner simulates 2K-step cones of 2K*(vmax+1) <= 512 cars; the
+    // initial plan is one 256-thread block's K-step cone
+    Kd = std::min<uint32_t>(Kd, 256 / (d.vmax_eff + 1));
     int coop = 0;
     CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, d.device));
     const uint32_t Gw = std::max<uint32_t>(1, std::min<uint32_t>(uint32_t(sms) - 1, (d.n + 255) / 256));
     // balanced, 16-aligned segments of at least kDrHalo cars (N >= 256 G)
     const uint32_t segsz = (d.n + Gw - 1) / Gw + 16;  // largest segment
     uint32_t cptd = 0;
-    for (uint32_t c : {4u, 8u, 16u})
-      if (!cptd && segsz + kDrHalo <= uint32_t(kDrTPB) * c) cptd = c;
-    if (coop && sms >= 2 && cptd && Kd >= 2 && uint64_t(d.L) > 2ull * Kd * d.vmax_eff) {
+    const uint32_t cap[3] = {dr_capacity<kDrTPB, 4>(), dr_capacity<kDrTPB, 8>(), dr_capacity<kDrTPB, 16>()};
+    for (int i = 0; i < 3 && !cptd; ++i)
+      if (segsz <= cap[i]) cptd = 4u << i;
+    if (coop && sms >= 2 && cptd && Kd >= 2 && d.vbytes == 1 && uint64_t(d.L) > 2ull * Kd * d.vmax_eff) {
       int occ = 0;
-      const void* fn = nullptr;
-      if (d.vbytes == 1) {
-        fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)
-           : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)
-                       : reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>);
-      } else {
-        fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 4>)
-           : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 8>)
-                       : reinterpret_cast<const void*>(&ring_dr_kernel<uint32_t, kDrTPB, 16>);
-      }
+      const void* fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)
+                     : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)
+                                 : reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>);
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kDrTPB, 0));
       const uint32_t G = Gw;
       if (occ >= 1 && G + 1 <= uint32_t(sms) * uint32_t(occ)) {

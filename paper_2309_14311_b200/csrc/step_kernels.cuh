@@ -40,7 +40,8 @@
 
 namespace nb200 {
 
-constexpr int kPlanMax = 16;
+constexpr int kPlanMax = 16;  // steps per temporal-blocked launch (TB kernel; its halo)
+constexpr int kPlanCap = 32;  // plan capacity of Ctl (the distributed-resident epochs)
 
 struct Ctl {
   unsigned long long t;  // steps completed on the device
@@ -52,10 +53,10 @@ struct Ctl {
   unsigned int E2;       // E * a^(-N): draw base of ids >= N - W
   unsigned int kplan;    // steps the plan below covers (temporal blocking)
   unsigned int err_step;
-  unsigned int Wk[kPlanMax];   // W_{t+j}
-  unsigned int Ek[kPlanMax];   // E_{t+j}
-  unsigned int E2k[kPlanMax];  // E2_{t+j}
-  unsigned int ck[kPlanMax];   // predicted c_{t+j}
+  unsigned int Wk[kPlanCap];   // W_{t+j}
+  unsigned int Ek[kPlanCap];   // E_{t+j}
+  unsigned int E2k[kPlanCap];  // E2_{t+j}
+  unsigned int ck[kPlanCap];   // predicted c_{t+j}
 };
 
 struct StepRec {

@@ -399,11 +399,13 @@ def test_temporal_blocking_long_run_vs_reference(ref, k_env, dr):
     assert (g["sumv"] == r["sumv"]).all()
 
 
-def test_distributed_resident_geometries(port, k_env):
+@pytest.mark.parametrize("kdr", ["16", "32"])
+def test_distributed_resident_geometries(port, k_env, kdr):
     """The distributed-resident kernel across its register geometries (4, 8
-    and 16 cars per thread), a vmax that shortens the epoch (K = 6), a
-    jammed ring, and a run longer than one launch (16384 steps)."""
-    os.environ.pop("NASCH_B200_K", None)
+    and 16 cars per thread), 16- and 32-step epochs (the 32-step planner
+    cone of a jammed ring needs 16 slots per lane), a vmax that shortens the
+    epoch, and a run longer than one launch (16384 steps)."""
+    os.environ["NASCH_B200_K"] = kdr
     os.environ["NASCH_B200_DR"] = "1"
     rng = np.random.default_rng(2024)
     cases = [(60000, 20000, 5, 0.13, 77), (1 << 20, 200001, 5, 0.25, 41), (2_000_000, 500_000, 5, 0.3, 23),

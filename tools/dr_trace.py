@@ -41,7 +41,7 @@ def main():
     buf = (ctypes.c_ulonglong * (256 * 8))()
     assert lib.nasch_b200_dr_trace(buf, 256 * 8) == 0
     t = np.frombuffer(buf, dtype=np.uint64).reshape(256, 8).astype(np.int64)
-    ne = min(256, (a.steps + 15) // 16)
+    ne = min(256, (a.steps + 31) // 32)
     t0 = t[0, 0] if t[0, 0] else t[0, 1]
     print("epoch " + " ".join(f"{n:>10s}" for n in NAMES))
     for i in range(min(ne, 12)):
