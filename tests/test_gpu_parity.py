@@ -465,3 +465,78 @@ def test_small_ring_kernels(port, resident_env, resident):
         g = gpu_run(L, N, vmax, p, 31 + trial, T, x0, v0, checksum=False, chunks=[T // 3, T])
         assert (g["x"] == o["x"]).all() and (g["v"] == o["v"]).all(), trial
         assert (g["sumv"] == o["sumv"]).all() and (g["wraps"] == o["wraps"]).all()
+
+
+# ---- distributed-resident (medium-ring) edge cases ---------------------------
+
+@pytest.mark.gpu
+def test_distributed_resident_edge_cases(port, k_env):
+    """Medium rings through the distributed-resident kernel: p = 0 and 1,
+    vmax = 1, a fully jammed ring (every cell but a few occupied), the
+    smallest eligible N, a ring whose last segment is tiny, checksum mode
+    and a set_state resume in the middle of a run."""
+    os.environ.pop("NASCH_B200_K", None)
+    os.environ["NASCH_B200_DR"] = "1"
+    cases = [(20000, 6000, 5, 0.0), (20000, 6000, 5, 1.0), (9000, 5000, 1, 0.3),
+             (6000, 5990, 5, 0.2), (8000, 4097, 5, 0.25), (300000, 37793, 7, 0.45)]
+    for trial, (L, N, vmax, p) in enumerate(cases):
+        x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, L - 1), 50 + trial)
+        T = 77
+        o = port.run(L, vmax, p, 9 + trial, T, x0.astype(np.uint64), v0.astype(np.uint64))
+        for checksum in (False, True):
+            e = nasch.Engine(params(L, N, vmax, p, T, 9 + trial))
+            e.set_checksum(checksum)
+            e.set_state(x0, v0)
+            assert e.steps_per_launch > 16, (L, N)
+            e.advance(T)
+            x, v = e.snapshot()
+            assert (x == o["x"]).all() and (v == o["v"]).all(), (trial, checksum)
+            assert (e.sumv_series() == o["sumv"]).all(), trial
+            if checksum:
+                assert e.checksum == o["checksum"], trial
+            e.close()
+    # resume: state captured at step 40 and re-loaded into a fresh engine
+    L, N = 50000, 12345
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 3)
+    full = port.run(L, 5, 0.3, 5, 120, x0.astype(np.uint64), v0.astype(np.uint64))
+    e = nasch.Engine(params(L, N, 5, 0.3, 120, 5))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.advance(40)
+    xs, vs = e.snapshot()
+    e2 = nasch.Engine(params(L, N, 5, 0.3, 120, 5))
+    e2.set_checksum(False)
+    e2.advance(40)
+    e2.set_state(xs, vs)
+    e2.advance(80)
+    x2, v2 = e2.snapshot()
+    assert (x2 == full["x"]).all() and (v2 == full["v"]).all()
+    # a rejected state (positions not increasing) leaves the ring untouched
+    bad = xs.copy()
+    bad[100], bad[101] = bad[101], bad[100]
+    with pytest.raises(Exception):
+        e.set_state(bad, vs)
+    e.advance(80)
+    x3, v3 = e.snapshot()
+    assert (x3 == full["x"]).all() and (v3 == full["v"]).all()
+
+
+@pytest.mark.gpu
+def test_distributed_resident_frames(tmp_path, k_env):
+    """Frames of a medium ring (DR kernel) are byte-identical with the
+    one-step-per-launch kernel's."""
+    outs = []
+    for dr, k in (("1", None), ("0", "1")):
+        os.environ["NASCH_B200_DR"] = dr
+        if k is None:
+            os.environ.pop("NASCH_B200_K", None)
+        else:
+            os.environ["NASCH_B200_K"] = k
+        p = params(30000, 7000, 5, 0.3, 90, 17, output="ascii", stride=13)
+        e = nasch.Engine(p)
+        e.run()
+        f = tmp_path / f"frames_{dr}.txt"
+        e.write_ascii(str(f))
+        outs.append((f.read_bytes(), e.checksum))
+        e.close()
+    assert outs[0] == outs[1]
