@@ -25,6 +25,17 @@ struct ConeTab {
   uint32_t step2[2 * kConeSlots];
 };
 
+// Only lin and step2[0, kConeSlots): for a block planning rings of
+// different N (the N-dependent factor is then one more mulmod).
+__device__ __forceinline__ void cone_tab_fill_lin(ConeTab& tab) {
+  const uint32_t a256 = mulmod(c_pow.lin[255], kA);
+  for (uint32_t i = threadIdx.x; i < kConeSlots; i += blockDim.x) {
+    const uint32_t a = i < 256 ? c_pow.lin[i] : mulmod(c_pow.lin[i - 256], a256);
+    tab.lin[i] = a;
+    tab.step2[i] = a << 1;
+  }
+}
+
 __device__ __forceinline__ void cone_tab_fill(ConeTab& tab, const RingArgs& ra) {
   const uint32_t a256 = mulmod(c_pow.lin[255], kA);
   for (uint32_t i = threadIdx.x; i < kConeSlots; i += blockDim.x) {
@@ -45,7 +56,7 @@ __device__ __forceinline__ void cone_tab_fill(ConeTab& tab, const RingArgs& ra) 
 // velocities -> crossings: one table lookup and two mulmod_x2; each car's
 // multiplier for either side of the rank seam (a^id, a^(id-N)) is
 // precomputed, so the seam test selects a register, not a product.
-template <typename VT, int CPW>
+template <typename VT, int CPW, bool kTabN = true>
 __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
                                   uint32_t kk, uint32_t M, uint32_t ofs, uint32_t kout, Ctl* out,
                                   const ConeTab& tab) {
@@ -100,7 +111,12 @@ __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const V
     uint32_t Wn = Wj + cj;
     const bool wrap = Wn >= N;
     if (wrap) Wn -= N;
-    E = mulmod_x2(tab.step2[cj + (wrap ? 0u : kConeSlots)], E);  // cj <= M < kConeSlots
+    if (kTabN) {
+      E = mulmod_x2(tab.step2[cj + (wrap ? 0u : kConeSlots)], E);  // cj <= M < kConeSlots
+    } else {  // table without the a^N half (cone_tab_fill_lin)
+      E = mulmod_x2(tab.step2[cj], E);
+      if (!wrap) E = mulmod_x2(ra.an << 1, E);
+    }
     Wj = Wn;
     if (j + 1 == ofs + kout) break;
   }
@@ -123,7 +139,7 @@ __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const V
 // behind them cannot cross and never influence them -- influence runs from
 // leader to follower).  At moderate density that is a fraction of kk*vmax,
 // and the per-lane work shrinks with it.  Requires L > kk*vmax.
-template <typename VT>
+template <typename VT, bool kTabN = true>
 __device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
                               uint32_t kk, uint32_t ofs, uint32_t kout, Ctl* out, const ConeTab& tab) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -138,10 +154,10 @@ __device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V
   }
   const uint32_t M = __reduce_add_sync(0xffffffffu, cnt);
   const uint32_t C = M + kk;
-  if (C <= 64) return cone_warp_run<VT, 2>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  if (C <= 128) return cone_warp_run<VT, 4>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  if (C <= 256) return cone_warp_run<VT, 8>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  return cone_warp_run<VT, 16>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 64) return cone_warp_run<VT, 2, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 128) return cone_warp_run<VT, 4, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 256) return cone_warp_run<VT, 8, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  return cone_warp_run<VT, 16, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
 }
 
 }  // namespace nb200

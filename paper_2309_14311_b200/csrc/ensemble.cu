@@ -26,6 +26,7 @@
 #include "engine.hpp"
 #include "ensemble.hpp"
 #include "minstd.hpp"
+#include "ensemble_tb.cuh"
 #include "step_kernels.cuh"
 
 namespace nb200 {
@@ -188,6 +189,18 @@ __global__ void ensemble_init_kernel(const RingDesc* __restrict__ rings, uint32_
   }
 }
 
+// init_state (model.cpp:30-40), tiled layout.
+__global__ void ens_tiled_init_kernel(const EnsRing* __restrict__ rings, uint32_t nrings,
+                                      uint32_t* __restrict__ X, uint8_t* __restrict__ V) {
+  for (uint32_t r = blockIdx.x; r < nrings; r += gridDim.x) {
+    const EnsRing d = rings[r];
+    for (uint32_t i = threadIdx.x; i < d.n; i += blockDim.x) {
+      X[d.off + i] = static_cast<uint32_t>(uint64_t(i) * d.L / d.n);
+      V[d.off + i] = 0;
+    }
+  }
+}
+
 uint32_t bits_for(uint64_t max_value) {
   uint32_t b = 0;
   while (b < 32 && (uint64_t(1) << b) <= max_value) ++b;
@@ -216,6 +229,46 @@ struct GpuEnsemble::Impl {
   uint64_t launches = 0;
   bool dirty = false;  // device descriptors newer than host mirror
   ~Impl();
+
+  // Tiled mode (ensemble_tb.cuh): every ring in warp tiles, K steps per
+  // launch; used when every ring is eligible (NASCH_B200_ENS_TILED=0 off).
+  bool tiled = false;
+  std::vector<EnsRing> trings;
+  EnsArgs ea{};
+  EnsRing* h_trings = nullptr;
+  int tgrid = 1;
+
+  void tpull() {
+    if (!dirty) return;
+    CKE(cudaMemcpyAsync(h_trings, ea.rings, trings.size() * sizeof(EnsRing), cudaMemcpyDeviceToHost, stream));
+    CKE(cudaStreamSynchronize(stream));
+    std::memcpy(trings.data(), h_trings, trings.size() * sizeof(EnsRing));
+    dirty = false;
+    for (const EnsRing& r : trings)
+      if (r.err) throw std::runtime_error("ensemble: origin-cone plan contradicted (engine state is invalid)");
+  }
+
+  void tpush() {
+    std::memcpy(h_trings, trings.data(), trings.size() * sizeof(EnsRing));
+    CKE(cudaMemcpyAsync(ea.rings, h_trings, trings.size() * sizeof(EnsRing), cudaMemcpyHostToDevice, stream));
+    CKE(cudaStreamSynchronize(stream));
+  }
+
+  void tlaunch(uint64_t steps) {
+    const int pgrid = static_cast<int>((trings.size() + 7) / 8);
+    for (uint64_t left = steps; left > 0;) {
+      const uint32_t kq = static_cast<uint32_t>(std::min<uint64_t>(left, kEtK));
+      ens_plan_kernel<<<pgrid, 256, 0, stream>>>(ea, kq);
+      ens_tb_kernel<kEtTPB><<<tgrid, kEtTPB, 0, stream>>>(ea);
+      CKE(cudaGetLastError());
+      launches += 2;
+      left -= kq;
+    }
+    ens_plan_kernel<<<pgrid, 256, 0, stream>>>(ea, 0u);  // fold the last launch
+    CKE(cudaGetLastError());
+    ++launches;
+    dirty = true;
+  }
 
   void pull() {
     if (!dirty || desc.empty()) return;
@@ -263,6 +316,73 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
   CKE(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d.device));
   CKE(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d.device));
   d.cap_cars = static_cast<size_t>(max_optin) / 4 - kEnsHeaderWords;
+
+  // Tiled mode when every ring fits the warp-tile step and its cone plan.
+  bool all_tiled = std::getenv("NASCH_B200_ENS_TILED") == nullptr ||
+                   std::string(std::getenv("NASCH_B200_ENS_TILED")) != "0";
+  for (const SimParams& p : rings) {
+    const uint64_t vm = std::min<uint64_t>(p.v_max, p.road_length - 1);
+    all_tiled = all_tiled && vm <= 31 && p.road_length > kEtK * vm && p.car_count >= kEtK * (vm + 1);
+  }
+  if (all_tiled) {
+    d.tiled = true;
+    uint64_t total = 0;
+    std::vector<EnsTile> tiles;
+    for (size_t r = 0; r < rings.size(); ++r) {
+      const SimParams& p = rings[r];
+      EnsRing er{};
+      er.off = total;
+      er.steps = p.steps;
+      er.n = static_cast<uint32_t>(p.car_count);
+      er.L = static_cast<uint32_t>(p.road_length);
+      er.vmax = static_cast<uint32_t>(std::min<uint64_t>(p.v_max, p.road_length - 1));
+      er.tp = deceleration_threshold(p.p);
+      er.s0 = seeded(p.seed);
+      er.an = powmod(kA, er.n);
+      er.an_inv = powmod(kA, kOrder - (er.n % kOrder));
+      d.trings.push_back(er);
+      for (uint32_t b = 0; b < er.n; b += kEtStore)
+        tiles.push_back(EnsTile{static_cast<uint32_t>(r), b, powmod(kA, b), 0u});
+      total += (er.n + 15) / 16 * 16;  // 16-car aligned rings: vector loads
+    }
+    const size_t pad = total + kEtLoad + 16;
+    for (int b = 0; b < 2; ++b) {
+      CKE(cudaMalloc(&d.ea.X[b], pad * 4));
+      CKE(cudaMalloc(&d.ea.V[b], pad));
+      CKE(cudaMemset(d.ea.X[b], 0, pad * 4));
+      CKE(cudaMemset(d.ea.V[b], 0, pad));
+    }
+    CKE(cudaMalloc(&d.ea.rings, d.trings.size() * sizeof(EnsRing)));
+    CKE(cudaMallocHost(&d.h_trings, d.trings.size() * sizeof(EnsRing)));
+    CKE(cudaMalloc(&d.ea.plans, d.trings.size() * sizeof(Ctl)));
+    CKE(cudaMalloc(&d.ea.counts, d.trings.size() * sizeof(EnsCount)));
+    CKE(cudaMemset(d.ea.counts, 0, d.trings.size() * sizeof(EnsCount)));
+    EnsTile* dt = nullptr;
+    CKE(cudaMalloc(&dt, tiles.size() * sizeof(EnsTile)));
+    CKE(cudaMemcpy(dt, tiles.data(), tiles.size() * sizeof(EnsTile), cudaMemcpyHostToDevice));
+    d.ea.tiles = dt;
+    std::vector<uint32_t> thr(32);
+    for (uint32_t l = 0; l < 32; ++l) thr[l] = powmod(kA, uint64_t(l) * kEtCPT);
+    uint32_t* dthr = nullptr;
+    CKE(cudaMalloc(&dthr, 32 * 4));
+    CKE(cudaMemcpy(dthr, thr.data(), 32 * 4, cudaMemcpyHostToDevice));
+    d.ea.thrpow = dthr;
+    d.ea.nrings = static_cast<uint32_t>(d.trings.size());
+    d.ea.ntiles = static_cast<uint32_t>(tiles.size());
+    d.ea.neg1 = 0xffffffffu;
+    int per_sm = 0;
+    CKE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ens_tb_kernel<kEtTPB>, kEtTPB, 0));
+    const uint64_t blocks_needed = (tiles.size() + kEtTPB / 32 - 1) / (kEtTPB / 32);
+    d.tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(blocks_needed, uint64_t(sms) * std::max(per_sm, 1))));
+    d.tpush();
+    ens_tiled_init_kernel<<<static_cast<int>(std::min<size_t>(d.trings.size(), 4096)), 256, 0, d.stream>>>(
+        d.ea.rings, d.ea.nrings, d.ea.X[0], d.ea.V[0]);
+    CKE(cudaGetLastError());
+    CKE(cudaStreamSynchronize(d.stream));
+    d.slot.assign(rings.size(), 0);
+    d.overflow.resize(rings.size());
+    return;
+  }
 
   // Which rings are resident, and their packing.
   d.slot.assign(rings.size(), -1);
@@ -340,6 +460,16 @@ GpuEnsemble::Impl::~Impl() {
   cudaFree(d_order);
   cudaFree(d_counter);
   cudaFreeHost(h_desc);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(ea.X[b]);
+    cudaFree(ea.V[b]);
+  }
+  cudaFree(ea.rings);
+  cudaFree(ea.plans);
+  cudaFree(ea.counts);
+  cudaFree(const_cast<EnsTile*>(ea.tiles));
+  cudaFree(const_cast<uint32_t*>(ea.thrpow));
+  cudaFreeHost(h_trings);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -366,6 +496,27 @@ void GpuEnsemble::set_state32(size_t ring, const uint32_t* x, const uint32_t* v,
   }
   const SimParams& p = d.params[ring];
   if (n != p.car_count) throw std::invalid_argument("state length must equal ncars");
+  if (d.tiled) {
+    d.tpull();
+    EnsRing& er = d.trings[ring];
+    std::vector<uint8_t> v8(n);
+    uint64_t s = 0;
+    for (size_t i = 0; i < n; ++i) {
+      if (x[i] >= er.L) throw std::invalid_argument("position out of range [0, length)");
+      if (i && x[i - 1] >= x[i]) throw std::invalid_argument("positions must be strictly increasing");
+      if (v[i] > p.v_max) throw std::invalid_argument("velocity above vmax");
+      if (v[i] > er.vmax) throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      v8[i] = static_cast<uint8_t>(v[i]);
+      s += v[i];
+    }
+    CKE(cudaMemcpyAsync(d.ea.X[er.buf] + er.off, x, n * 4, cudaMemcpyHostToDevice, d.stream));
+    CKE(cudaMemcpyAsync(d.ea.V[er.buf] + er.off, v8.data(), n, cudaMemcpyHostToDevice, d.stream));
+    er.W = 0;
+    er.k = 0;
+    er.last_sumv = static_cast<uint32_t>(s);
+    d.tpush();
+    return;
+  }
   d.pull();
   RingDesc& rd = d.desc[d.slot[ring]];
   std::vector<uint8_t> v8(n);
@@ -389,6 +540,10 @@ void GpuEnsemble::set_state32(size_t ring, const uint32_t* x, const uint32_t* v,
 void GpuEnsemble::enqueue(uint64_t steps) {
   Impl& d = *impl_;
   CKE(cudaSetDevice(d.device));
+  if (d.tiled) {
+    if (steps) d.tlaunch(steps);
+    return;
+  }
   d.launch(steps);
   for (auto& o : d.overflow)
     if (o) o->enqueue(steps);
@@ -398,6 +553,7 @@ void GpuEnsemble::synchronize() {
   Impl& d = *impl_;
   CKE(cudaSetDevice(d.device));
   CKE(cudaStreamSynchronize(d.stream));
+  if (d.tiled) d.tpull();  // raises on a plan contradiction
   for (auto& o : d.overflow)
     if (o) o->synchronize();
 }
@@ -410,6 +566,10 @@ void GpuEnsemble::advance(uint64_t steps) {
 uint64_t GpuEnsemble::steps_done(size_t ring) {
   Impl& d = *impl_;
   if (ring >= d.params.size()) throw std::invalid_argument("ring index out of range");
+  if (d.tiled) {
+    d.tpull();
+    return d.trings[ring].t;
+  }
   if (d.overflow[ring]) return d.overflow[ring]->steps_done();
   d.pull();
   return d.desc[d.slot[ring]].t;
@@ -418,6 +578,11 @@ uint64_t GpuEnsemble::steps_done(size_t ring) {
 void GpuEnsemble::sumv_totals(uint64_t* out, size_t cap) {
   Impl& d = *impl_;
   CKE(cudaSetDevice(d.device));
+  if (d.tiled) {
+    d.tpull();
+    for (size_t r = 0; r < d.params.size() && r < cap; ++r) out[r] = d.trings[r].sumv_total;
+    return;
+  }
   d.pull();
   for (size_t r = 0; r < d.params.size() && r < cap; ++r) {
     if (d.overflow[r]) {
@@ -436,6 +601,11 @@ void GpuEnsemble::sumv_totals(uint64_t* out, size_t cap) {
 void GpuEnsemble::sumv_last(uint64_t* out, size_t cap) {
   Impl& d = *impl_;
   CKE(cudaSetDevice(d.device));
+  if (d.tiled) {
+    d.tpull();
+    for (size_t r = 0; r < d.params.size() && r < cap; ++r) out[r] = d.trings[r].last_sumv;
+    return;
+  }
   d.pull();
   for (size_t r = 0; r < d.params.size() && r < cap; ++r) {
     if (d.overflow[r]) {
@@ -453,6 +623,23 @@ void GpuEnsemble::state(size_t ring, uint64_t* x, uint64_t* v) {
   Impl& d = *impl_;
   if (ring >= d.params.size()) throw std::invalid_argument("ring index out of range");
   CKE(cudaSetDevice(d.device));
+  if (d.tiled) {
+    d.tpull();
+    const EnsRing& er = d.trings[ring];
+    std::vector<uint32_t> hx(er.n);
+    std::vector<uint8_t> hv(er.n);
+    CKE(cudaMemcpyAsync(hx.data(), d.ea.X[er.buf] + er.off, size_t(er.n) * 4, cudaMemcpyDeviceToHost, d.stream));
+    CKE(cudaMemcpyAsync(hv.data(), d.ea.V[er.buf] + er.off, er.n, cudaMemcpyDeviceToHost, d.stream));
+    CKE(cudaStreamSynchronize(d.stream));
+    const uint32_t head = (er.n - er.W) % er.n;  // rank-0 car
+    for (uint32_t k = 0; k < er.n; ++k) {
+      uint32_t id = head + k;
+      if (id >= er.n) id -= er.n;
+      if (x) x[k] = hx[id];
+      if (v) v[k] = hv[id];
+    }
+    return;
+  }
   if (d.overflow[ring]) {
     d.overflow[ring]->state(x, v);
     return;

@@ -43,7 +43,22 @@ def test_ensemble_matches_oracle_per_ring(port):
         assert int(last[r]) == int(o["sumv"][-1]), r
 
 
-def test_ensemble_per_step_series_and_injected_state(port):
+@pytest.fixture
+def tiled_env():
+    import os
+    old = os.environ.get("NASCH_B200_ENS_TILED")
+    yield os.environ
+    if old is None:
+        os.environ.pop("NASCH_B200_ENS_TILED", None)
+    else:
+        os.environ["NASCH_B200_ENS_TILED"] = old
+
+
+@pytest.mark.parametrize("tiled", ["1", "0"])
+def test_ensemble_per_step_series_and_injected_state(port, tiled_env, tiled):
+    """Per-step velocity sums and injected states, through the warp-tile
+    ensemble step (ensemble_tb.cuh) and the shared-memory one."""
+    tiled_env["NASCH_B200_ENS_TILED"] = tiled
     specs = [(100000, 5000, 5, 0.13, 60, 11), (100000, 50000, 5, 0.7, 60, 12),
              (100000, 27500, 5, 0.0, 60, 13), (1000, 1000, 5, 0.4, 60, 14)]
     ens = nasch.Ensemble([mk(*s) for s in specs])
@@ -97,3 +112,36 @@ def test_ensemble_equals_single_ring_engine():
     xs, vs = ens.snapshot(0)
     assert (xe == xs).all() and (ve == vs).all()
     assert int(ens.sumv_totals()[0]) == int(e.sumv_series().sum())
+
+
+def test_tiled_ensemble_random_rings(port, tiled_env):
+    """The warp-tile ensemble on rings of every awkward size: shorter than
+    one warp tile (the tile wraps several times), 496..512 cars, N not a
+    multiple of 16, dense jams, vmax up to 31, p in {0, 1}, and rings with
+    fewer configured steps than the others (they stop; the rest go on)."""
+    tiled_env["NASCH_B200_ENS_TILED"] = "1"
+    rng = np.random.default_rng(11)
+    specs = []
+    for i in range(48):
+        vmax = int(rng.choice([1, 2, 5, 9, 31]))
+        L = int(rng.integers(16 * vmax + 1, 120000))
+        nmin = 16 * (vmax + 1)
+        if nmin > L:
+            continue
+        N = int(rng.choice([nmin, 300, 496, 497, 511, 512, 1000, 4095, int(rng.integers(nmin, L + 1))]))
+        N = max(nmin, min(N, L))
+        p = float(rng.choice([0.0, 0.13, 0.5, 1.0]))
+        T = int(rng.choice([37, 80]))
+        specs.append((L, N, vmax, p, T, int(rng.integers(0, 2**40))))
+    ens = nasch.Ensemble([mk(*s) for s in specs])
+    ens.advance(21)
+    ens.advance(1000)  # each ring clamps at its own T
+    tot = ens.sumv_totals()
+    last = ens.sumv_last()
+    for r, (L, N, vmax, p, T, seed) in enumerate(specs):
+        o = oracle_ring(port, L, N, vmax, p, seed, T)
+        x, v = ens.snapshot(r)
+        assert ens.steps_done(r) == T, r
+        assert (x == o["x"]).all() and (v == o["v"]).all(), (r, specs[r])
+        assert int(tot[r]) == int(o["sumv"].sum()), r
+        assert int(last[r]) == int(o["sumv"][-1]), r
