@@ -127,7 +127,10 @@ __global__ void __launch_bounds__(256) ens_plan_kernel(const EnsArgs ea, const u
 }
 
 template <int TPB>
-__global__ void __launch_bounds__(TPB, 4) ens_tb_kernel(const EnsArgs ea) {
+#ifndef NB_ET_MINB
+#define NB_ET_MINB 4
+#endif
+__global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs ea) {
   constexpr int CPT = kEtCPT;
   constexpr int NW = TPB / 32;
   __shared__ uint32_t s_acc[kEtK][TPB];  // per-thread per-step velocity sums (u8 lanes)
@@ -224,14 +227,14 @@ __global__ void __launch_bounds__(TPB, 4) ens_tb_kernel(const EnsArgs ea) {
           v[c] = static_cast<uint32_t>(max(vc + dec, 0));
           x[c] += v[c];
         }
-        uint32_t sum = 0;
-        if (own_all) {
-          sum = VSum<uint32_t, CPT>::sum(v);
-        } else {
+        if (own_all) {  // separate branches (as tb_kernel.cuh): no per-car selects
+          s_acc[j][threadIdx.x] += VSum<uint32_t, CPT>::sum(v);
+        } else if (own) {
+          uint32_t sum = 0;
 #pragma unroll
           for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
+          s_acc[j][threadIdx.x] += sum;
         }
-        s_acc[j][threadIdx.x] += sum;
       } else {
         uint32_t sum = 0, crs = 0;
 #pragma unroll
