@@ -57,18 +57,42 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic():
-    """Per-launch DRAM bytes of the step kernel from the committed ncu
-    capture summary (profiles/), or None."""
+def ncu_step_kernel():
+    """The step kernel's committed ncu capture summary (profiles/) for this
+    workload, or {}."""
     path = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
     try:
         with open(path) as f:
             d = json.load(f)
         if d.get("L") == CONFIG["L"] and d.get("N") == CONFIG["N"]:
-            return float(d["dram_bytes_per_launch"])
+            return d
     except Exception:
         pass
-    return None
+    return {}
+
+
+def ncu_traffic():
+    """Per-launch DRAM bytes of the step kernel (ncu), or None."""
+    d = ncu_step_kernel()
+    return float(d["dram_bytes_per_launch"]) if "dram_bytes_per_launch" in d else None
+
+
+def issue_bound(launch_ms, spl, n, clocks):
+    """The roof that binds once temporal blocking removes HBM: integer
+    instruction issue.  Warp instructions per launch come from the ncu
+    capture (profiles/); the peak is 1 warp instruction per cycle per SMSP
+    (4 per SM) at the SM clock sampled during the timed region."""
+    d = ncu_step_kernel()
+    if "warp_inst_per_launch" not in d or not torch.cuda.is_available():
+        return None
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    mhz = clocks.get("sm_mhz") or 1965.0
+    peak = sms * 4 * mhz * 1e6
+    inst = d["warp_inst_per_launch"]
+    achieved = inst / (launch_ms / 1e3)
+    return {"unit": "warp-inst/s", "achieved": achieved, "peak": peak, "frac": achieved / peak,
+            "warp_inst_per_launch": inst, "thread_inst_per_update": inst * 32 / (n * spl),
+            "source": "ncu smsp__inst_executed.sum (" + d.get("source", "") + ") / live launch time"}
 
 
 class ClockSampler:
@@ -316,6 +340,7 @@ def run_ours(args, rank, world, local_rank):
                          "note": "temporal blocking: the state crosses HBM once per "
                                  f"{spl} steps, so frac > 1 vs the per-step roofline; "
                                  "the kernel is integer-issue bound (DESIGN.md 4.2)"},
+            "issue_bound": issue_bound(launch_ms, spl, N, clk.summary()),
             "e2e": {"value": e2e_value, "unit": "car-updates/s", "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
                     "breakdown_ms_rank0": {k: round(v, 2) for k, v in e2e_parts.items()},

@@ -102,6 +102,7 @@ def main():
         with open(os.path.join(os.path.dirname(a.out), "ncu_step_kernel.json"), "w") as f:
             json.dump({"L": a.L, "N": a.N, "steps_per_launch": a.steps_per_launch,
                        "kernel": d["kernel"], "dram_bytes_per_launch": d["dram_bytes"],
+                       "warp_inst_per_launch": float(d["smsp__inst_executed.sum"]["value"]),
                        "seconds_per_launch_under_ncu": d["seconds"],
                        "source": os.path.basename(a.out) + ".json"}, f, indent=1)
     print(open(a.out + ".md").read())
