@@ -134,6 +134,16 @@ nasch_status nasch_sim_set_state(nasch_sim* sim, const uint64_t* positions,
 nasch_status nasch_sim_set_state32(nasch_sim* sim, const uint32_t* positions,
                                    const uint32_t* velocities, size_t count);
 
+/* nasch_sim_state (reference nasch.h:115-118) split in two: _async copies
+ * the current state on the device and returns; the host transfer and
+ * widening into the caller's arrays proceed while the caller advances the
+ * simulation, and are complete when nasch_sim_state_wait returns.  At most
+ * one snapshot is in flight (a second _async waits for the first).  The
+ * arrays must stay valid until the wait. */
+nasch_status nasch_sim_state_async(nasch_sim* sim, uint64_t* positions,
+                                   uint64_t* velocities, size_t capacity);
+nasch_status nasch_sim_state_wait(nasch_sim* sim);
+
 /* The per-step trajectory checksum needs every step's state on the host
  * (serial FNV-1a, engine.cpp:173-181).  On by default, as in the
  * reference; pass 0 to stop folding further steps (checksum() then keeps

@@ -67,6 +67,8 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_physical_cores": (C.c_uint, []),
     # B200 extensions
     "nasch_sim_set_state": (C.c_int, [_P, _u64p, _u64p, C.c_size_t]),
+    "nasch_sim_state_async": (C.c_int, [_P, _u64p, _u64p, C.c_size_t]),
+    "nasch_sim_state_wait": (C.c_int, [_P]),
     "nasch_sim_set_state32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t]),
     "nasch_sim_set_checksum": (C.c_int, [_P, C.c_int]),
     "nasch_sim_sumv_series": (C.c_int, [_P, _u64p, C.c_size_t, _szp]),

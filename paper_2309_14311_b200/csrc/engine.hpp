@@ -48,6 +48,11 @@ class RingEngine {
   virtual void observables(double* density, double* mean_velocity, double* flow) = 0;
   // Rank (increasing position) order, widened to u64; either may be null.
   virtual void state(uint64_t* positions, uint64_t* velocities) = 0;
+  // Extension: the same snapshot, returned before the host-side copy and
+  // widening are done (they overlap the caller's next advance); the output
+  // arrays are complete after state_wait().  Default: synchronous.
+  virtual void state_async(uint64_t* positions, uint64_t* velocities) { state(positions, velocities); }
+  virtual void state_wait() {}
   // Extension: exact velocity sum / wrap count after each completed step.
   virtual size_t sumv_series(uint64_t* out, size_t cap) = 0;
   virtual size_t wrap_series(uint64_t* out, size_t cap) = 0;
@@ -82,6 +87,8 @@ class GpuRing : public RingEngine {
   const SimParams& params() const override;
   void observables(double* density, double* mean_velocity, double* flow) override;
   void state(uint64_t* positions, uint64_t* velocities) override;
+  void state_async(uint64_t* positions, uint64_t* velocities) override;
+  void state_wait() override;
   size_t sumv_series(uint64_t* out, size_t cap) override;
   size_t wrap_series(uint64_t* out, size_t cap) override;
   void set_checksum(bool enabled) override;

@@ -199,6 +199,19 @@ class Engine:
         _check(_lib().nasch_sim_state(self._h, _u64p(x), _u64p(v), self.ncars))
         return x, v
 
+    def snapshot_async(self, out_x, out_v) -> None:
+        """Start a snapshot into (out_x, out_v) (u64, length ncars) that
+        completes while the caller advances; call snapshot_wait() before
+        reading the arrays (nasch_sim_state_async)."""
+        assert out_x.dtype == np.uint64 and out_v.dtype == np.uint64
+        assert out_x.flags.c_contiguous and out_v.flags.c_contiguous
+        self._pending = (out_x, out_v)  # keep the buffers alive
+        _check(_lib().nasch_sim_state_async(self._h, _u64p(out_x), _u64p(out_v), self.ncars))
+
+    def snapshot_wait(self) -> None:
+        _check(_lib().nasch_sim_state_wait(self._h))
+        self._pending = None
+
     def observables(self) -> tuple[float, float, float]:
         """(density, mean_velocity, flow) as nasch_sim_observables."""
         d, m, f = C.c_double(), C.c_double(), C.c_double()

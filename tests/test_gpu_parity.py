@@ -540,3 +540,31 @@ def test_distributed_resident_frames(tmp_path, k_env):
         outs.append((f.read_bytes(), e.checksum))
         e.close()
     assert outs[0] == outs[1]
+
+
+def test_async_snapshots_match_sync(port):
+    """nasch_sim_state_async: snapshots taken while the ring keeps stepping
+    equal the synchronous ones (TB and DR rings), and the final state is
+    unaffected."""
+    for (L, N) in [(2_000_000, 600_000), (60_000, 20_000)]:
+        x0, v0 = nasch.fill_uniform_state(L, N, 5, 4)
+        ref = nasch.Engine(params(L, N, 5, 0.3, 200, 8))
+        ref.set_checksum(False)
+        ref.set_state(x0, v0)
+        e = nasch.Engine(params(L, N, 5, 0.3, 200, 8))
+        e.set_checksum(False)
+        e.set_state(x0, v0)
+        bufs = [(np.empty(N, np.uint64), np.empty(N, np.uint64)) for _ in range(2)]
+        for i in range(5):
+            e.advance(40)
+            ref.advance(40)
+            if i:
+                e.snapshot_wait()
+                px, pv = bufs[(i - 1) % 2]
+                assert (px == want[0]).all() and (pv == want[1]).all(), (N, i)
+            want = ref.snapshot()
+            e.snapshot_async(*bufs[i % 2])
+        e.snapshot_wait()
+        assert (bufs[0][0] == want[0]).all() and (bufs[0][1] == want[1]).all()
+        x, v = e.snapshot()
+        assert (x == want[0]).all() and (v == want[1]).all()

@@ -51,17 +51,28 @@ def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None,
     e.advance(8)  # warm-up
     snaps = []
     if snapshot_every:
-        sx = np.empty(N, np.uint64)
-        sv = np.empty(N, np.uint64)
+        # double-buffered snapshots: snapshot i is copied on the device and
+        # widened on the host while the next advance runs
+        bufs = [(np.empty(N, np.uint64), np.empty(N, np.uint64)) for _ in range(2)]
+        for bx, bv in bufs:  # fault the pages in outside the timed region
+            bx.fill(0)
+            bv.fill(0)
+        e.snapshot_async(*bufs[1])  # allocates the staging buffers once
+        e.snapshot_wait()
 
         def body():
-            done = 0
+            done, i = 0, 0
             while done < T:
                 k = min(snapshot_every, T - done)
                 e.advance(k)
-                e.snapshot(out_x=sx, out_v=sv)
-                snaps.append(int(sx[-1]))
+                if i:
+                    e.snapshot_wait()
+                    snaps.append(int(bufs[(i - 1) % 2][0][-1]))
+                e.snapshot_async(*bufs[i % 2])
+                i += 1
                 done += k
+            e.snapshot_wait()
+            snaps.append(int(bufs[(i - 1) % 2][0][-1]))
     else:
         def body():
             e.enqueue(T)
