@@ -179,10 +179,14 @@ struct GpuRing::Impl {
     } else if (tb) {
       if (vbytes == 1) launch_tb<uint8_t>(k); else launch_tb<uint32_t>(k);
     } else if (resident) {
+      // Block width by ring size: a per-step barrier across 32 warps costs
+      // more than a few extra cars per thread on a tiny ring (C1: 200 cars).
       if (vbytes == 1) {
-        ring_resident_kernel<uint8_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
+        if (n <= 256) ring_resident_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args, k);
+        else ring_resident_kernel<uint8_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
       } else {
-        ring_resident_kernel<uint32_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
+        if (n <= 256) ring_resident_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args, k);
+        else ring_resident_kernel<uint32_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
       }
     } else {
       if (vbytes == 1) {

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
   const int b = static_cast<int>(ctl->buf);
   uint32_t* X = xbuf(ra, b);
   VT* V = vbuf_w<VT>(ra, b);
-  if (tid < 256) apw[tid] = powmod(kA, tid);
+  for (uint32_t i = tid; i < 256; i += TPB) apw[i] = c_pow.lin[i];
   for (uint32_t i = tid; i < N; i += TPB) {
     sx[i] = X[i];
     sv[i] = static_cast<uint32_t>(V[i]);
