@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
   }
   __shared__ uint32_t s_W[kPlanCap], s_E[kPlanCap], s_E2[kPlanCap], s_ck[kPlanCap];
   __shared__ uint32_t s_head[NW][2 * kDrHalo];  // each warp tile's first cars, for the warp behind
-  __shared__ Acc s_acc[kDrKMax][TPB];
+  __shared__ Acc s_wacc[kDrKMax][NW];  // per-warp, per-step velocity sums
   Ctl* ctl = ra.ctl;
   DrSync* sync = da.sync;
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
@@ -308,8 +308,7 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
   const bool own_all = own == (1u << CPT) - 1u;
   const bool nowrap = base + CPT <= N;  // ids of this thread's cars run consecutively
   const uint32_t nE = (steps + da.K - 1) / da.K;
-#pragma unroll
-  for (int j = 0; j < int(kDrKMax); ++j) s_acc[j][threadIdx.x] = 0;
+  for (uint32_t i = threadIdx.x; i < kDrKMax * NW; i += TPB) (&s_wacc[0][0])[i] = 0;
   for (uint32_t e = 0; e < nE; ++e) {
     const uint32_t k = min(da.K, steps - e * da.K);
     const uint64_t te = t0 + uint64_t(e) * da.K;
@@ -386,14 +385,15 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
             v[c] = static_cast<uint32_t>(max(vc + dec, 0));
             x[c] += v[c];
           }
+          uint32_t sum = 0;
           if (own_all) {
-            s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+            sum = VSum<uint32_t, CPT>::sum(v);
           } else if (own) {
-            Acc sum = 0;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
-            s_acc[j][threadIdx.x] += sum;
           }
+          sum = __reduce_add_sync(0xffffffffu, sum);
+          if (lane == 0) s_wacc[j][warp] = sum;
         } else {
           // Any car: seam side per car (precomputed multipliers), headway
           // and position modulo L as unsigned min's (L < 2^31).
@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
             sum += mine ? v[c] : 0u;
             crs += (mine && xs >= L) ? 1u : 0u;
           }
-          s_acc[j][threadIdx.x] += sum;
+          const uint32_t ws = __reduce_add_sync(0xffffffffu, static_cast<uint32_t>(sum));
+          if (lane == 0) s_wacc[j][warp] = ws;
           crs = __reduce_add_sync(0xffffffffu, crs);
           if (lane == 0 && crs) atomicAdd(&ra.rec[(te + j) % kRecCap].c, crs);
         }
@@ -466,17 +467,13 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
       }
     }
     __syncthreads();
-    for (uint32_t j = warp; j < k; j += NW) {
+    if (threadIdx.x < k) {
       unsigned long long acc = 0;
 #pragma unroll
-      for (int q = 0; q < TPB / 32; ++q) acc += s_acc[j][lane + 32 * q];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (lane == 0 && acc) atomicAdd(&ra.rec[(te + j) % kRecCap].sumv, acc);
+      for (int w = 0; w < NW; ++w) acc += s_wacc[threadIdx.x][w];
+      if (acc) atomicAdd(&ra.rec[(te + threadIdx.x) % kRecCap].sumv, acc);
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < int(kDrKMax); ++j) s_acc[j][threadIdx.x] = 0;
     if (threadIdx.x == 0) {
       st_release_u32(&sync->flags[g], e + 1);
       if (g == 0) DR_TRACE(e, 2);

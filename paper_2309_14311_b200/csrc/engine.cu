@@ -89,6 +89,7 @@ struct GpuRing::Impl {
   bool medium = false;    // TB with 512-car tiles (medium rings)
   bool dr = false;        // distributed-resident medium ring (dr_kernel.cuh)
   uint32_t dr_G = 0, dr_cpt = 0;
+  int dr_geom = 0;  // index into kDrGeoms
   Ctl* dplans = nullptr;
   DrSync* dsync = nullptr;
   uint32_t* dmbox = nullptr;
@@ -147,19 +148,21 @@ struct GpuRing::Impl {
   StepRec* hrec = nullptr;
   Ctl* hctl = nullptr;
 
-  template <typename VT, int CPT>
+  template <typename VT, int TPB, int CPT>
   void launch_dr_cpt(uint32_t k) {
     DrArgs da{dplans, dmbox, dsync, dseg, dr_G, K};
     void* kargs[] = {&args, &da, &k};
     CK(cudaMemsetAsync(dsync, 0, (2 + dr_G) * sizeof(unsigned int), stream));
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, kDrTPB, CPT>),
-                                   dim3(dr_G + 1), dim3(kDrTPB), kargs, 0, stream));
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, TPB, CPT>),
+                                   dim3(dr_G + 1), dim3(TPB), kargs, 0, stream));
   }
   template <typename VT>
   void launch_dr(uint32_t k) {
-    if (dr_cpt == 4) launch_dr_cpt<VT, 4>(k);
-    else if (dr_cpt == 8) launch_dr_cpt<VT, 8>(k);
-    else launch_dr_cpt<VT, 16>(k);
+    switch (dr_geom) {
+      case 0: launch_dr_cpt<VT, kDrTPB, 4>(k); break;
+      case 1: launch_dr_cpt<VT, kDrTPB, 8>(k); break;
+      default: launch_dr_cpt<VT, kDrTPB, 16>(k); break;
+    }
   }
 
   template <typename VT>
@@ -575,15 +578,22 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
     // balanced, 16-aligned segments of at least kDrHalo cars (N >= 256 G)
     const uint32_t segsz = (d.n + Gw - 1) / Gw + 16;  // largest segment
     uint32_t cptd = 0;
-    const uint32_t cap[3] = {dr_capacity<kDrTPB, 4>(), dr_capacity<kDrTPB, 8>(), dr_capacity<kDrTPB, 16>()};
-    for (int i = 0; i < 3 && !cptd; ++i)
-      if (segsz <= cap[i]) cptd = 4u << i;
+    // cars per thread by segment size, smallest capacity first (512-thread
+    // blocks with 4 or 8 cars per thread measured 3-4 % slower on C2);
+    // NASCH_B200_DR_GEOM forces one (index) for experiments
+    struct G2 { int tpb; uint32_t cpt; uint32_t cap; const void* fn; };
+    const G2 geoms[3] = {
+        {kDrTPB, 4, dr_capacity<kDrTPB, 4>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)},
+        {kDrTPB, 8, dr_capacity<kDrTPB, 8>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)},
+        {kDrTPB, 16, dr_capacity<kDrTPB, 16>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>)}};
+    const long gforce = env_long("NASCH_B200_DR_GEOM", -1);
+    int gi = -1;
+    for (int i = 0; i < 3; ++i)
+      if ((gforce < 0 || gforce == i) && gi < 0 && segsz <= geoms[i].cap) gi = i;
+    if (gi >= 0) cptd = geoms[gi].cpt;
     if (coop && sms >= 2 && cptd && Kd >= 2 && d.vbytes == 1 && uint64_t(d.L) > 2ull * Kd * d.vmax_eff) {
       int occ = 0;
-      const void* fn = cptd == 4 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)
-                     : cptd == 8 ? reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)
-                                 : reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>);
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kDrTPB, 0));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, geoms[gi].fn, geoms[gi].tpb, 0));
       const uint32_t G = Gw;
       if (occ >= 1 && G + 1 <= uint32_t(sms) * uint32_t(occ)) {
         d.dr = true;
@@ -591,6 +601,7 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
         d.K = Kd;
         d.dr_G = G;
         d.dr_cpt = cptd;
+        d.dr_geom = gi;
         for (uint32_t g = 0; g < G; ++g) dr_seg.push_back(static_cast<uint32_t>(uint64_t(g) * d.n / G) & ~15u);
         dr_seg.push_back(d.n);
       }
