@@ -83,22 +83,35 @@ __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const V
     apB[c] = mulmod(a, ra.an_inv) << 1;      // at or past it: E a^(id-N)
   }
   const uint32_t an_inv2 = ra.an_inv << 1;
+  uint32_t rear = 0;  // bit c: slot counts toward the step's crossings
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) rear |= (lane * CPW + c < M) ? (1u << c) : 0u;
+  // E_{j+1} = E_j * a^c_j [* a^N unless W wraps]: lane l precomputes the
+  // candidate for c_j = l while the cars move, so the chain after the
+  // crossing count is one shuffle (c_j >= 32 or a wrap: the table path).
+  const uint32_t candm = kTabN ? tab.step2[kConeSlots + lane] : 0u;
+  const uint32_t an2 = ra.an << 1;
   uint32_t Wj = W, Wofs = W;
   uint32_t rW = 0, rE = 0, rE2 = 0, rc = 0;  // lane j keeps plan step ofs + j
   for (uint32_t j = 0; j < kk; ++j) {
     const uint32_t bound = N - Wj;
     uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
     if (lane == 31) xn = x[CPW - 1];
+    const uint32_t cand = kTabN ? mulmod_x2(candm, E) : mulmod_x2(an2, mulmod_x2(tab.step2[lane], E));
     uint32_t cnt = 0;
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
-      const uint32_t i = lane * CPW + c;
       const uint32_t s = mulmod_x2(idv[c] < bound ? apA[c] : apB[c], E);
       const uint32_t xl = (c + 1 < CPW) ? x[c + 1] : xn;
-      uint32_t xnew, cr;
-      v[c] = car_rule(x[c], xl, v[c], s, L, vmax, tp, xnew, cr);
-      x[c] = xnew;
-      cnt += (i < M && cr) ? 1u : 0u;
+      // car_rule with the modular headway / position as unsigned min's
+      uint32_t d = xl - x[c];
+      d = min(d, d + L);
+      const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+      const int vn = max(vc - (s < tp ? 1 : 0), 0);
+      v[c] = static_cast<uint32_t>(vn);
+      const uint32_t xs = x[c] + v[c];
+      x[c] = min(xs, xs - L);
+      cnt += ((rear >> c) & 1u) && xs >= L ? 1u : 0u;
     }
     const uint32_t cj = __reduce_add_sync(0xffffffffu, cnt);
     if (j == ofs) Wofs = Wj;
@@ -111,11 +124,14 @@ __device__ uint32_t cone_warp_run(const RingArgs& ra, const uint32_t* X, const V
     uint32_t Wn = Wj + cj;
     const bool wrap = Wn >= N;
     if (wrap) Wn -= N;
-    if (kTabN) {
+    const uint32_t fast = __shfl_sync(0xffffffffu, cand, cj & 31u);
+    if (cj < 32 && !wrap) {
+      E = fast;
+    } else if (kTabN) {
       E = mulmod_x2(tab.step2[cj + (wrap ? 0u : kConeSlots)], E);  // cj <= M < kConeSlots
     } else {  // table without the a^N half (cone_tab_fill_lin)
       E = mulmod_x2(tab.step2[cj], E);
-      if (!wrap) E = mulmod_x2(ra.an << 1, E);
+      if (!wrap) E = mulmod_x2(an2, E);
     }
     Wj = Wn;
     if (j + 1 == ofs + kout) break;
@@ -158,6 +174,143 @@ __device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V
   if (C <= 128) return cone_warp_run<VT, 4, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
   if (C <= 256) return cone_warp_run<VT, 8, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
   return cone_warp_run<VT, 16, kTabN>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+}
+
+// ---- four-warp variant ------------------------------------------------------
+//
+// The same cone simulation spread over 4 warps (128 threads, CPW slots each),
+// synchronised by one named barrier per step: a lone warp issues every car
+// of the cone itself and is issue-latency bound (~250 ns per step); four
+// warps share the cars and each carries the short per-step bookkeeping
+// (count -> E) redundantly.  Per step each warp publishes its crossing count
+// and its first car's new position in parity-alternating slots.
+constexpr int kConeMwThreads = 128;
+
+__device__ __forceinline__ void cone_mw_bar() {
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
+template <typename VT, int CPW>
+__device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
+                                uint32_t kk, uint32_t M, uint32_t ofs, uint32_t kout, Ctl* out,
+                                const ConeTab& tab) {
+  __shared__ uint32_t s_cnt[2][4], s_lead[2][4], s_pow[2];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint32_t C = M + kk;
+  const uint32_t id0 = cone_slot_id(N, W, M, 0);
+  if (warp < 2) {
+    const uint32_t r = warp == 0 ? powmod_warp(id0) : powmod_warp(draw_exponent(t, N, W));
+    if (lane == 0) s_pow[warp] = r;
+  }
+  uint32_t x[CPW], v[CPW], apA[CPW], apB[CPW], idv[CPW];
+  cone_mw_bar();
+  const uint32_t aid0 = s_pow[0];
+  uint32_t E = mulmod(ra.s0, s_pow[1]);
+  uint32_t rear = 0;
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const uint32_t i = tid * CPW + c;
+    const bool act = i < C;
+    uint32_t id = id0 + (act ? i : 0u);
+    const bool wrapped = id >= N;
+    if (wrapped) id -= N;
+    idv[c] = id;
+    x[c] = act ? __ldcg(X + id) : 0u;
+    v[c] = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+    uint32_t a = mulmod(aid0, tab.lin[act ? i : 0u]);
+    if (wrapped) a = mulmod(a, ra.an_inv);
+    apA[c] = a << 1;
+    apB[c] = mulmod(a, ra.an_inv) << 1;
+    rear |= (i < M) ? (1u << c) : 0u;
+  }
+  if (lane == 0) s_lead[0][warp] = x[0];
+  cone_mw_bar();
+  const uint32_t an_inv2 = ra.an_inv << 1;
+  const uint32_t candm = tab.step2[kConeSlots + lane];
+  uint32_t Wj = W, Wofs = W;
+  uint32_t rW = 0, rE = 0, rE2 = 0, rc = 0;  // warp 0, lane j: plan step ofs + j
+  for (uint32_t j = 0; j < kk; ++j) {
+    const uint32_t par = j & 1u;
+    const uint32_t bound = N - Wj;
+    uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+    if (lane == 31) xn = warp < 3 ? s_lead[par][warp + 1] : x[CPW - 1];
+    const uint32_t cand = mulmod_x2(candm, E);
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      const uint32_t s = mulmod_x2(idv[c] < bound ? apA[c] : apB[c], E);
+      const uint32_t xl = (c + 1 < CPW) ? x[c + 1] : xn;
+      uint32_t d = xl - x[c];
+      d = min(d, d + L);
+      const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+      const int vn = max(vc - (s < tp ? 1 : 0), 0);
+      v[c] = static_cast<uint32_t>(vn);
+      const uint32_t xs = x[c] + v[c];
+      x[c] = min(xs, xs - L);
+      cnt += ((rear >> c) & 1u) && xs >= L ? 1u : 0u;
+    }
+    const uint32_t wc = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) {
+      s_cnt[par][warp] = wc;
+      s_lead[par ^ 1u][warp] = x[0];
+    }
+    cone_mw_bar();
+    const uint32_t cj = s_cnt[par][0] + s_cnt[par][1] + s_cnt[par][2] + s_cnt[par][3];
+    if (j == ofs) Wofs = Wj;
+    if (warp == 0 && j >= ofs && lane == j - ofs) {
+      rW = Wj;
+      rE = E;
+      rE2 = mulmod_x2(an_inv2, E);
+      rc = cj;
+    }
+    uint32_t Wn = Wj + cj;
+    const bool wrap = Wn >= N;
+    if (wrap) Wn -= N;
+    const uint32_t fast = __shfl_sync(0xffffffffu, cand, cj & 31u);
+    E = (cj < 32 && !wrap) ? fast : mulmod_x2(tab.step2[cj + (wrap ? 0u : kConeSlots)], E);
+    Wj = Wn;
+    if (j + 1 == ofs + kout) break;
+  }
+  if (warp == 0) {
+    if (lane < kout) {
+      out->Wk[lane] = rW;
+      out->Ek[lane] = rE;
+      out->E2k[lane] = rE2;
+      out->ck[lane] = rc;
+    }
+    if (lane == 0) {
+      out->kplan = kout;
+      out->E = rE;
+      out->E2 = rE2;
+    }
+  }
+  return Wofs;
+}
+
+// Entry for threads 0..127 of a block (tables with the a^N half).
+template <typename VT>
+__device__ uint32_t cone_mw(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
+                            uint32_t kk, uint32_t ofs, uint32_t kout, Ctl* out, const ConeTab& tab) {
+  __shared__ uint32_t s_m[4];
+  const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
+  const uint32_t N = ra.n, L = ra.L;
+  const uint32_t Mmax = kk * ra.vmax;
+  const uint32_t id0 = cone_slot_id(N, W, Mmax, 0);
+  uint32_t cnt = 0;
+  for (uint32_t i = tid; i < Mmax; i += kConeMwThreads) {
+    uint32_t id = id0 + i;
+    if (id >= N) id -= N;
+    cnt += __ldcg(X + id) >= L - Mmax ? 1u : 0u;
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  if (lane == 0) s_m[warp] = cnt;
+  cone_mw_bar();
+  const uint32_t M = s_m[0] + s_m[1] + s_m[2] + s_m[3];
+  const uint32_t C = M + kk;
+  if (C <= 128) return cone_mw_run<VT, 1>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 256) return cone_mw_run<VT, 2>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  return cone_mw_run<VT, 4>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
 }
 
 }  // namespace nb200

@@ -215,8 +215,8 @@ __device__ void dr_planner(const RingArgs& ra, const DrArgs& da, const uint32_t 
     const int be = (b0 + static_cast<int>(e)) & 1;
     Ctl* dst = da.plans + ((e + 1) & 1u);
     uint32_t Wn = 0;
-    if (threadIdx.x < 32)
-      Wn = cone_warp<VT>(ra, xbuf(ra, be), vbuf<VT>(ra, be), te, We, k + K, k, K, dst, s_tab);
+    if (threadIdx.x < kConeMwThreads)
+      Wn = cone_mw<VT>(ra, xbuf(ra, be), vbuf<VT>(ra, be), te, We, k + K, k, K, dst, s_tab);
     const uint64_t tn = te + k;
     for (uint32_t j = threadIdx.x; j < K; j += TPB) {
       StepRec* r = ra.rec + ((tn + j) % kRecCap);

@@ -566,8 +566,8 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // (NASCH_B200_DR=0 disables it).
   std::vector<uint32_t> dr_seg;
   if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 1) != 0) {
-    // 16-step epochs: at 32 the 64-step pipelined cone outlasts an epoch
-    const long kreq_dr = env_long("NASCH_B200_K", 16);
+    // 32-step epochs (C2: 4.0e11 vs 3.4e11 at 16 with the four-warp cone)
+    const long kreq_dr = env_long("NASCH_B200_K", kDrKMax);
     uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq_dr, kDrKMax)));
     // the planner simulates 2K-step cones of 2K*(vmax+1) <= 512 cars; the
     // initial plan is one 256-thread block's K-step cone
