@@ -194,7 +194,8 @@ template <typename VT, int CPW>
 __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
                                 uint32_t kk, uint32_t M, uint32_t ofs, uint32_t kout, Ctl* out,
                                 const ConeTab& tab) {
-  __shared__ uint32_t s_cnt[2][4], s_lead[2][4], s_pow[2];
+  __shared__ uint4 s_cnt[2];  // per-warp crossing counts, one 16-byte load
+  __shared__ uint32_t s_lead[2][4], s_pow[2];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
   const uint32_t C = M + kk;
@@ -250,13 +251,15 @@ __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT*
       x[c] = min(xs, xs - L);
       cnt += ((rear >> c) & 1u) && xs >= L ? 1u : 0u;
     }
-    const uint32_t wc = __reduce_add_sync(0xffffffffu, cnt);
+    const uint32_t wc = CPW == 1 ? __popc(__ballot_sync(0xffffffffu, cnt != 0))
+                                 : __reduce_add_sync(0xffffffffu, cnt);
     if (lane == 0) {
-      s_cnt[par][warp] = wc;
+      reinterpret_cast<uint32_t*>(&s_cnt[par])[warp] = wc;
       s_lead[par ^ 1u][warp] = x[0];
     }
     cone_mw_bar();
-    const uint32_t cj = s_cnt[par][0] + s_cnt[par][1] + s_cnt[par][2] + s_cnt[par][3];
+    const uint4 c4 = s_cnt[par];
+    const uint32_t cj = (c4.x + c4.y) + (c4.z + c4.w);
     if (j == ofs) Wofs = Wj;
     if (warp == 0 && j >= ofs && lane == j - ofs) {
       rW = Wj;
