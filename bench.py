@@ -82,6 +82,7 @@ def issue_bound(launch_ms, spl, n, clocks):
     instruction issue.  Warp instructions per launch come from the ncu
     capture (profiles/); the peak is 1 warp instruction per cycle per SMSP
     (4 per SM) at the SM clock sampled during the timed region."""
+    import torch
     d = ncu_step_kernel()
     if "warp_inst_per_launch" not in d or not torch.cuda.is_available():
         return None

@@ -18,9 +18,11 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "engine.hpp"
+#include "host_simd.hpp"
 #include "minstd.hpp"
 #include "step_kernels.cuh"
 #include "tb_config.hpp"
@@ -482,15 +484,19 @@ struct GpuRing::Impl {
       const size_t c1 = std::min<size_t>(n, c0 + kChunk);
       parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
         int e = 0;
-        for (size_t i = c0 + a; i < c0 + b && !e; ++i) {
-          const uint64_t xi = hx_in[i], vi = hv_in[i];
-          if (xi >= L) e = 1;
-          else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
-          else if (vi > params.v_max) e = 3;
-          else if (vi > vlim) e = 4;
-          hx[i] = static_cast<uint32_t>(xi);
-          if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
-          else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
+        if constexpr (std::is_same<T, uint64_t>::value) {
+          e = narrow_validate(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, hx, hv, vbytes);
+        } else {
+          for (size_t i = c0 + a; i < c0 + b && !e; ++i) {
+            const uint64_t xi = hx_in[i], vi = hv_in[i];
+            if (xi >= L) e = 1;
+            else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
+            else if (vi > params.v_max) e = 3;
+            else if (vi > vlim) e = 4;
+            hx[i] = static_cast<uint32_t>(xi);
+            if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
+            else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
+          }
         }
         if (e) {
           int expected = 0;
@@ -835,10 +841,11 @@ void GpuRing::state(uint64_t* positions, uint64_t* velocities) {
       parallel_chunks(p.r1 - p.r0, [&](size_t lo, size_t hi) {
         lo += p.r0;
         hi += p.r0;
-        if (positions)
-          for (size_t i = lo; i < hi; ++i) positions[i] = d.hx[i];
-        if (velocities)
-          for (size_t i = lo; i < hi; ++i) velocities[i] = d.hvel(i);
+        if (positions) widen_u32(d.hx + lo, positions + lo, hi - lo);
+        if (velocities) {
+          if (d.vbytes == 1) widen_u8(static_cast<const uint8_t*>(d.hv) + lo, velocities + lo, hi - lo);
+          else widen_u32(static_cast<const uint32_t*>(d.hv) + lo, velocities + lo, hi - lo);
+        }
       });
     }
     cudaEventDestroy(p.ev);
@@ -899,13 +906,10 @@ void GpuRing::state_async(uint64_t* positions, uint64_t* velocities) {
           parallel_chunks(pc.r1 - pc.r0, [&](size_t lo, size_t hi) {
             lo += pc.r0;
             hi += pc.r0;
-            if (positions)
-              for (size_t i = lo; i < hi; ++i) positions[i] = d.snap_hx[i];
+            if (positions) widen_u32(d.snap_hx + lo, positions + lo, hi - lo);
             if (velocities) {
-              if (vbytes == 1)
-                for (size_t i = lo; i < hi; ++i) velocities[i] = static_cast<const uint8_t*>(d.snap_hv)[i];
-              else
-                for (size_t i = lo; i < hi; ++i) velocities[i] = static_cast<const uint32_t*>(d.snap_hv)[i];
+              if (vbytes == 1) widen_u8(static_cast<const uint8_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
+              else widen_u32(static_cast<const uint32_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
             }
           });
         }

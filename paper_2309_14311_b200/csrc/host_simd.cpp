@@ -1,0 +1,150 @@
+// host_simd.cpp -- see host_simd.hpp.  AVX-512 paths are selected at run
+// time (__builtin_cpu_supports); the scalar loops are the reference
+// semantics and the fallback.
+#include "host_simd.hpp"
+
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+
+namespace nb200 {
+
+namespace {
+
+void widen_u32_scalar(const uint32_t* src, uint64_t* dst, size_t n) {
+  for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+void widen_u8_scalar(const uint8_t* src, uint64_t* dst, size_t n) {
+  for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
+#if defined(__x86_64__)
+bool have_avx512() {
+  static const bool ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
+  return ok;
+}
+
+__attribute__((target("avx512f,avx512bw"))) void widen_u32_avx512(const uint32_t* src, uint64_t* dst, size_t n) {
+  size_t i = 0;
+  // scalar head until dst is 64-byte aligned (streaming stores need it)
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 63u)) {
+    dst[i] = src[i];
+    ++i;
+  }
+  for (; i + 16 <= n; i += 16) {
+    const __m512i s = _mm512_loadu_si512(reinterpret_cast<const void*>(src + i));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), _mm512_cvtepu32_epi64(_mm512_castsi512_si256(s)));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 8),
+                        _mm512_cvtepu32_epi64(_mm512_extracti64x4_epi64(s, 1)));
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
+
+__attribute__((target("avx512f,avx512bw"))) void widen_u8_avx512(const uint8_t* src, uint64_t* dst, size_t n) {
+  size_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 63u)) {
+    dst[i] = src[i];
+    ++i;
+  }
+  for (; i + 16 <= n; i += 16) {
+    const __m128i s = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), _mm512_cvtepu8_epi64(s));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 8), _mm512_cvtepu8_epi64(_mm_srli_si128(s, 8)));
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
+
+// 8 cars at a time: narrow with vpmovqd / vpmovqb, rules as masks.
+__attribute__((target("avx512f,avx512bw"))) int narrow_avx512(const uint64_t* x, const uint64_t* v, size_t lo,
+                                                              size_t hi, uint64_t L, uint64_t vmax,
+                                                              uint64_t vlim, uint32_t* x32, void* vout,
+                                                              int vbytes) {
+  const __m512i vL = _mm512_set1_epi64(static_cast<long long>(L));
+  const __m512i vVmax = _mm512_set1_epi64(static_cast<long long>(vmax));
+  const __m512i vVlim = _mm512_set1_epi64(static_cast<long long>(vlim));
+  size_t i = lo;
+  // the first car has no predecessor: scalar until x[i-1] exists
+  for (; i < hi && i == 0; ++i) {
+    const uint64_t xi = x[i], vi = v[i];
+    if (xi >= L) return 1;
+    if (vi > vmax) return 3;
+    if (vi > vlim) return 4;
+    x32[i] = static_cast<uint32_t>(xi);
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
+    else static_cast<uint32_t*>(vout)[i] = static_cast<uint32_t>(vi);
+  }
+  for (; i + 8 <= hi; i += 8) {
+    const __m512i xs = _mm512_loadu_si512(reinterpret_cast<const void*>(x + i));
+    const __m512i vs = _mm512_loadu_si512(reinterpret_cast<const void*>(v + i));
+    const __m512i prevs = _mm512_loadu_si512(reinterpret_cast<const void*>(x + i - 1));  // i >= 1
+    const __mmask8 bad_l = _mm512_cmpge_epu64_mask(xs, vL);
+    const __mmask8 bad_inc = _mm512_cmple_epu64_mask(xs, prevs);
+    const __mmask8 bad_vmax = _mm512_cmpgt_epu64_mask(vs, vVmax);
+    const __mmask8 bad_vlim = _mm512_cmpgt_epu64_mask(vs, vVlim);
+    if (bad_l | bad_inc | bad_vmax | bad_vlim) {
+      // first offending car, first rule in the scalar order
+      for (size_t k = i; k < i + 8; ++k) {
+        if (x[k] >= L) return 1;
+        if (k && x[k - 1] >= x[k]) return 2;
+        if (v[k] > vmax) return 3;
+        if (v[k] > vlim) return 4;
+      }
+    }
+    _mm256_storeu_si256(reinterpret_cast<__m256i*>(x32 + i), _mm512_cvtepi64_epi32(xs));
+    if (vbytes == 1) {
+      _mm_storel_epi64(reinterpret_cast<__m128i*>(static_cast<uint8_t*>(vout) + i), _mm512_cvtepi64_epi8(vs));
+    } else {
+      _mm256_storeu_si256(reinterpret_cast<__m256i*>(static_cast<uint32_t*>(vout) + i), _mm512_cvtepi64_epi32(vs));
+    }
+  }
+  for (; i < hi; ++i) {
+    const uint64_t xi = x[i], vi = v[i];
+    if (xi >= L) return 1;
+    if (i && x[i - 1] >= xi) return 2;
+    if (vi > vmax) return 3;
+    if (vi > vlim) return 4;
+    x32[i] = static_cast<uint32_t>(xi);
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
+    else static_cast<uint32_t*>(vout)[i] = static_cast<uint32_t>(vi);
+  }
+  return 0;
+}
+#endif
+
+}  // namespace
+
+void widen_u32(const uint32_t* src, uint64_t* dst, size_t n) {
+#if defined(__x86_64__)
+  if (have_avx512() && n >= 64) return widen_u32_avx512(src, dst, n);
+#endif
+  widen_u32_scalar(src, dst, n);
+}
+
+void widen_u8(const uint8_t* src, uint64_t* dst, size_t n) {
+#if defined(__x86_64__)
+  if (have_avx512() && n >= 64) return widen_u8_avx512(src, dst, n);
+#endif
+  widen_u8_scalar(src, dst, n);
+}
+
+int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
+                    uint64_t vlim, uint32_t* x32, void* vout, int vbytes) {
+#if defined(__x86_64__)
+  if (have_avx512()) return narrow_avx512(x, v, lo, hi, L, vmax, vlim, x32, vout, vbytes);
+#endif
+  for (size_t i = lo; i < hi; ++i) {
+    const uint64_t xi = x[i], vi = v[i];
+    if (xi >= L) return 1;
+    if (i && x[i - 1] >= xi) return 2;
+    if (vi > vmax) return 3;
+    if (vi > vlim) return 4;
+    x32[i] = static_cast<uint32_t>(xi);
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
+    else static_cast<uint32_t*>(vout)[i] = static_cast<uint32_t>(vi);
+  }
+  return 0;
+}
+
+}  // namespace nb200
