@@ -75,6 +75,18 @@ __attribute__((target("avx512f,avx512bw"))) int narrow_avx512(const uint64_t* x,
     if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
     else static_cast<uint32_t*>(vout)[i] = static_cast<uint32_t>(vi);
   }
+  // scalar until i is a multiple of 8 (32-byte aligned non-temporal stores
+  // into the page-aligned staging)
+  for (; i < hi && (i & 7u); ++i) {
+    const uint64_t xi = x[i], vi = v[i];
+    if (xi >= L) return 1;
+    if (x[i - 1] >= xi) return 2;
+    if (vi > vmax) return 3;
+    if (vi > vlim) return 4;
+    x32[i] = static_cast<uint32_t>(xi);
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
+    else static_cast<uint32_t*>(vout)[i] = static_cast<uint32_t>(vi);
+  }
   for (; i + 8 <= hi; i += 8) {
     const __m512i xs = _mm512_loadu_si512(reinterpret_cast<const void*>(x + i));
     const __m512i vs = _mm512_loadu_si512(reinterpret_cast<const void*>(v + i));
@@ -92,13 +104,15 @@ __attribute__((target("avx512f,avx512bw"))) int narrow_avx512(const uint64_t* x,
         if (v[k] > vlim) return 4;
       }
     }
-    _mm256_storeu_si256(reinterpret_cast<__m256i*>(x32 + i), _mm512_cvtepi64_epi32(xs));
+    _mm256_stream_si256(reinterpret_cast<__m256i*>(x32 + i), _mm512_cvtepi64_epi32(xs));
     if (vbytes == 1) {
-      _mm_storel_epi64(reinterpret_cast<__m128i*>(static_cast<uint8_t*>(vout) + i), _mm512_cvtepi64_epi8(vs));
+      _mm_stream_si64(reinterpret_cast<long long*>(static_cast<uint8_t*>(vout) + i),
+                      _mm_cvtsi128_si64(_mm512_cvtepi64_epi8(vs)));
     } else {
-      _mm256_storeu_si256(reinterpret_cast<__m256i*>(static_cast<uint32_t*>(vout) + i), _mm512_cvtepi64_epi32(vs));
+      _mm256_stream_si256(reinterpret_cast<__m256i*>(static_cast<uint32_t*>(vout) + i), _mm512_cvtepi64_epi32(vs));
     }
   }
+  _mm_sfence();
   for (; i < hi; ++i) {
     const uint64_t xi = x[i], vi = v[i];
     if (xi >= L) return 1;
