@@ -568,3 +568,47 @@ def test_async_snapshots_match_sync(port):
         assert (bufs[0][0] == want[0]).all() and (bufs[0][1] == want[1]).all()
         x, v = e.snapshot()
         assert (x == want[0]).all() and (v == want[1]).all()
+
+
+def test_set_state_validation_rules_and_order():
+    """set_state rejects each rule at every position of the vectorised
+    narrowing (first car, inside an 8-car group, group boundary, tail) with
+    the first violation in car order and rule order x >= L, not increasing,
+    v > vmax, v > L-1; a rejected state leaves the ring untouched."""
+    L, N, vmax = 50_000, 20_000, 5
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 21)
+    x0 = x0.astype(np.uint64)
+    v0 = v0.astype(np.uint64)
+    e = nasch.Engine(params(L, N, vmax, 0.2, 50, 3))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.advance(5)
+    ref_x, ref_v = e.snapshot()
+    msgs = {1: "position out of range", 2: "strictly increasing", 3: "above vmax"}
+    for pos in (0, 1, 7, 8, 9, 15, 16, 4095, N // 2 + 3, N - 9, N - 1):
+        for rule in (1, 2, 3):
+            x, v = x0.copy(), v0.copy()
+            if rule == 1:
+                x[pos] = L + pos
+            elif rule == 2:
+                x[pos] = x[pos - 1] if pos else x[0]
+                if pos == 0:
+                    x[1] = x[0]  # car 1 not above car 0
+            else:
+                v[pos] = vmax + 1
+            with pytest.raises(nasch.NaschError) as ei:
+                e.set_state(x, v)
+            assert msgs[rule] in str(ei.value), (pos, rule, str(ei.value))
+    # earlier car wins over a later one; rule order within one car
+    x, v = x0.copy(), v0.copy()
+    v[100] = vmax + 1
+    x[200] = L
+    with pytest.raises(nasch.NaschError, match="above vmax"):
+        e.set_state(x, v)
+    x, v = x0.copy(), v0.copy()
+    x[300] = L
+    v[300] = vmax + 1
+    with pytest.raises(nasch.NaschError, match="out of range"):
+        e.set_state(x, v)
+    xs, vs = e.snapshot()
+    assert (xs == ref_x).all() and (vs == ref_v).all()
