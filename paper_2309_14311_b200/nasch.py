@@ -355,3 +355,22 @@ def nccl_unique_id() -> bytes:
 
 def physical_cores() -> int:
     return _lib().nasch_physical_cores()
+
+
+def partition_rings(ncars, world: int):
+    """Contiguous ring ranges for `world` ranks, balanced by total cars
+    (an ensemble shards with no communication while
+    stepping; N varies 10x across a density sweep, so equal ring counts would
+    not balance).  Returns [(lo, hi)] per rank; every ring in exactly one."""
+    n = np.asarray(ncars, dtype=np.int64)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    csum = np.concatenate([[0], np.cumsum(n)])
+    total = int(csum[-1])
+    cuts = [0]
+    for r in range(1, world):
+        # first ring whose start reaches r/world of the cars
+        cuts.append(int(np.searchsorted(csum, (total * r + world - 1) // world, side="left")))
+    cuts.append(len(n))
+    cuts = [min(max(c, cuts[i - 1] if i else 0), len(n)) for i, c in enumerate(cuts)]
+    return [(cuts[r], cuts[r + 1]) for r in range(world)]
