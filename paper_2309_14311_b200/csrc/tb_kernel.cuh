@@ -1,11 +1,14 @@
 // tb_kernel.cuh -- temporal-blocked NaSch step kernel (k <= 16 steps per
 // launch).  See step_kernels.cuh for the shared reformulation (ID order,
-// counter-based draws, integer threshold) and DESIGN.md section 4.2.
+// counter-based draws, integer threshold) and DESIGN.md section 4.1.
 //
-// Tile = LOAD consecutive cars (STORE owned + HALO ahead), held in registers
-// (CPT cars per thread) for all k steps; one __syncthreads per step hands
-// each warp's first position to the warp behind it.  Per step a thread takes
-// one of two paths:
+// Tiles of consecutive cars (owned + a HALO of cars ahead) are held in
+// registers (CPT cars per thread) for all k steps.  Warp tiles (WT, the
+// default for large rings): each warp owns 32*CPT - HALO cars with its own
+// halo and passes leaders by shuffle only -- no barrier inside the launch.
+// Block tiles (medium rings): one halo per block, one __syncthreads per
+// step hands each warp's first position to the warp behind it.  Per step a
+// thread takes one of two paths:
 //   plain  -- its cars cannot reach the origin within the launch
 //             (max x < L - k*vmax at tile start) and the rank seam is not at
 //             or inside its cars: gap = leader - x - 1, no mod L, no crossing
