@@ -382,9 +382,14 @@ struct GpuRing::Impl {
         enqueue_steps(chunk);
         left -= chunk;
         if (frame_due()) {
-          drain();
-          fetch_rank_order();
-          record_frame_staged();
+          // overlapped with the next chunk: device copy now, host copy and
+          // widening into the frame on the snapshot thread
+          frames.emplace_back();
+          Frame& f = frames.back();
+          f.step = steps_done;
+          f.positions.resize(n);
+          f.velocities.resize(n);
+          snap_start(f.positions.data(), f.velocities.data());
         }
       }
       if (sync) drain();
@@ -408,6 +413,74 @@ struct GpuRing::Impl {
     }
     if (sync) drain();
   }
+
+  // Starts an asynchronous rank-ordered snapshot into (positions,
+  // velocities): a device copy stream-ordered before any later step, then
+  // D2H + widening on a host thread (see GpuRing::state_async).
+  void snap_start(uint64_t* positions, uint64_t* velocities) {
+  Impl& d = *this;
+  d.snap_join();  // one snapshot in flight: the staging buffers are reused
+  d.drain();
+  if (!d.snap_x) {
+    CK(cudaMalloc(&d.snap_x, size_t(d.n) * 4));
+    CK(cudaMalloc(&d.snap_v, size_t(d.n) * d.vbytes));
+    CK(cudaMallocHost(&d.snap_hx, size_t(d.n) * 4));
+    CK(cudaMallocHost(&d.snap_hv, size_t(d.n) * d.vbytes));
+    CK(cudaStreamCreateWithFlags(&d.snap_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&d.snap_ready, cudaEventDisableTiming));
+  }
+  const int cur = static_cast<int>(d.buf_host);
+  CK(cudaMemcpyAsync(d.snap_x, d.x[cur], size_t(d.n) * 4, cudaMemcpyDeviceToDevice, d.stream));
+  CK(cudaMemcpyAsync(d.snap_v, d.v[cur], size_t(d.n) * d.vbytes, cudaMemcpyDeviceToDevice, d.stream));
+  CK(cudaEventRecord(d.snap_ready, d.stream));
+  const uint32_t n = d.n, head = (d.n - d.W_host) % d.n;
+  const int vbytes = d.vbytes, device = d.device;
+  d.snap_thread = std::thread([&d, positions, velocities, n, head, vbytes, device] {
+    try {
+      CK(cudaSetDevice(device));
+      CK(cudaStreamWaitEvent(d.snap_stream, d.snap_ready, 0));
+      // rank r holds id (head + r) mod n: two contiguous pieces
+      constexpr uint32_t kChunk = 1u << 24;
+      struct Piece { uint32_t r0, r1, id0; cudaEvent_t ev; };
+      std::vector<Piece> pieces;
+      for (uint32_t r0 = 0; r0 < n;) {
+        const uint32_t id0 = head + r0 < n ? head + r0 : head + r0 - n;
+        const uint32_t r1 = std::min<uint32_t>({n, r0 + kChunk, r0 + (n - id0)});
+        Piece pc{r0, r1, id0, nullptr};
+        CK(cudaEventCreateWithFlags(&pc.ev, cudaEventDisableTiming));
+        const size_t m = r1 - r0;
+        if (positions)
+          CK(cudaMemcpyAsync(d.snap_hx + r0, d.snap_x + id0, m * 4, cudaMemcpyDeviceToHost, d.snap_stream));
+        if (velocities)
+          CK(cudaMemcpyAsync(static_cast<char*>(d.snap_hv) + size_t(r0) * vbytes,
+                             static_cast<const char*>(d.snap_v) + size_t(id0) * vbytes, m * vbytes,
+                             cudaMemcpyDeviceToHost, d.snap_stream));
+        CK(cudaEventRecord(pc.ev, d.snap_stream));
+        pieces.push_back(pc);
+        r0 = r1;
+      }
+      cudaError_t err = cudaSuccess;
+      for (const Piece& pc : pieces) {
+        if (err == cudaSuccess) err = cudaEventSynchronize(pc.ev);
+        if (err == cudaSuccess) {
+          parallel_chunks(pc.r1 - pc.r0, [&](size_t lo, size_t hi) {
+            lo += pc.r0;
+            hi += pc.r0;
+            if (positions) widen_u32(d.snap_hx + lo, positions + lo, hi - lo);
+            if (velocities) {
+              if (vbytes == 1) widen_u8(static_cast<const uint8_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
+              else widen_u32(static_cast<const uint32_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
+            }
+          });
+        }
+        cudaEventDestroy(pc.ev);
+      }
+      CK(err);
+    } catch (...) {
+      d.snap_error = std::current_exception();
+    }
+  });
+}
 
   // ---- on-device trajectory checksum ---------------------------------
   unsigned long long* fnv_T[2] = {nullptr, nullptr};
@@ -791,7 +864,10 @@ uint64_t GpuRing::checksum() const {
   impl_->pull_hash();
   return impl_->hash;
 }
-const std::vector<Frame>& GpuRing::frames() const { return impl_->frames; }
+const std::vector<Frame>& GpuRing::frames() const {
+  impl_->snap_join();  // the last frame may still be in flight
+  return impl_->frames;
+}
 const SimParams& GpuRing::params() const { return impl_->params; }
 
 void GpuRing::observables(double* density, double* mean_velocity, double* flow) {
@@ -857,69 +933,8 @@ void GpuRing::state(uint64_t* positions, uint64_t* velocities) {
 // advance at once; the D2H of that copy and the widening run on a host
 // thread meanwhile (BASELINE config 5: a 6e7-car snapshot every 1000 steps).
 void GpuRing::state_async(uint64_t* positions, uint64_t* velocities) {
-  Impl& d = *impl_;
-  CK(cudaSetDevice(d.device));
-  d.snap_join();  // one snapshot in flight: the staging buffers are reused
-  d.drain();
-  if (!d.snap_x) {
-    CK(cudaMalloc(&d.snap_x, size_t(d.n) * 4));
-    CK(cudaMalloc(&d.snap_v, size_t(d.n) * d.vbytes));
-    CK(cudaMallocHost(&d.snap_hx, size_t(d.n) * 4));
-    CK(cudaMallocHost(&d.snap_hv, size_t(d.n) * d.vbytes));
-    CK(cudaStreamCreateWithFlags(&d.snap_stream, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&d.snap_ready, cudaEventDisableTiming));
-  }
-  const int cur = static_cast<int>(d.buf_host);
-  CK(cudaMemcpyAsync(d.snap_x, d.x[cur], size_t(d.n) * 4, cudaMemcpyDeviceToDevice, d.stream));
-  CK(cudaMemcpyAsync(d.snap_v, d.v[cur], size_t(d.n) * d.vbytes, cudaMemcpyDeviceToDevice, d.stream));
-  CK(cudaEventRecord(d.snap_ready, d.stream));
-  const uint32_t n = d.n, head = (d.n - d.W_host) % d.n;
-  const int vbytes = d.vbytes, device = d.device;
-  d.snap_thread = std::thread([&d, positions, velocities, n, head, vbytes, device] {
-    try {
-      CK(cudaSetDevice(device));
-      CK(cudaStreamWaitEvent(d.snap_stream, d.snap_ready, 0));
-      // rank r holds id (head + r) mod n: two contiguous pieces
-      constexpr uint32_t kChunk = 1u << 24;
-      struct Piece { uint32_t r0, r1, id0; cudaEvent_t ev; };
-      std::vector<Piece> pieces;
-      for (uint32_t r0 = 0; r0 < n;) {
-        const uint32_t id0 = head + r0 < n ? head + r0 : head + r0 - n;
-        const uint32_t r1 = std::min<uint32_t>({n, r0 + kChunk, r0 + (n - id0)});
-        Piece pc{r0, r1, id0, nullptr};
-        CK(cudaEventCreateWithFlags(&pc.ev, cudaEventDisableTiming));
-        const size_t m = r1 - r0;
-        if (positions)
-          CK(cudaMemcpyAsync(d.snap_hx + r0, d.snap_x + id0, m * 4, cudaMemcpyDeviceToHost, d.snap_stream));
-        if (velocities)
-          CK(cudaMemcpyAsync(static_cast<char*>(d.snap_hv) + size_t(r0) * vbytes,
-                             static_cast<const char*>(d.snap_v) + size_t(id0) * vbytes, m * vbytes,
-                             cudaMemcpyDeviceToHost, d.snap_stream));
-        CK(cudaEventRecord(pc.ev, d.snap_stream));
-        pieces.push_back(pc);
-        r0 = r1;
-      }
-      cudaError_t err = cudaSuccess;
-      for (const Piece& pc : pieces) {
-        if (err == cudaSuccess) err = cudaEventSynchronize(pc.ev);
-        if (err == cudaSuccess) {
-          parallel_chunks(pc.r1 - pc.r0, [&](size_t lo, size_t hi) {
-            lo += pc.r0;
-            hi += pc.r0;
-            if (positions) widen_u32(d.snap_hx + lo, positions + lo, hi - lo);
-            if (velocities) {
-              if (vbytes == 1) widen_u8(static_cast<const uint8_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
-              else widen_u32(static_cast<const uint32_t*>(d.snap_hv) + lo, velocities + lo, hi - lo);
-            }
-          });
-        }
-        cudaEventDestroy(pc.ev);
-      }
-      CK(err);
-    } catch (...) {
-      d.snap_error = std::current_exception();
-    }
-  });
+  CK(cudaSetDevice(impl_->device));
+  impl_->snap_start(positions, velocities);
 }
 
 void GpuRing::state_wait() { impl_->snap_join(); }
