@@ -186,6 +186,11 @@ __device__ uint32_t cone_warp(const RingArgs& ra, const uint32_t* X, const VT* V
 // and its first car's new position in parity-alternating slots.
 constexpr int kConeMwThreads = 128;
 
+#ifdef NB_DR_TRACE
+// Diagnostic build: cycles spent in the cone step loop and steps run.
+__device__ unsigned long long g_cone_cycles[2];
+#endif
+
 __device__ __forceinline__ void cone_mw_bar() {
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
@@ -227,6 +232,9 @@ __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT*
   }
   if (lane == 0) s_lead[0][warp] = x[0];
   cone_mw_bar();
+#ifdef NB_DR_TRACE
+  const long long c_start = clock64();
+#endif
   const uint32_t an_inv2 = ra.an_inv << 1;
   const uint32_t candm = tab.step2[kConeSlots + lane];
   uint32_t Wj = W, Wofs = W;
@@ -275,6 +283,12 @@ __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT*
     Wj = Wn;
     if (j + 1 == ofs + kout) break;
   }
+#ifdef NB_DR_TRACE
+  if (tid == 0) {
+    atomicAdd(&g_cone_cycles[0], static_cast<unsigned long long>(clock64() - c_start));
+    atomicAdd(&g_cone_cycles[1], static_cast<unsigned long long>(ofs + kout));
+  }
+#endif
   if (warp == 0) {
     if (lane < kout) {
       out->Wk[lane] = rW;

@@ -55,6 +55,9 @@ def main():
     print(f"{'pl_pub(e)':>10s} -> {'w0_ready(e+1)':<12s} median {int(np.median(seg)):8d} ns")
     seg = t[2:ne - 1, 4] - t[1:ne - 2, 3]
     print(f"{'wlast_sig(e)':>10s} -> {'pl_all(e+1)':<12s} median {int(np.median(seg)):8d} ns")
+    cc = (ctypes.c_ulonglong * 2)()
+    if lib.nasch_b200_cone_cycles(cc) == 0 and cc[1]:
+        print(f"planner cone loop: {cc[0] / cc[1]:.0f} cycles per cone step ({cc[1]} steps)")
     wb = (ctypes.c_ulonglong * (64 * 160 * 4))()
     assert lib.nasch_b200_dr_wtrace(wb, 64 * 160 * 4) == 0
     w = np.frombuffer(wb, dtype=np.uint64).reshape(64, 160, 4).astype(np.int64)
