@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
   constexpr int CPT = kEtCPT;
   constexpr int NW = TPB / 32;
   __shared__ uint32_t s_acc[kEtK][TPB];  // per-thread per-step velocity sums (u8 lanes)
+  __shared__ uint32_t s_plan[NW][3][kEtK];  // the warp's ring plan: W, E, E2 per step
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < int(kEtK); ++j) s_acc[j][threadIdx.x] = 0;
@@ -147,16 +148,15 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
     const unsigned long long off = rp->off;
     const bool b = rp->buf != 0;
     const Ctl* pl = ea.plans + td.ring;
-    uint32_t pW = 0, pE = 0, pE2 = 0;  // lane j holds plan step j
     if (lane < k) {
-      pW = pl->Wk[lane];
-      pE = pl->Ek[lane];
-      pE2 = pl->E2k[lane];
+      s_plan[warp][0][lane] = pl->Wk[lane];
+      s_plan[warp][1][lane] = pl->Ek[lane];
+      s_plan[warp][2][lane] = pl->E2k[lane];
     }
+    __syncwarp();
     const uint32_t* X = (b ? ea.X[1] : ea.X[0]) + off;
     const uint8_t* V = (b ? ea.V[1] : ea.V[0]) + off;
-    uint32_t* Xo = (b ? ea.X[0] : ea.X[1]) + off;
-    uint8_t* Vo = (b ? ea.V[0] : ea.V[1]) + off;
+
     const uint32_t u0 = lane * CPT;
     const uint32_t base = td.base + u0;  // local id of car 0 (may pass N in the ring's last tile)
     const bool nowrap = td.base + kEtLoad <= N;  // warp-uniform
@@ -208,9 +208,8 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
     // tile has threads that wrap)
     const bool plain = base + CPT <= N && xmax < L - k * vmax;
     for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t E = __shfl_sync(0xffffffffu, pE, j);
-      const uint32_t E2 = __shfl_sync(0xffffffffu, pE2, j);
-      const uint32_t bound = N - __shfl_sync(0xffffffffu, pW, j);
+      const uint32_t E = s_plan[warp][1][j], E2 = s_plan[warp][2][j];
+      const uint32_t bound = N - s_plan[warp][0][j];
       uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
       if (lane == 31) xn = x[CPT - 1];  // tile front: unknown leader, k <= halo
       const bool tplain = plain && !(base < bound && bound <= base + CPT);
@@ -266,6 +265,12 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
       s_acc[j][threadIdx.x] = 0;
       if (lane == 0 && sv) atomicAdd(&ea.counts[td.ring].sumv[j], static_cast<unsigned long long>(sv));
     }
+    // output pointers rebuilt here (kernel parameters + the ring's offset)
+    // rather than kept live through the step loop
+    const unsigned long long off2 = rp->off;
+    const bool b2 = rp->buf != 0;
+    uint32_t* Xo = (b2 ? ea.X[0] : ea.X[1]) + off2;
+    uint8_t* Vo = (b2 ? ea.V[0] : ea.V[1]) + off2;
     if (own_all && nowrap) {
 #pragma unroll
       for (int q = 0; q < CPT / 4; ++q)
