@@ -195,24 +195,20 @@ __device__ __forceinline__ void cone_mw_bar() {
   asm volatile("bar.sync 1, 128;" ::: "memory");
 }
 
-template <typename VT, int CPW>
-__device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
-                                uint32_t kk, uint32_t M, uint32_t ofs, uint32_t kout, Ctl* out,
-                                const ConeTab& tab) {
+// Slot i of the cone is superset entry sofs + i, whose car (x, v) the
+// caller staged in shared memory (sx, sv); aid0 = a^(id of slot 0), E0 the
+// draw base of step t.
+template <int CPW>
+__device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* sx, const uint32_t* sv, uint32_t sofs,
+                                uint32_t id0, uint32_t aid0, uint32_t E0, uint32_t W, uint32_t kk, uint32_t M,
+                                uint32_t ofs, uint32_t kout, Ctl* out, const ConeTab& tab) {
   __shared__ uint4 s_cnt[2];  // per-warp crossing counts, one 16-byte load
-  __shared__ uint32_t s_lead[2][4], s_pow[2];
+  __shared__ uint32_t s_lead[2][4];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
   const uint32_t C = M + kk;
-  const uint32_t id0 = cone_slot_id(N, W, M, 0);
-  if (warp < 2) {
-    const uint32_t r = warp == 0 ? powmod_warp(id0) : powmod_warp(draw_exponent(t, N, W));
-    if (lane == 0) s_pow[warp] = r;
-  }
   uint32_t x[CPW], v[CPW], apA[CPW], apB[CPW], idv[CPW];
-  cone_mw_bar();
-  const uint32_t aid0 = s_pow[0];
-  uint32_t E = mulmod(ra.s0, s_pow[1]);
+  uint32_t E = E0;
   uint32_t rear = 0;
 #pragma unroll
   for (int c = 0; c < CPW; ++c) {
@@ -222,8 +218,8 @@ __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT*
     const bool wrapped = id >= N;
     if (wrapped) id -= N;
     idv[c] = id;
-    x[c] = act ? __ldcg(X + id) : 0u;
-    v[c] = act ? static_cast<uint32_t>(__ldcg(V + id)) : 0u;
+    x[c] = act ? sx[sofs + i] : 0u;
+    v[c] = act ? sv[sofs + i] : 0u;
     uint32_t a = mulmod(aid0, tab.lin[act ? i : 0u]);
     if (wrapped) a = mulmod(a, ra.an_inv);
     apA[c] = a << 1;
@@ -305,29 +301,48 @@ __device__ uint32_t cone_mw_run(const RingArgs& ra, const uint32_t* X, const VT*
   return Wofs;
 }
 
-// Entry for threads 0..127 of a block (tables with the a^N half).
+// Entry for threads 0..127 of a block (tables with the a^N half).  One
+// L2 round trip: the whole superset (the last kk*vmax ranks and kk leaders)
+// is staged in shared memory, the active-zone size M counted from it, and
+// the two big powers computed while the loads are in flight.
 template <typename VT>
 __device__ uint32_t cone_mw(const RingArgs& ra, const uint32_t* X, const VT* V, uint64_t t, uint32_t W,
                             uint32_t kk, uint32_t ofs, uint32_t kout, Ctl* out, const ConeTab& tab) {
-  __shared__ uint32_t s_m[4];
+  __shared__ uint32_t s_x[kConeSlots], s_v[kConeSlots];
+  __shared__ uint32_t s_m[4], s_pow[2];
   const uint32_t tid = threadIdx.x, lane = tid & 31u, warp = tid >> 5;
   const uint32_t N = ra.n, L = ra.L;
   const uint32_t Mmax = kk * ra.vmax;
-  const uint32_t id0 = cone_slot_id(N, W, Mmax, 0);
+  const uint32_t S = Mmax + kk;  // <= kConeSlots
+  const uint32_t id0max = cone_slot_id(N, W, Mmax, 0);
   uint32_t cnt = 0;
-  for (uint32_t i = tid; i < Mmax; i += kConeMwThreads) {
-    uint32_t id = id0 + i;
+  for (uint32_t i = tid; i < S; i += kConeMwThreads) {
+    uint32_t id = id0max + i;
     if (id >= N) id -= N;
-    cnt += __ldcg(X + id) >= L - Mmax ? 1u : 0u;
+    const uint32_t xi = __ldcg(X + id);
+    s_x[i] = xi;
+    s_v[i] = static_cast<uint32_t>(__ldcg(V + id));
+    cnt += (i < Mmax && xi >= L - Mmax) ? 1u : 0u;
+  }
+  if (warp < 2) {
+    const uint32_t r = warp == 0 ? powmod_warp(id0max) : powmod_warp(draw_exponent(t, N, W));
+    if (lane == 0) s_pow[warp] = r;
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
   if (lane == 0) s_m[warp] = cnt;
   cone_mw_bar();
   const uint32_t M = s_m[0] + s_m[1] + s_m[2] + s_m[3];
+  const uint32_t sofs = Mmax - M;  // the cone starts M ranks before rank 0
+  uint32_t id0 = id0max + sofs;
+  if (id0 >= N) id0 -= N;
+  // a^id0 = a^id0max * a^sofs (times a^-N when id0 wrapped past N-1)
+  uint32_t aid0 = mulmod(s_pow[0], tab.lin[sofs]);
+  if (id0max + sofs >= N) aid0 = mulmod(aid0, ra.an_inv);
+  const uint32_t E0 = mulmod(ra.s0, s_pow[1]);
   const uint32_t C = M + kk;
-  if (C <= 128) return cone_mw_run<VT, 1>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  if (C <= 256) return cone_mw_run<VT, 2>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
-  return cone_mw_run<VT, 4>(ra, X, V, t, W, kk, M, ofs, kout, out, tab);
+  if (C <= 128) return cone_mw_run<1>(ra, s_x, s_v, sofs, id0, aid0, E0, W, kk, M, ofs, kout, out, tab);
+  if (C <= 256) return cone_mw_run<2>(ra, s_x, s_v, sofs, id0, aid0, E0, W, kk, M, ofs, kout, out, tab);
+  return cone_mw_run<4>(ra, s_x, s_v, sofs, id0, aid0, E0, W, kk, M, ofs, kout, out, tab);
 }
 
 }  // namespace nb200

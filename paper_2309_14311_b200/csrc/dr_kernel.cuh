@@ -176,10 +176,12 @@ __device__ __noinline__ bool dr_wait_all(const DrSync* sync, uint32_t G, unsigne
   return true;
 }
 
-// Crossing counts of the k steps from te (all workers done) against plan pl.
-__device__ __forceinline__ void dr_verify(const RingArgs& ra, const Ctl* pl, uint64_t te, uint32_t k, Ctl* ctl) {
-  if (threadIdx.x < k) {
-    const uint32_t j = threadIdx.x;
+// Crossing counts of the k steps from te (all workers done) against plan
+// pl; thread j (= threadIdx.x - first) checks step j.
+__device__ __forceinline__ void dr_verify(const RingArgs& ra, const Ctl* pl, uint64_t te, uint32_t k, Ctl* ctl,
+                                          uint32_t first = 0) {
+  if (threadIdx.x >= first && threadIdx.x - first < k) {
+    const uint32_t j = threadIdx.x - first;
     StepRec* r = ra.rec + ((te + j) % kRecCap);
     const uint32_t c = __ldcg(&r->c);
     const uint32_t ck = __ldcg(&pl->ck[j]);
@@ -191,7 +193,9 @@ __device__ __forceinline__ void dr_verify(const RingArgs& ra, const Ctl* pl, uin
 
 template <typename VT, int TPB>
 __device__ void dr_planner(const RingArgs& ra, const DrArgs& da, const uint32_t steps) {
+  static_assert(TPB >= kConeMwThreads + 32, "cone warps plus verification warps");
   __shared__ ConeTab s_tab;
+  __shared__ Ctl s_out;  // the cone's plan, copied out once plan(e-1) was checked
   Ctl* ctl = ra.ctl;
   DrSync* sync = da.sync;
   const uint64_t t0 = ctl->t;
@@ -210,13 +214,28 @@ __device__ void dr_planner(const RingArgs& ra, const DrArgs& da, const uint32_t 
     // plan(e-1), whose slot receives plan(e+1).
     if (e > 0 && !dr_wait_all(sync, da.G, e, ctl)) return;
     if (threadIdx.x == 0) DR_TRACE(e, 4);
-    if (e > 0) dr_verify(ra, e == 1 ? ctl : da.plans + ((e - 1) & 1u), te - K, K, ctl);
-    __syncthreads();
     const int be = (b0 + static_cast<int>(e)) & 1;
-    Ctl* dst = da.plans + ((e + 1) & 1u);
+    Ctl* dst = da.plans + ((e + 1) & 1u);  // plan(e-1)'s slot
     uint32_t Wn = 0;
-    if (threadIdx.x < kConeMwThreads)
-      Wn = cone_mw<VT>(ra, xbuf(ra, be), vbuf<VT>(ra, be), te, We, k + K, k, K, dst, s_tab);
+    if (threadIdx.x < kConeMwThreads) {
+      Wn = cone_mw<VT>(ra, xbuf(ra, be), vbuf<VT>(ra, be), te, We, k + K, k, K, &s_out, s_tab);
+    } else if (e > 0) {
+      // meanwhile the other warps check epoch e-1 against plan(e-1), which
+      // dst still holds
+      dr_verify(ra, e == 1 ? ctl : dst, te - K, K, ctl, kConeMwThreads);
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < K; j += TPB) {
+      dst->Wk[j] = s_out.Wk[j];
+      dst->Ek[j] = s_out.Ek[j];
+      dst->E2k[j] = s_out.E2k[j];
+      dst->ck[j] = s_out.ck[j];
+    }
+    if (threadIdx.x == 0) {
+      dst->kplan = s_out.kplan;
+      dst->E = s_out.E;
+      dst->E2 = s_out.E2;
+    }
     const uint64_t tn = te + k;
     for (uint32_t j = threadIdx.x; j < K; j += TPB) {
       StepRec* r = ra.rec + ((tn + j) % kRecCap);
