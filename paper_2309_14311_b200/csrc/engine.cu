@@ -154,6 +154,7 @@ struct GpuRing::Impl {
   int vbytes = 1;   // 1 => u8 velocities, 4 => u32
   bool tb = false;  // temporal-blocked mode
   bool resident = false;  // small ring: one CTA runs whole chunks of steps
+  bool warp_ring = true;  // tiny rings (N <= 512): one warp, cars in registers
   bool medium = false;    // TB with 512-car tiles (medium rings)
   bool dr = false;        // distributed-resident medium ring (dr_kernel.cuh)
   uint32_t dr_G = 0, dr_cpt = 0;
@@ -253,10 +254,16 @@ struct GpuRing::Impl {
       // Block width by ring size: a per-step barrier across 32 warps costs
       // more than a few extra cars per thread on a tiny ring (C1: 200 cars).
       if (vbytes == 1) {
-        if (n <= 256) ring_resident_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args, k);
+        if (warp_ring && n <= 128) ring_warp_kernel<uint8_t, 4><<<1, 32, 0, stream>>>(args, k);
+        else if (warp_ring && n <= 256) ring_warp_kernel<uint8_t, 8><<<1, 32, 0, stream>>>(args, k);
+        else if (warp_ring && n <= 512) ring_warp_kernel<uint8_t, 16><<<1, 32, 0, stream>>>(args, k);
+        else if (n <= 256) ring_resident_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args, k);
         else ring_resident_kernel<uint8_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
       } else {
-        if (n <= 256) ring_resident_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args, k);
+        if (warp_ring && n <= 128) ring_warp_kernel<uint32_t, 4><<<1, 32, 0, stream>>>(args, k);
+        else if (warp_ring && n <= 256) ring_warp_kernel<uint32_t, 8><<<1, 32, 0, stream>>>(args, k);
+        else if (warp_ring && n <= 512) ring_warp_kernel<uint32_t, 16><<<1, 32, 0, stream>>>(args, k);
+        else if (n <= 256) ring_resident_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args, k);
         else ring_resident_kernel<uint32_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
       }
     } else {
@@ -706,6 +713,7 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // Small rings run whole chunks of steps in one shared-memory-resident CTA
   // (NASCH_B200_RESIDENT=0 forces the one-step-per-launch kernel instead).
   d.resident = !d.tb && d.n <= kResidentMaxCars && env_long("NASCH_B200_RESIDENT", 1) != 0;
+  d.warp_ring = env_long("NASCH_B200_WARPRING", 1) != 0;
   // Medium rings: the distributed-resident kernel (dr_kernel.cuh) keeps the
   // ring in registers on every SM for whole chunks of steps
   // (NASCH_B200_DR=0 disables it).

@@ -126,4 +126,98 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
   }
 }
 
+// Tiny rings (N <= 32 * CPW): one warp keeps every car in registers (CPW
+// consecutive cars per lane) for a whole chunk of steps -- no barrier at
+// all: leaders by shuffle (the leader of car N-1 is lane 0's first car),
+// crossing count and velocity sum by warp reductions, W and E advanced by
+// every lane.  Each car's draw multiplier is its own register (a^id, and
+// a^(id-N) for the far side of the rank seam), so the draws of a lane's
+// cars are independent products rather than a chain.  BASELINE config 1
+// (200 cars) is bound by this per-step latency.
+template <typename VT, int CPW>
+__global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, const uint32_t steps) {
+  __shared__ uint32_t apw[256];
+  Ctl* ctl = ra.ctl;
+  const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
+  const uint32_t lane = threadIdx.x;
+  const uint64_t t0 = ctl->t;
+  const int b = static_cast<int>(ctl->buf);
+  uint32_t* X = xbuf(ra, b);
+  VT* V = vbuf_w<VT>(ra, b);
+  for (uint32_t i = lane; i < 256; i += 32) apw[i] = c_pow.lin[i];
+  uint32_t x[CPW], v[CPW], apA[CPW], apB[CPW];
+  uint32_t live = 0;  // bit c: car lane*CPW + c exists
+  const uint32_t first = lane * CPW;
+  const uint32_t a0 = first < N ? powmod(kA, first) : 1u;
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const uint32_t id = first + c;
+    const bool ok = id < N;
+    live |= ok ? (1u << c) : 0u;
+    x[c] = ok ? X[id] : 0u;
+    v[c] = ok ? static_cast<uint32_t>(V[id]) : 0u;
+    const uint32_t a = mulmod(a0, c_pow.lin[c]);
+    apA[c] = a << 1;
+    apB[c] = mulmod(a, ra.an_inv) << 1;
+  }
+  // the lane holding car N-1 and its slot
+  const uint32_t last_lane = (N - 1) / CPW, last_c = (N - 1) % CPW;
+  uint32_t W = ctl->W, E = ctl->E;
+  __syncwarp();
+  for (uint32_t st = 0; st < steps; ++st) {
+    const uint32_t bound = N - W;
+    const uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+    const uint32_t x00 = __shfl_sync(0xffffffffu, x[0], 0);  // leader of car N-1
+    uint32_t sum = 0, crs = 0;
+#pragma unroll
+    for (int c = 0; c < CPW; ++c) {
+      const uint32_t id = first + c;
+      const uint32_t s = mulmod_x2(id < bound ? apA[c] : apB[c], E);
+      const uint32_t xl = (lane == last_lane && c == int(last_c)) ? x00 : (c + 1 < CPW ? x[c + 1] : xn);
+      uint32_t d = xl - x[c];
+      d = min(d, d + L);  // leader past the origin (or N = 1: d = 0, gap = L - 1 via vmax <= L - 1)
+      const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+      const int vnew = max(vc - (s < tp ? 1 : 0), 0);
+      const uint32_t xs = x[c] + static_cast<uint32_t>(vnew);
+      const bool ok = (live >> c) & 1u;
+      if (ok) {
+        v[c] = static_cast<uint32_t>(vnew);
+        x[c] = min(xs, xs - L);
+        sum += v[c];
+        crs += xs >= L ? 1u : 0u;
+      }
+    }
+    const uint32_t cj = __reduce_add_sync(0xffffffffu, crs);
+    sum = __reduce_add_sync(0xffffffffu, sum);
+    if (lane == 0) {
+      StepRec* r = ra.rec + ((t0 + st) % kRecCap);
+      r->sumv = sum;
+      r->c = cj;
+      r->W = W;
+    }
+    uint32_t Wn = W + cj;
+    const bool wrap = Wn >= N;
+    if (wrap) Wn -= N;
+    const uint32_t ac = cj < 256 ? apw[cj] : powmod(kA, cj);
+    E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
+    W = Wn;
+  }
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    if ((live >> c) & 1u) {
+      X[first + c] = x[c];
+      V[first + c] = static_cast<VT>(v[c]);
+    }
+  }
+  if (lane == 0) {
+    StepRec* nrec = ra.rec + ((t0 + steps) % kRecCap);
+    nrec->sumv = 0;
+    nrec->c = 0;
+    ctl->t = t0 + steps;
+    ctl->W = W;
+    ctl->E = E;
+    ctl->E2 = mulmod_d(E, ra.an_inv);
+  }
+}
+
 }  // namespace nb200
