@@ -616,3 +616,26 @@ def test_set_state_validation_rules_and_order():
         e.set_state(x, v)
     xs, vs = e.snapshot()
     assert (xs == ref_x).all() and (vs == ref_v).all()
+
+
+@pytest.mark.parametrize("dr", ["1", "0"])
+def test_long_run_past_record_ring(port, k_env, dr):
+    """70,000 steps: past the 65,536-slot device step-record ring and over
+    several multi-chunk launches (DR: 16,384 steps per launch; TB: graph
+    chains), with the per-step series drained in pieces."""
+    os.environ.pop("NASCH_B200_K", None)
+    os.environ["NASCH_B200_DR"] = dr
+    L, N, T = 12000, 5000, 70000
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 13)
+    o = port.run(L, 5, 0.35, 13, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    e = nasch.Engine(params(L, N, 5, 0.35, T, 13))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.advance(30000)
+    s1 = e.sumv_series()
+    e.advance(T)
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    s = e.sumv_series()
+    assert len(s) == T and (s == o["sumv"]).all() and (s[:30000] == s1).all()
+    assert (e.wrap_series() == o["wraps"]).all()
