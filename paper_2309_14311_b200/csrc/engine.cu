@@ -1,12 +1,19 @@
 // engine.cu -- host side of the B200 ring engine (GpuRing) and the uniform
-// initial-state generator.  Kernels: step_kernels.cuh.
+// initial-state generator.
 //
-// Mode selection (per simulation, fixed at construction):
-//   TB  -- nasch_tb_kernel, K steps per launch (temporal blocking) with the
-//          origin-cone plan; used when the ring is long enough
-//          (N >= 2*2048, L > K*vmax, K*(vmax+1) <= 256).
-//   K1  -- nasch_step_kernel, one step per launch; any ring.
-// Both are bit-identical to the reference; tests cover each.
+// Mode selection (per simulation, fixed at construction; DESIGN.md 4):
+//   warp ring -- N <= 512: ring_warp_kernel, one warp, cars in registers,
+//                whole chunks of steps per launch (resident_kernel.cuh).
+//   resident  -- N <= 4096: ring_resident_kernel, one CTA, shared memory.
+//   DR        -- 4096 < N <= ~560k: ring_dr_kernel, the ring in registers
+//                across all SMs, a planner CTA one epoch ahead
+//                (dr_kernel.cuh, cone_warp.cuh).
+//   TB        -- larger rings: nasch_tb_kernel, K steps per launch from
+//                registers with the origin-cone plan (tb_kernel.cuh).
+//   K1        -- nasch_step_kernel, one step per launch: rings no other
+//                mode admits (e.g. vmax too large for a K >= 2 cone).
+// All are bit-identical to the reference; tests force each one
+// (NASCH_B200_DR / _RESIDENT / _WARPRING / _K / _TILE).
 #include <cuda_runtime.h>
 
 #include <algorithm>
