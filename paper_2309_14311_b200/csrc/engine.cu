@@ -351,6 +351,10 @@ struct GpuRing::Impl {
     }
     CK(cudaMemcpyAsync(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
+    if (hctl->err == 3) {
+      throw std::runtime_error("distributed-resident launch aborted: a CTA waited more than ~2 s for a "
+                               "neighbour or the planner (engine state is invalid)");
+    }
     if (hctl->err) {
       throw std::runtime_error("origin-cone plan contradicted at step " +
                                std::to_string(hctl->err_step) + " (engine state is invalid)");
