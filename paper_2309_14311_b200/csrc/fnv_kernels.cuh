@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) fnv_chunk_kernel(const RingArgs ra, unsig
 }
 
 // Pairwise composition: table 2i then table 2i+1 -> out table i.
-__global__ void __launch_bounds__(256) fnv_compose_kernel(const unsigned long long* Tin,
+static __global__ void __launch_bounds__(256) fnv_compose_kernel(const unsigned long long* Tin,
                                                           const unsigned long long* Pin, uint32_t nin,
                                                           unsigned long long* Tout,
                                                           unsigned long long* Pout) {
@@ -94,10 +94,27 @@ __global__ void __launch_bounds__(256) fnv_compose_kernel(const unsigned long lo
   if (l == 0) Pout[i] = P2 * P1;
 }
 
-__global__ void fnv_apply_kernel(const unsigned long long* T, const unsigned long long* Pt,
+static __global__ void fnv_apply_kernel(const unsigned long long* T, const unsigned long long* Pt,
                                  unsigned long long* hash) {
   const unsigned long long h = *hash;
   *hash = Pt[0] * h + T[h & 0xffu];
+}
+
+// Chunk tables of a contiguous slice of values (a shard's piece of the
+// rank-ordered row): block = 4096-value chunk of vals[0, count).
+template <typename T>
+__global__ void __launch_bounds__(256) fnv_slice_chunk_kernel(const T* __restrict__ vals, uint32_t count,
+                                                              unsigned long long* Tt, unsigned long long* Pt) {
+  __shared__ uint32_t sv[kFnvChunk];
+  const uint32_t lo = blockIdx.x * kFnvChunk;
+  const uint32_t cnt = count - lo < kFnvChunk ? count - lo : kFnvChunk;
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) sv[i] = static_cast<uint32_t>(vals[lo + i]);
+  __syncthreads();
+  unsigned long long h = threadIdx.x;
+  for (uint32_t i = 0; i < cnt; ++i) h = fnv_value(h, sv[i]);
+  const unsigned long long pn = fnv_pow(kFnvP, 8ull * cnt);
+  Tt[size_t(blockIdx.x) * 256 + threadIdx.x] = h - pn * threadIdx.x;
+  if (threadIdx.x == 0) Pt[blockIdx.x] = pn;
 }
 
 }  // namespace nb200

@@ -27,6 +27,7 @@
 
 #include "engine.hpp"
 #include "minstd.hpp"
+#include "fnv_kernels.cuh"
 #include "shard_kernels.cuh"
 #include "step_kernels.cuh"
 #include "tb_config.hpp"
@@ -80,15 +81,6 @@ struct NcclApi {
     if (r != ncclSuccess) throw std::runtime_error(std::string("NCCL error in ") + what + ": " + error_string(r));
   }
 };
-
-inline uint64_t fnv_u32s(uint64_t h, uint32_t value) {
-  constexpr uint64_t p4 = kFnvPrime * kFnvPrime * kFnvPrime * kFnvPrime;
-  h = (h ^ (value & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 8) & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 16) & 0xffu)) * kFnvPrime;
-  h = (h ^ (value >> 24)) * kFnvPrime;
-  return h * p4;
-}
 
 template <typename F>
 void par_chunks(size_t n, F&& f) {
@@ -153,6 +145,10 @@ struct ShardedRing::Impl {
     RingArgs args{};
     StepRec* hrec = nullptr;
     Ctl* hctl = nullptr;
+    // on-device checksum: chunk tables of this shard's pieces of the row
+    unsigned long long* fT[2] = {nullptr, nullptr};
+    unsigned long long* fP[2] = {nullptr, nullptr};
+    unsigned long long* hpiece = nullptr;  // pinned: up to 4 pieces x (256 + 1)
   };
 
   SimParams params;
@@ -462,12 +458,84 @@ struct ShardedRing::Impl {
     frames.push_back(std::move(f));
   }
 
-  void hash_staged() {
-    uint64_t h = hash;
-    for (uint32_t i = 0; i < n; ++i) h = fnv_u32s(h, hx[i]);
-    for (uint32_t i = 0; i < n; ++i) h = fnv_u32s(h, hvel(i));
-    hash = h;
+  // The trajectory checksum without moving the ring: each shard reduces its
+  // pieces of the rank-ordered row (positions, then velocities; at most two
+  // contiguous id ranges each) to one FNV chunk map on its own GPU
+  // (fnv_kernels.cuh), and the host composes the <= 4G maps in row order
+  // and applies the result to the running digest.
+  void gpu_hash_step() {
+    const uint32_t head = (n - W_host) % n;
+    struct Piece {
+      uint64_t row0;
+      size_t shard, slot;
+    };
+    std::vector<Piece> pieces;
+    for (size_t si = 0; si < sh.size(); ++si) {
+      Shard& s = sh[si];
+      CKS(cudaSetDevice(s.device));
+      if (!s.fT[0]) {
+        const size_t maxch = (s.nl + kFnvChunk - 1) / kFnvChunk;
+        for (int b = 0; b < 2; ++b) {
+          CKS(cudaMalloc(&s.fT[b], maxch * 256 * sizeof(unsigned long long)));
+          CKS(cudaMalloc(&s.fP[b], maxch * sizeof(unsigned long long)));
+        }
+        CKS(cudaMallocHost(&s.hpiece, 4 * 257 * sizeof(unsigned long long)));
+      }
+      // local id ranges in row order: split where the rank-0 car sits
+      std::pair<uint32_t, uint32_t> rng[2];
+      int nr = 0;
+      if (head > s.gofs && head < s.gofs + s.nl) {
+        rng[nr++] = {head - s.gofs, s.nl};
+        rng[nr++] = {0, head - s.gofs};
+      } else {
+        rng[nr++] = {0, s.nl};
+      }
+      size_t slot = 0;
+      for (int field = 0; field < 2; ++field) {
+        for (int q = 0; q < nr; ++q) {
+          const uint32_t a = rng[q].first, cnt = rng[q].second - rng[q].first;
+          const uint64_t r0 = (uint64_t(s.gofs) + a + n - head) % n;
+          const uint32_t nch = (cnt + kFnvChunk - 1) / kFnvChunk;
+          if (field == 0) {
+            fnv_slice_chunk_kernel<uint32_t><<<nch, 256, 0, s.stream>>>(s.x[buf_host] + a, cnt, s.fT[0], s.fP[0]);
+          } else if (vbytes == 1) {
+            fnv_slice_chunk_kernel<uint8_t><<<nch, 256, 0, s.stream>>>(
+                static_cast<const uint8_t*>(s.v[buf_host]) + a, cnt, s.fT[0], s.fP[0]);
+          } else {
+            fnv_slice_chunk_kernel<uint32_t><<<nch, 256, 0, s.stream>>>(
+                static_cast<const uint32_t*>(s.v[buf_host]) + a, cnt, s.fT[0], s.fP[0]);
+          }
+          CKS(cudaGetLastError());
+          int in = 0;
+          for (uint32_t m = nch; m > 1; m = (m + 1) / 2) {
+            fnv_compose_kernel<<<(m + 1) / 2, 256, 0, s.stream>>>(s.fT[in], s.fP[in], m, s.fT[in ^ 1], s.fP[in ^ 1]);
+            in ^= 1;
+          }
+          CKS(cudaMemcpyAsync(s.hpiece + slot * 257, s.fT[in], 256 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s.stream));
+          CKS(cudaMemcpyAsync(s.hpiece + slot * 257 + 256, s.fP[in], sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s.stream));
+          pieces.push_back({field ? n + r0 : r0, si, slot});
+          ++slot;
+        }
+      }
+    }
+    sync_all();
+    std::sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) { return a.row0 < b.row0; });
+    // compose in row order: (P1, T1) then (P2, T2) = (P2 P1, l -> P2 T1[l] + T2[(P1 l + T1[l]) & 0xff])
+    unsigned long long P = 1, T[256];
+    for (int l = 0; l < 256; ++l) T[l] = 0;
+    for (const Piece& pc : pieces) {
+      const unsigned long long* t2 = sh[pc.shard].hpiece + pc.slot * 257;
+      const unsigned long long p2 = t2[256];
+      unsigned long long nt[256];
+      for (int l = 0; l < 256; ++l) nt[l] = p2 * T[l] + t2[(P * static_cast<unsigned long long>(l) + T[l]) & 0xffu];
+      P = p2 * P;
+      std::memcpy(T, nt, sizeof T);
+    }
+    hash = P * hash + T[hash & 0xffu];
   }
+
 
   void enqueue_steps(uint64_t count) {
     while (count > 0) {
@@ -503,9 +571,11 @@ struct ShardedRing::Impl {
     for (uint64_t k = 0; k < count; ++k) {
       launch(1);
       drain();
-      fetch_rank_order();
-      hash_staged();
-      if (frame_due()) record_frame_staged();
+      gpu_hash_step();
+      if (frame_due()) {
+        fetch_rank_order();
+        record_frame_staged();
+      }
     }
   }
 
@@ -634,6 +704,11 @@ ShardedRing::Impl::~Impl() {
     cudaFree(s.rec);
     cudaFree(s.blkpow);
     cudaFree(s.thrpow);
+    for (int b = 0; b < 2; ++b) {
+      cudaFree(s.fT[b]);
+      cudaFree(s.fP[b]);
+    }
+    cudaFreeHost(s.hpiece);
     cudaFree(s.send);
     cudaFree(s.recv);
     cudaFree(s.lo_dev);

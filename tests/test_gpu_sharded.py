@@ -122,3 +122,18 @@ def test_too_small_to_shard_runs_on_one_gpu(port):
     assert e.checksum == o["checksum"]
     with pytest.raises(nasch.NaschError, match="too small"):  # explicit distributed use
         nasch.Engine.distributed(mk(1000, 100, 5, 0.3, 10, 1), 0, 4, nasch.nccl_unique_id())
+
+
+def test_shard_checksum_on_device_many_chunks(port, k_env):
+    """The segmented ring's on-device checksum: every shard's pieces of the
+    rank-ordered row span several 4096-value chunks, the rank-0 car sits
+    inside a shard (its pieces split), and the composed digest equals the
+    reference's serial FNV-1a at every step count."""
+    os.environ.pop("NASCH_B200_K", None)
+    L, N, vmax, p, T = 200000, 40000, 5, 0.3, 60
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 31)
+    o = port.run(L, vmax, p, 9, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    for G in (2, 3, 5):
+        g = run_engine(mk(L, N, vmax, p, T, 9), G, CUDA, x0, v0, checksum=True, chunks=[17, T])
+        assert g["checksum"] == o["checksum"], G
+        assert (g["x"] == o["x"]).all()
