@@ -23,6 +23,7 @@
 
 #include "engine.hpp"
 #include "minstd.hpp"
+#include "fnv_kernels.cuh"
 #include "step_kernels.cuh"
 
 namespace nb200 {
@@ -40,14 +41,6 @@ constexpr uint32_t kCellsPerBlock = 4096;
 constexpr int kGridTPB = 256;  // 16 cells per thread
 constexpr uint8_t kEmpty = 0xff;
 
-inline uint64_t fnv_u32g(uint64_t h, uint32_t value) {
-  constexpr uint64_t p4 = kFnvPrime * kFnvPrime * kFnvPrime * kFnvPrime;
-  h = (h ^ (value & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 8) & 0xffu)) * kFnvPrime;
-  h = (h ^ ((value >> 16) & 0xffu)) * kFnvPrime;
-  h = (h ^ (value >> 24)) * kFnvPrime;
-  return h * p4;
-}
 
 __global__ void grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L, uint32_t* counts) {
   const uint32_t b = blockIdx.x;
@@ -212,7 +205,51 @@ struct GpuGrid::Impl {
   bool checksum_on = true;
   std::vector<uint64_t> sumv_host, wraps_host;
   std::vector<Frame> frames;
+  // on-device checksum (fnv_kernels.cuh): chunk maps of the compacted,
+  // rank-ordered row, composed and applied to a device digest
+  unsigned long long* fT[2] = {nullptr, nullptr};
+  unsigned long long* fP[2] = {nullptr, nullptr};
+  unsigned long long* dhash = nullptr;
   ~Impl();
+
+  void compact() {
+    grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
+    grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, prefix, xs, vs);
+    CKG(cudaGetLastError());
+    launches += 3;
+  }
+
+  // Folds the current row (positions, then velocities) into the device
+  // digest: no transfer of the state.
+  void hash_step() {
+    const uint32_t nch = (N + kFnvChunk - 1) / kFnvChunk;
+    if (!dhash) {
+      for (int b = 0; b < 2; ++b) {
+        CKG(cudaMalloc(&fT[b], size_t(2) * nch * 256 * sizeof(unsigned long long)));
+        CKG(cudaMalloc(&fP[b], size_t(2) * nch * sizeof(unsigned long long)));
+      }
+      CKG(cudaMalloc(&dhash, sizeof(unsigned long long)));
+      CKG(cudaMemcpyAsync(dhash, &hash, sizeof hash, cudaMemcpyHostToDevice, stream));
+    }
+    compact();
+    fnv_slice_chunk_kernel<uint32_t><<<nch, 256, 0, stream>>>(xs, N, fT[0], fP[0]);
+    fnv_slice_chunk_kernel<uint8_t><<<nch, 256, 0, stream>>>(vs, N, fT[0] + size_t(nch) * 256, fP[0] + nch);
+    int in = 0;
+    for (uint32_t m = 2 * nch; m > 1; m = (m + 1) / 2) {
+      fnv_compose_kernel<<<(m + 1) / 2, 256, 0, stream>>>(fT[in], fP[in], m, fT[in ^ 1], fP[in ^ 1]);
+      in ^= 1;
+    }
+    fnv_apply_kernel<<<1, 1, 0, stream>>>(fT[in], fP[in], dhash);
+    CKG(cudaGetLastError());
+    launches += 4;
+  }
+
+  void pull_hash() {
+    if (!dhash) return;
+    CKG(cudaMemcpyAsync(&hash, dhash, sizeof hash, cudaMemcpyDeviceToHost, stream));
+    CKG(cudaStreamSynchronize(stream));
+  }
 
   void step() {
     const GridArgs g{L, N, vmax, deceleration_threshold(params.p), seeded(params.seed), steps_done};
@@ -233,11 +270,7 @@ struct GpuGrid::Impl {
 
   // grid_to_agent (model.cpp:87-97): occupied cells in ascending order.
   void fetch() {
-    grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
-    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
-    grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, prefix, xs, vs);
-    CKG(cudaGetLastError());
-    launches += 3;
+    compact();
     CKG(cudaMemcpyAsync(hx, xs, size_t(N) * 4, cudaMemcpyDeviceToHost, stream));
     CKG(cudaMemcpyAsync(hv, vs, N, cudaMemcpyDeviceToHost, stream));
     CKG(cudaStreamSynchronize(stream));
@@ -305,6 +338,11 @@ GpuGrid::Impl::~Impl() {
   cudaFree(xs);
   cudaFree(vs);
   cudaFree(rec);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(fT[b]);
+    cudaFree(fP[b]);
+  }
+  cudaFree(dhash);
   cudaFreeHost(hrec);
   cudaFreeHost(hx);
   cudaFreeHost(hv);
@@ -350,22 +388,22 @@ void GpuGrid::advance(uint64_t steps) {
   const uint64_t count = std::min(steps, d.params.steps - d.steps_done);
   for (uint64_t k = 0; k < count; ++k) {  // engine.cpp:186-196
     d.step();
-    const bool frame = d.frame_due();
-    if (d.checksum_on || frame) d.fetch();
-    if (d.checksum_on) {
-      uint64_t h = d.hash;
-      for (uint32_t i = 0; i < d.N; ++i) h = fnv_u32g(h, d.hx[i]);
-      for (uint32_t i = 0; i < d.N; ++i) h = fnv_u32g(h, d.hv[i]);
-      d.hash = h;
+    if (d.checksum_on) d.hash_step();
+    if (d.frame_due()) {
+      d.fetch();
+      d.record_frame();
     }
-    if (frame) d.record_frame();
   }
 }
 
 void GpuGrid::enqueue(uint64_t steps) { advance(steps); }
 void GpuGrid::synchronize() { CKG(cudaStreamSynchronize(impl_->stream)); }
 uint64_t GpuGrid::steps_done() const { return impl_->steps_done; }
-uint64_t GpuGrid::checksum() const { return impl_->hash; }
+uint64_t GpuGrid::checksum() const {
+  CKG(cudaSetDevice(impl_->device));
+  impl_->pull_hash();
+  return impl_->hash;
+}
 const std::vector<Frame>& GpuGrid::frames() const { return impl_->frames; }
 const SimParams& GpuGrid::params() const { return impl_->params; }
 

@@ -61,3 +61,17 @@ def test_grid_large_ring_vs_oracle(port):
     x, v = g.snapshot()
     assert (x == o["x"]).all() and (v == o["v"]).all()
     assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
+
+
+def test_grid_device_checksum_many_chunks(port):
+    """The grid engine's on-device checksum over a row of many 4096-value
+    chunks (positions and velocities) equals the reference's serial fold."""
+    L, N, vmax, p, T = 100003, 20011, 5, 0.35, 40
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 7)
+    o = port.run(L, vmax, p, 3, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    g = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=3), 1, GRID)
+    g.set_state(x0, v0)
+    g.advance(T)
+    assert g.checksum == o["checksum"]
+    x, v = g.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
