@@ -207,6 +207,14 @@ nasch_status nasch_sim_new_distributed(const nasch_params* params, unsigned rank
 /* Global car ids this process holds: [first, first + count). */
 nasch_status nasch_sim_shard_range(const nasch_sim* sim, uint64_t* first,
                                    uint64_t* count);
+/* How the segments exchange their halo and origin-cone records each
+ * launch: 0 = one segment (nothing to exchange), 1 = collective (stream-
+ * ordered peer copies in one process, NCCL all-gather across processes),
+ * 2 = peer memory (the step kernel's last block stores the record into
+ * every segment's HBM over NVLink and raises a flag; the default when the
+ * GPUs can map each other's memory; env NASCH_B200_XCHG=collective forces
+ * 1).  Construction and set_state always use the collective path. */
+unsigned nasch_sim_exchange_mode(const nasch_sim* sim);
 
 /* ---- ensembles of independent rings (extension) ------------------------
  * One handle advances many independent simulations at once -- BASELINE

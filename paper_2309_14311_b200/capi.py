@@ -79,6 +79,7 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_sim_cuda_stream": (C.c_void_p, [_P]),
     "nasch_sim_kernel_launches": (_u64, [_P]),
     "nasch_sim_steps_per_launch": (C.c_uint, [_P]),
+    "nasch_sim_exchange_mode": (C.c_uint, [_P]),
     "nasch_fill_uniform_state": (C.c_int, [_u64, _u64, _u64, _u64, _u32p, _u32p]),
     "nasch_b200_version": (C.c_char_p, []),
     "nasch_b200_draw_threshold": (C.c_uint32, [C.c_double]),

@@ -65,6 +65,9 @@ class RingEngine {
   virtual int steps_per_launch() const = 0;
   // Global ids held by this process: [first, first + count).
   virtual void shard_range(uint64_t* first, uint64_t* count) const = 0;
+  // Segment exchange in use: 0 none (one segment), 1 collective (peer
+  // copies / NCCL all-gather), 2 peer memory (stores from the step kernel).
+  virtual int exchange_mode() const { return 0; }
 };
 
 class GpuRing : public RingEngine {
@@ -135,6 +138,7 @@ class ShardedRing : public RingEngine {
   uint64_t kernel_launches() const override;
   int steps_per_launch() const override;
   void shard_range(uint64_t* first, uint64_t* count) const override;
+  int exchange_mode() const override;
 
  private:
   struct Impl;

@@ -141,6 +141,10 @@ struct ShardedRing::Impl {
     uint32_t* thrpow = nullptr;
     uint32_t* send = nullptr;
     uint32_t* recv = nullptr;
+    // peer-memory exchange: [kFlagWords flags][2][G][kXchgWords] receive area
+    uint32_t* xarea = nullptr;
+    void** ptab = nullptr;            // device [2G]: every shard's rec area, then flag array
+    std::vector<void*> ipc_opened;    // peer areas mapped with cudaIpcOpenMemHandle
     uint32_t* lo_dev = nullptr;
     RingArgs args{};
     StepRec* hrec = nullptr;
@@ -158,6 +162,13 @@ struct ShardedRing::Impl {
   std::vector<uint32_t> lo;  // G+1 segment starts
   bool use_nccl = false;
   ncclComm_t comm = nullptr;
+  // Steady-state exchange: records pushed into peer HBM by the step
+  // kernel's last block (tb_body<PUSH>), flags awaited by the plan kernel.
+  // Construction / set_state always exchange through the collective path
+  // (peer copies or NCCL all-gather), which also absorbs any skew between
+  // the ranks' host threads.
+  bool p2p = false;
+  uint32_t xseq = 0;  // launches published through the peer exchange
   std::vector<Shard> sh;  // shards held by this process
   bool exchanged_once = false;
   ~Impl();
@@ -230,6 +241,10 @@ struct ShardedRing::Impl {
     CKS(cudaMalloc(&s.rec, sizeof(StepRec) * kRecCap));
     CKS(cudaMalloc(&s.send, kXchgWords * 4));
     CKS(cudaMalloc(&s.recv, size_t(G) * kXchgWords * 4));
+    const size_t xbytes = (kFlagWords + 2 * size_t(G) * kXchgWords) * 4;
+    CKS(cudaMalloc(&s.xarea, xbytes));
+    CKS(cudaMemset(s.xarea, 0, xbytes));
+    CKS(cudaMalloc(&s.ptab, 2 * size_t(G) * sizeof(void*)));
     CKS(cudaMalloc(&s.lo_dev, (G + 1) * 4));
     CKS(cudaMemcpy(s.lo_dev, lo.data(), (G + 1) * 4, cudaMemcpyHostToDevice));
     CKS(cudaMallocHost(&s.hrec, sizeof(StepRec) * kRecCap));
@@ -278,6 +293,111 @@ struct ShardedRing::Impl {
     CKS(cudaGetLastError());
   }
 
+  // ---- peer-memory exchange setup ------------------------------------
+  static bool p2p_wanted() {
+    const char* e = std::getenv("NASCH_B200_XCHG");
+    return !(e && std::strcmp(e, "collective") == 0);
+  }
+
+  // Shards of this process: plain device pointers, peer access enabled
+  // between distinct GPUs (NVLink); any pair that cannot map the other's
+  // memory keeps the collective exchange.
+  void setup_p2p_local() {
+    if (!p2p_wanted() || G > kFlagWords) return;
+    for (const Shard& a : sh)
+      for (const Shard& b : sh) {
+        if (a.device == b.device) continue;
+        int ok = 0;
+        CKS(cudaDeviceCanAccessPeer(&ok, a.device, b.device));
+        if (!ok) return;
+      }
+    for (const Shard& a : sh)
+      for (const Shard& b : sh) {
+        if (a.device == b.device) continue;
+        CKS(cudaSetDevice(a.device));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CKS(e);
+      }
+    std::vector<void*> tab(2 * size_t(G));
+    for (unsigned h = 0; h < G; ++h) {
+      tab[h] = sh[h].xarea + kFlagWords;
+      tab[G + h] = sh[h].xarea;
+    }
+    for (Shard& s : sh) {
+      CKS(cudaSetDevice(s.device));
+      CKS(cudaMemcpy(s.ptab, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    }
+    p2p = true;
+  }
+
+  // One shard per process: the ranks swap cudaIpcMemHandle_t of their
+  // receive areas over the NCCL communicator, map every peer's area, and
+  // agree (a second all-gather) to switch only if every rank mapped every
+  // peer.
+  void setup_p2p_ipc() {
+    if (!p2p_wanted() || G > kFlagWords) return;
+    Shard& s = sh[0];
+    NcclApi& api = NcclApi::get();
+    CKS(cudaSetDevice(s.device));
+    constexpr size_t kSlot = 128;  // one cudaIpcMemHandle_t (64 B) + status, per rank
+    static_assert(sizeof(cudaIpcMemHandle_t) <= kSlot - 8, "handle slot");
+    std::vector<unsigned char> mine(kSlot, 0), all(kSlot * G, 0);
+    cudaIpcMemHandle_t h{};
+    const bool got = cudaIpcGetMemHandle(&h, s.xarea) == cudaSuccess;
+    if (!got) cudaGetLastError();
+    std::memcpy(mine.data(), &h, sizeof h);
+    mine[kSlot - 1] = got ? 1 : 0;
+    unsigned char* dbuf = nullptr;
+    CKS(cudaMalloc(&dbuf, kSlot * (G + 1)));
+    struct Free {
+      unsigned char* p;
+      ~Free() { cudaFree(p); }
+    } guard{dbuf};
+    CKS(cudaMemcpy(dbuf, mine.data(), kSlot, cudaMemcpyHostToDevice));
+    api.check(api.all_gather(dbuf, dbuf + kSlot, kSlot, ncclUint8, comm, s.stream), "ncclAllGather(ipc)");
+    CKS(cudaStreamSynchronize(s.stream));
+    CKS(cudaMemcpy(all.data(), dbuf + kSlot, kSlot * G, cudaMemcpyDeviceToHost));
+    std::vector<void*> tab(2 * size_t(G), nullptr);
+    bool ok = true;
+    for (unsigned r = 0; r < G && ok; ++r) {
+      if (r == s.g) {
+        tab[r] = s.xarea;
+        continue;
+      }
+      if (!all[kSlot * r + kSlot - 1]) {
+        ok = false;
+        break;
+      }
+      cudaIpcMemHandle_t ph;
+      std::memcpy(&ph, all.data() + kSlot * r, sizeof ph);
+      void* p = nullptr;
+      if (cudaIpcOpenMemHandle(&p, ph, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+        break;
+      }
+      s.ipc_opened.push_back(p);
+      tab[r] = p;
+    }
+    // agree: every rank switches, or none does
+    const uint32_t flag = ok ? 1u : 0u;
+    CKS(cudaMemcpy(dbuf, &flag, 4, cudaMemcpyHostToDevice));
+    api.check(api.all_gather(dbuf, dbuf + kSlot, 4, ncclUint8, comm, s.stream), "ncclAllGather(ipc ok)");
+    CKS(cudaStreamSynchronize(s.stream));
+    std::vector<uint32_t> oks(G);
+    CKS(cudaMemcpy(oks.data(), dbuf + kSlot, 4 * size_t(G), cudaMemcpyDeviceToHost));
+    for (uint32_t v : oks) ok = ok && v == 1u;
+    if (!ok) return;  // the opened mappings are released by ~Impl
+    std::vector<void*> dev(2 * size_t(G));
+    for (unsigned r = 0; r < G; ++r) {
+      dev[r] = static_cast<uint32_t*>(tab[r]) + kFlagWords;
+      dev[G + r] = tab[r];
+    }
+    CKS(cudaMemcpy(s.ptab, dev.data(), dev.size() * sizeof(void*), cudaMemcpyHostToDevice));
+    p2p = true;
+  }
+
   // ---- the per-launch pipeline ---------------------------------------
   void pack_all() {
     for (Shard& s : sh) {
@@ -317,8 +437,10 @@ struct ShardedRing::Impl {
   void plan_all() {
     for (Shard& s : sh) {
       CKS(cudaSetDevice(s.device));
-      if (vbytes == 1) shard_plan_kernel<uint8_t><<<1, kConeMax, 0, s.stream>>>(s.args, s.recv, s.lo_dev, G, s.g);
-      else shard_plan_kernel<uint32_t><<<1, kConeMax, 0, s.stream>>>(s.args, s.recv, s.lo_dev, G, s.g);
+      if (vbytes == 1)
+        shard_plan_kernel<uint8_t><<<1, kConeMax, 0, s.stream>>>(s.args, s.recv, s.lo_dev, G, s.g, nullptr, 0u);
+      else
+        shard_plan_kernel<uint32_t><<<1, kConeMax, 0, s.stream>>>(s.args, s.recv, s.lo_dev, G, s.g, nullptr, 0u);
       CKS(cudaGetLastError());
       CKS(cudaEventRecord(s.ev_done, s.stream));
       ++launches;
@@ -333,6 +455,11 @@ struct ShardedRing::Impl {
   }
 
   void launch(uint32_t k) {
+    if (p2p) {
+      launch_p2p(k);
+      steps_done += k;
+      return;
+    }
     for (Shard& s : sh) {
       CKS(cudaSetDevice(s.device));
       if (vbytes == 1) nasch_tb_kernel<uint8_t, kTPB, kCPT, kHalo, kTbWT><<<s.grid, kTPB, 0, s.stream>>>(s.args, k);
@@ -342,6 +469,44 @@ struct ShardedRing::Impl {
     }
     exchange_and_plan();
     steps_done += k;
+  }
+
+  // Two kernels per launch and no host-side exchange: the step kernel
+  // publishes the record into every shard's HBM; the plan kernel waits on
+  // the flags.  Shards of one process additionally order the plan after
+  // every shard's step kernel with events, so no kernel ever waits on a
+  // kernel that might not be running (several shards may share one GPU).
+  void launch_p2p(uint32_t k) {
+    const uint32_t seq = ++xseq;
+    for (Shard& s : sh) {
+      CKS(cudaSetDevice(s.device));
+      XchgArgs xa;
+      xa.rec = reinterpret_cast<uint32_t* const*>(s.ptab);
+      xa.flag = reinterpret_cast<uint32_t* const*>(s.ptab + G);
+      xa.g = s.g;
+      xa.G = G;
+      xa.seq = seq;
+      if (vbytes == 1)
+        nasch_tb_push_kernel<uint8_t, kTPB, kCPT, kHalo, kTbWT><<<s.grid, kTPB, 0, s.stream>>>(s.args, k, xa);
+      else
+        nasch_tb_push_kernel<uint32_t, kTPB, kCPT, kHalo, kTbWT><<<s.grid, kTPB, 0, s.stream>>>(s.args, k, xa);
+      CKS(cudaGetLastError());
+      if (!use_nccl) CKS(cudaEventRecord(s.ev_packed, s.stream));
+      ++launches;
+    }
+    for (Shard& s : sh) {
+      CKS(cudaSetDevice(s.device));
+      if (!use_nccl)
+        for (const Shard& o : sh) CKS(cudaStreamWaitEvent(s.stream, o.ev_packed, 0));
+      const uint32_t* rec = s.xarea + kFlagWords;
+      if (vbytes == 1)
+        shard_plan_kernel<uint8_t><<<1, kConeMax, 0, s.stream>>>(s.args, rec, s.lo_dev, G, s.g, s.xarea, seq);
+      else
+        shard_plan_kernel<uint32_t><<<1, kConeMax, 0, s.stream>>>(s.args, rec, s.lo_dev, G, s.g, s.xarea, seq);
+      CKS(cudaGetLastError());
+      CKS(cudaEventRecord(s.ev_done, s.stream));
+      ++launches;
+    }
   }
 
   void reset_ctl() {
@@ -385,6 +550,9 @@ struct ShardedRing::Impl {
     }
     sync_all();
     for (const Shard& s : sh) {
+      if (s.hctl->err == 3u)
+        throw std::runtime_error("peer exchange timed out on shard " + std::to_string(s.g) +
+                                 " (a rank stopped publishing; engine state is invalid)");
       if (s.hctl->t != steps_done)
         throw std::runtime_error("device step counter out of sync on shard " + std::to_string(s.g));
       if (s.hctl->W != sh[0].hctl->W || s.hctl->buf != sh[0].hctl->buf)
@@ -666,6 +834,7 @@ ShardedRing::ShardedRing(const SimParams& params, unsigned shards) : impl_(new I
   int cur = 0;
   CKS(cudaGetDevice(&cur));
   for (unsigned g = 0; g < shards; ++g) d.make_shard(g, ndev > 1 ? static_cast<int>(g % ndev) : cur);
+  d.setup_p2p_local();
   CKS(cudaSetDevice(cur));
   d.finish_construction();
 }
@@ -684,6 +853,7 @@ ShardedRing::ShardedRing(const SimParams& params, unsigned rank, unsigned world,
   api.check(api.comm_init_rank(&d.comm, static_cast<int>(world), id, static_cast<int>(rank)),
             "ncclCommInitRank");
   d.make_shard(rank, cur);
+  d.setup_p2p_ipc();
   d.finish_construction();
 }
 
@@ -711,6 +881,9 @@ ShardedRing::Impl::~Impl() {
     cudaFreeHost(s.hpiece);
     cudaFree(s.send);
     cudaFree(s.recv);
+    for (void* p : s.ipc_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(s.xarea);
+    cudaFree(s.ptab);
     cudaFree(s.lo_dev);
     cudaFreeHost(s.hrec);
     cudaFreeHost(s.hctl);
@@ -780,6 +953,7 @@ void ShardedRing::set_checksum(bool enabled) {
 }
 void* ShardedRing::cuda_stream() const { return impl_->sh.empty() ? nullptr : impl_->sh[0].stream; }
 uint64_t ShardedRing::kernel_launches() const { return impl_->launches; }
+int ShardedRing::exchange_mode() const { return impl_->p2p ? 2 : 1; }
 int ShardedRing::steps_per_launch() const { return static_cast<int>(impl_->K); }
 
 void ShardedRing::shard_range(uint64_t* first, uint64_t* count) const {

@@ -24,13 +24,19 @@
 #include <cstdint>
 #include <type_traits>
 
+#include "shard_kernels.cuh"
 #include "step_kernels.cuh"
 #include "tb_config.hpp"
 
 namespace nb200 {
 
-template <typename VT, int TPB, int CPT, int HALO, bool WT>
-__global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
+// The launch body.  PUSH (segmented ring, peer-memory exchange only): the
+// launch's last block also publishes this segment's exchange record for the
+// next launch straight into every segment's receive slots (shard_push,
+// shard_kernels.cuh) -- the pack and the all-gather fused into the step
+// kernel.  PUSH = false compiles to the plain kernel (dead code removed).
+template <typename VT, int TPB, int CPT, int HALO, bool WT, bool PUSH>
+__device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, const XchgArgs& xa) {
   using G = TbGeom<TPB, CPT, HALO, WT>;
   constexpr uint32_t LOAD = G::kLoad;     // cars spanned per block tile
   constexpr uint32_t STORE = G::kStore;   // cars owned (stored) per block tile
@@ -253,6 +259,7 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
       ctl->buf = static_cast<unsigned int>(b ^ 1);
       ctl->ticket = 0;
     }
+    if constexpr (PUSH) shard_push<VT, TPB>(ra, Xo, Vo, Wn, xa);
     return;
   }
   cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
@@ -267,6 +274,18 @@ __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArg
     ctl->buf = static_cast<unsigned int>(b ^ 1);
     ctl->ticket = 0;
   }
+}
+
+template <typename VT, int TPB, int CPT, int HALO, bool WT>
+__global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
+  tb_body<VT, TPB, CPT, HALO, WT, false>(ra, k, XchgArgs{});
+}
+
+// Segmented ring with the peer-memory exchange (sharded.cu, kXchgP2P).
+template <typename VT, int TPB, int CPT, int HALO, bool WT>
+__global__ void __launch_bounds__(TPB, NB_TB_MINB)
+    nasch_tb_push_kernel(const RingArgs ra, const uint32_t k, const XchgArgs xa) {
+  tb_body<VT, TPB, CPT, HALO, WT, true>(ra, k, xa);
 }
 
 }  // namespace nb200

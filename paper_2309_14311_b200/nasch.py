@@ -186,6 +186,11 @@ class Engine:
         return _lib().nasch_sim_steps_per_launch(self._h)
 
     @property
+    def exchange_mode(self) -> int:
+        """0 one segment, 1 collective exchange, 2 peer-memory exchange."""
+        return _lib().nasch_sim_exchange_mode(self._h)
+
+    @property
     def cuda_stream(self) -> int:
         return _lib().nasch_sim_cuda_stream(self._h) or 0
 

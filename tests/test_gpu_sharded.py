@@ -21,6 +21,22 @@ def mk(L, N, vmax, p, steps, seed, output="none", stride=1):
                            output=output, stride=stride)
 
 
+@pytest.fixture(params=["p2p", "collective"])
+def xchg(request):
+    """Both segment exchanges: records stored into peer HBM by the step
+    kernel (default) and the collective path (peer copies / NCCL)."""
+    old = os.environ.get("NASCH_B200_XCHG")
+    os.environ["NASCH_B200_XCHG"] = request.param
+    yield request.param
+    if old is None:
+        os.environ.pop("NASCH_B200_XCHG", None)
+    else:
+        os.environ["NASCH_B200_XCHG"] = old
+
+
+MODE = {"p2p": 2, "collective": 1}
+
+
 @pytest.fixture
 def k_env():
     old = os.environ.get("NASCH_B200_K")
@@ -33,6 +49,7 @@ def k_env():
 
 def run_engine(params, workers, kind, x0=None, v0=None, steps=None, checksum=False, chunks=None):
     e = nasch.Engine(params, workers, kind)
+    mode = e.exchange_mode
     e.set_checksum(checksum)
     if x0 is not None:
         e.set_state(x0, v0)
@@ -40,13 +57,13 @@ def run_engine(params, workers, kind, x0=None, v0=None, steps=None, checksum=Fal
         e.advance(c)
     x, v = e.snapshot()
     out = dict(x=x, v=v, sumv=e.sumv_series(), wraps=e.wrap_series(), checksum=e.checksum,
-               obs=e.observables(), spl=e.steps_per_launch)
+               obs=e.observables(), spl=e.steps_per_launch, mode=mode)
     e.close()
     return out
 
 
 @pytest.mark.parametrize("G", [2, 3, 4, 7])
-def test_shards_match_oracle(port, G):
+def test_shards_match_oracle(port, xchg, G):
     rng = np.random.default_rng(G)
     for trial, (L, N, vmax, p) in enumerate([(40000, 6000, 5, 0.13), (9000, 8000, 5, 0.5),
                                              (3 * 10**5, 25000, 12, 0.3), (20000, 2000, 3, 0.9)]):
@@ -55,6 +72,7 @@ def test_shards_match_oracle(port, G):
         T = 70
         o = port.run(L, vmax, p, 5 + trial, T, x0, v0, want_checksum=False)
         g = run_engine(mk(L, N, vmax, p, T, 5 + trial), G, CUDA, x0, v0, chunks=[13, 57])
+        assert g["mode"] == MODE[xchg]
         assert (g["x"] == o["x"]).all() and (g["v"] == o["v"]).all(), (G, trial)
         assert (g["sumv"] == o["sumv"]).all()
         assert (g["wraps"] == o["wraps"]).all()
@@ -72,7 +90,7 @@ def test_shard_depths_and_checksum(port, k_env, K):
     assert (g["x"] == o["x"]).all() and (g["sumv"] == o["sumv"]).all()
 
 
-def test_shards_equal_single_gpu_engine_long_run():
+def test_shards_equal_single_gpu_engine_long_run(xchg):
     L, N = 2 * 10**6, 4 * 10**5
     x0, v0 = nasch.fill_uniform_state(L, N, 5, 4)
     ref = run_engine(mk(L, N, 5, 0.25, 600, 8), 1, 0, x0, v0)
@@ -96,15 +114,17 @@ def test_shard_frames_match_single(tmp_path):
     assert open(tmp_path / "a.txt").read() == open(tmp_path / "b.txt").read()
 
 
-def test_nccl_distributed_path_single_rank(port):
+def test_nccl_distributed_path_single_rank(port, xchg):
     """The one-process-per-GPU constructor with a 1-rank NCCL communicator:
-    exercises libnccl loading, communicator setup and the ncclAllGather
-    exchange on the real device."""
+    exercises libnccl loading, communicator setup, the ncclAllGather
+    exchange on the real device and, for p2p, the cudaIpcMemHandle swap and
+    agreement over NCCL, the push from the step kernel and the flag wait."""
     L, N, vmax, p, T = 30000, 9000, 5, 0.2, 48
     x0, v0 = nasch.fill_uniform_state(L, N, 5, 12)
     o = port.run(L, vmax, p, 4, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
     e = nasch.Engine.distributed(mk(L, N, vmax, p, T, 4), 0, 1, nasch.nccl_unique_id())
     assert e.shard_range() == (0, N)
+    assert e.exchange_mode == MODE[xchg]
     e.set_state(x0, v0)
     e.advance(T)
     x, v = e.snapshot()
@@ -137,3 +157,32 @@ def test_shard_checksum_on_device_many_chunks(port, k_env):
         g = run_engine(mk(L, N, vmax, p, T, 9), G, CUDA, x0, v0, checksum=True, chunks=[17, T])
         assert g["checksum"] == o["checksum"], G
         assert (g["x"] == o["x"]).all()
+
+
+def test_p2p_exchange_resume_and_many_launches(port, xchg):
+    """set_state in the middle of a peer-exchange run (the collective
+    re-initialisation, then the launch counter and slot parity carry on),
+    K = 16 launches past both receive slots many times, and the result is
+    the oracle's."""
+    L, N, vmax, p = 60000, 12000, 5, 0.4
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 17)
+    x0 = x0.astype(np.uint64)
+    v0 = v0.astype(np.uint64)
+    o1 = port.run(L, vmax, p, 6, 37, x0, v0, want_checksum=False)
+    e = nasch.Engine(mk(L, N, vmax, p, 500, 6), 3, CUDA)
+    assert e.exchange_mode == MODE[xchg]
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.advance(37)
+    x, v = e.snapshot()
+    assert (x == o1["x"]).all() and (v == o1["v"]).all()
+    # a different state mid-run: every fifth car stopped
+    x2, v2 = x.copy(), v.copy()
+    v2[::5] = 0
+    o2 = port.run(L, vmax, p, 6, 200, x2, v2, want_checksum=False, rng_state=o1["rng"])
+    e.set_state(x2, v2)
+    e.advance(200)
+    x, v = e.snapshot()
+    assert (x == o2["x"]).all() and (v == o2["v"]).all()
+    assert (e.sumv_series()[-200:] == o2["sumv"]).all()
+    e.close()
