@@ -63,7 +63,7 @@ def _shard(g, G, launches, seed, shm_names, out):
 def test_two_slots_suffice_under_skew(G):
     from multiprocessing import shared_memory
 
-    ctx = mp.get_context("fork")
+    ctx = mp.get_context("spawn")
     shms = [shared_memory.SharedMemory(create=True, size=8 * (G + 2 * G * W)) for _ in range(G)]
     try:
         for s in shms:
