@@ -808,7 +808,11 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   } else {
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, nasch_step_kernel<uint32_t, kTPB, kCPT1>, kTPB, 0));
   }
-  d.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
+  // Temporal-blocked kernels: several block waves (tb_config.hpp kTbWaves);
+  // the one-step kernel stays persistent (HBM-bound, one wave).
+  const uint32_t waves = d.tb ? static_cast<uint32_t>(std::max<long>(1, env_long("NASCH_B200_WAVES", kTbWaves))) : 1u;
+  d.grid = static_cast<int>(std::max<uint64_t>(
+      1, std::min<uint64_t>(ntiles, uint64_t(sms) * std::max(per_sm, 1) * waves)));
   // Test knob: force a grid size, to show results do not depend on the
   // launch geometry (the reference's W-invariance, test_engine.cpp:136-152).
   const long gwant = env_long("NASCH_B200_GRID", 0);
@@ -816,7 +820,9 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
 
   // Geometry-dependent draw multipliers a^(first id of block / thread).
   std::vector<uint32_t> blk(d.grid), thr(tpb);
-  for (int b = 0; b < d.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * tile);
+  const uint32_t a_tile = powmod(kA, tile);
+  blk[0] = 1;
+  for (int b = 1; b < d.grid; ++b) blk[b] = mulmod(blk[b - 1], a_tile);
   for (int t = 0; t < tpb; ++t) {
     const uint32_t ofs = !d.tb ? t * cpt : d.medium ? TbMedium::offset(t) : TbLarge::offset(t);
     thr[t] = powmod(kA, ofs);

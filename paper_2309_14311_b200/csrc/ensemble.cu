@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <stdexcept>
@@ -26,6 +27,7 @@
 #include "engine.hpp"
 #include "ensemble.hpp"
 #include "minstd.hpp"
+#include "tb_config.hpp"
 #include "ensemble_tb.cuh"
 #include "step_kernels.cuh"
 
@@ -373,7 +375,10 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
     int per_sm = 0;
     CKE(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ens_tb_kernel<kEtTPB>, kEtTPB, 0));
     const uint64_t blocks_needed = (tiles.size() + kEtTPB / 32 - 1) / (kEtTPB / 32);
-    d.tgrid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(blocks_needed, uint64_t(sms) * std::max(per_sm, 1))));
+    const char* we = std::getenv("NASCH_B200_WAVES");
+    const long waves = std::max<long>(1, we && *we ? std::strtol(we, nullptr, 10) : kTbWaves);
+    d.tgrid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(blocks_needed, uint64_t(sms) * std::max(per_sm, 1) * uint64_t(waves))));
     d.tpush();
     ens_tiled_init_kernel<<<static_cast<int>(std::min<size_t>(d.trings.size(), 4096)), 256, 0, d.stream>>>(
         d.ea.rings, d.ea.nrings, d.ea.X[0], d.ea.V[0]);

@@ -252,9 +252,14 @@ struct ShardedRing::Impl {
     int sms = 0, per_sm = 0;
     CKS(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
     if (vbytes == 1) occupancy<uint8_t>(&per_sm); else occupancy<uint32_t>(&per_sm);
-    s.grid = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(ntiles, uint32_t(sms) * std::max(per_sm, 1))));
+    const char* we = std::getenv("NASCH_B200_WAVES");
+    const long waves = std::max<long>(1, we && *we ? std::strtol(we, nullptr, 10) : kTbWaves);
+    s.grid = static_cast<int>(std::max<uint64_t>(
+        1, std::min<uint64_t>(ntiles, uint64_t(sms) * std::max(per_sm, 1) * uint64_t(waves))));
     std::vector<uint32_t> blk(s.grid), thr(kTPB);
-    for (int b = 0; b < s.grid; ++b) blk[b] = powmod(kA, uint64_t(b) * kStore);
+    const uint32_t a_tile = powmod(kA, kStore);
+    blk[0] = 1;
+    for (int b = 1; b < s.grid; ++b) blk[b] = mulmod(blk[b - 1], a_tile);
     for (int t = 0; t < kTPB; ++t) thr[t] = powmod(kA, TbLarge::offset(t));
     CKS(cudaMalloc(&s.blkpow, blk.size() * 4));
     CKS(cudaMalloc(&s.thrpow, thr.size() * 4));

@@ -40,6 +40,17 @@ struct TbGeom {
   }
 };
 
+// Grid of the temporal-blocked kernels: kTbWaves times the resident blocks
+// (148 SMs x 5), so the hardware hands tiles out in ~10 block waves.  A
+// persistent grid (one wave, static grid-stride tiles) finishes when its
+// slowest SM does: on C3 one wave measured 1.63e12 car-updates/s, 2 waves
+// 1.68e12, 4 1.73e12, 10 1.75e12, 40 1.72e12, one tile per block 1.65e12
+// (round 1, tools/grid_sweep.py).  Env NASCH_B200_WAVES overrides.
+#ifndef NB_TB_WAVES
+#define NB_TB_WAVES 10
+#endif
+constexpr int kTbWaves = NB_TB_WAVES;
+
 constexpr int kTbTPB = NB_TB_TPB;                   // threads per tile
 constexpr int kTbCPT = NB_TB_CPT;                   // consecutive cars per thread
 constexpr int kTbHalo = 16;                         // cars ahead re-read per tile (>= K)
