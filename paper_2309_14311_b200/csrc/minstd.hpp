@@ -46,12 +46,15 @@ __device__ __forceinline__ uint32_t mulmod_d(uint32_t x, uint32_t y) {
 }
 
 // Same product with the multiplier given doubled (x2 = 2x < 2^32): the fold
-// term p >> 31 is then the high word of x2*y, one IMAD.HI on the FMA pipe
-// instead of a 64-bit funnel shift on the ALU pipe.
+// term p >> 31 is then the high word of x2*y.  The product is one 64-bit
+// IMAD.WIDE.U32 (FMA pipe) and hi + (lo >> 1) one LEA.HI (ALU pipe);
+// separate mul.lo/mul.hi let ptxas fold the shift into IMAD.HI's 64-bit
+// addend, which needs a zeroed register per car (an extra IMAD.MOV/HFMA2):
+// measured +6 % on C3/C5/C4 for the wide form (round 1,
+// tools/variant_bench.py).
 __device__ __forceinline__ uint32_t mulmod_x2(uint32_t x2, uint32_t y) {
   uint32_t lo, hi;
-  asm("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(x2), "r"(y));
-  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(x2), "r"(y));
+  asm("{ .reg .u64 p; mul.wide.u32 p, %2, %3; mov.b64 {%0, %1}, p; }" : "=r"(lo), "=r"(hi) : "r"(x2), "r"(y));
   // x2*y = 2p: lo holds bits 1..31 of p shifted up one; p & m = lo >> 1
   const uint32_t r = (lo >> 1) + hi;
   return min(r, r - kM);

@@ -152,10 +152,12 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           // Balanced between the FMA and ALU pipes (both issue a warp
-          // instruction every 2 cycles per SMSP): draw via mulmod_x2 (2 IMAD
-          // + 2 ALU), headway x*(-1) + leader as one IMAD (neg1 is a launch
-          // parameter, so ptxas cannot turn it into an ALU IADD3; measured
-          // +10 % on C3), deceleration flag as the sign of s - tp.
+          // instruction every 2 cycles per SMSP): draw via mulmod_x2 (IMAD.WIDE
+          // + LEA.HI + VIADDMNMX), headway x*(-1) + leader as one IMAD (neg1
+          // is a launch parameter, so ptxas cannot turn it into an ALU IADD3;
+          // measured +10 % on C3), deceleration flag as the sign of s - tp
+          // (ptxas fuses it with the add: LEA.HI.SX32; forcing it onto the
+          // FMA pipe as IMAD.HI measured 8 % slower).
           const uint32_t s = mulmod_x2(ap[c], Es);
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
           const uint32_t d = x[c] * ra.neg1 + xl;

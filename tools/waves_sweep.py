@@ -18,7 +18,11 @@ import json, os, sys
 sys.path.insert(0, os.path.join(os.environ["R"], "tools"))
 import bench_configs as bc
 name = sys.argv[1]
-if name == "C3":
+if name == "C1":
+    r = bc.ring("C1", 1000, 200, 0.13, 1000, 42, 0)
+elif name == "C2":
+    r = bc.ring("C2", 10**6, 2 * 10**5, 0.25, 10**4, 2, 5)
+elif name == "C3":
     r = bc.ring("C3", 10**9, 2 * 10**8, 0.13, 512, 3, 0)
 elif name == "C5":
     r = bc.ring("C5", 10**8, 6 * 10**7, 0.5, 2000, 5, 0)
