@@ -162,10 +162,17 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
   }
   // the lane holding car N-1 and its slot
   const uint32_t last_lane = (N - 1) / CPW, last_c = (N - 1) % CPW;
+  // Next draw base for c = lane crossings, both cases, doubled for
+  // mulmod_x2: E' = E a^c when W wraps past N, else E a^(N+c).  Each step
+  // computes both candidates while its cars move, so the serial chain after
+  // the crossing count is one shuffle (c < 32; larger counts take the table).
+  const uint32_t candw2 = c_pow.lin[lane] << 1;
+  const uint32_t candn2 = mulmod(ra.an, c_pow.lin[lane]) << 1;
   uint32_t W = ctl->W, E = ctl->E;
   __syncwarp();
   for (uint32_t st = 0; st < steps; ++st) {
     const uint32_t bound = N - W;
+    const uint32_t nextw = mulmod_x2(candw2, E), nextn = mulmod_x2(candn2, E);
     const uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
     const uint32_t x00 = __shfl_sync(0xffffffffu, x[0], 0);  // leader of car N-1
     uint32_t sum = 0, crs = 0;
@@ -198,8 +205,13 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
     uint32_t Wn = W + cj;
     const bool wrap = Wn >= N;
     if (wrap) Wn -= N;
-    const uint32_t ac = cj < 256 ? apw[cj] : powmod(kA, cj);
-    E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
+    const uint32_t fast = __shfl_sync(0xffffffffu, wrap ? nextw : nextn, cj & 31u);
+    if (cj < 32) {
+      E = fast;
+    } else {
+      const uint32_t ac = cj < 256 ? apw[cj] : powmod(kA, cj);
+      E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
+    }
     W = Wn;
   }
 #pragma unroll
