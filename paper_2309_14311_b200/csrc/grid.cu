@@ -6,12 +6,18 @@
 // order (= rank order, so draw #(t*N + rank + 1)), brakes to the distance to
 // the next occupied cell, and scatters every car to (x + v) mod L.
 // Here one step is four launches over L one-byte cells (0xff = empty):
-//   count   occupied cells per 4096-cell block
-//   scan    exclusive prefix over the block counts (rank of a block's first car)
+//   count   occupied cells per 4096-cell block (16-byte loads, byte compares
+//           in SIMD-within-a-register form)
+//   scan    exclusive prefix over the block counts (rank of a block's first
+//           car), one block: per-thread chunk sums + warp-shuffle scan
 //   clear   the next cell array
-//   move    per occupied cell: in-block rank by warp ballots, gap by looking
-//           ahead at most min(vmax, L-1) cells, the counter-based draw, and
-//           the scatter; exact per-step velocity sum and wrap count.
+//   move    per occupied cell: in-block rank by warp scans, gap by looking
+//           ahead at most min(vmax, L-1) cells, the counter-based draw
+//           E_t a^rank (a^rank from three 4096-entry power tables for a
+//           thread's first car, then one multiply per car), and the
+//           scatter; exact per-step velocity sum and wrap count.
+// Steps are enqueued without a host round trip; the per-step records are
+// drained in batches.  HBM traffic per step: about 3 L + N bytes.
 // Bit-identical to the agent engines (tests/test_gpu_grid.py).
 #include <cuda_runtime.h>
 
@@ -42,12 +48,24 @@ constexpr int kGridTPB = 256;  // 16 cells per thread
 constexpr uint8_t kEmpty = 0xff;
 
 
-__global__ void grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L, uint32_t* counts) {
-  const uint32_t b = blockIdx.x;
-  const uint32_t lo = b * kCellsPerBlock;
+// Occupied bytes (!= 0xff) among the 16 cells [lo, lo + 16).
+__device__ __forceinline__ uint32_t occupied16(const uint8_t* __restrict__ cells, uint32_t lo, uint32_t L) {
+  if (lo + 16 <= L) {
+    const uint4 w = *reinterpret_cast<const uint4*>(cells + lo);
+    return (__popc(__vcmpne4(w.x, 0xffffffffu)) + __popc(__vcmpne4(w.y, 0xffffffffu)) +
+            __popc(__vcmpne4(w.z, 0xffffffffu)) + __popc(__vcmpne4(w.w, 0xffffffffu))) >> 3;
+  }
   uint32_t c = 0;
-  for (uint32_t i = lo + threadIdx.x; i < min(L, lo + kCellsPerBlock); i += blockDim.x)
-    c += cells[i] != kEmpty;
+  for (uint32_t i = lo; i < min(L, lo + 16); ++i) c += cells[i] != kEmpty;
+  return c;
+}
+
+// One thread per 16 consecutive cells of the block (as the move kernel).
+__global__ void __launch_bounds__(kGridTPB) grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L,
+                                                              uint32_t* counts) {
+  const uint32_t b = blockIdx.x;
+  const uint32_t lo = b * kCellsPerBlock + threadIdx.x * 16u;
+  uint32_t c = lo < L ? occupied16(cells, lo, L) : 0u;
   c = __reduce_add_sync(0xffffffffu, c);
   __shared__ uint32_t s[kGridTPB / 32];
   if ((threadIdx.x & 31) == 0) s[threadIdx.x / 32] = c;
@@ -59,53 +77,90 @@ __global__ void grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L,
   }
 }
 
-// Single-block exclusive scan of nb block counts.
-__global__ void grid_scan_kernel(const uint32_t* counts, uint32_t nb, uint32_t* prefix) {
-  __shared__ uint32_t s_tot[1024];
+// Single-block (1024 threads) exclusive scan of nb block counts: each
+// thread sums a contiguous chunk, the chunk sums are scanned with warp
+// shuffles, and each thread writes its chunk's prefixes.
+__global__ void __launch_bounds__(1024) grid_scan_kernel(const uint32_t* counts, uint32_t nb, uint32_t* prefix) {
+  __shared__ uint32_t s_w[32];
   const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
   const uint32_t lo = threadIdx.x * per, hi = min(nb, lo + per);
   uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; ++i) sum += counts[i];
-  s_tot[threadIdx.x] = sum;
+  for (uint32_t i = lo; i < hi; ++i) sum += __ldg(counts + i);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += n;
+  }
+  if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (uint32_t t = 0; t < blockDim.x; ++t) {
-      const uint32_t v = s_tot[t];
-      s_tot[t] = run;
-      run += v;
+  if (warp == 0) {
+    uint32_t w = s_w[lane], wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t n = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= static_cast<uint32_t>(o)) wi += n;
     }
+    s_w[lane] = wi - w;
   }
   __syncthreads();
-  uint32_t run = s_tot[threadIdx.x];
+  uint32_t run = s_w[warp] + incl - sum;
   for (uint32_t i = lo; i < hi; ++i) {
     prefix[i] = run;
-    run += counts[i];
+    run += __ldg(counts + i);
   }
 }
 
 struct GridArgs {
-  uint32_t L, N, vmax, tp, s0;
+  uint32_t L, N, vmax, tp;
+  uint32_t E;                 // s0 a^(t N + 1): the draw of the rank-0 car at step t
+  const uint32_t* pw;         // [3][4096]: a^j, a^(4096 j), a^(4096^2 j)
   unsigned long long t;
 };
 
-// One thread per 16 consecutive cells of the block.
+// Bit k set iff byte k of w is occupied (!= 0xff), k < 4.
+__device__ __forceinline__ uint32_t occ_bits4(uint32_t w) {
+  return ((__vcmpne4(w, 0xffffffffu) & 0x01010101u) * 0x01020408u) >> 24;
+}
+
+// One thread per 16 consecutive cells of the block.  Gaps come from a
+// 32-cell occupancy mask (this thread's cells and the next thread's) when
+// vmax <= 16 and the cells do not reach the end of the road; otherwise by
+// looking ahead in the cell array.
 __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __restrict__ cells,
                                                              uint8_t* __restrict__ next,
                                                              const uint32_t* __restrict__ prefix,
                                                              GridArgs g, StepRec* rec) {
   constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
   const uint32_t lo = blockIdx.x * kCellsPerBlock + threadIdx.x * CPT;
-  uint8_t c[CPT];
-  uint32_t occ = 0;
+  static_assert(CPT == 16, "one 16-byte load per thread");
+  uint32_t ws[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+  if (lo + CPT <= g.L) {
+    const uint4 w = *reinterpret_cast<const uint4*>(cells + lo);
+    ws[0] = w.x;
+    ws[1] = w.y;
+    ws[2] = w.z;
+    ws[3] = w.w;
+  } else {
 #pragma unroll
-  for (uint32_t k = 0; k < CPT; ++k) {
-    c[k] = (lo + k < g.L) ? cells[lo + k] : kEmpty;
-    occ += c[k] != kEmpty;
+    for (uint32_t k = 0; k < CPT; ++k)
+      if (lo + k < g.L) ws[k / 4] = (ws[k / 4] & ~(0xffu << (8 * (k % 4)))) | (uint32_t(cells[lo + k]) << (8 * (k % 4)));
   }
+  const uint32_t m16 = occ_bits4(ws[0]) | (occ_bits4(ws[1]) << 4) | (occ_bits4(ws[2]) << 8) | (occ_bits4(ws[3]) << 12);
+  const uint32_t occ = __popc(m16);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the next 16 cells' occupancy: the next lane's, or (lane 31) loaded
+  uint32_t nm16 = __shfl_down_sync(0xffffffffu, m16, 1);
+  const uint32_t look = min(g.vmax, g.L - 1);
+  const bool fastgap = look <= 16 && lo + 2 * CPT <= g.L;
+  if (lane == 31 && fastgap) {
+    const uint4 w = *reinterpret_cast<const uint4*>(cells + lo + CPT);
+    nm16 = occ_bits4(w.x) | (occ_bits4(w.y) << 4) | (occ_bits4(w.z) << 8) | (occ_bits4(w.w) << 12);
+  }
+  const uint32_t m32 = m16 | (nm16 << 16);
   // in-block exclusive rank of this thread's first car
   uint32_t incl = occ;
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
@@ -117,25 +172,33 @@ __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __re
   uint32_t wbase = 0;
   for (uint32_t w = 0; w < warp; ++w) wbase += s_w[w];
   uint32_t rank = prefix[blockIdx.x] + wbase + incl - occ;
-  const uint32_t look = min(g.vmax, g.L - 1);
+  // a^rank of this thread's first car from the three power tables
+  uint32_t ap = mulmod(mulmod(__ldg(g.pw + (rank & 4095u)), __ldg(g.pw + 4096 + ((rank >> 12) & 4095u))),
+                       __ldg(g.pw + 8192 + (rank >> 24)));
   uint32_t sum = 0, wraps = 0;
 #pragma unroll
   for (uint32_t k = 0; k < CPT; ++k) {
-    if (c[k] == kEmpty) continue;
+    if (!((m16 >> k) & 1u)) continue;
     const uint32_t x = lo + k;
+    const uint32_t ck = (ws[k / 4] >> (8 * (k % 4))) & 0xffu;
     // distance to the next occupied cell, only needed below vmax
     uint32_t gap = look;
-    for (uint32_t d = 1; d <= look; ++d) {
-      uint32_t y = x + d;
-      if (y >= g.L) y -= g.L;
-      const uint8_t cy = (k + d < CPT && x + d < g.L) ? c[k + d] : cells[y];
-      if (cy != kEmpty) {
-        gap = d - 1;
-        break;
+    if (fastgap) {
+      const uint32_t rest = m32 >> (k + 1);  // bit d-1: cell x + d
+      if (rest) gap = min(static_cast<uint32_t>(__ffs(rest)) - 1u, look);
+    } else {
+      for (uint32_t d = 1; d <= look; ++d) {
+        uint32_t y = x + d;
+        if (y >= g.L) y -= g.L;
+        if (cells[y] != kEmpty) {
+          gap = d - 1;
+          break;
+        }
       }
     }
-    uint32_t v = min(min(static_cast<uint32_t>(c[k]) + 1, g.vmax), gap);
-    const uint32_t s = mulmod(g.s0, powmod(kA, draw_exponent(g.t, g.N, rank)));
+    uint32_t v = min(min(ck + 1, g.vmax), gap);
+    const uint32_t s = mulmod(g.E, ap);  // draw #(t N + rank + 1)
+    ap = mulmod(ap, kA);
     if (s < g.tp && v > 0) --v;
     uint32_t nx = x + v;
     if (nx >= g.L) {
@@ -198,7 +261,9 @@ struct GpuGrid::Impl {
   uint32_t *counts = nullptr, *prefix = nullptr, *xs = nullptr;
   uint8_t* vs = nullptr;
   StepRec* rec = nullptr;
-  StepRec* hrec = nullptr;
+  StepRec* hrec = nullptr;  // pinned [kRecCap]
+  uint32_t* pw = nullptr;   // device power tables (GridArgs::pw)
+  uint64_t drained = 0;
   uint32_t* hx = nullptr;
   uint8_t* hv = nullptr;
   uint64_t steps_done = 0, hash = kFnvBasis, launches = 0, sumv0 = 0;
@@ -251,8 +316,11 @@ struct GpuGrid::Impl {
     CKG(cudaStreamSynchronize(stream));
   }
 
+  // One step, enqueued: no host round trip (records drained in batches).
   void step() {
-    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), seeded(params.seed), steps_done};
+    if (steps_done - drained >= kRecCap / 2) drain();
+    const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
+    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, pw, steps_done};
     CKG(cudaMemsetAsync(rec + (steps_done % kRecCap), 0, sizeof(StepRec), stream));
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
     grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
@@ -262,10 +330,25 @@ struct GpuGrid::Impl {
     launches += 3;
     cur ^= 1;
     ++steps_done;
-    CKG(cudaMemcpyAsync(hrec, rec + ((steps_done - 1) % kRecCap), sizeof(StepRec), cudaMemcpyDeviceToHost, stream));
+  }
+
+  // Per-step records of [drained, steps_done) to the host series.
+  void drain() {
+    if (drained == steps_done) return;
+    const uint64_t first = drained, count = steps_done - drained;
+    uint64_t done = 0;
+    while (done < count) {
+      const uint64_t slot = (first + done) % kRecCap;
+      const uint64_t seg = std::min<uint64_t>(count - done, kRecCap - slot);
+      CKG(cudaMemcpyAsync(hrec + done, rec + slot, seg * sizeof(StepRec), cudaMemcpyDeviceToHost, stream));
+      done += seg;
+    }
     CKG(cudaStreamSynchronize(stream));
-    sumv_host.push_back(hrec->sumv);
-    wraps_host.push_back(hrec->c);
+    for (uint64_t k = 0; k < count; ++k) {
+      sumv_host.push_back(hrec[k].sumv);
+      wraps_host.push_back(hrec[k].c);
+    }
+    drained = steps_done;
   }
 
   // grid_to_agent (model.cpp:87-97): occupied cells in ascending order.
@@ -315,7 +398,17 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   CKG(cudaMalloc(&d.xs, size_t(d.N) * 4));
   CKG(cudaMalloc(&d.vs, d.N));
   CKG(cudaMalloc(&d.rec, sizeof(StepRec) * kRecCap));
-  CKG(cudaMallocHost(&d.hrec, sizeof(StepRec)));
+  CKG(cudaMallocHost(&d.hrec, sizeof(StepRec) * kRecCap));
+  {
+    std::vector<uint32_t> tab(3 * 4096);
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t step = powmod(kA, uint64_t(1) << (12 * k));
+      tab[k * 4096] = 1;
+      for (int j = 1; j < 4096; ++j) tab[k * 4096 + j] = mulmod(tab[k * 4096 + j - 1], step);
+    }
+    CKG(cudaMalloc(&d.pw, tab.size() * 4));
+    CKG(cudaMemcpy(d.pw, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice));
+  }
   CKG(cudaMallocHost(&d.hx, size_t(d.N) * 4));
   CKG(cudaMallocHost(&d.hv, d.N));
   CKG(cudaMemsetAsync(d.cells[0], kEmpty, d.L, d.stream));
@@ -338,6 +431,7 @@ GpuGrid::Impl::~Impl() {
   cudaFree(xs);
   cudaFree(vs);
   cudaFree(rec);
+  cudaFree(pw);
   for (int b = 0; b < 2; ++b) {
     cudaFree(fT[b]);
     cudaFree(fP[b]);
@@ -354,6 +448,7 @@ GpuGrid::~GpuGrid() = default;
 void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   Impl& d = *impl_;
   if (n != d.N) throw std::invalid_argument("state length must equal ncars");
+  d.drain();
   std::vector<uint8_t> cells(d.L, kEmpty);
   uint64_t s = 0;
   for (size_t i = 0; i < n; ++i) {
@@ -364,7 +459,8 @@ void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
     cells[x[i]] = static_cast<uint8_t>(v[i]);
     s += v[i];
   }
-  CKG(cudaMemcpy(d.cells[d.cur], cells.data(), d.L, cudaMemcpyHostToDevice));
+  CKG(cudaMemcpyAsync(d.cells[d.cur], cells.data(), d.L, cudaMemcpyHostToDevice, d.stream));
+  CKG(cudaStreamSynchronize(d.stream));
   d.sumv0 = s;
   d.sumv_host.clear();
   d.wraps_host.clear();
@@ -394,10 +490,25 @@ void GpuGrid::advance(uint64_t steps) {
       d.record_frame();
     }
   }
+  d.drain();
 }
 
-void GpuGrid::enqueue(uint64_t steps) { advance(steps); }
-void GpuGrid::synchronize() { CKG(cudaStreamSynchronize(impl_->stream)); }
+// Asynchronous form: the steps are enqueued; synchronize() completes them.
+void GpuGrid::enqueue(uint64_t steps) {
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  if (d.checksum_on || d.params.output_mode != OutputMode::none) {
+    advance(steps);
+    return;
+  }
+  const uint64_t count = std::min(steps, d.params.steps - d.steps_done);
+  for (uint64_t k = 0; k < count; ++k) d.step();
+}
+void GpuGrid::synchronize() {
+  CKG(cudaSetDevice(impl_->device));
+  impl_->drain();
+  CKG(cudaStreamSynchronize(impl_->stream));
+}
 uint64_t GpuGrid::steps_done() const { return impl_->steps_done; }
 uint64_t GpuGrid::checksum() const {
   CKG(cudaSetDevice(impl_->device));
@@ -408,7 +519,9 @@ const std::vector<Frame>& GpuGrid::frames() const { return impl_->frames; }
 const SimParams& GpuGrid::params() const { return impl_->params; }
 
 void GpuGrid::observables(double* density, double* mean_velocity, double* flow) {
-  const Impl& d = *impl_;
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  d.drain();
   const uint64_t total = d.sumv_host.empty() ? d.sumv0 : d.sumv_host.back();
   const double n = static_cast<double>(d.params.car_count);
   const double mean = static_cast<double>(total) / n;
@@ -429,14 +542,18 @@ void GpuGrid::state(uint64_t* positions, uint64_t* velocities) {
 }
 
 size_t GpuGrid::sumv_series(uint64_t* out, size_t cap) {
-  const Impl& d = *impl_;
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  d.drain();
   const size_t k = std::min(cap, d.sumv_host.size());
   if (out) std::memcpy(out, d.sumv_host.data(), k * sizeof(uint64_t));
   return d.sumv_host.size();
 }
 
 size_t GpuGrid::wrap_series(uint64_t* out, size_t cap) {
-  const Impl& d = *impl_;
+  Impl& d = *impl_;
+  CKG(cudaSetDevice(d.device));
+  d.drain();
   const size_t k = std::min(cap, d.wraps_host.size());
   if (out) std::memcpy(out, d.wraps_host.data(), k * sizeof(uint64_t));
   return d.wraps_host.size();
