@@ -9,15 +9,17 @@
 //   count   occupied cells per 4096-cell block (16-byte loads, byte compares
 //           in SIMD-within-a-register form)
 //   scan    exclusive prefix over the block counts (rank of a block's first
-//           car), one block: per-thread chunk sums + warp-shuffle scan
-//   clear   the next cell array
-//   move    per occupied cell: in-block rank by warp scans, gap by looking
-//           ahead at most min(vmax, L-1) cells, the counter-based draw
-//           E_t a^rank (a^rank from three 4096-entry power tables for a
-//           thread's first car, then one multiply per car), and the
-//           scatter; exact per-step velocity sum and wrap count.
+//           car) in two levels: 1024 counts per block, then the group totals
+//   move    block b assembles the NEXT array's cells [4096 b, 4096 b + 4096)
+//           in shared memory from its own cars and the cars of the vmax
+//           cells before it, and writes them with 16-byte stores (no
+//           clearing pass, no byte scatter in HBM); each warp compacts its
+//           cars first (lanes work on cars, not cells); per car: gap to the
+//           next car of the list, the counter-based draw E_t a^rank (a^rank
+//           from three 4096-entry power tables for a lane's first car, then
+//           one multiply by a^32 per car); exact velocity sum and wrap count.
 // Steps are enqueued without a host round trip; the per-step records are
-// drained in batches.  HBM traffic per step: about 3 L + N bytes.
+// drained in batches.  HBM traffic per step: about 3 L bytes.
 // Bit-identical to the agent engines (tests/test_gpu_grid.py).
 #include <cuda_runtime.h>
 
@@ -77,17 +79,13 @@ __global__ void __launch_bounds__(kGridTPB) grid_count_kernel(const uint8_t* __r
   }
 }
 
-// Single-block (1024 threads) exclusive scan of nb block counts: each
-// thread sums a contiguous chunk, the chunk sums are scanned with warp
-// shuffles, and each thread writes its chunk's prefixes.
-__global__ void __launch_bounds__(1024) grid_scan_kernel(const uint32_t* counts, uint32_t nb, uint32_t* prefix) {
-  __shared__ uint32_t s_w[32];
-  const uint32_t per = (nb + blockDim.x - 1) / blockDim.x;
-  const uint32_t lo = threadIdx.x * per, hi = min(nb, lo + per);
-  uint32_t sum = 0;
-  for (uint32_t i = lo; i < hi; ++i) sum += __ldg(counts + i);
+// Exclusive scan of the nb block counts in two levels: grid_scan_local
+// (1024 counts per block, warp-shuffle scan) writes each block's local
+// prefix and the 1024-block group totals; grid_scan_top scans the <= 1024
+// group totals.  A block's first rank is local[b] + top[b >> 10].
+__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s_w, uint32_t* total) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint32_t incl = sum;
+  uint32_t incl = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
@@ -96,25 +94,41 @@ __global__ void __launch_bounds__(1024) grid_scan_kernel(const uint32_t* counts,
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = s_w[lane], wi = w;
+    const uint32_t w = lane < blockDim.x / 32 ? s_w[lane] : 0u;
+    uint32_t wi = w;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t n = __shfl_up_sync(0xffffffffu, wi, o);
       if (lane >= static_cast<uint32_t>(o)) wi += n;
     }
     s_w[lane] = wi - w;
+    if (lane == 31) *total = wi;
   }
   __syncthreads();
-  uint32_t run = s_w[warp] + incl - sum;
-  for (uint32_t i = lo; i < hi; ++i) {
-    prefix[i] = run;
-    run += __ldg(counts + i);
-  }
+  return s_w[warp] + incl - v;
+}
+
+__global__ void __launch_bounds__(1024) grid_scan_local(const uint32_t* counts, uint32_t nb, uint32_t* local,
+                                                        uint32_t* group) {
+  __shared__ uint32_t s_w[32], s_tot;
+  const uint32_t i = blockIdx.x * 1024u + threadIdx.x;
+  const uint32_t v = i < nb ? counts[i] : 0u;
+  const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
+  if (i < nb) local[i] = ex;
+  if (threadIdx.x == 0) group[blockIdx.x] = s_tot;
+}
+
+__global__ void __launch_bounds__(1024) grid_scan_top(uint32_t* group, uint32_t ng) {
+  __shared__ uint32_t s_w[32], s_tot;
+  const uint32_t v = threadIdx.x < ng ? group[threadIdx.x] : 0u;
+  const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
+  if (threadIdx.x < ng) group[threadIdx.x] = ex;
 }
 
 struct GridArgs {
   uint32_t L, N, vmax, tp;
   uint32_t E;                 // s0 a^(t N + 1): the draw of the rank-0 car at step t
+  uint32_t a32;               // a^32 (a lane's next car is 32 ranks on)
   const uint32_t* pw;         // [3][4096]: a^j, a^(4096 j), a^(4096^2 j)
   unsigned long long t;
 };
@@ -124,17 +138,48 @@ __device__ __forceinline__ uint32_t occ_bits4(uint32_t w) {
   return ((__vcmpne4(w, 0xffffffffu) & 0x01010101u) * 0x01020408u) >> 24;
 }
 
-// One thread per 16 consecutive cells of the block.  Gaps come from a
-// 32-cell occupancy mask (this thread's cells and the next thread's) when
-// vmax <= 16 and the cells do not reach the end of the road; otherwise by
-// looking ahead in the cell array.
+// The draw of the car of rank r: E a^r, a^r from the three power tables.
+__device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
+  return mulmod(mulmod(__ldg(pw + (r & 4095u)), __ldg(pw + 4096 + ((r >> 12) & 4095u))),
+                __ldg(pw + 8192 + (r >> 24)));
+}
+
+// Gap ahead of the car at x by reading the cell array (any vmax, wraps).
+__device__ __forceinline__ uint32_t gap_scan(const uint8_t* __restrict__ cells, uint32_t x, uint32_t look,
+                                             uint32_t L) {
+  for (uint32_t d = 1; d <= look; ++d) {
+    uint32_t y = x + d;
+    if (y >= L) y -= L;
+    if (cells[y] != kEmpty) return d - 1;
+  }
+  return look;
+}
+
+// Block b owns the OUTPUT cells [B0, B0 + 4096) of the next array and
+// assembles them in shared memory: its own cars (one thread per 16 input
+// cells, as the count kernel) land there unless they pass B0 + 4096 or wrap
+// past L, and the cars of the `look` cells before B0 (mod L), computed once
+// more by warp 0, land there when they cross into it.  The block then
+// writes its 4096 cells with 16-byte stores: no clearing pass and no
+// partial-sector scatter in HBM.  Each car's velocity and crossing are
+// counted by the block that owns its input cell.  Within a warp the cars of
+// its 512 cells are first compacted in shared memory (position order), so
+// every lane works on cars, not on empty cells, and a car's gap is the next
+// entry of the list (the warp's last car reads ahead in the cell array).
 __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __restrict__ cells,
                                                              uint8_t* __restrict__ next,
-                                                             const uint32_t* __restrict__ prefix,
+                                                             const uint32_t* __restrict__ local,
+                                                             const uint32_t* __restrict__ group,
                                                              GridArgs g, StepRec* rec) {
   constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
-  const uint32_t lo = blockIdx.x * kCellsPerBlock + threadIdx.x * CPT;
   static_assert(CPT == 16, "one 16-byte load per thread");
+  __shared__ __align__(16) uint8_t s_out[kCellsPerBlock];
+  __shared__ uint32_t s_w[kGridTPB / 32];
+  __shared__ uint16_t s_cx[kGridTPB / 32][32 * CPT];  // a warp's cars: cell offset from B0 ...
+  __shared__ uint8_t s_cv[kGridTPB / 32][32 * CPT];   // ... and velocity, in position order
+  const uint32_t B0 = blockIdx.x * kCellsPerBlock;
+  const uint32_t lo = B0 + threadIdx.x * CPT;
+  reinterpret_cast<uint4*>(s_out)[threadIdx.x] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
   uint32_t ws[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
   if (lo + CPT <= g.L) {
     const uint4 w = *reinterpret_cast<const uint4*>(cells + lo);
@@ -150,64 +195,85 @@ __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __re
   const uint32_t m16 = occ_bits4(ws[0]) | (occ_bits4(ws[1]) << 4) | (occ_bits4(ws[2]) << 8) | (occ_bits4(ws[3]) << 12);
   const uint32_t occ = __popc(m16);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // the next 16 cells' occupancy: the next lane's, or (lane 31) loaded
-  uint32_t nm16 = __shfl_down_sync(0xffffffffu, m16, 1);
-  const uint32_t look = min(g.vmax, g.L - 1);
-  const bool fastgap = look <= 16 && lo + 2 * CPT <= g.L;
-  if (lane == 31 && fastgap) {
-    const uint4 w = *reinterpret_cast<const uint4*>(cells + lo + CPT);
-    nm16 = occ_bits4(w.x) | (occ_bits4(w.y) << 4) | (occ_bits4(w.z) << 8) | (occ_bits4(w.w) << 12);
-  }
-  const uint32_t m32 = m16 | (nm16 << 16);
-  // in-block exclusive rank of this thread's first car
+  // Compact the warp's cars (512 cells) into shared memory in position
+  // order, then give lane l the cars l, l + 32, ...: every lane busy, the
+  // gap of all but the warp's last car is the next car in the list.
   uint32_t incl = occ;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= static_cast<uint32_t>(o)) incl += n;
   }
-  __shared__ uint32_t s_w[kGridTPB / 32];
+  const uint32_t wcnt = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) s_w[warp] = incl;
-  __syncthreads();
+  {
+    uint32_t m = m16, q = incl - occ;
+    while (m) {
+      const uint32_t k = __ffs(m) - 1u;
+      m &= m - 1u;
+      s_cx[warp][q] = static_cast<uint16_t>(lo - B0 + k);
+      const uint32_t wk = k < 8 ? (k < 4 ? ws[0] : ws[1]) : (k < 12 ? ws[2] : ws[3]);  // no local array
+      s_cv[warp][q] = static_cast<uint8_t>(wk >> (8 * (k % 4)));
+      ++q;
+    }
+  }
+  __syncthreads();  // also orders the s_out clear before any car lands
   uint32_t wbase = 0;
   for (uint32_t w = 0; w < warp; ++w) wbase += s_w[w];
-  uint32_t rank = prefix[blockIdx.x] + wbase + incl - occ;
-  // a^rank of this thread's first car from the three power tables
-  uint32_t ap = mulmod(mulmod(__ldg(g.pw + (rank & 4095u)), __ldg(g.pw + 4096 + ((rank >> 12) & 4095u))),
-                       __ldg(g.pw + 8192 + (rank >> 24)));
+  const uint32_t rank0 = __ldg(local + blockIdx.x) + __ldg(group + (blockIdx.x >> 10));
+  const uint32_t look = min(g.vmax, g.L - 1);
+  const uint32_t B1 = min(B0 + kCellsPerBlock, g.L);  // end of this block's output cells
   uint32_t sum = 0, wraps = 0;
-#pragma unroll
-  for (uint32_t k = 0; k < CPT; ++k) {
-    if (!((m16 >> k) & 1u)) continue;
-    const uint32_t x = lo + k;
-    const uint32_t ck = (ws[k / 4] >> (8 * (k % 4))) & 0xffu;
-    // distance to the next occupied cell, only needed below vmax
-    uint32_t gap = look;
-    if (fastgap) {
-      const uint32_t rest = m32 >> (k + 1);  // bit d-1: cell x + d
-      if (rest) gap = min(static_cast<uint32_t>(__ffs(rest)) - 1u, look);
-    } else {
-      for (uint32_t d = 1; d <= look; ++d) {
-        uint32_t y = x + d;
-        if (y >= g.L) y -= g.L;
-        if (cells[y] != kEmpty) {
-          gap = d - 1;
-          break;
-        }
+  if (lane < wcnt) {
+    uint32_t ap = apow_rank(g.pw, rank0 + wbase + lane);
+    for (uint32_t j = lane; j < wcnt; j += 32) {
+      const uint32_t x = B0 + s_cx[warp][j];
+      const uint32_t ck = s_cv[warp][j];
+      const uint32_t gap = j + 1 < wcnt ? min(static_cast<uint32_t>(s_cx[warp][j + 1]) + B0 - x - 1u, look)
+                                        : gap_scan(cells, x, look, g.L);
+      uint32_t v = min(min(ck + 1, g.vmax), gap);
+      const uint32_t s = mulmod(g.E, ap);  // draw #(t N + rank + 1)
+      ap = mulmod(ap, g.a32);
+      if (s < g.tp && v > 0) --v;
+      uint32_t nx = x + v;
+      if (nx >= g.L) {
+        nx -= g.L;
+        ++wraps;
       }
+      if (nx >= B0 && nx < B1) s_out[nx - B0] = static_cast<uint8_t>(v);
+      sum += v;
     }
-    uint32_t v = min(min(ck + 1, g.vmax), gap);
-    const uint32_t s = mulmod(g.E, ap);  // draw #(t N + rank + 1)
-    ap = mulmod(ap, kA);
-    if (s < g.tp && v > 0) --v;
-    uint32_t nx = x + v;
-    if (nx >= g.L) {
-      nx -= g.L;
-      ++wraps;
+  }
+  // Warp 0: cars of the `look` cells before B0 (mod L) that land in this
+  // block.  Their ranks count back from the block's first rank (mod N).
+  if (warp == 0 && g.L > kCellsPerBlock) {
+    uint32_t after = 0;  // occupied cells between the current chunk and B0
+    for (uint32_t c0 = 0; c0 < look; c0 += 32) {
+      const uint32_t j = c0 + lane + 1;  // cell B0 - j
+      const uint32_t y = j <= look ? (B0 >= j ? B0 - j : B0 + g.L - j) : 0u;
+      const bool occd = j <= look && cells[y] != kEmpty;
+      const uint32_t bal = __ballot_sync(0xffffffffu, occd);
+      if (occd) {
+        // ranks: cars at B0-1, B0-2, ... are rank0-1, rank0-2, ...
+        const uint32_t nearer = __popc(bal & ((1u << lane) - 1u));  // occupied cells closer to B0
+        uint32_t r = rank0 + g.N - (after + nearer + 1);
+        if (r >= g.N) r -= g.N;
+        const uint32_t cy = cells[y];
+        uint32_t v = min(min(cy + 1, g.vmax), gap_scan(cells, y, look, g.L));
+        const uint32_t sd = mulmod(g.E, apow_rank(g.pw, r));
+        if (sd < g.tp && v > 0) --v;
+        uint32_t nx = y + v;
+        if (nx >= g.L) nx -= g.L;
+        if (nx >= B0 && nx < B1) s_out[nx - B0] = static_cast<uint8_t>(v);
+      }
+      after += __popc(bal);
     }
-    next[nx] = static_cast<uint8_t>(v);
-    sum += v;
-    ++rank;
+  }
+  __syncthreads();
+  if (B0 + (threadIdx.x + 1) * CPT <= g.L) {
+    reinterpret_cast<uint4*>(next + B0)[threadIdx.x] = reinterpret_cast<const uint4*>(s_out)[threadIdx.x];
+  } else {
+    for (uint32_t k = threadIdx.x * CPT; k < (threadIdx.x + 1) * CPT && B0 + k < g.L; ++k) next[B0 + k] = s_out[k];
   }
   sum = __reduce_add_sync(0xffffffffu, sum);
   wraps = __reduce_add_sync(0xffffffffu, wraps);
@@ -219,7 +285,8 @@ __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __re
 }
 
 __global__ void grid_compact_kernel(const uint8_t* __restrict__ cells, uint32_t L,
-                                    const uint32_t* __restrict__ prefix, uint32_t* xs, uint8_t* vs) {
+                                    const uint32_t* __restrict__ local, const uint32_t* __restrict__ group,
+                                    uint32_t* xs, uint8_t* vs) {
   constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
   const uint32_t lo = blockIdx.x * kCellsPerBlock + threadIdx.x * CPT;
   uint32_t occ = 0;
@@ -233,7 +300,7 @@ __global__ void grid_compact_kernel(const uint8_t* __restrict__ cells, uint32_t 
   __shared__ uint32_t s_w[kGridTPB / 32];
   if (lane == 31) s_w[warp] = incl;
   __syncthreads();
-  uint32_t r = prefix[blockIdx.x] + incl - occ;
+  uint32_t r = local[blockIdx.x] + group[blockIdx.x >> 10] + incl - occ;
   for (uint32_t w = 0; w < warp; ++w) r += s_w[w];
   for (uint32_t k = 0; k < CPT; ++k) {
     if (lo + k < L && cells[lo + k] != kEmpty) {
@@ -258,7 +325,8 @@ struct GpuGrid::Impl {
   uint32_t L = 0, N = 0, vmax = 0, nb = 0;
   uint8_t* cells[2] = {nullptr, nullptr};
   int cur = 0;
-  uint32_t *counts = nullptr, *prefix = nullptr, *xs = nullptr;
+  uint32_t *counts = nullptr, *local = nullptr, *group = nullptr, *xs = nullptr;
+  uint32_t ng = 0;  // 1024-block groups of the two-level scan
   uint8_t* vs = nullptr;
   StepRec* rec = nullptr;
   StepRec* hrec = nullptr;  // pinned [kRecCap]
@@ -277,12 +345,17 @@ struct GpuGrid::Impl {
   unsigned long long* dhash = nullptr;
   ~Impl();
 
+  void scan() {
+    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group);
+    grid_scan_top<<<1, 1024, 0, stream>>>(group, ng);
+  }
+
   void compact() {
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
-    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
-    grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, prefix, xs, vs);
+    scan();
+    grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, local, group, xs, vs);
     CKG(cudaGetLastError());
-    launches += 3;
+    launches += 4;
   }
 
   // Folds the current row (positions, then velocities) into the device
@@ -320,14 +393,13 @@ struct GpuGrid::Impl {
   void step() {
     if (steps_done - drained >= kRecCap / 2) drain();
     const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
-    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, pw, steps_done};
+    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, powmod(kA, 32), pw, steps_done};
     CKG(cudaMemsetAsync(rec + (steps_done % kRecCap), 0, sizeof(StepRec), stream));
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
-    grid_scan_kernel<<<1, 1024, 0, stream>>>(counts, nb, prefix);
-    CKG(cudaMemsetAsync(cells[cur ^ 1], kEmpty, L, stream));
-    grid_move_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], prefix, g, rec);
+    scan();
+    grid_move_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], local, group, g, rec);
     CKG(cudaGetLastError());
-    launches += 3;
+    launches += 4;
     cur ^= 1;
     ++steps_done;
   }
@@ -394,7 +466,9 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   CKG(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) CKG(cudaMalloc(&d.cells[b], d.L));
   CKG(cudaMalloc(&d.counts, size_t(d.nb) * 4));
-  CKG(cudaMalloc(&d.prefix, size_t(d.nb) * 4));
+  d.ng = (d.nb + 1023) / 1024;
+  CKG(cudaMalloc(&d.local, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.group, size_t(d.ng) * 4));
   CKG(cudaMalloc(&d.xs, size_t(d.N) * 4));
   CKG(cudaMalloc(&d.vs, d.N));
   CKG(cudaMalloc(&d.rec, sizeof(StepRec) * kRecCap));
@@ -427,7 +501,8 @@ GpuGrid::Impl::~Impl() {
   if (stream) cudaStreamSynchronize(stream);
   for (int b = 0; b < 2; ++b) cudaFree(cells[b]);
   cudaFree(counts);
-  cudaFree(prefix);
+  cudaFree(local);
+  cudaFree(group);
   cudaFree(xs);
   cudaFree(vs);
   cudaFree(rec);
