@@ -44,11 +44,14 @@ def ev_time(stream, fn):
 
 def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None, cores=1):
     x, v = nasch.fill_uniform_state(L, N, vinit, seed)
-    prm = nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T + 8, seed=seed)
+    # untimed warm-up as bench.py: >= 512 steps (launch-graph capture on the
+    # first chunk, SM clock ramp from idle), capped at T for the small rings
+    warm = max(8, min(512, T))
+    prm = nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T + warm, seed=seed)
     e = nasch.Engine(prm)
     e.set_checksum(False)
     e.set_state(x, v)
-    e.advance(8)  # warm-up
+    e.advance(warm)
     snaps = []
     if snapshot_every:
         # double-buffered snapshots: snapshot i is copied on the device and
