@@ -104,9 +104,13 @@ class HostPool {
   }
 
  private:
+  // Workers: NASCH_B200_HOST_THREADS, else the hardware threads (at most 64).
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    for (unsigned t = 1; t < std::min(hw, 32u); ++t) workers_.emplace_back([this] { loop(); });
+    const char* e = std::getenv("NASCH_B200_HOST_THREADS");
+    const long want = e && *e ? std::strtol(e, nullptr, 10) : long(hw);
+    const unsigned n = static_cast<unsigned>(std::max(1l, std::min(want, 64l)));
+    for (unsigned t = 1; t < n; ++t) workers_.emplace_back([this] { loop(); });
   }
   void loop() {
     for (;;) {
