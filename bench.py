@@ -259,8 +259,9 @@ def run_ours(args, rank, world, local_rank):
     # ---- device-resident throughput -----------------------------------
     prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=W_run + K, seed=seed)
     if world > 1:
-        # one ring, G contiguous segments, halo + cone window all-gathered
-        # over NCCL once per K-step launch
+        # one ring, G contiguous segments; the halo + cone-window records
+        # are stored into the peer GPUs' HBM by the step kernel once per
+        # K-step launch (NCCL all-gather as fallback; DESIGN.md sections 4.6, 6)
         box = [nasch.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         nccl_id = box[0]

@@ -58,6 +58,8 @@ struct NcclApi {
   ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 
@@ -72,9 +74,10 @@ struct NcclApi {
     get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(handle, "ncclGetUniqueId"));
     comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(handle, "ncclCommInitRank"));
     all_gather = reinterpret_cast<decltype(all_gather)>(dlsym(handle, "ncclAllGather"));
+    all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(handle, "ncclAllReduce"));
     comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(handle, "ncclCommDestroy"));
     error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
-    if (!get_unique_id || !comm_init_rank || !all_gather || !comm_destroy || !error_string)
+    if (!get_unique_id || !comm_init_rank || !all_gather || !all_reduce || !comm_destroy || !error_string)
       throw std::runtime_error("libnccl.so.2 lacks a required symbol");
   }
   void check(ncclResult_t r, const char* what) const {
@@ -169,6 +172,14 @@ struct ShardedRing::Impl {
   // the ranks' host threads.
   bool p2p = false;
   uint32_t xseq = 0;  // launches published through the peer exchange
+  // One process per GPU: this rank's per-step crossing counts and the
+  // planned (whole-ring) counts of drained steps not yet checked; their sum
+  // over the ranks must equal the plan (verify_ranks, at every collective
+  // synchronisation point).
+  std::vector<uint32_t> pend_c, pend_plan;
+  uint64_t pend_first = 0;
+  uint32_t* dcheck = nullptr;  // device scratch for the all-reduce
+  size_t dcheck_cap = 0;
   std::vector<Shard> sh;  // shards held by this process
   bool exchanged_once = false;
   ~Impl();
@@ -572,12 +583,47 @@ struct ShardedRing::Impl {
       if (!use_nccl && c != sh[0].hrec[k].cplan)
         throw std::runtime_error("origin-cone plan contradicted at step " + std::to_string(first + k) +
                                  " (engine state is invalid)");
+      if (use_nccl) {
+        if (pend_c.empty()) pend_first = first + k;
+        pend_c.push_back(static_cast<uint32_t>(c));
+        pend_plan.push_back(sh[0].hrec[k].cplan);
+      }
       sumv_host.push_back(sv);
       wraps_host.push_back(use_nccl ? sh[0].hrec[k].cplan : c);
     }
     W_host = sh[0].hctl->W;
     buf_host = sh[0].hctl->buf;
     drained = steps_done;
+  }
+
+  // Collective (every rank calls it at the same point of the same call
+  // sequence: the end of advance and synchronize): all-reduce the drained
+  // steps' crossing counts and compare the ring's totals with the plan.
+  void verify_ranks() {
+    if (!use_nccl || pend_c.empty()) return;
+    Shard& s = sh[0];
+    CKS(cudaSetDevice(s.device));
+    const size_t n = pend_c.size();
+    if (n > dcheck_cap) {
+      if (dcheck) CKS(cudaFree(dcheck));
+      dcheck = nullptr;
+      CKS(cudaMalloc(&dcheck, n * 4));
+      dcheck_cap = n;
+    }
+    NcclApi& api = NcclApi::get();
+    CKS(cudaMemcpyAsync(dcheck, pend_c.data(), n * 4, cudaMemcpyHostToDevice, s.stream));
+    api.check(api.all_reduce(dcheck, dcheck, n, ncclUint32, ncclSum, comm, s.stream), "ncclAllReduce(crossings)");
+    std::vector<uint32_t> tot(n);
+    CKS(cudaMemcpyAsync(tot.data(), dcheck, n * 4, cudaMemcpyDeviceToHost, s.stream));
+    CKS(cudaStreamSynchronize(s.stream));
+    const uint64_t first = pend_first;
+    pend_c.clear();
+    std::vector<uint32_t> plan;
+    plan.swap(pend_plan);
+    for (size_t k = 0; k < n; ++k)
+      if (tot[k] != plan[k])
+        throw std::runtime_error("origin-cone plan contradicted at step " + std::to_string(first + k) +
+                                 " (summed over the ranks; engine state is invalid)");
   }
 
   void require_local(const char* what) const {
@@ -738,7 +784,10 @@ struct ShardedRing::Impl {
           record_frame_staged();
         }
       }
-      if (sync) drain();
+      if (sync) {
+        drain();
+        verify_ranks();
+      }
       return;
     }
     for (uint64_t k = 0; k < count; ++k) {
@@ -783,6 +832,7 @@ struct ShardedRing::Impl {
       default: break;
     }
     drain();
+    verify_ranks();
     for (Shard& s : sh) {
       CKS(cudaSetDevice(s.device));
       std::vector<uint32_t> sx(s.nl);
@@ -896,6 +946,8 @@ ShardedRing::Impl::~Impl() {
     if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.stream) cudaStreamDestroy(s.stream);
   }
+  if (!d.sh.empty()) cudaSetDevice(d.sh[0].device);
+  cudaFree(d.dcheck);
   if (d.comm) NcclApi::get().comm_destroy(d.comm);
   cudaFreeHost(d.hx);
   cudaFreeHost(d.hv);
@@ -905,7 +957,10 @@ void ShardedRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) { im
 void ShardedRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) { impl_->load_state(x, v, n); }
 void ShardedRing::advance(uint64_t steps) { impl_->advance(steps, true); }
 void ShardedRing::enqueue(uint64_t steps) { impl_->advance(steps, false); }
-void ShardedRing::synchronize() { impl_->drain(); }
+void ShardedRing::synchronize() {
+  impl_->drain();
+  impl_->verify_ranks();
+}
 uint64_t ShardedRing::steps_done() const { return impl_->steps_done; }
 uint64_t ShardedRing::checksum() const { return impl_->hash; }
 const std::vector<Frame>& ShardedRing::frames() const { return impl_->frames; }
