@@ -9,8 +9,9 @@
 //   GpuRing      the whole ring on the current GPU
 //   ShardedRing  contiguous car segments on several GPUs (or several
 //                segments on one GPU), exchanging a halo + the origin-cone
-//                window once per launch: in-process peer copies, or NCCL with
-//                one process per GPU (sharded.cu)
+//                window once per launch: stores into peer HBM from the step
+//                kernel (default), or peer copies / NCCL all-gather with one
+//                process per GPU (sharded.cu)
 #pragma once
 #include <cstddef>
 #include <cstdint>

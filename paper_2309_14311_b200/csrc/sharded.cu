@@ -4,14 +4,18 @@
 // Shard g holds global ids [lo_g, lo_g+1) with lo_g = floor(g*N/G) -- the
 // reference's own block formula (src/engine.cpp:31-42) -- plus a 16-car halo
 // inline after its cars.  Each launch advances every shard K steps with the
-// temporal-blocked kernel (tb_kernel.cuh, sharded mode), then
-//   pack  -> all-gather of 2 KB records -> plan (+ halo copy)
-// (shard_kernels.cuh).  Draws are indexed by global rank, so the trajectory
-// is bit-identical for any shard count, as the reference's is for any
-// OpenMP team size.  The all-gather is NCCL (one process per GPU) or, for
-// shards of one process, stream-ordered peer copies with events: that mode
-// also runs several shards on ONE GPU, which is how the sharded path is
-// tested bit-exactly here.
+// temporal-blocked kernel (tb_kernel.cuh, sharded mode); the shards then
+// exchange one 2 KB record each (first cars + the origin-cone slots they
+// own) and every shard plans the next launch from the same window
+// (shard_kernels.cuh).  Default exchange: the step kernel's last block
+// stores the record into every shard's HBM (peer pointers; IPC-mapped
+// across processes) and raises a flag the plan kernel waits on.  Collective
+// exchange (construction, set_state, or NASCH_B200_XCHG=collective): pack ->
+// NCCL all-gather (one process per GPU) or stream-ordered peer copies
+// (shards of one process) -> plan.  Shards of one process may share ONE GPU,
+// which is how the sharded path is tested bit-exactly here.  Draws are
+// indexed by global rank, so the trajectory is bit-identical for any shard
+// count, as the reference's is for any OpenMP team size.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: the library is opened at run time
