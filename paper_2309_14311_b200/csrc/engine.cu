@@ -265,9 +265,16 @@ struct GpuRing::Impl {
       // Block width by ring size: a per-step barrier across 32 warps costs
       // more than a few extra cars per thread on a tiny ring (C1: 200 cars).
       if (vbytes == 1) {
-        if (warp_ring && n <= 128) ring_warp_kernel<uint8_t, 4><<<1, 32, 0, stream>>>(args, k);
-        else if (warp_ring && n <= 256) ring_warp_kernel<uint8_t, 8><<<1, 32, 0, stream>>>(args, k);
-        else if (warp_ring && n <= 512) ring_warp_kernel<uint8_t, 16><<<1, 32, 0, stream>>>(args, k);
+        if (warp_ring && n <= 128) {
+          if (n % 4 == 0) ring_warp_kernel<uint8_t, 4, true><<<1, 32, 0, stream>>>(args, k);
+          else ring_warp_kernel<uint8_t, 4><<<1, 32, 0, stream>>>(args, k);
+        } else if (warp_ring && n <= 256) {
+          if (n % 8 == 0) ring_warp_kernel<uint8_t, 8, true><<<1, 32, 0, stream>>>(args, k);
+          else ring_warp_kernel<uint8_t, 8><<<1, 32, 0, stream>>>(args, k);
+        } else if (warp_ring && n <= 512) {
+          if (n % 16 == 0) ring_warp_kernel<uint8_t, 16, true><<<1, 32, 0, stream>>>(args, k);
+          else ring_warp_kernel<uint8_t, 16><<<1, 32, 0, stream>>>(args, k);
+        }
         else if (n <= 256) ring_resident_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args, k);
         else ring_resident_kernel<uint8_t, kResidentTPB><<<1, kResidentTPB, 0, stream>>>(args, k);
       } else {

@@ -134,7 +134,12 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
 // a^(id-N) for the far side of the rank seam), so the draws of a lane's
 // cars are independent products rather than a chain.  BASELINE config 1
 // (200 cars) is bound by this per-step latency.
-template <typename VT, int CPW>
+//
+// EXACT (N a multiple of CPW, e.g. C1: 200 = 25 x 8): every lane holds CPW
+// live cars or none, so the per-car work has no liveness predicate and no
+// leader select -- the last live lane's external leader is car 0, chosen
+// once per step -- and the dead lanes' sums are masked once per step.
+template <typename VT, int CPW, bool EXACT = false>
 __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, const uint32_t steps) {
   __shared__ uint32_t apw[256];
   Ctl* ctl = ra.ctl;
@@ -173,9 +178,28 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
   for (uint32_t st = 0; st < steps; ++st) {
     const uint32_t bound = N - W;
     const uint32_t nextw = mulmod_x2(candw2, E), nextn = mulmod_x2(candn2, E);
-    const uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
+    uint32_t xn = __shfl_down_sync(0xffffffffu, x[0], 1);
     const uint32_t x00 = __shfl_sync(0xffffffffu, x[0], 0);  // leader of car N-1
     uint32_t sum = 0, crs = 0;
+    if constexpr (EXACT) {
+      if (lane == last_lane) xn = x00;
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        const uint32_t s = mulmod_x2(first + c < bound ? apA[c] : apB[c], E);
+        const uint32_t xl = c + 1 < CPW ? x[c + 1] : xn;
+        uint32_t d = xl - x[c];
+        d = min(d, d + L);  // leader past the origin: + L
+        const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
+        int dec;
+        asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+        v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+        const uint32_t xs = x[c] + v[c];
+        x[c] = min(xs, xs - L);
+        sum += v[c];
+        crs += xs >= L ? 1u : 0u;
+      }
+      if (!live) sum = crs = 0;  // dead lane
+    } else
 #pragma unroll
     for (int c = 0; c < CPW; ++c) {
       const uint32_t id = first + c;

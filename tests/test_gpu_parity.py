@@ -453,8 +453,9 @@ def resident_env():
 @pytest.mark.parametrize("resident", ["0", "1", "cta"])
 def test_small_ring_kernels(port, resident_env, resident):
     """Rings below the temporal-blocking threshold: the one-warp register
-    kernel (N <= 512, default), the one-CTA shared-memory kernel and the
-    one-step-per-launch kernel agree with the oracle, including vmax > 255
+    kernel (N <= 512, default; N a multiple of the cars per lane takes its
+    EXACT path: 200, 512, 128, 320, 96), the one-CTA shared-memory kernel and
+    the one-step-per-launch kernel agree with the oracle, including vmax > 255
     (u32 velocity lanes), N = 1 and long runs."""
     os.environ["NASCH_B200_RESIDENT"] = "0" if resident == "0" else "1"
     os.environ["NASCH_B200_WARPRING"] = "0" if resident == "cta" else "1"
@@ -462,7 +463,8 @@ def test_small_ring_kernels(port, resident_env, resident):
     for trial, (L, N, vmax, p, T) in enumerate([(1000, 200, 5, 0.13, 1000), (4096, 4000, 5, 0.3, 300),
                                                 (6000, 900, 300, 0.2, 200), (50, 49, 5, 0.5, 500),
                                                 (3, 1, 5, 0.5, 100), (700, 512, 9, 0.4, 300),
-                                                (300, 130, 300, 0.3, 200), (129, 128, 5, 0.6, 400)]):
+                                                (300, 130, 300, 0.3, 200), (129, 128, 5, 0.6, 400),
+                                                (400, 320, 5, 0.3, 300), (2000, 96, 7, 0.1, 500)]):
         x0 = np.sort(rng.choice(L, N, replace=False)).astype(np.uint64)
         v0 = rng.integers(0, min(vmax, L - 1) + 1, N).astype(np.uint64)
         o = port.run(L, vmax, p, 31 + trial, T, x0, v0)
