@@ -277,6 +277,8 @@ def run_ours(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = eng.kernel_launches
+    xmode = {0: "none (one segment)", 1: "collective (NCCL all-gather)",
+             2: "peer memory (records stored by the step kernel into the peers' HBM)"}[eng.exchange_mode]
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         eng.enqueue(K)
@@ -379,7 +381,8 @@ def run_ours(args, rank, world, local_rank):
                        "timed_steps": f"steps {W_run}..{W_run + K - 1} of the run",
                        "l2": "no flush: 2.0 GB ping-pong state >> 126 MB L2",
                        "checksum": "off (nasch_sim_set_checksum(0); the reference cannot disable it)",
-                       "parallelism": "1 GPU" if world == 1 else f"{world} ranks"},
+                       "parallelism": "1 GPU" if world == 1 else f"{world} ranks",
+                       **({"segment_exchange": xmode} if world > 1 else {})},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_update": SURVEY_BYTES_PER_UPDATE,
@@ -390,7 +393,7 @@ def run_ours(args, rank, world, local_rank):
                          "state_gbs_moved": moved_gbs,
                          "note": "temporal blocking: the state crosses HBM once per "
                                  f"{spl} steps, so frac > 1 vs the per-step roofline; "
-                                 "the kernel is integer-issue bound (DESIGN.md 4.2)"},
+                                 "the kernel is integer-issue bound (DESIGN.md 4.1)"},
             "issue_bound": issue_bound(launch_ms, spl, N, clk.summary()),
             "e2e": {"value": e2e_value, "unit": "car-updates/s", "h2d_bytes_per_step": e2e_h2d,
                     "d2h_bytes_per_step": e2e_d2h,
