@@ -199,7 +199,10 @@ uint32_t nasch_b200_draw_threshold(double p);
  * reports its own segment: sumv/mean-velocity series are this rank's
  * partial sums (the whole-ring series is their sum over ranks), the wrap
  * series is the whole ring's, and whole-ring calls (state, observables,
- * checksum, frames) return NASCH_ERR_INVALID. */
+ * frames) return NASCH_ERR_INVALID.  The trajectory checksum is off by
+ * default; nasch_sim_set_checksum(sim, 1) on every rank turns it on (each
+ * step's FNV chunk maps are all-gathered over NCCL and every rank composes
+ * the whole-ring digest). */
 nasch_status nasch_nccl_unique_id(void* out128);
 nasch_status nasch_sim_new_distributed(const nasch_params* params, unsigned rank,
                                        unsigned world, const void* nccl_id,

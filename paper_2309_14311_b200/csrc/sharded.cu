@@ -184,6 +184,7 @@ struct ShardedRing::Impl {
   uint64_t pend_first = 0;
   uint32_t* dcheck = nullptr;  // device scratch for the all-reduce
   size_t dcheck_cap = 0;
+  unsigned long long* dhash_x = nullptr;  // checksum piece exchange (one process per GPU)
   std::vector<Shard> sh;  // shards held by this process
   bool exchanged_once = false;
   ~Impl();
@@ -744,12 +745,42 @@ struct ShardedRing::Impl {
       }
     }
     sync_all();
+    // One process per GPU: every rank's piece maps go to every rank (one
+    // all-gather of fixed 4-piece records), and all ranks compose the same
+    // row, so the checksum is available on each of them.
+    std::vector<unsigned long long> all;  // [rank][piece][row0, 256 T, P]
+    if (use_nccl) {
+      constexpr size_t kRec = 4 * 258;
+      Shard& s = sh[0];
+      std::vector<unsigned long long> mine(kRec, ~0ull);
+      for (const Piece& pc : pieces) {
+        unsigned long long* d = mine.data() + pc.slot * 258;
+        d[0] = pc.row0;
+        std::memcpy(d + 1, s.hpiece + pc.slot * 257, 257 * sizeof(unsigned long long));
+      }
+      if (!dhash_x) CKS(cudaMalloc(&dhash_x, (G + 1) * kRec * sizeof(unsigned long long)));
+      NcclApi& api = NcclApi::get();
+      CKS(cudaMemcpyAsync(dhash_x, mine.data(), kRec * 8, cudaMemcpyHostToDevice, s.stream));
+      api.check(api.all_gather(dhash_x, dhash_x + kRec, kRec, ncclUint64, comm, s.stream), "ncclAllGather(checksum)");
+      all.resize(G * kRec);
+      CKS(cudaMemcpyAsync(all.data(), dhash_x + kRec, all.size() * 8, cudaMemcpyDeviceToHost, s.stream));
+      CKS(cudaStreamSynchronize(s.stream));
+      pieces.clear();
+      for (size_t r = 0; r < G; ++r)
+        for (size_t q = 0; q < 4; ++q) {
+          const unsigned long long* d = all.data() + (r * 4 + q) * 258;
+          if (d[0] != ~0ull) pieces.push_back({d[0], r, q});
+        }
+    }
+    auto piece_map = [&](const Piece& pc) -> const unsigned long long* {
+      return use_nccl ? all.data() + (pc.shard * 4 + pc.slot) * 258 + 1 : sh[pc.shard].hpiece + pc.slot * 257;
+    };
     std::sort(pieces.begin(), pieces.end(), [](const Piece& a, const Piece& b) { return a.row0 < b.row0; });
     // compose in row order: (P1, T1) then (P2, T2) = (P2 P1, l -> P2 T1[l] + T2[(P1 l + T1[l]) & 0xff])
     unsigned long long P = 1, T[256];
     for (int l = 0; l < 256; ++l) T[l] = 0;
     for (const Piece& pc : pieces) {
-      const unsigned long long* t2 = sh[pc.shard].hpiece + pc.slot * 257;
+      const unsigned long long* t2 = piece_map(pc);
       const unsigned long long p2 = t2[256];
       unsigned long long nt[256];
       for (int l = 0; l < 256; ++l) nt[l] = p2 * T[l] + t2[(P * static_cast<unsigned long long>(l) + T[l]) & 0xffu];
@@ -803,6 +834,7 @@ struct ShardedRing::Impl {
         record_frame_staged();
       }
     }
+    verify_ranks();
   }
 
   template <typename T>
@@ -880,7 +912,7 @@ struct ShardedRing::Impl {
         record_frame_staged();
       }
     } else {
-      checksum_on = false;  // a distributed shard never holds the whole ring
+      checksum_on = false;  // off by default (one all-gather per step when switched on)
     }
   }
 };
@@ -952,6 +984,7 @@ ShardedRing::Impl::~Impl() {
   }
   if (!d.sh.empty()) cudaSetDevice(d.sh[0].device);
   cudaFree(d.dcheck);
+  cudaFree(d.dhash_x);
   if (d.comm) NcclApi::get().comm_destroy(d.comm);
   cudaFreeHost(d.hx);
   cudaFreeHost(d.hv);
@@ -1012,7 +1045,7 @@ size_t ShardedRing::wrap_series(uint64_t* out, size_t cap) {
 }
 
 void ShardedRing::set_checksum(bool enabled) {
-  if (enabled) impl_->require_local("the trajectory checksum");
+
   impl_->checksum_on = enabled;
 }
 void* ShardedRing::cuda_stream() const { return impl_->sh.empty() ? nullptr : impl_->sh[0].stream; }

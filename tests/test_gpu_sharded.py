@@ -186,3 +186,21 @@ def test_p2p_exchange_resume_and_many_launches(port, xchg):
     assert (x == o2["x"]).all() and (v == o2["v"]).all()
     assert (e.sumv_series()[-200:] == o2["sumv"]).all()
     e.close()
+
+
+def test_distributed_checksum_single_rank(port, xchg):
+    """The one-process-per-GPU ring with the trajectory checksum switched
+    on: per-step piece maps all-gathered over NCCL (1-rank communicator)
+    and composed on the host equal the reference's serial FNV-1a."""
+    L, N, vmax, p, T = 40000, 12000, 5, 0.3, 40
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 8)
+    o = port.run(L, vmax, p, 3, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    e = nasch.Engine.distributed(mk(L, N, vmax, p, T, 3), 0, 1, nasch.nccl_unique_id())
+    e.set_checksum(True)
+    e.set_state(x0, v0)
+    e.advance(17)
+    e.advance(T)
+    assert e.checksum == o["checksum"]
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    e.close()
