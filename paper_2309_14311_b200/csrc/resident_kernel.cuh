@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
   const uint32_t candw2 = c_pow.lin[lane] << 1;
   const uint32_t candn2 = mulmod(ra.an, c_pow.lin[lane]) << 1;
   uint32_t W = ctl->W, E = ctl->E;
+  uint32_t rsum = 0, rc = 0, rW = 0;  // batched step record (lane = step mod 32)
   __syncwarp();
   for (uint32_t st = 0; st < steps; ++st) {
     const uint32_t bound = N - W;
@@ -220,11 +221,20 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
     }
     const uint32_t cj = __reduce_add_sync(0xffffffffu, crs);
     sum = __reduce_add_sync(0xffffffffu, sum);
-    if (lane == 0) {
-      StepRec* r = ra.rec + ((t0 + st) % kRecCap);
-      r->sumv = sum;
-      r->c = cj;
-      r->W = W;
+    // Step records in batches of 32: lane (st mod 32) keeps this step's,
+    // and the warp stores 32 at once (no per-step store on the chain).
+    if (lane == (st & 31u)) {
+      rsum = sum;
+      rc = cj;
+      rW = W;
+    }
+    if ((st & 31u) == 31u || st + 1 == steps) {
+      if (lane <= (st & 31u)) {
+        StepRec* r = ra.rec + ((t0 + (st & ~31u) + lane) % kRecCap);
+        r->sumv = rsum;
+        r->c = rc;
+        r->W = rW;
+      }
     }
     uint32_t Wn = W + cj;
     const bool wrap = Wn >= N;
