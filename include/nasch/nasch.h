@@ -195,14 +195,19 @@ uint32_t nasch_b200_draw_threshold(double p);
  * engine.cpp:31-42) over the visible GPUs of this process; the trajectory is
  * bit-identical for every G.  One process per GPU instead: rank 0 calls
  * nasch_nccl_unique_id, the launcher broadcasts the 128 bytes, and every rank
- * calls nasch_sim_new_distributed.  A distributed sim advances, times and
- * reports its own segment: sumv/mean-velocity series are this rank's
- * partial sums (the whole-ring series is their sum over ranks), the wrap
- * series is the whole ring's, and whole-ring calls (state, observables,
- * frames) return NASCH_ERR_INVALID.  The trajectory checksum is off by
- * default; nasch_sim_set_checksum(sim, 1) on every rank turns it on (each
- * step's FNV chunk maps are all-gathered over NCCL and every rank composes
- * the whole-ring digest). */
+ * calls nasch_sim_new_distributed.  A distributed sim steps its own segment;
+ * the calls that see the whole ring are COLLECTIVE -- every rank makes them,
+ * in the same order: advance/run, synchronize, set_state, state,
+ * observables, the sumv / mean-velocity / wrap series (whole-ring values on
+ * every rank: one all-reduce of the drained steps' records), and frame
+ * capture inside advance (every rank records whole-ring frames).  state()
+ * broadcasts each segment over NCCL; a rank passing NULL arrays only takes
+ * part.  enqueue and the segment calls below are local.  A failure one rank
+ * detects outside a collective is raised on every rank at the next
+ * collective call.  The trajectory checksum is off by default;
+ * nasch_sim_set_checksum(sim, 1) on every rank turns it on (each step's FNV
+ * chunk maps are all-gathered over NCCL and every rank composes the
+ * whole-ring digest). */
 nasch_status nasch_nccl_unique_id(void* out128);
 nasch_status nasch_sim_new_distributed(const nasch_params* params, unsigned rank,
                                        unsigned world, const void* nccl_id,
@@ -218,6 +223,24 @@ nasch_status nasch_sim_shard_range(const nasch_sim* sim, uint64_t* first,
  * GPUs can map each other's memory; env NASCH_B200_XCHG=collective forces
  * 1).  Construction and set_state always use the collective path. */
 unsigned nasch_sim_exchange_mode(const nasch_sim* sim);
+/* Segment snapshot: the cars this process
+ * holds (nasch_sim_shard_range), widened to u64, element k at rank
+ * (*first_rank + k) mod N -- each rank writes its own piece of a snapshot
+ * with no collective.  On a sim holding the whole ring: nasch_sim_state
+ * with *first_rank = 0.  The _async form copies the segment on the device
+ * and returns; nasch_sim_state_wait completes the host copy. */
+nasch_status nasch_sim_state_segment(nasch_sim* sim, uint64_t* positions,
+                                     uint64_t* velocities, size_t capacity,
+                                     uint64_t* first_rank);
+nasch_status nasch_sim_state_segment_async(nasch_sim* sim, uint64_t* positions,
+                                           uint64_t* velocities, size_t capacity,
+                                           uint64_t* first_rank);
+/* Collective set_state from each rank's own segment of the new rank-ordered
+ * state (count = this rank's shard_range count); validation of the links
+ * between segments and of every rule is agreed over NCCL, so all ranks
+ * accept or reject together.  On a sim holding the whole ring: set_state. */
+nasch_status nasch_sim_set_state_segment(nasch_sim* sim, const uint64_t* positions,
+                                         const uint64_t* velocities, size_t count);
 
 /* ---- ensembles of independent rings (extension) ------------------------
  * One handle advances many independent simulations at once -- BASELINE
@@ -234,6 +257,11 @@ size_t nasch_ensemble_size(const nasch_ensemble* ens);
 nasch_status nasch_ensemble_set_state32(nasch_ensemble* ens, size_t ring,
                                         const uint32_t* positions,
                                         const uint32_t* velocities, size_t count);
+/* Every ring's state at once: rings concatenated in ring order, ring r's
+ * count = its ncars (total = sum of ncars); validated on all host cores,
+ * one upload.  Same rules as nasch_ensemble_set_state32. */
+nasch_status nasch_ensemble_set_state_all32(nasch_ensemble* ens, const uint32_t* positions,
+                                            const uint32_t* velocities, size_t total);
 /* Every ring advances min(steps, its remaining steps). */
 nasch_status nasch_ensemble_advance(nasch_ensemble* ens, uint64_t steps);
 nasch_status nasch_ensemble_enqueue(nasch_ensemble* ens, uint64_t steps);

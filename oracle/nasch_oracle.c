@@ -205,3 +205,47 @@ int or_run(uint64_t L, uint64_t vmax, double p, uint64_t* rng, uint64_t steps,
   free(tmp);
   return 0;
 }
+
+/*
+ * The BASELINE.json input generator: seeded
+ * uniform DISTINCT sorted positions by selection sampling over the cells
+ * 0..L-1 (cell c is taken with probability need/left, decided on 32
+ * splitmix64 bits as floor(r * left / 2^32) < need), and velocities
+ * uniform in [0, vmax_init] from a second splitmix64 stream.  This is not
+ * a reference function -- the reference only has init_state -- but the
+ * generator that feeds BOTH arms of the benchmark; it is restated here so
+ * the reference arm (bench.py --impl reference) never loads the product
+ * library.  tests/test_oracle.py checks it equal to
+ * nasch_fill_uniform_state of libnasch_b200.so.  Returns 0, or 1 if
+ * N > L or L >= 2^32.
+ */
+static uint64_t or_splitmix64(uint64_t* s) {
+  uint64_t z = (*s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+int or_fill_uniform_state(uint64_t L, uint64_t N, uint64_t vmax_init, uint64_t seed,
+                          uint32_t* x, uint32_t* v) {
+  if (N > L || L > 0xffffffffull) return 1;
+  uint64_t s = seed * 0x2545f4914f6cdd1dull + 0x1234567ull;
+  uint64_t need = N, k = 0, c = 0;
+  while (need > 0 && c < L) {
+    const uint64_t left = L - c;
+    if (need == left) { /* every remaining cell is taken */
+      while (c < L) x[k++] = (uint32_t)c++;
+      break;
+    }
+    const uint64_t r = or_splitmix64(&s) >> 32;
+    if (((r * left) >> 32) < need) {
+      x[k++] = (uint32_t)c;
+      --need;
+    }
+    ++c;
+  }
+  uint64_t sv = seed ^ 0xa5a5a5a5deadbeefull;
+  for (uint64_t i = 0; i < N; ++i)
+    v[i] = vmax_init ? (uint32_t)(((or_splitmix64(&sv) >> 32) * (vmax_init + 1)) >> 32) : 0u;
+  return 0;
+}

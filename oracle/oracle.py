@@ -78,6 +78,10 @@ class Port:
                                C.c_uint64, _u64p, _u64p, C.c_size_t, _u64p,
                                _u64p, _u64p]
         lib.or_run.restype = C.c_int
+        _u32p = C.POINTER(C.c_uint32)
+        lib.or_fill_uniform_state.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64,
+                                              C.c_uint64, _u32p, _u32p]
+        lib.or_fill_uniform_state.restype = C.c_int
         self.lib = lib
 
     # -- PRNG ------------------------------------------------------------
@@ -101,6 +105,20 @@ class Port:
         mul, add = C.c_uint64(), C.c_uint64()
         self.lib.or_jump_coefficients(k, C.byref(mul), C.byref(add))
         return mul.value, add.value
+
+    # -- BASELINE input generator (not a reference function) ----------------
+    def fill_uniform_state(self, L: int, N: int, vmax_init: int, seed: int):
+        """Seeded uniform distinct sorted positions and velocities in
+        [0, vmax_init], both u32 -- the same inputs nasch_fill_uniform_state
+        gives the GPU arm (tests/test_oracle.py checks equality)."""
+        x = np.empty(N, np.uint32)
+        v = np.empty(N, np.uint32)
+        u32 = C.POINTER(C.c_uint32)
+        rc = self.lib.or_fill_uniform_state(L, N, vmax_init, seed, x.ctypes.data_as(u32),
+                                            v.ctypes.data_as(u32))
+        if rc:
+            raise ValueError("need N <= L < 2^32")
+        return x, v
 
     # -- model -----------------------------------------------------------
     def init_state(self, L: int, N: int):
@@ -164,7 +182,7 @@ class Ref:
         lib = C.CDLL(path)
         lib.refh_run.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
                                  C.c_uint64, C.c_uint64, C.c_uint, _u64p, _u64p,
-                                 C.c_int, _u64p, _u64p, _u64p, _u64p,
+                                 C.c_int, _u64p, _u64p, _u64p, _u64p, _u64p,
                                  C.POINTER(C.c_double)]
         lib.refh_run.restype = C.c_int
         lib.refh_last_error.restype = C.c_char_p
@@ -176,18 +194,21 @@ class Ref:
 
     def run(self, L, N, vmax, p, seed, steps, *, workers=1, x0=None, v0=None,
             per_step=True, want_state=True):
-        """Returns dict(x, v, sumv, checksum, seconds)."""
+        """Returns dict(x, v, sumv, wraps, checksum, seconds); sumv / wraps
+        (per-step velocity sums and crossing counts) only with per_step."""
         x0 = None if x0 is None else np.ascontiguousarray(x0, np.uint64)
         v0 = None if v0 is None else np.ascontiguousarray(v0, np.uint64)
         x = np.empty(N, np.uint64) if want_state else None
         v = np.empty(N, np.uint64) if want_state else None
         sumv = np.empty(max(steps, 1), np.uint64) if per_step else None
+        wraps = np.empty(max(steps, 1), np.uint64) if per_step else None
         h = C.c_uint64()
         sec = C.c_double()
         rc = self.lib.refh_run(L, N, vmax, p, seed, steps, workers, _ptr(x0),
                                _ptr(v0), 1 if per_step else 0, _ptr(x),
-                               _ptr(v), _ptr(sumv), C.byref(h), C.byref(sec))
+                               _ptr(v), _ptr(sumv), _ptr(wraps), C.byref(h), C.byref(sec))
         if rc != 0:
             raise RuntimeError(self.lib.refh_last_error().decode())
         return dict(x=x, v=v, sumv=None if sumv is None else sumv[:steps],
+                    wraps=None if wraps is None else wraps[:steps],
                     checksum=h.value, seconds=sec.value)

@@ -54,14 +54,16 @@ unsigned refh_physical_cores(void) { return nasch::detect_physical_cores(); }
 // Runs the reference Engine for `steps` steps with `workers` OpenMP
 // workers.  x0/v0 (rank order, length N) replace init_state when non-null.
 // per_step != 0: advance(1) at a time and record the exact velocity sum
-// after every step into sumv_series (if non-null).  per_step == 0: one
+// after every step into sumv_series and the step's crossing count (the
+// sum of the workers' wrap_counts_, src/engine.cpp:144-153) into
+// wrap_series (each if non-null).  per_step == 0: one
 // advance(steps) call, timed with steady_clock exactly like
 // `nasch bench` (tools/nasch_cli.cpp:346-351); *seconds receives it.
 int refh_run(uint64_t L, uint64_t N, uint64_t vmax, double p, uint64_t seed,
              uint64_t steps, unsigned workers, const uint64_t* x0,
              const uint64_t* v0, int per_step, uint64_t* x_out,
-             uint64_t* v_out, uint64_t* sumv_series, uint64_t* checksum,
-             double* seconds) {
+             uint64_t* v_out, uint64_t* sumv_series, uint64_t* wrap_series,
+             uint64_t* checksum, double* seconds) {
   try {
     const nasch::SimParams params = make_params(L, N, vmax, p, seed, steps);
     nasch::Engine engine(params, workers);
@@ -75,6 +77,11 @@ int refh_run(uint64_t L, uint64_t N, uint64_t vmax, double p, uint64_t seed,
           uint64_t total = 0;
           for (uint64_t vi : engine.agent_.velocities) total += vi;
           sumv_series[t] = total;
+        }
+        if (wrap_series) {
+          uint64_t wrapped = 0;
+          for (uint64_t c : engine.wrap_counts_) wrapped += c;
+          wrap_series[t] = wrapped;
         }
       }
     } else {

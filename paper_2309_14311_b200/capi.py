@@ -87,11 +87,15 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "nasch_sim_new_distributed": (C.c_int, [_P, C.c_uint, C.c_uint, C.c_void_p, C.POINTER(_P)]),
     "nasch_sim_shard_range": (C.c_int, [_P, _u64p, _u64p]),
+    "nasch_sim_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
+    "nasch_sim_state_segment_async": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
+    "nasch_sim_set_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t]),
     # ensembles
     "nasch_ensemble_new": (C.c_int, [C.POINTER(_P), C.c_size_t, C.POINTER(_P)]),
     "nasch_ensemble_free": (None, [_P]),
     "nasch_ensemble_size": (C.c_size_t, [_P]),
     "nasch_ensemble_set_state32": (C.c_int, [_P, C.c_size_t, _u32p, _u32p, C.c_size_t]),
+    "nasch_ensemble_set_state_all32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t]),
     "nasch_ensemble_advance": (C.c_int, [_P, _u64]),
     "nasch_ensemble_enqueue": (C.c_int, [_P, _u64]),
     "nasch_ensemble_synchronize": (C.c_int, [_P]),

@@ -64,91 +64,6 @@ constexpr int kGraphLaunches = 16;
 constexpr int kResidentTPB = 1024;
 constexpr uint32_t kResidentChunk = kRecCap / 4;  // steps per resident launch
 
-// Persistent host worker pool for the ABI's conversion loops (a C3 state()
-// splits into ~13 pieces of 16 threads each: spawning threads per piece
-// cost milliseconds).  Callers post one batch of chunk jobs and help run it;
-// several callers (the main thread and a snapshot thread) may post at once.
-class HostPool {
- public:
-  static HostPool& get() {
-    // never destroyed: a snapshot thread may still use it during exit
-    static HostPool* pool = new HostPool;
-    return *pool;
-  }
-  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
-  // Runs job(i) for i in [0, count); returns when all are done.  The
-  // batch state is shared with the queued helpers, so a helper that starts
-  // after the batch finished finds no work and touches nothing else.
-  void run(unsigned count, std::function<void(unsigned)> job) {
-    struct State {
-      std::atomic<unsigned> next{0}, done{0};
-      unsigned count = 0;
-      std::function<void(unsigned)> job;
-    };
-    auto st = std::make_shared<State>();
-    st->count = count;
-    st->job = std::move(job);
-    auto drain = [st] {
-      for (unsigned i; (i = st->next.fetch_add(1)) < st->count;) {
-        st->job(i);
-        st->done.fetch_add(1);
-      }
-    };
-    {
-      std::lock_guard<std::mutex> lk(m_);
-      for (unsigned w = 0; w + 1 < count && w < workers_.size(); ++w) tasks_.push_back(drain);
-    }
-    cv_.notify_all();
-    drain();
-    while (st->done.load() < count) std::this_thread::yield();
-  }
-
- private:
-  // Workers: NASCH_B200_HOST_THREADS, else the hardware threads (at most 64).
-  HostPool() {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const char* e = std::getenv("NASCH_B200_HOST_THREADS");
-    const long want = e && *e ? std::strtol(e, nullptr, 10) : long(hw);
-    const unsigned n = static_cast<unsigned>(std::max(1l, std::min(want, 64l)));
-    for (unsigned t = 1; t < n; ++t) workers_.emplace_back([this] { loop(); });
-  }
-  void loop() {
-    for (;;) {
-      std::function<void()> t;
-      {
-        std::unique_lock<std::mutex> lk(m_);
-        cv_.wait(lk, [&] { return stop_ || !tasks_.empty(); });
-        if (stop_ && tasks_.empty()) return;
-        t = std::move(tasks_.front());
-        tasks_.pop_front();
-      }
-      t();
-    }
-  }
-  std::vector<std::thread> workers_;
-  std::deque<std::function<void()>> tasks_;
-  std::mutex m_;
-  std::condition_variable cv_;
-  bool stop_ = false;  // never set: the pool lives for the process
-};
-
-// Runs f(lo, hi) over [0, n) in parallel host chunks (input validation and
-// u64 <-> u32 conversion at the ABI; large rings only).
-template <typename F>
-void parallel_chunks(size_t n, F&& f) {
-  HostPool& pool = HostPool::get();
-  const unsigned nt = static_cast<unsigned>(std::min<size_t>(pool.size(), n / (1u << 20) + 1));
-  if (nt <= 1) {
-    f(size_t(0), n);
-    return;
-  }
-  const size_t chunk = (n + nt - 1) / nt;
-  pool.run(nt, [&](unsigned t) {
-    const size_t lo = t * chunk, hi = std::min(n, lo + chunk);
-    if (lo < hi) f(lo, hi);
-  });
-}
-
 long env_long(const char* name, long fallback) {
   const char* s = std::getenv(name);
   if (!s || !*s) return fallback;

@@ -54,6 +54,20 @@ class RingEngine {
   // arrays are complete after state_wait().  Default: synchronous.
   virtual void state_async(uint64_t* positions, uint64_t* velocities) { state(positions, velocities); }
   virtual void state_wait() {}
+  // Extension for rings split over processes: the cars this process holds
+  // (shard_range), element k at rank (*first_rank + k) mod N.  Not a
+  // collective call.  Engines holding the whole ring return it in rank
+  // order with *first_rank = 0.  The async form completes at state_wait().
+  virtual void state_segment(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {
+    state(positions, velocities);
+    if (first_rank) *first_rank = 0;
+  }
+  virtual void state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {
+    state_segment(positions, velocities, first_rank);
+  }
+  // Extension: set_state from this process's segment only (the ids of
+  // shard_range in the new rank order); the whole ring elsewhere.
+  virtual void set_state_segment(const uint64_t* x, const uint64_t* v, size_t n) { set_state(x, v, n); }
   // Extension: exact velocity sum / wrap count after each completed step.
   virtual size_t sumv_series(uint64_t* out, size_t cap) = 0;
   virtual size_t wrap_series(uint64_t* out, size_t cap) = 0;
@@ -132,6 +146,10 @@ class ShardedRing : public RingEngine {
   const SimParams& params() const override;
   void observables(double* density, double* mean_velocity, double* flow) override;
   void state(uint64_t* positions, uint64_t* velocities) override;
+  void state_segment(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) override;
+  void state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) override;
+  void state_wait() override;
+  void set_state_segment(const uint64_t* x, const uint64_t* v, size_t n) override;
   size_t sumv_series(uint64_t* out, size_t cap) override;
   size_t wrap_series(uint64_t* out, size_t cap) override;
   void set_checksum(bool enabled) override;

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -25,6 +26,7 @@
 #include <vector>
 
 #include "engine.hpp"
+#include "host_simd.hpp"
 #include "ensemble.hpp"
 #include "minstd.hpp"
 #include "tb_config.hpp"
@@ -239,6 +241,10 @@ struct GpuEnsemble::Impl {
   EnsArgs ea{};
   EnsRing* h_trings = nullptr;
   int tgrid = 1;
+  // pinned staging in the tiled layout (set_state_all32)
+  size_t stage_cars = 0;
+  uint32_t* h_stage_x = nullptr;
+  uint8_t* h_stage_v = nullptr;
 
   void tpull() {
     if (!dirty) return;
@@ -348,6 +354,7 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
       total += (er.n + 15) / 16 * 16;  // 16-car aligned rings: vector loads
     }
     const size_t pad = total + kEtLoad + 16;
+    d.stage_cars = total;
     for (int b = 0; b < 2; ++b) {
       CKE(cudaMalloc(&d.ea.X[b], pad * 4));
       CKE(cudaMalloc(&d.ea.V[b], pad));
@@ -475,6 +482,8 @@ GpuEnsemble::Impl::~Impl() {
   cudaFree(const_cast<EnsTile*>(ea.tiles));
   cudaFree(const_cast<uint32_t*>(ea.thrpow));
   cudaFreeHost(h_trings);
+  cudaFreeHost(h_stage_x);
+  cudaFreeHost(h_stage_v);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -540,6 +549,81 @@ void GpuEnsemble::set_state32(size_t ring, const uint32_t* x, const uint32_t* v,
   for (size_t i = 0; i < n; ++i) s += v[i];
   rd.last_sumv = static_cast<uint32_t>(s);
   d.push();
+}
+
+void GpuEnsemble::set_state_all32(const uint32_t* x, const uint32_t* v, size_t total) {
+  Impl& d = *impl_;
+  CKE(cudaSetDevice(d.device));
+  const size_t R = d.params.size();
+  std::vector<size_t> start(R + 1, 0);
+  for (size_t r = 0; r < R; ++r) start[r + 1] = start[r] + d.params[r].car_count;
+  if (total != start[R]) throw std::invalid_argument("state length must equal the ensemble's total car count");
+  if (!d.tiled) {  // shared-memory layout: ring by ring
+    for (size_t r = 0; r < R; ++r)
+      set_state32(r, x + start[r], v + start[r], start[r + 1] - start[r]);
+    return;
+  }
+  d.tpull();
+  const size_t pad = d.stage_cars;
+  if (!d.h_stage_x) {
+    CKE(cudaMallocHost(&d.h_stage_x, pad * 4));
+    CKE(cudaMallocHost(&d.h_stage_v, pad));
+    std::memset(d.h_stage_x, 0, pad * 4);
+    std::memset(d.h_stage_v, 0, pad);
+  }
+  // rings validated and packed into the tiled layout in parallel; the
+  // lowest failing ring's rule is reported
+  std::vector<int> err(R, 0);
+  std::vector<uint32_t> sums(R, 0);
+  const unsigned jobs = static_cast<unsigned>(std::min<size_t>(R, 4 * size_t(host_threads())));
+  host_run(jobs, [&](unsigned j) {
+    for (size_t r = j; r < R; r += jobs) {
+      const EnsRing& er = d.trings[r];
+      const SimParams& p = d.params[r];
+      const uint32_t* xr = x + start[r];
+      const uint32_t* vr = v + start[r];
+      uint32_t* ox = d.h_stage_x + er.off;
+      uint8_t* ov = d.h_stage_v + er.off;
+      uint64_t s = 0;
+      int e = 0;
+      for (size_t i = 0; i < er.n && !e; ++i) {
+        if (xr[i] >= er.L) e = 1;
+        else if (i && xr[i - 1] >= xr[i]) e = 2;
+        else if (vr[i] > p.v_max) e = 3;
+        else if (vr[i] > er.vmax) e = 4;
+        ox[i] = xr[i];
+        ov[i] = static_cast<uint8_t>(vr[i]);
+        s += vr[i];
+      }
+      err[r] = e;
+      sums[r] = static_cast<uint32_t>(s);
+    }
+  });
+  for (size_t r = 0; r < R; ++r) {
+    switch (err[r]) {
+      case 1: throw std::invalid_argument("position out of range [0, length)");
+      case 2: throw std::invalid_argument("positions must be strictly increasing");
+      case 3: throw std::invalid_argument("velocity above vmax");
+      case 4: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      default: break;
+    }
+  }
+  // one upload into each buffer a ring reads from (the other buffer of a
+  // ring is its step output, so overwriting it there is harmless)
+  bool used[2] = {false, false};
+  for (const EnsRing& er : d.trings) used[er.buf & 1u] = true;
+  for (int b = 0; b < 2; ++b) {
+    if (!used[b]) continue;
+    CKE(cudaMemcpyAsync(d.ea.X[b], d.h_stage_x, pad * 4, cudaMemcpyHostToDevice, d.stream));
+    CKE(cudaMemcpyAsync(d.ea.V[b], d.h_stage_v, pad, cudaMemcpyHostToDevice, d.stream));
+  }
+  for (size_t r = 0; r < R; ++r) {
+    EnsRing& er = d.trings[r];
+    er.W = 0;
+    er.k = 0;
+    er.last_sumv = sums[r];
+  }
+  d.tpush();
 }
 
 void GpuEnsemble::enqueue(uint64_t steps) {

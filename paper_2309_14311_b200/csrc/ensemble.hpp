@@ -29,6 +29,9 @@ class GpuEnsemble {
   size_t size() const;
   // Rank-ordered state of one ring (same validation as GpuRing::set_state).
   void set_state32(size_t ring, const uint32_t* x, const uint32_t* v, size_t n);
+  // Every ring at once: rings concatenated in ring order (total = sum of
+  // ncars), validated in parallel host chunks, one upload.
+  void set_state_all32(const uint32_t* x, const uint32_t* v, size_t total);
   // Advances every ring by min(steps, its remaining steps); synchronous.
   void advance(uint64_t steps);
   void enqueue(uint64_t steps);

@@ -3,6 +3,16 @@
 // semantics and the fallback.
 #include "host_simd.hpp"
 
+#include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <cstdlib>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <vector>
+
 #if defined(__x86_64__)
 #include <immintrin.h>
 #endif
@@ -10,6 +20,79 @@
 namespace nb200 {
 
 namespace {
+
+// Persistent host worker pool for the ABI's conversion loops (a C3 state()
+// splits into ~13 pieces of 16 threads each: spawning threads per piece
+// cost milliseconds).  Callers post one batch of chunk jobs and help run it;
+// several callers (the main thread and a snapshot thread) may post at once.
+class HostPool {
+ public:
+  static HostPool& get() {
+    // never destroyed: a snapshot thread may still use it during exit
+    static HostPool* pool = new HostPool;
+    return *pool;
+  }
+  unsigned size() const { return static_cast<unsigned>(workers_.size()) + 1; }
+  // Runs job(i) for i in [0, count); returns when all are done.  The
+  // batch state is shared with the queued helpers, so a helper that starts
+  // after the batch finished finds no work and touches nothing else.
+  void run(unsigned count, std::function<void(unsigned)> job) {
+    struct State {
+      std::atomic<unsigned> next{0}, done{0};
+      unsigned count = 0;
+      std::function<void(unsigned)> job;
+    };
+    auto st = std::make_shared<State>();
+    st->count = count;
+    st->job = std::move(job);
+    auto drain = [st] {
+      for (unsigned i; (i = st->next.fetch_add(1)) < st->count;) {
+        st->job(i);
+        st->done.fetch_add(1);
+      }
+    };
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      for (unsigned w = 0; w + 1 < count && w < workers_.size(); ++w) tasks_.push_back(drain);
+    }
+    cv_.notify_all();
+    drain();
+    while (st->done.load() < count) std::this_thread::yield();
+  }
+
+ private:
+  // Workers: NASCH_B200_HOST_THREADS, else the hardware threads shared by
+  // the processes of this node (LOCAL_WORLD_SIZE, set by torchrun, so eight
+  // ranks of one box do not each spin a thread per core), at most 64.
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const char* e = std::getenv("NASCH_B200_HOST_THREADS");
+    const char* lw = std::getenv("LOCAL_WORLD_SIZE");
+    const long local = lw && *lw ? std::max(1l, std::strtol(lw, nullptr, 10)) : 1l;
+    const long want = e && *e ? std::strtol(e, nullptr, 10) : std::max(1l, long(hw) / local);
+    const unsigned n = static_cast<unsigned>(std::max(1l, std::min(want, 64l)));
+    for (unsigned t = 1; t < n; ++t) workers_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    for (;;) {
+      std::function<void()> t;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return stop_ || !tasks_.empty(); });
+        if (stop_ && tasks_.empty()) return;
+        t = std::move(tasks_.front());
+        tasks_.pop_front();
+      }
+      t();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::deque<std::function<void()>> tasks_;
+  std::mutex m_;
+  std::condition_variable cv_;
+  bool stop_ = false;  // never set: the pool lives for the process
+};
+
 
 void widen_u32_scalar(const uint32_t* src, uint64_t* dst, size_t n) {
   for (size_t i = 0; i < n; ++i) dst[i] = src[i];
@@ -160,5 +243,9 @@ int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, 
   }
   return 0;
 }
+
+unsigned host_threads() { return HostPool::get().size(); }
+
+void host_run(unsigned count, std::function<void(unsigned)> job) { HostPool::get().run(count, std::move(job)); }
 
 }  // namespace nb200

@@ -5,7 +5,9 @@
 // writes use non-temporal stores (no read-for-ownership of the destination).
 #pragma once
 #include <cstddef>
+#include <algorithm>
 #include <cstdint>
+#include <functional>
 
 namespace nb200 {
 
@@ -19,5 +21,26 @@ void widen_u8(const uint8_t* src, uint64_t* dst, size_t n);
 // [lo, hi); `prev` is x[lo - 1] (ignored when lo == 0).
 int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
                     uint64_t vlim, uint32_t* x32, void* vout, int vbytes);
+
+// Persistent host worker pool (host_simd.cpp): job(i) for i in [0, count)
+// on the pool's threads and the caller; returns when all are done.
+unsigned host_threads();
+void host_run(unsigned count, std::function<void(unsigned)> job);
+
+// Runs f(lo, hi) over [0, n) in parallel host chunks (input validation and
+// u64 <-> u32 conversion at the ABI; large rings only).
+template <typename F>
+void parallel_chunks(size_t n, F&& f) {
+  const unsigned nt = static_cast<unsigned>(std::min<size_t>(host_threads(), n / (1u << 20) + 1));
+  if (nt <= 1) {
+    f(size_t(0), n);
+    return;
+  }
+  const size_t chunk = (n + nt - 1) / nt;
+  host_run(nt, [&](unsigned t) {
+    const size_t lo = t * chunk, hi = std::min(n, lo + chunk);
+    if (lo < hi) f(lo, hi);
+  });
+}
 
 }  // namespace nb200

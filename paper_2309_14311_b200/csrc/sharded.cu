@@ -27,9 +27,12 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <type_traits>
+#include <exception>
 #include <vector>
 
 #include "engine.hpp"
+#include "host_simd.hpp"
 #include "minstd.hpp"
 #include "fnv_kernels.cuh"
 #include "shard_kernels.cuh"
@@ -64,6 +67,8 @@ struct NcclApi {
                              cudaStream_t) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 
@@ -79,33 +84,17 @@ struct NcclApi {
     comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(handle, "ncclCommInitRank"));
     all_gather = reinterpret_cast<decltype(all_gather)>(dlsym(handle, "ncclAllGather"));
     all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(handle, "ncclAllReduce"));
+    broadcast = reinterpret_cast<decltype(broadcast)>(dlsym(handle, "ncclBroadcast"));
     comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(handle, "ncclCommDestroy"));
     error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
-    if (!get_unique_id || !comm_init_rank || !all_gather || !all_reduce || !comm_destroy || !error_string)
+    if (!get_unique_id || !comm_init_rank || !all_gather || !all_reduce || !broadcast || !comm_destroy ||
+        !error_string)
       throw std::runtime_error("libnccl.so.2 lacks a required symbol");
   }
   void check(ncclResult_t r, const char* what) const {
     if (r != ncclSuccess) throw std::runtime_error(std::string("NCCL error in ") + what + ": " + error_string(r));
   }
 };
-
-template <typename F>
-void par_chunks(size_t n, F&& f) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const unsigned nt = static_cast<unsigned>(std::min<size_t>(std::min(hw, 32u), n / (1u << 20) + 1));
-  if (nt <= 1) {
-    f(size_t(0), n);
-    return;
-  }
-  const size_t chunk = (n + nt - 1) / nt;
-  std::vector<std::thread> pool;
-  for (unsigned t = 0; t < nt; ++t) {
-    const size_t lo = t * chunk, hi = std::min(n, lo + chunk);
-    if (lo >= hi) break;
-    pool.emplace_back([&f, lo, hi] { f(lo, hi); });
-  }
-  for (auto& th : pool) th.join();
-}
 
 }  // namespace
 
@@ -160,6 +149,13 @@ struct ShardedRing::Impl {
     unsigned long long* fT[2] = {nullptr, nullptr};
     unsigned long long* fP[2] = {nullptr, nullptr};
     unsigned long long* hpiece = nullptr;  // pinned: up to 4 pieces x (256 + 1)
+    // pinned staging of this shard's segment: set_state narrowing and
+    // segment snapshots (allocated on first use)
+    uint32_t* hx_stage = nullptr;
+    void* hv_stage = nullptr;
+    // device copy of the segment for an asynchronous segment snapshot
+    uint32_t* snap_x = nullptr;
+    void* snap_v = nullptr;
   };
 
   SimParams params;
@@ -180,10 +176,24 @@ struct ShardedRing::Impl {
   // planned (whole-ring) counts of drained steps not yet checked; their sum
   // over the ranks must equal the plan (verify_ranks, at every collective
   // synchronisation point).
+  // The drained steps' local velocity sums go through the same all-reduce,
+  // so every rank ends up with the WHOLE ring's per-step series.
   std::vector<uint32_t> pend_c, pend_plan;
+  std::vector<uint64_t> pend_sv;
   uint64_t pend_first = 0;
-  uint32_t* dcheck = nullptr;  // device scratch for the all-reduce
+  uint64_t* dcheck = nullptr;  // device scratch for the all-reduce
   size_t dcheck_cap = 0;
+  // One process per GPU: a failure detected outside a collective call
+  // (drain) is kept here and raised on EVERY rank at the next collective
+  // synchronisation point (verify_ranks), so no rank is left waiting in a
+  // collective its peer never reaches.  Once raised, the engine is
+  // poisoned: every later call repeats the error.
+  std::string local_err, poisoned;
+  // asynchronous segment snapshot (one process per GPU)
+  cudaStream_t snap_stream = nullptr;
+  cudaEvent_t snap_ready = nullptr;
+  std::thread snap_thread;
+  std::exception_ptr snap_error;
   unsigned long long* dhash_x = nullptr;  // checksum piece exchange (one process per GPU)
   std::vector<Shard> sh;  // shards held by this process
   bool exchanged_once = false;
@@ -555,6 +565,8 @@ struct ShardedRing::Impl {
   }
 
   // Per-step records of [drained, steps_done), summed over local shards.
+  // Local only (no collective): with one process per GPU the records wait
+  // in pend_* for verify_ranks, and any inconsistency is deferred there.
   void drain() {
     if (drained == steps_done) return;
     const uint64_t first = drained, count = steps_done - drained;
@@ -571,13 +583,17 @@ struct ShardedRing::Impl {
     }
     sync_all();
     for (const Shard& s : sh) {
+      std::string e;
       if (s.hctl->err == 3u)
-        throw std::runtime_error("peer exchange timed out on shard " + std::to_string(s.g) +
-                                 " (a rank stopped publishing; engine state is invalid)");
-      if (s.hctl->t != steps_done)
-        throw std::runtime_error("device step counter out of sync on shard " + std::to_string(s.g));
-      if (s.hctl->W != sh[0].hctl->W || s.hctl->buf != sh[0].hctl->buf)
-        throw std::runtime_error("shards disagree on the rank offset");
+        e = "peer exchange timed out on shard " + std::to_string(s.g) +
+            " (a rank stopped publishing; engine state is invalid)";
+      else if (s.hctl->t != steps_done)
+        e = "device step counter out of sync on shard " + std::to_string(s.g);
+      else if (s.hctl->W != sh[0].hctl->W || s.hctl->buf != sh[0].hctl->buf)
+        e = "shards disagree on the rank offset";
+      if (e.empty()) continue;
+      if (!use_nccl) throw std::runtime_error(e);
+      if (local_err.empty()) local_err = e;
     }
     for (uint64_t k = 0; k < count; ++k) {
       uint64_t sv = 0, c = 0;
@@ -585,83 +601,141 @@ struct ShardedRing::Impl {
         sv += s.hrec[k].sumv;
         c += s.hrec[k].c;
       }
-      if (!use_nccl && c != sh[0].hrec[k].cplan)
-        throw std::runtime_error("origin-cone plan contradicted at step " + std::to_string(first + k) +
-                                 " (engine state is invalid)");
       if (use_nccl) {
         if (pend_c.empty()) pend_first = first + k;
         pend_c.push_back(static_cast<uint32_t>(c));
         pend_plan.push_back(sh[0].hrec[k].cplan);
+        pend_sv.push_back(sv);
+        continue;
       }
+      if (c != sh[0].hrec[k].cplan)
+        throw std::runtime_error("origin-cone plan contradicted at step " + std::to_string(first + k) +
+                                 " (engine state is invalid)");
       sumv_host.push_back(sv);
-      wraps_host.push_back(use_nccl ? sh[0].hrec[k].cplan : c);
+      wraps_host.push_back(c);
     }
     W_host = sh[0].hctl->W;
     buf_host = sh[0].hctl->buf;
     drained = steps_done;
   }
 
-  // Collective (every rank calls it at the same point of the same call
-  // sequence: the end of advance and synchronize): all-reduce the drained
-  // steps' crossing counts and compare the ring's totals with the plan.
+  void check_poison() const {
+    if (!poisoned.empty()) throw std::runtime_error(poisoned);
+  }
+
+  // Collective with one process per GPU (every rank calls it at the same
+  // point of the same call sequence: the end of advance, synchronize, the
+  // series / observables / state accessors, set_state): one all-reduce of
+  // the drained steps' crossing counts, velocity sums and an error flag.
+  // The ring's crossing totals are compared with the plan, the velocity
+  // sums become the whole ring's series, and a failure seen by any rank is
+  // raised by all of them.  Other modes: drain only.
   void verify_ranks() {
-    if (!use_nccl || pend_c.empty()) return;
+    check_poison();
+    drain();
+    if (!use_nccl) return;
     Shard& s = sh[0];
     CKS(cudaSetDevice(s.device));
     const size_t n = pend_c.size();
-    if (n > dcheck_cap) {
+    const size_t words = 2 * n + 1;
+    if (words > dcheck_cap) {
       if (dcheck) CKS(cudaFree(dcheck));
       dcheck = nullptr;
-      CKS(cudaMalloc(&dcheck, n * 4));
-      dcheck_cap = n;
+      CKS(cudaMalloc(&dcheck, words * 8));
+      dcheck_cap = words;
     }
+    std::vector<uint64_t> buf(words);
+    for (size_t k = 0; k < n; ++k) {
+      buf[k] = pend_c[k];
+      buf[n + k] = pend_sv[k];
+    }
+    buf[2 * n] = local_err.empty() ? 0u : 1u;
     NcclApi& api = NcclApi::get();
-    CKS(cudaMemcpyAsync(dcheck, pend_c.data(), n * 4, cudaMemcpyHostToDevice, s.stream));
-    api.check(api.all_reduce(dcheck, dcheck, n, ncclUint32, ncclSum, comm, s.stream), "ncclAllReduce(crossings)");
-    std::vector<uint32_t> tot(n);
-    CKS(cudaMemcpyAsync(tot.data(), dcheck, n * 4, cudaMemcpyDeviceToHost, s.stream));
+    CKS(cudaMemcpyAsync(dcheck, buf.data(), words * 8, cudaMemcpyHostToDevice, s.stream));
+    api.check(api.all_reduce(dcheck, dcheck, words, ncclUint64, ncclSum, comm, s.stream),
+              "ncclAllReduce(step records)");
+    CKS(cudaMemcpyAsync(buf.data(), dcheck, words * 8, cudaMemcpyDeviceToHost, s.stream));
     CKS(cudaStreamSynchronize(s.stream));
     const uint64_t first = pend_first;
-    pend_c.clear();
     std::vector<uint32_t> plan;
     plan.swap(pend_plan);
-    for (size_t k = 0; k < n; ++k)
-      if (tot[k] != plan[k])
-        throw std::runtime_error("origin-cone plan contradicted at step " + std::to_string(first + k) +
-                                 " (summed over the ranks; engine state is invalid)");
-  }
-
-  void require_local(const char* what) const {
-    if (use_nccl && G > 1)
-      throw std::invalid_argument(std::string(what) + " needs the whole ring; this process holds one "
-                                  "shard of a distributed ring");
-  }
-
-  // Whole ring in rank order into the staging buffers (in-process mode).
-  void fetch_rank_order() {
-    require_local("state");
-    std::vector<uint32_t> gx(n);
-    std::vector<uint8_t> gv8(vbytes == 1 ? n : 0);
-    std::vector<uint32_t> gv32(vbytes == 4 ? n : 0);
-    for (Shard& s : sh) {
-      CKS(cudaSetDevice(s.device));
-      CKS(cudaMemcpyAsync(gx.data() + s.gofs, s.x[buf_host], size_t(s.nl) * 4, cudaMemcpyDeviceToHost, s.stream));
-      if (vbytes == 1)
-        CKS(cudaMemcpyAsync(gv8.data() + s.gofs, s.v[buf_host], s.nl, cudaMemcpyDeviceToHost, s.stream));
-      else
-        CKS(cudaMemcpyAsync(gv32.data() + s.gofs, s.v[buf_host], size_t(s.nl) * 4, cudaMemcpyDeviceToHost, s.stream));
+    pend_c.clear();
+    pend_sv.clear();
+    if (buf[2 * n]) {
+      poisoned = local_err.empty() ? "another rank of the distributed ring failed (engine state is invalid)"
+                                   : local_err + " (raised on every rank; engine state is invalid)";
+      throw std::runtime_error(poisoned);
     }
-    sync_all();
-    const uint32_t head = (n - W_host) % n;
-    par_chunks(n, [&](size_t a, size_t b) {
-      for (size_t k = a; k < b; ++k) {
-        size_t id = head + k;
-        if (id >= n) id -= n;
-        hx[k] = gx[id];
-        if (vbytes == 1) static_cast<uint8_t*>(hv)[k] = gv8[id];
-        else static_cast<uint32_t*>(hv)[k] = gv32[id];
+    for (size_t k = 0; k < n; ++k)
+      if (buf[k] != plan[k]) {
+        poisoned = "origin-cone plan contradicted at step " + std::to_string(first + k) +
+                   " (summed over the ranks; engine state is invalid)";
+        throw std::runtime_error(poisoned);
       }
-    });
+    for (size_t k = 0; k < n; ++k) {
+      sumv_host.push_back(buf[n + k]);
+      wraps_host.push_back(plan[k]);
+    }
+  }
+
+  void ensure_full_staging() {
+    if (hx) return;
+    CKS(cudaMallocHost(&hx, size_t(n) * 4));
+    CKS(cudaMallocHost(&hv, size_t(n) * vbytes));
+  }
+
+  void ensure_stage(Shard& s) {
+    if (s.hx_stage) return;
+    CKS(cudaMallocHost(&s.hx_stage, size_t(s.nl) * 4 + 64));
+    CKS(cudaMallocHost(&s.hv_stage, size_t(s.nl) * vbytes + 64));
+  }
+
+  // Device -> pinned staging of the ids [id0, id0 + cnt) held at (dx, dv),
+  // placed at their ranks (rank = (id + W) mod N: at most two pieces).
+  void d2h_at_ranks(const uint32_t* dx, const void* dv, uint32_t id0, uint32_t cnt, cudaStream_t st) {
+    const uint32_t r0 = static_cast<uint32_t>((uint64_t(id0) + W_host) % n);
+    const uint32_t m1 = std::min<uint32_t>(cnt, n - r0);
+    const char* dvb = static_cast<const char*>(dv);
+    char* hvb = static_cast<char*>(hv);
+    CKS(cudaMemcpyAsync(hx + r0, dx, size_t(m1) * 4, cudaMemcpyDeviceToHost, st));
+    CKS(cudaMemcpyAsync(hvb + size_t(r0) * vbytes, dvb, size_t(m1) * vbytes, cudaMemcpyDeviceToHost, st));
+    if (m1 < cnt) {
+      CKS(cudaMemcpyAsync(hx, dx + m1, size_t(cnt - m1) * 4, cudaMemcpyDeviceToHost, st));
+      CKS(cudaMemcpyAsync(hvb, dvb + size_t(m1) * vbytes, size_t(cnt - m1) * vbytes, cudaMemcpyDeviceToHost, st));
+    }
+  }
+
+  // The whole ring in rank order into the pinned staging (hx, hv); needs
+  // drained == steps_done.  Segments of this process: stream-ordered D2H
+  // straight to their ranks.  One process per GPU (collective: every rank
+  // calls it): segment r is broadcast from rank r into every other rank's
+  // idle ping-pong buffer (NCCL over NVLink) and copied down by the ranks
+  // that want the ring (`want`); the others only take part.
+  void gather_rank_order(bool want) {
+    if (want) ensure_full_staging();
+    if (!use_nccl) {
+      for (Shard& s : sh) {
+        CKS(cudaSetDevice(s.device));
+        d2h_at_ranks(s.x[buf_host], s.v[buf_host], s.gofs, s.nl, s.stream);
+      }
+      sync_all();
+      return;
+    }
+    Shard& s = sh[0];
+    CKS(cudaSetDevice(s.device));
+    NcclApi& api = NcclApi::get();
+    const unsigned idle = buf_host ^ 1u;
+    for (unsigned r = 0; r < G; ++r) {
+      const uint32_t nl_r = lo[r + 1] - lo[r];
+      uint32_t* xb = r == s.g ? s.x[buf_host] : s.x[idle];
+      void* vb = r == s.g ? s.v[buf_host] : s.v[idle];
+      api.check(api.broadcast(xb, xb, size_t(nl_r) * 4, ncclUint8, static_cast<int>(r), comm, s.stream),
+                "ncclBroadcast(state x)");
+      api.check(api.broadcast(vb, vb, size_t(nl_r) * vbytes, ncclUint8, static_cast<int>(r), comm, s.stream),
+                "ncclBroadcast(state v)");
+      if (want) d2h_at_ranks(xb, vb, lo[r], nl_r, s.stream);
+    }
+    CKS(cudaStreamSynchronize(s.stream));
   }
 
   uint32_t hvel(size_t i) const {
@@ -673,13 +747,114 @@ struct ShardedRing::Impl {
            steps_done % params.output_stride == 0;
   }
 
-  void record_frame_staged() {
+  // src/engine.cpp:81-86 -- every rank records the whole ring (collective
+  // with one process per GPU, like the reference's frames in one process).
+  void record_frame() {
+    drain();
+    gather_rank_order(true);
     Frame f;
     f.step = steps_done;
-    f.positions.assign(hx, hx + n);
+    f.positions.resize(n);
     f.velocities.resize(n);
-    for (uint32_t i = 0; i < n; ++i) f.velocities[i] = hvel(i);
+    widen_staging(f.positions.data(), f.velocities.data());
     frames.push_back(std::move(f));
+  }
+
+  // Rank-ordered staging -> caller's u64 arrays (either may be null).
+  void widen_staging(uint64_t* positions, uint64_t* velocities) const {
+    parallel_chunks(n, [&](size_t a, size_t b) {
+      if (positions) widen_u32(hx + a, positions + a, b - a);
+      if (velocities) {
+        if (vbytes == 1) widen_u8(static_cast<const uint8_t*>(hv) + a, velocities + a, b - a);
+        else widen_u32(static_cast<const uint32_t*>(hv) + a, velocities + a, b - a);
+      }
+    });
+  }
+
+  // This process's segment (one process per GPU) in id order, D2H from
+  // (dx, dv) in 16M-car pieces on `st`, each widened into the caller's
+  // arrays while the next one is in flight.
+  void segment_to_host(Shard& s, const uint32_t* dx, const void* dv, uint64_t* positions, uint64_t* velocities,
+                       cudaStream_t st) {
+    ensure_stage(s);
+    constexpr uint32_t kChunk = 1u << 24;
+    std::vector<cudaEvent_t> evs;
+    for (uint32_t c0 = 0; c0 < s.nl; c0 += kChunk) {
+      const uint32_t m = std::min<uint32_t>(kChunk, s.nl - c0);
+      cudaEvent_t ev;
+      CKS(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      if (positions) CKS(cudaMemcpyAsync(s.hx_stage + c0, dx + c0, size_t(m) * 4, cudaMemcpyDeviceToHost, st));
+      if (velocities)
+        CKS(cudaMemcpyAsync(static_cast<char*>(s.hv_stage) + size_t(c0) * vbytes,
+                            static_cast<const char*>(dv) + size_t(c0) * vbytes, size_t(m) * vbytes,
+                            cudaMemcpyDeviceToHost, st));
+      CKS(cudaEventRecord(ev, st));
+      evs.push_back(ev);
+    }
+    cudaError_t err = cudaSuccess;
+    for (size_t i = 0; i < evs.size(); ++i) {
+      if (err == cudaSuccess) err = cudaEventSynchronize(evs[i]);
+      if (err == cudaSuccess) {
+        const size_t c0 = i * size_t(kChunk), m = std::min<size_t>(kChunk, s.nl - c0);
+        parallel_chunks(m, [&](size_t a, size_t b) {
+          a += c0;
+          b += c0;
+          if (positions) widen_u32(s.hx_stage + a, positions + a, b - a);
+          if (velocities) {
+            if (vbytes == 1) widen_u8(static_cast<const uint8_t*>(s.hv_stage) + a, velocities + a, b - a);
+            else widen_u32(static_cast<const uint32_t*>(s.hv_stage) + a, velocities + a, b - a);
+          }
+        });
+      }
+      cudaEventDestroy(evs[i]);
+    }
+    CKS(err);
+  }
+
+  void snap_join() {
+    if (snap_thread.joinable()) snap_thread.join();
+    if (snap_error) {
+      std::exception_ptr e = snap_error;
+      snap_error = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+
+  // Segment snapshot: the rank of the segment's first car, after a local
+  // drain (no collective: each rank writes its own piece).
+  uint64_t segment_first_rank() const { return (uint64_t(sh[0].gofs) + W_host) % n; }
+
+  void state_segment(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank, bool async) {
+    check_poison();
+    snap_join();
+    drain();
+    Shard& s = sh[0];
+    CKS(cudaSetDevice(s.device));
+    if (first_rank) *first_rank = segment_first_rank();
+    if (!async) {
+      segment_to_host(s, s.x[buf_host], s.v[buf_host], positions, velocities, s.stream);
+      return;
+    }
+    // device copy now (stream-ordered before the next step), D2H and
+    // widening on a host thread while the ring keeps stepping
+    if (!s.snap_x) {
+      CKS(cudaMalloc(&s.snap_x, size_t(s.nl) * 4));
+      CKS(cudaMalloc(&s.snap_v, size_t(s.nl) * vbytes));
+      CKS(cudaStreamCreateWithFlags(&snap_stream, cudaStreamNonBlocking));
+      CKS(cudaEventCreateWithFlags(&snap_ready, cudaEventDisableTiming));
+    }
+    CKS(cudaMemcpyAsync(s.snap_x, s.x[buf_host], size_t(s.nl) * 4, cudaMemcpyDeviceToDevice, s.stream));
+    CKS(cudaMemcpyAsync(s.snap_v, s.v[buf_host], size_t(s.nl) * vbytes, cudaMemcpyDeviceToDevice, s.stream));
+    CKS(cudaEventRecord(snap_ready, s.stream));
+    snap_thread = std::thread([this, &s, positions, velocities] {
+      try {
+        CKS(cudaSetDevice(s.device));
+        CKS(cudaStreamWaitEvent(snap_stream, snap_ready, 0));
+        segment_to_host(s, s.snap_x, s.snap_v, positions, velocities, snap_stream);
+      } catch (...) {
+        snap_error = std::current_exception();
+      }
+    });
   }
 
   // The trajectory checksum without moving the ring: each shard reduces its
@@ -801,8 +976,12 @@ struct ShardedRing::Impl {
   }
 
   void advance(uint64_t steps, bool sync) {
+    check_poison();
     const uint64_t count = std::min(steps, params.steps - steps_done);
-    if (count == 0) return;
+    if (count == 0) {
+      if (sync) verify_ranks();
+      return;
+    }
     if (!checksum_on) {
       uint64_t left = count;
       while (left > 0) {
@@ -813,107 +992,158 @@ struct ShardedRing::Impl {
         }
         enqueue_steps(chunk);
         left -= chunk;
-        if (frame_due()) {
-          drain();
-          fetch_rank_order();
-          record_frame_staged();
-        }
+        if (frame_due()) record_frame();
       }
-      if (sync) {
-        drain();
-        verify_ranks();
-      }
+      if (sync) verify_ranks();
       return;
     }
     for (uint64_t k = 0; k < count; ++k) {
       launch(1);
       drain();
       gpu_hash_step();
-      if (frame_due()) {
-        fetch_rank_order();
-        record_frame_staged();
-      }
+      if (frame_due()) record_frame();
     }
     verify_ranks();
   }
 
+  // Validates and narrows one segment's rank-ordered input (xs, vs: the
+  // segment's cars, element 0 first) into the shard's pinned staging while
+  // earlier 16M-car pieces are in flight to its idle ping-pong buffer.
+  // Returns the first violated rule (0 none; see narrow_validate) and adds
+  // the segment's velocity sum.
   template <typename T>
-  void load_state(const T* xin, const T* vin, size_t cnt) {
-    if (cnt != n) throw std::invalid_argument("state length must equal ncars");
-    std::atomic<int> err{0};
-    std::atomic<uint64_t> vsum{0};
+  int stage_segment(Shard& s, const T* xs, const T* vs, unsigned dst, uint64_t* vsum) {
+    ensure_stage(s);
+    CKS(cudaSetDevice(s.device));
     const uint64_t vlim = std::min<uint64_t>(params.v_max, vmax_eff);
-    par_chunks(n, [&](size_t a, size_t b) {
-      int e = 0;
-      uint64_t s = 0;
-      for (size_t i = a; i < b && !e; ++i) {
-        const uint64_t xi = xin[i], vi = vin[i];
-        if (xi >= L) e = 1;
-        else if (i && static_cast<uint64_t>(xin[i - 1]) >= xi) e = 2;
-        else if (vi > params.v_max) e = 3;
-        else if (vi > vlim) e = 4;
-        s += vi;
-      }
-      vsum += s;
-      if (e) {
-        int expected = 0;
-        err.compare_exchange_strong(expected, e);
-      }
-    });
-    switch (err.load()) {
+    std::atomic<int> err{0};
+    std::atomic<uint64_t> sum{0};
+    constexpr size_t kChunk = size_t(1) << 24;
+    for (size_t c0 = 0; c0 < s.nl && !err.load(); c0 += kChunk) {
+      const size_t c1 = std::min<size_t>(s.nl, c0 + kChunk);
+      parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
+        a += c0;
+        b += c0;
+        int e = 0;
+        uint64_t acc = 0;
+        if constexpr (std::is_same<T, uint64_t>::value) {
+          e = narrow_validate(xs, vs, a, b, L, params.v_max, vlim, s.hx_stage, s.hv_stage, vbytes);
+          if (!e) {
+            if (vbytes == 1)
+              for (size_t i = a; i < b; ++i) acc += static_cast<const uint8_t*>(s.hv_stage)[i];
+            else
+              for (size_t i = a; i < b; ++i) acc += static_cast<const uint32_t*>(s.hv_stage)[i];
+          }
+        } else {
+          for (size_t i = a; i < b && !e; ++i) {
+            const uint64_t xi = xs[i], vi = vs[i];
+            if (xi >= L) e = 1;
+            else if (i && static_cast<uint64_t>(xs[i - 1]) >= xi) e = 2;
+            else if (vi > params.v_max) e = 3;
+            else if (vi > vlim) e = 4;
+            s.hx_stage[i] = static_cast<uint32_t>(xi);
+            if (vbytes == 1) static_cast<uint8_t*>(s.hv_stage)[i] = static_cast<uint8_t>(vi);
+            else static_cast<uint32_t*>(s.hv_stage)[i] = static_cast<uint32_t>(vi);
+            acc += vi;
+          }
+        }
+        sum += acc;
+        if (e) {
+          int expected = 0;
+          err.compare_exchange_strong(expected, e);
+        }
+      });
+      CKS(cudaMemcpyAsync(s.x[dst] + c0, s.hx_stage + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, s.stream));
+      CKS(cudaMemcpyAsync(static_cast<char*>(s.v[dst]) + c0 * vbytes,
+                          static_cast<const char*>(s.hv_stage) + c0 * vbytes, (c1 - c0) * vbytes,
+                          cudaMemcpyHostToDevice, s.stream));
+    }
+    *vsum += sum.load();
+    return err.load();
+  }
+
+  // set_state.  `segment_only`: the input holds this process's segment only
+  // (one process per GPU: ids [first, first + count) of shard_range);
+  // otherwise the whole rank-ordered ring, of which each shard reads only
+  // its own ids.  Every rank validates and converts only its own cars
+  // (AVX-512, pipelined with the upload into the idle ping-pong buffer);
+  // the links between segments (last car of g < first car of g+1) and the
+  // error codes are agreed in one small all-gather, so every rank accepts
+  // or rejects the state together and a rejected state leaves the ring
+  // untouched.
+  template <typename T>
+  void load_state(const T* xin, const T* vin, size_t cnt, bool segment_only) {
+    snap_join();
+    verify_ranks();  // collective with one process per GPU
+    const bool own_only = use_nccl && segment_only;
+    int e = cnt != (own_only ? size_t(sh[0].nl) : size_t(n)) ? 5 : 0;
+    const unsigned dst = buf_host ^ 1u;
+    uint64_t vsum = 0;
+    std::vector<uint64_t> firstx(sh.size(), 0), lastx(sh.size(), 0);
+    for (size_t i = 0; i < sh.size() && !e; ++i) {
+      Shard& s = sh[i];
+      const size_t off = own_only ? 0 : s.gofs;
+      e = stage_segment(s, xin + off, vin + off, dst, &vsum);
+      firstx[i] = xin[off];
+      lastx[i] = xin[off + s.nl - 1];
+    }
+    sync_all();
+    if (!use_nccl) {
+      for (size_t i = 0; i + 1 < sh.size() && !e; ++i)
+        if (lastx[i] >= firstx[i + 1]) e = 2;
+    } else {
+      // [err, first x, last x, velocity sum] of every rank
+      Shard& s = sh[0];
+      CKS(cudaSetDevice(s.device));
+      uint64_t mine[4] = {uint64_t(e), firstx[0], lastx[0], vsum};
+      uint64_t* dbuf = nullptr;
+      CKS(cudaMalloc(&dbuf, 4 * 8 * (size_t(G) + 1)));
+      struct Free {
+        uint64_t* p;
+        ~Free() { cudaFree(p); }
+      } guard{dbuf};
+      std::vector<uint64_t> all(4 * size_t(G));
+      CKS(cudaMemcpyAsync(dbuf, mine, 32, cudaMemcpyHostToDevice, s.stream));
+      NcclApi& api = NcclApi::get();
+      api.check(api.all_gather(dbuf, dbuf + 4, 4, ncclUint64, comm, s.stream), "ncclAllGather(set_state)");
+      CKS(cudaMemcpyAsync(all.data(), dbuf + 4, all.size() * 8, cudaMemcpyDeviceToHost, s.stream));
+      CKS(cudaStreamSynchronize(s.stream));
+      e = 0;
+      vsum = 0;
+      for (unsigned r = 0; r < G && !e; ++r) e = static_cast<int>(all[4 * r]);
+      for (unsigned r = 0; r + 1 < G && !e; ++r)
+        if (all[4 * r + 2] >= all[4 * (r + 1) + 1]) e = 2;
+      for (unsigned r = 0; r < G; ++r) vsum += all[4 * r + 3];
+    }
+    switch (e) {
       case 1: throw std::invalid_argument("position out of range [0, length)");
       case 2: throw std::invalid_argument("positions must be strictly increasing");
       case 3: throw std::invalid_argument("velocity above vmax");
       case 4: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      case 5:
+        throw std::invalid_argument(own_only ? "segment length must equal this rank's shard_range count"
+                                             : "state length must equal ncars");
       default: break;
     }
-    drain();
-    verify_ranks();
-    for (Shard& s : sh) {
-      CKS(cudaSetDevice(s.device));
-      std::vector<uint32_t> sx(s.nl);
-      std::vector<uint8_t> sv8(vbytes == 1 ? s.nl : 0);
-      std::vector<uint32_t> sv32(vbytes == 4 ? s.nl : 0);
-      for (uint32_t i = 0; i < s.nl; ++i) {
-        sx[i] = static_cast<uint32_t>(xin[s.gofs + i]);
-        if (vbytes == 1) sv8[i] = static_cast<uint8_t>(vin[s.gofs + i]);
-        else sv32[i] = static_cast<uint32_t>(vin[s.gofs + i]);
-      }
-      CKS(cudaMemcpyAsync(s.x[buf_host], sx.data(), size_t(s.nl) * 4, cudaMemcpyHostToDevice, s.stream));
-      if (vbytes == 1)
-        CKS(cudaMemcpyAsync(s.v[buf_host], sv8.data(), s.nl, cudaMemcpyHostToDevice, s.stream));
-      else
-        CKS(cudaMemcpyAsync(s.v[buf_host], sv32.data(), size_t(s.nl) * 4, cudaMemcpyHostToDevice, s.stream));
-      CKS(cudaStreamSynchronize(s.stream));
-    }
+    buf_host = dst;
     reset_ctl();
     sync_all();
-    sumv0 = vsum.load();
+    sumv0 = vsum;
     series_base = steps_done;
     sumv_host.clear();
     wraps_host.clear();
-    if (steps_done == 0 && !(use_nccl && G > 1)) {
+    if (steps_done == 0) {
       frames.clear();
-      if (frame_due()) {
-        fetch_rank_order();
-        record_frame_staged();
-      }
+      if (frame_due()) record_frame();
     }
   }
 
   void finish_construction() {
     reset_ctl();
     sync_all();
-    if (!(use_nccl && G > 1)) {
-      CKS(cudaMallocHost(&hx, size_t(n) * 4));
-      CKS(cudaMallocHost(&hv, size_t(n) * vbytes));
-      if (frame_due()) {
-        fetch_rank_order();
-        record_frame_staged();
-      }
-    } else {
-      checksum_on = false;  // off by default (one all-gather per step when switched on)
-    }
+    if (!use_nccl) ensure_full_staging();
+    else checksum_on = false;  // off by default (one all-gather per step when switched on)
+    if (frame_due()) record_frame();
   }
 };
 
@@ -954,6 +1184,9 @@ ShardedRing::~ShardedRing() = default;
 
 ShardedRing::Impl::~Impl() {
   Impl& d = *this;
+  if (d.snap_thread.joinable()) d.snap_thread.join();
+  if (d.snap_ready) cudaEventDestroy(d.snap_ready);
+  if (d.snap_stream) cudaStreamDestroy(d.snap_stream);
   for (auto& s : d.sh) {
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
@@ -978,6 +1211,10 @@ ShardedRing::Impl::~Impl() {
     cudaFree(s.lo_dev);
     cudaFreeHost(s.hrec);
     cudaFreeHost(s.hctl);
+    cudaFreeHost(s.hx_stage);
+    cudaFreeHost(s.hv_stage);
+    cudaFree(s.snap_x);
+    cudaFree(s.snap_v);
     if (s.ev_packed) cudaEventDestroy(s.ev_packed);
     if (s.ev_done) cudaEventDestroy(s.ev_done);
     if (s.stream) cudaStreamDestroy(s.stream);
@@ -990,23 +1227,27 @@ ShardedRing::Impl::~Impl() {
   cudaFreeHost(d.hv);
 }
 
-void ShardedRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) { impl_->load_state(x, v, n); }
-void ShardedRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) { impl_->load_state(x, v, n); }
+void ShardedRing::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
+  impl_->load_state(x, v, n, false);
+}
+void ShardedRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) {
+  impl_->load_state(x, v, n, false);
+}
+void ShardedRing::set_state_segment(const uint64_t* x, const uint64_t* v, size_t n) {
+  impl_->load_state(x, v, n, true);
+}
 void ShardedRing::advance(uint64_t steps) { impl_->advance(steps, true); }
 void ShardedRing::enqueue(uint64_t steps) { impl_->advance(steps, false); }
-void ShardedRing::synchronize() {
-  impl_->drain();
-  impl_->verify_ranks();
-}
+void ShardedRing::synchronize() { impl_->verify_ranks(); }
 uint64_t ShardedRing::steps_done() const { return impl_->steps_done; }
 uint64_t ShardedRing::checksum() const { return impl_->hash; }
 const std::vector<Frame>& ShardedRing::frames() const { return impl_->frames; }
 const SimParams& ShardedRing::params() const { return impl_->params; }
 
+// Collective with one process per GPU: the whole ring's velocity sum.
 void ShardedRing::observables(double* density, double* mean_velocity, double* flow) {
   Impl& d = *impl_;
-  d.require_local("observables");
-  d.drain();
+  d.verify_ranks();
   const uint64_t total = d.sumv_host.empty() ? d.sumv0 : d.sumv_host.back();
   const double n = static_cast<double>(d.params.car_count);
   const double mean = static_cast<double>(total) / n;
@@ -1016,21 +1257,43 @@ void ShardedRing::observables(double* density, double* mean_velocity, double* fl
   if (flow) *flow = dens * mean;
 }
 
+// Collective with one process per GPU: every rank passing a non-null array
+// receives the whole ring in rank order (segments broadcast over NCCL).
 void ShardedRing::state(uint64_t* positions, uint64_t* velocities) {
   Impl& d = *impl_;
-  d.drain();
-  d.fetch_rank_order();
-  par_chunks(d.n, [&](size_t a, size_t b) {
-    for (size_t i = a; i < b; ++i) {
-      if (positions) positions[i] = d.hx[i];
-      if (velocities) velocities[i] = d.hvel(i);
-    }
-  });
+  d.snap_join();
+  d.verify_ranks();
+  const bool want = positions || velocities;
+  d.gather_rank_order(want);
+  if (want) d.widen_staging(positions, velocities);
 }
+
+// Not collective: this process's segment (the whole ring, rank order, when
+// the process holds every segment).
+void ShardedRing::state_segment(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {
+  Impl& d = *impl_;
+  if (!d.use_nccl) {
+    state(positions, velocities);
+    if (first_rank) *first_rank = 0;
+    return;
+  }
+  d.state_segment(positions, velocities, first_rank, false);
+}
+
+void ShardedRing::state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {
+  Impl& d = *impl_;
+  if (!d.use_nccl) {
+    state_segment(positions, velocities, first_rank);
+    return;
+  }
+  d.state_segment(positions, velocities, first_rank, true);
+}
+
+void ShardedRing::state_wait() { impl_->snap_join(); }
 
 size_t ShardedRing::sumv_series(uint64_t* out, size_t cap) {
   Impl& d = *impl_;
-  d.drain();
+  d.verify_ranks();
   const size_t k = std::min(cap, d.sumv_host.size());
   if (out) std::memcpy(out, d.sumv_host.data(), k * sizeof(uint64_t));
   return d.sumv_host.size();
@@ -1038,16 +1301,13 @@ size_t ShardedRing::sumv_series(uint64_t* out, size_t cap) {
 
 size_t ShardedRing::wrap_series(uint64_t* out, size_t cap) {
   Impl& d = *impl_;
-  d.drain();
+  d.verify_ranks();
   const size_t k = std::min(cap, d.wraps_host.size());
   if (out) std::memcpy(out, d.wraps_host.data(), k * sizeof(uint64_t));
   return d.wraps_host.size();
 }
 
-void ShardedRing::set_checksum(bool enabled) {
-
-  impl_->checksum_on = enabled;
-}
+void ShardedRing::set_checksum(bool enabled) { impl_->checksum_on = enabled; }
 void* ShardedRing::cuda_stream() const { return impl_->sh.empty() ? nullptr : impl_->sh[0].stream; }
 uint64_t ShardedRing::kernel_launches() const { return impl_->launches; }
 int ShardedRing::exchange_mode() const { return impl_->p2p ? 2 : 1; }

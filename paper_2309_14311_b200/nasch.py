@@ -58,6 +58,19 @@ def _u32p(a):
     return a.ctypes.data_as(C.POINTER(C.c_uint32))
 
 
+def _out_u64(a, n: int, name: str):
+    """A caller-supplied output array must be a writable, C-contiguous u64
+    vector of at least n elements: the C ABI writes n values through the
+    raw pointer."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.uint64 or a.ndim != 1:
+        raise TypeError(f"{name} must be a 1-D numpy uint64 array")
+    if not a.flags.c_contiguous or not a.flags.writeable:
+        raise ValueError(f"{name} must be C-contiguous and writable")
+    if len(a) < n:
+        raise ValueError(f"{name} holds {len(a)} values; the ring has {n} cars")
+    return a
+
+
 class SimParams:
     """Owned nasch_params handle (defaults vmax=5, p=0.13, output none)."""
 
@@ -199,19 +212,55 @@ class Engine:
 
     def snapshot(self, *, out_x=None, out_v=None):
         """Current (positions, velocities) in increasing-position order."""
-        x = np.empty(self.ncars, np.uint64) if out_x is None else out_x
-        v = np.empty(self.ncars, np.uint64) if out_v is None else out_v
-        _check(_lib().nasch_sim_state(self._h, _u64p(x), _u64p(v), self.ncars))
+        x = np.empty(self.ncars, np.uint64) if out_x is None else _out_u64(out_x, self.ncars, "out_x")
+        v = np.empty(self.ncars, np.uint64) if out_v is None else _out_u64(out_v, self.ncars, "out_v")
+        _check(_lib().nasch_sim_state(self._h, _u64p(x), _u64p(v), min(len(x), len(v))))
         return x, v
 
     def snapshot_async(self, out_x, out_v) -> None:
         """Start a snapshot into (out_x, out_v) (u64, length ncars) that
         completes while the caller advances; call snapshot_wait() before
         reading the arrays (nasch_sim_state_async)."""
-        assert out_x.dtype == np.uint64 and out_v.dtype == np.uint64
-        assert out_x.flags.c_contiguous and out_v.flags.c_contiguous
+        _out_u64(out_x, self.ncars, "out_x")
+        _out_u64(out_v, self.ncars, "out_v")
         self._pending = (out_x, out_v)  # keep the buffers alive
-        _check(_lib().nasch_sim_state_async(self._h, _u64p(out_x), _u64p(out_v), self.ncars))
+        _check(_lib().nasch_sim_state_async(self._h, _u64p(out_x), _u64p(out_v),
+                                            min(len(out_x), len(out_v))))
+
+    def segment_snapshot(self, *, out_x=None, out_v=None):
+        """The cars this process holds (shard_range), widened to u64:
+        (x, v, first_rank) with element k at rank (first_rank + k) mod N
+        (nasch_sim_state_segment; not a collective call).  A sim holding the
+        whole ring returns it in rank order with first_rank 0."""
+        _, count = self.shard_range()
+        x = np.empty(count, np.uint64) if out_x is None else _out_u64(out_x, count, "out_x")
+        v = np.empty(count, np.uint64) if out_v is None else _out_u64(out_v, count, "out_v")
+        first = C.c_uint64()
+        _check(_lib().nasch_sim_state_segment(self._h, _u64p(x), _u64p(v), min(len(x), len(v)),
+                                              C.byref(first)))
+        return x, v, first.value
+
+    def segment_snapshot_async(self, out_x, out_v) -> int:
+        """Start a segment snapshot into (out_x, out_v); returns first_rank.
+        The arrays are complete after snapshot_wait()."""
+        _, count = self.shard_range()
+        _out_u64(out_x, count, "out_x")
+        _out_u64(out_v, count, "out_v")
+        self._pending = (out_x, out_v)
+        first = C.c_uint64()
+        _check(_lib().nasch_sim_state_segment_async(self._h, _u64p(out_x), _u64p(out_v),
+                                                    min(len(out_x), len(out_v)), C.byref(first)))
+        return first.value
+
+    def set_segment_state(self, x, v) -> None:
+        """Collective set_state from this process's segment of the new
+        rank-ordered state (nasch_sim_set_state_segment)."""
+        x = np.ascontiguousarray(x, np.uint64)
+        v = np.ascontiguousarray(v, np.uint64)
+        if x.ndim != 1 or v.ndim != 1 or len(x) != len(v):
+            raise ValueError(f"positions and velocities must be 1-D of equal length "
+                             f"(got {x.shape} and {v.shape})")
+        _check(_lib().nasch_sim_set_state_segment(self._h, _u64p(x), _u64p(v), len(x)))
 
     def snapshot_wait(self) -> None:
         _check(_lib().nasch_sim_state_wait(self._h))
@@ -226,6 +275,9 @@ class Engine:
     def set_state(self, x, v) -> None:
         x = np.ascontiguousarray(x)
         v = np.ascontiguousarray(v)
+        if x.ndim != 1 or v.ndim != 1 or len(x) != len(v):
+            raise ValueError(f"positions and velocities must be 1-D of equal length "
+                             f"(got {x.shape} and {v.shape})")
         if x.dtype == np.uint32 and v.dtype == np.uint32:
             _check(_lib().nasch_sim_set_state32(self._h, _u32p(x), _u32p(v), len(x)))
         else:
@@ -292,7 +344,20 @@ class Ensemble:
     def set_state(self, ring: int, x, v) -> None:
         x = np.ascontiguousarray(x, np.uint32)
         v = np.ascontiguousarray(v, np.uint32)
+        if x.ndim != 1 or v.ndim != 1 or len(x) != len(v):
+            raise ValueError(f"positions and velocities must be 1-D of equal length "
+                             f"(got {x.shape} and {v.shape})")
         _check(_lib().nasch_ensemble_set_state32(self._h, ring, _u32p(x), _u32p(v), len(x)))
+
+    def set_state_all(self, x, v) -> None:
+        """Every ring at once: rank-ordered rings concatenated in ring order
+        (nasch_ensemble_set_state_all32)."""
+        x = np.ascontiguousarray(x, np.uint32)
+        v = np.ascontiguousarray(v, np.uint32)
+        if x.ndim != 1 or v.ndim != 1 or len(x) != len(v):
+            raise ValueError(f"positions and velocities must be 1-D of equal length "
+                             f"(got {x.shape} and {v.shape})")
+        _check(_lib().nasch_ensemble_set_state_all32(self._h, _u32p(x), _u32p(v), len(x)))
 
     def advance(self, steps: int) -> None:
         _check(_lib().nasch_ensemble_advance(self._h, steps))

@@ -1,0 +1,156 @@
+"""Full-size parity for the configurations the benchmark numbers are quoted on.
+
+Each test runs the SAME engine path the benchmark times -- default launch
+geometry, temporal-blocked launches of K steps, the grid-stride tile walk
+of a 2e8-car ring -- at the BASELINE.json size and compares it bit for bit
+with the reference itself (oracle/_ref: the unmodified reference sources,
+its OpenMP Engine on all host cores):
+
+* C3 (L=1e9, N=2e8, p=0.13): 48 steps = three full 16-step launches, every
+  step's velocity sum and crossing count, final positions and velocities.
+* C5 (L=1e8, N=6e7, p=0.5, k=8 as BASELINE names it, and k=16): 64 steps,
+  plus an asynchronous snapshot taken at step 64 while the ring keeps
+  stepping.
+* C4: one 64-ring slice of the fundamental-diagram sweep (every density,
+  one p) for the full 5000 steps; per-ring velocity totals (the
+  time-averaged flux numerators) bit-equal with the reference run ring by
+  ring at one worker each (engine.cpp:101-184).
+* The one-warp small-ring kernel past the device step-record ring with
+  chunk lengths that are not multiples of 32.
+"""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+from paper_2309_14311_b200 import nasch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def params(L, N, vmax, p, steps, seed):
+    return nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=steps, seed=seed)
+
+
+@pytest.fixture
+def k_env():
+    old = os.environ.get("NASCH_B200_K")
+    yield
+    if old is None:
+        os.environ.pop("NASCH_B200_K", None)
+    else:
+        os.environ["NASCH_B200_K"] = old
+
+
+def cores(ref):
+    return max(1, ref.physical_cores() or os.cpu_count() or 1)
+
+
+def test_config3_full_size_three_launches_vs_reference(ref):
+    """C3 exactly as bench.py runs it: 2e8 cars, three full 16-step
+    launches (enqueued one launch at a time, as the timed region does)."""
+    L, N, p, seed, T = 10**9, 2 * 10**8, 0.13, 3, 48
+    x0, v0 = nasch.fill_uniform_state(L, N, 0, seed)
+    e = nasch.Engine(params(L, N, 5, p, 1000, seed))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    assert e.steps_per_launch == 16
+    for _ in range(T // 16):
+        e.enqueue(16)
+    e.synchronize()
+    x, v = e.snapshot()
+    sumv, wraps = e.sumv_series(), e.wrap_series()
+    e.close()
+    r = ref.run(L, N, 5, p, seed, T, x0=x0.astype(np.uint64), v0=v0.astype(np.uint64),
+                workers=cores(ref))
+    del x0, v0
+    assert (sumv == r["sumv"]).all(), "per-step velocity sums differ"
+    assert (wraps == r["wraps"]).all(), "per-step crossing counts differ"
+    assert (x == r["x"]).all(), "positions differ"
+    assert (v == r["v"]).all(), "velocities differ"
+
+
+@pytest.mark.parametrize("K", [8, 16])
+def test_config5_full_size_vs_reference_with_snapshot(ref, k_env, K):
+    """C5 (jam-dominated, p=0.5) at k=8 (BASELINE's k) and k=16: 64 steps,
+    every step's sums/crossings, and an asynchronous snapshot at step 64
+    that completes while 16 further steps run."""
+    L, N, p, seed, T = 10**8, 6 * 10**7, 0.5, 5, 64
+    os.environ["NASCH_B200_K"] = str(K)
+    x0, v0 = nasch.fill_uniform_state(L, N, 0, seed)
+    e = nasch.Engine(params(L, N, 5, p, 20000, seed))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    assert e.steps_per_launch == K
+    e.advance(T)
+    sx = np.empty(N, np.uint64)
+    sv = np.empty(N, np.uint64)
+    e.snapshot_async(sx, sv)
+    e.enqueue(16)  # the ring keeps stepping while the snapshot lands
+    e.snapshot_wait()
+    e.synchronize()
+    sumv, wraps = e.sumv_series()[:T], e.wrap_series()[:T]
+    e.close()
+    r = ref.run(L, N, 5, p, seed, T, x0=x0.astype(np.uint64), v0=v0.astype(np.uint64),
+                workers=cores(ref))
+    assert (sumv == r["sumv"]).all() and (wraps == r["wraps"]).all()
+    assert (sx == r["x"]).all() and (sv == r["v"]).all()
+
+
+def c4_slice(p_index=5, replica=0):
+    """64 rings of BASELINE config 4: every density j, one p, one seed
+    replica (the same (N, p, seed) formula as bench.py's C4 leg)."""
+    ps = [0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7]
+    return [(5000 + (45000 * j) // 63, ps[p_index], 1 + replica * 1000 + p_index * 100 + j)
+            for j in range(64)]
+
+
+def test_config4_slice_full_length_vs_reference(ref):
+    L, T = 10**5, 5000
+    specs = c4_slice()
+    ens = nasch.Ensemble([params(L, N, 5, p, T, sd) for N, p, sd in specs])
+    xs, vs = [], []
+    for N, _, sd in specs:
+        x, v = nasch.fill_uniform_state(L, N, 0, sd)
+        xs.append(x)
+        vs.append(v)
+    ens.set_state_all(np.concatenate(xs), np.concatenate(vs))
+    ens.advance(T)
+    tot, last = ens.sumv_totals(), ens.sumv_last()
+    assert all(ens.steps_done(i) == T for i in range(len(specs)))
+    ens.close()
+
+    def one(i):
+        N, p, sd = specs[i]
+        r = ref.run(L, N, 5, p, sd, T, x0=xs[i].astype(np.uint64), v0=vs[i].astype(np.uint64),
+                    workers=1, want_state=False)
+        return int(r["sumv"].sum(dtype=np.uint64)), int(r["sumv"][-1])
+
+    with ThreadPoolExecutor(cores(ref)) as pool:
+        want = list(pool.map(one, range(len(specs))))
+    assert [int(t) for t in tot] == [w[0] for w in want], "time-averaged flux totals differ"
+    assert [int(t) for t in last] == [w[1] for w in want]
+
+
+@pytest.mark.parametrize("N", [200, 203, 509])
+def test_warp_ring_past_record_ring_ragged_chunks(port, N):
+    """The one-warp kernel (N <= 512; 200 is the EXACT instantiation) over
+    69,901 steps -- past the 65,536-slot device step-record ring -- in
+    chunks that are not multiples of 32, against the oracle."""
+    L, p, seed = 5 * N, 0.13, 42
+    chunks = [31, 1000, 65537, 3333]
+    T = sum(chunks)
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 7)
+    e = nasch.Engine(params(L, N, 5, p, T, seed))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    for c in chunks:
+        e.advance(c)
+    x, v = e.snapshot()
+    sumv, wraps = e.sumv_series(), e.wrap_series()
+    e.close()
+    o = port.run(L, 5, p, seed, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    assert len(sumv) == T
+    assert (sumv == o["sumv"]).all() and (wraps == o["wraps"]).all()
+    assert (x == o["x"]).all() and (v == o["v"]).all()

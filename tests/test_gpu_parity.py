@@ -49,7 +49,7 @@ def assert_same(g, o, checksum=True):
     assert (g["x"] == o["x"]).all(), "positions differ"
     assert (g["v"] == o["v"]).all(), "velocities differ"
     assert (g["sumv"] == o["sumv"]).all(), "per-step velocity sums differ"
-    if "wraps" in o:
+    if o.get("wraps") is not None:
         assert (g["wraps"] == o["wraps"]).all(), "per-step wrap counts differ"
     if checksum:
         assert g["checksum"] == o["checksum"]

@@ -204,3 +204,76 @@ def test_distributed_checksum_single_rank(port, xchg):
     x, v = e.snapshot()
     assert (x == o["x"]).all() and (v == o["v"]).all()
     e.close()
+
+
+def test_distributed_whole_ring_calls_and_segment_snapshots(port, xchg, tmp_path):
+    """The collective whole-ring calls of a one-process-per-GPU ring (1-rank
+    communicator: the same NCCL broadcast / all-reduce / all-gather code
+    paths): state gathered over ncclBroadcast, observables and series from
+    the all-reduced step records, frames, set_state from the segment,
+    synchronous and asynchronous segment snapshots (element k at rank
+    first_rank + k), all equal to the oracle."""
+    L, N, vmax, p, T = 50000, 11000, 5, 0.35, 45
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 21)
+    x0 = x0.astype(np.uint64)
+    v0 = v0.astype(np.uint64)
+    o = port.run(L, vmax, p, 8, T, x0, v0, want_checksum=False)
+    e = nasch.Engine.distributed(mk(L, N, vmax, p, 200, 8, output="ascii", stride=9), 0, 1,
+                                 nasch.nccl_unique_id())
+    e.set_checksum(False)
+    e.set_segment_state(x0, v0)  # this rank's segment = the whole ring
+    e.advance(T)
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    d, m, f = e.observables()
+    assert m == float(o["sumv"][-1]) / N and d == N / L
+    sx, sv, first = e.segment_snapshot()
+    r = (first + np.arange(N, dtype=np.uint64)) % np.uint64(N)
+    assert (sx == o["x"][r]).all() and (sv == o["v"][r]).all()
+    ax = np.empty(N, np.uint64)
+    av = np.empty(N, np.uint64)
+    first2 = e.segment_snapshot_async(ax, av)
+    e.enqueue(20)  # keeps stepping while the snapshot lands
+    e.snapshot_wait()
+    e.synchronize()
+    assert first2 == first and (ax == sx).all() and (av == sv).all()
+    # frames: the single-GPU engine's, byte for byte
+    a = nasch.Engine(mk(L, N, vmax, p, 200, 8, output="ascii", stride=9))
+    a.set_checksum(False)
+    a.set_state(x0, v0)
+    a.advance(T + 20)
+    assert a.frame_count == e.frame_count == (T + 20 + 8) // 9
+    a.write_ascii(str(tmp_path / "a.txt"))
+    e.write_ascii(str(tmp_path / "b.txt"))
+    assert open(tmp_path / "a.txt").read() == open(tmp_path / "b.txt").read()
+    # a rejected segment leaves the ring untouched, on every rank alike
+    before = e.snapshot()
+    bad = x0.copy()
+    bad[5] = bad[4]
+    with pytest.raises(nasch.NaschError, match="strictly increasing"):
+        e.set_segment_state(bad, v0)
+    with pytest.raises(nasch.NaschError, match="segment length"):
+        e.set_segment_state(x0[:-1], v0[:-1])
+    after = e.snapshot()
+    assert (after[0] == before[0]).all() and (after[1] == before[1]).all()
+    e.close()
+    a.close()
+
+
+def test_in_process_shards_segment_api(port):
+    """Engines holding the whole ring: the segment snapshot is the rank-
+    ordered state with first_rank 0 and set_state_segment is set_state."""
+    L, N, vmax, p, T = 40000, 9000, 5, 0.25, 33
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 3)
+    x0 = x0.astype(np.uint64)
+    v0 = v0.astype(np.uint64)
+    o = port.run(L, vmax, p, 2, T, x0, v0, want_checksum=False)
+    for G, kind in ((1, 0), (3, CUDA)):
+        e = nasch.Engine(mk(L, N, vmax, p, T, 2), G, kind)
+        e.set_checksum(False)
+        e.set_segment_state(x0, v0)
+        e.advance(T)
+        sx, sv, first = e.segment_snapshot()
+        assert first == 0 and (sx == o["x"]).all() and (sv == o["v"]).all()
+        e.close()

@@ -228,6 +228,7 @@ def test_oracle_equals_reference_injected_state(port, ref):
         b = ref.run(L, N, vmax, p, trial, 50, x0=x0, v0=v0, workers=3)
         assert (a["x"] == b["x"]).all() and (a["v"] == b["v"]).all()
         assert (a["sumv"] == b["sumv"]).all() and a["checksum"] == b["checksum"]
+        assert (a["wraps"] == b["wraps"]).all()  # the reference's own wrap_counts_
 
 
 def test_reference_uniform_mean_pin(ref, port):
@@ -240,3 +241,18 @@ def test_reference_uniform_mean_pin(ref, port):
     for _ in range(1000000):
         total += f(C.byref(s))
     assert abs(total / 1e6 - 0.4997635306662361) <= 1e-12 * 0.4997635306662361
+
+
+@pytest.mark.parametrize("L,N,vmax_init,seed", [
+    (1000, 200, 0, 42), (10**6, 2 * 10**5, 5, 7), (50, 50, 3, 1), (50, 49, 3, 2),
+    (97, 1, 5, 3), (10**5, 5000, 0, 11), (3 * 10**7, 100, 5, 3)])
+def test_input_generator_matches_library(port, L, N, vmax_init, seed):
+    """The oracle's restatement of the BASELINE input generator (used by the
+    reference arm, which must not load the product library) equals the
+    library's nasch_fill_uniform_state value for value."""
+    from paper_2309_14311_b200 import nasch
+    a = port.fill_uniform_state(L, N, vmax_init, seed)
+    b = nasch.fill_uniform_state(L, N, vmax_init, seed)
+    assert (a[0] == b[0]).all() and (a[1] == b[1]).all()
+    assert len(a[0]) == N and (np.diff(a[0].astype(np.int64)) > 0).all() and int(a[0][-1]) < L
+    assert int(a[1].max()) <= vmax_init
