@@ -26,11 +26,12 @@ e2e         the same metric through the C ABI with host buffers: set_state
             series and the final state (each rank: its segment) read back to
             host u64 arrays, wall clock, max over ranks
 roofline    SURVEY.md 8(d): 16 algorithmic bytes per car-update (int32 x and
-            v read and written once per step) x N*16 updates per launch / the
-            average duration of the full 16-step launches, from per-launch
-            CUDA events inside the timed region; peak = MEASURED_PEAKS.json.
-            Temporal blocking moves the state once per 16 steps, so frac > 1;
-            the roof that binds is integer issue ("issue_bound")
+            v read and written once per step) x N*k updates per launch / the
+            average duration of the timed region's k-step launches (k =
+            min(K, 32)), from per-launch CUDA events inside the timed region;
+            peak = MEASURED_PEAKS.json.  Temporal blocking moves the state
+            once per k steps, so frac > 1; the roof that binds is integer
+            issue ("issue_bound")
 cpu_baseline  the reference's own OpenMP Engine (oracle/_ref, compiled
             unmodified) on this host's cores, bounded step prefix
 --impl reference  only that CPU measurement, as its own JSON line (its
@@ -80,15 +81,17 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_step_kernel():
+def ncu_step_kernel(k_launch):
     """The step kernel's committed ncu capture summary (profiles/) for this
-    workload, or {}."""
+    workload at this launch depth, or {}."""
     path = os.path.join(ROOT, "profiles", "ncu_step_kernel.json")
     try:
         with open(path) as f:
             d = json.load(f)
         if d.get("L") == CONFIG["L"] and d.get("N") == CONFIG["N"]:
-            return d
+            for c in d.get("captures", []):
+                if c.get("steps_per_launch") == k_launch:
+                    return c
     except Exception:
         pass
     return {}
@@ -100,7 +103,7 @@ def issue_bound(launch_ms, spl, n, clocks, world):
     capture (profiles/, one GPU); the peak is 1 warp instruction per cycle
     per SMSP (4 per SM) at the SM clock sampled during the timed region."""
     import torch
-    d = ncu_step_kernel()
+    d = ncu_step_kernel(spl)
     if "warp_inst_per_launch" not in d or not torch.cuda.is_available() or world != 1:
         return None
     sms = torch.cuda.get_device_properties(0).multi_processor_count
@@ -421,13 +424,15 @@ def c3_leg(args, d: Dist):
             torch.cuda.synchronize()
             launches = eng.kernel_launches - l0
             prev = ev0
+            k_top = max(k for k, _ in marks)  # the launch depth the region runs at
             for k, e in marks:
-                if k == spl:
+                if k == k_top:
                     full_launch_ms.append(prev.elapsed_time(e))
                 prev = e
             passes.append(d.max(ev0.elapsed_time(marks[-1][1])))
     ms = statistics.median(passes)
-    launch_ms = d.max(statistics.median(full_launch_ms)) if full_launch_ms else ms / K * spl
+    k_launch = min(spl, K)  # steps per launch of the timed region's launches
+    launch_ms = d.max(statistics.median(full_launch_ms))
     xmode = {0: "none (one segment)", 1: "collective (NCCL all-gather)",
              2: "peer memory (records stored by the step kernel into the peers' HBM)"}[eng.exchange_mode]
     sumv = eng.sumv_series()  # whole ring on every rank (collective)
@@ -456,8 +461,10 @@ def c3_leg(args, d: Dist):
     first, count = eng2.shard_range()
     # caller-owned output buffers, already faulted in (a serving loop reuses
     # them; first-touch page faults are not the engine's cost)
-    outx = np.zeros(count, np.uint64)
-    outv = np.zeros(count, np.uint64)
+    outx = np.empty(count, np.uint64)
+    outv = np.empty(count, np.uint64)
+    outx.fill(0)  # np.zeros would leave the pages unmapped until the engine writes them
+    outv.fill(0)
     eng2.set_checksum(False)
     eng2.advance(0)
     d.barrier()
@@ -486,11 +493,12 @@ def c3_leg(args, d: Dist):
     # ---- roofline --------------------------------------------------------
     peak, peak_src = peaks()
     peak *= d.world  # aggregate over the ranks' HBM
-    achieved = SURVEY_BYTES_PER_UPDATE * N * spl / (launch_ms / 1000.0) / 1e9
-    traffic = ncu_step_kernel().get("dram_bytes_per_launch") if d.world == 1 else None
+    achieved = SURVEY_BYTES_PER_UPDATE * N * k_launch / (launch_ms / 1000.0) / 1e9
+    traffic = ncu_step_kernel(k_launch).get("dram_bytes_per_launch") if d.world == 1 else None
     clocks = clk.summary()
-    kernel = (f"nasch_tb_kernel<uint8_t,128,16,16,1> ({spl} steps per launch)" if d.world == 1
-              else f"nasch_tb_push_kernel<uint8_t,128,16,16,1> + shard_plan_kernel ({spl} steps per launch)")
+    kernel = (f"nasch_tb_kernel<uint8_t,128,32,32,1> + cone_init_kernel<uint8_t,256> "
+              f"({spl} steps per launch)" if d.world == 1
+              else f"nasch_tb_push_kernel<uint8_t,128,32,32,1> + shard_plan_kernel ({spl} steps per launch)")
     line = {"metric": "car-updates/s", "value": value, "unit": "car-updates/s",
             "n_gpus": d.world, "steps": K, "warmup": W, "ms_per_step": step_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
@@ -507,18 +515,19 @@ def c3_leg(args, d: Dist):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_update": SURVEY_BYTES_PER_UPDATE,
-                         "units_per_launch": N * spl, "steps_per_launch": spl,
+                         "units_per_launch": N * k_launch, "steps_per_launch": k_launch,
+                         "max_steps_per_launch": spl,
                          "kernel_ms_avg": launch_ms,
-                         "kernel_ms_source": f"median of {len(full_launch_ms)} full {spl}-step launches "
-                                             "(CUDA events between launches on the engine stream), "
-                                             "max over ranks",
+                         "kernel_ms_source": f"median of {len(full_launch_ms)} {k_launch}-step launches "
+                                             "(CUDA events between launches on the engine stream; "
+                                             "step kernel + next-launch plan kernel), max over ranks",
                          "peak_source": peak_src, "kernel": kernel,
                          "state_bytes_moved_per_launch": BYTES_MOVED_PER_UPDATE * N,
                          "state_gbs_moved": BYTES_MOVED_PER_UPDATE * N / (launch_ms / 1000.0) / 1e9,
                          "note": "temporal blocking: the state crosses HBM once per "
-                                 f"{spl} steps, so frac > 1 vs the per-step roofline; "
+                                 f"{k_launch} steps, so frac > 1 vs the per-step roofline; "
                                  "the binding roof is integer issue (issue_bound, DESIGN.md 4.1)"},
-            "issue_bound": issue_bound(launch_ms, spl, N, clocks, d.world),
+            "issue_bound": issue_bound(launch_ms, k_launch, N, clocks, d.world),
             "e2e": e2e,
             "gpu_launches": int(launches),
             "clocks": clocks,

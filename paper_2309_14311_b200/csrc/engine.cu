@@ -162,11 +162,14 @@ struct GpuRing::Impl {
 
   template <typename VT>
   void launch_tb(uint32_t k) {
-    if (medium) {
-      nasch_tb_kernel<VT, kTbmTPB, kTbmCPT, kTbHalo, false><<<grid, kTbmTPB, 0, stream>>>(args, k);
-      return;
+    if (medium) nasch_tb_kernel<VT, kTbmTPB, kTbmCPT, kTbHalo, false><<<grid, kTbmTPB, 0, stream>>>(args, k);
+    else nasch_tb_kernel<VT, kTbTPB, kTbCPT, kTbHalo, kTbWT><<<grid, kTbTPB, 0, stream>>>(args, k);
+    // the next launch's plan, when its cone does not fit the step kernel's
+    // last block (K (vmax + 1) > threads per block)
+    if (!tb_plan_inline(K, vmax_eff, medium ? kTbmTPB : kTbTPB)) {
+      cone_init_kernel<VT, 256><<<1, 256, 0, stream>>>(args);
+      ++launches;
     }
-    nasch_tb_kernel<VT, kTbTPB, kTbCPT, kTbHalo, kTbWT><<<grid, kTbTPB, 0, stream>>>(args, k);
   }
 
   // One launch advancing k steps (k == 1 in single-step mode; any k in
@@ -236,14 +239,9 @@ struct GpuRing::Impl {
       cone_init_kernel<uint8_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);
       CK(cudaGetLastError());
     } else if (tb) {
-      // the cone runs on one block of the TB kernel's width (K*(vmax+1) <= TPB)
-      if (vbytes == 1) {
-        if (medium) cone_init_kernel<uint8_t, kTbmTPB><<<1, kTbmTPB, 0, stream>>>(args);
-        else cone_init_kernel<uint8_t, kTbTPB><<<1, kTbTPB, 0, stream>>>(args);
-      } else {
-        if (medium) cone_init_kernel<uint32_t, kTbmTPB><<<1, kTbmTPB, 0, stream>>>(args);
-        else cone_init_kernel<uint32_t, kTbTPB><<<1, kTbTPB, 0, stream>>>(args);
-      }
+      // the first plan: K (vmax + 1) <= 256 cone cars
+      if (vbytes == 1) cone_init_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args);
+      else cone_init_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args);
       CK(cudaGetLastError());
     }
     W_host = 0;
@@ -642,8 +640,11 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   const int tb_tpb = d.medium ? kTbmTPB : kTbTPB;
   const uint32_t tb_load = d.medium ? kTbmLoad : kTbLoad;
   const long kreq = env_long("NASCH_B200_K", kPlanMax);
-  uint32_t K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
-  K = std::min<uint32_t>(K, tb_tpb / (d.vmax_eff + 1));
+  uint32_t K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, std::min(kPlanMax, kTbHalo))));
+  // the plan simulates K (vmax + 1) cone cars on at most 256 threads
+  // (inline in the launch's last block when they fit it, tb_plan_inline)
+  K = std::min<uint32_t>(K, 256u / (d.vmax_eff + 1));
+  (void)tb_tpb;
   d.tb = K >= 2 && d.n >= std::max(4096u, 2 * tb_load) && uint64_t(d.L) > uint64_t(K) * d.vmax_eff;
   d.K = d.tb ? K : 1;
   if (!d.tb) d.medium = false;
@@ -1021,6 +1022,17 @@ void fill_uniform_state(uint64_t L, uint64_t N, uint64_t vmax_init, uint64_t see
 }
 
 }  // namespace nb200
+
+#ifdef NB_TB_TRACE
+extern "C" int nasch_b200_tb_trace(unsigned long long* out, int reset) {
+  if (reset) {
+    std::vector<unsigned long long> init(64 * 8, 0);
+    for (int i = 0; i < 64; ++i) init[i * 8 + 0] = init[i * 8 + 2] = ~0ull;
+    return cudaMemcpyToSymbol(nb200::g_tb_trace, init.data(), init.size() * 8) == cudaSuccess ? 0 : 1;
+  }
+  return cudaMemcpyFromSymbol(out, nb200::g_tb_trace, 64 * 8 * 8) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 #ifdef NB_DR_TRACE
 extern "C" int nasch_b200_dr_trace(unsigned long long* out, size_t n) {

@@ -104,8 +104,24 @@ constexpr PowTables make_pow_tables() {
   return t;
 }
 
+// Doubled powers 2 a^c (c < 64): the per-car draw multipliers of the
+// temporal-blocked kernel, read as constant-bank operands of IMAD.WIDE.
+struct Pow2Table {
+  uint32_t v[64];
+};
+constexpr Pow2Table make_pow2_table() {
+  Pow2Table t{};
+  uint32_t a = 1;
+  for (int i = 0; i < 64; ++i) {
+    t.v[i] = a << 1;
+    a = cx_mulmod(a, kA);
+  }
+  return t;
+}
+
 #if defined(__CUDACC__)
 static __constant__ PowTables c_pow = make_pow_tables();
+static __constant__ Pow2Table c_apow2 = make_pow2_table();
 
 // a^e mod m computed by a whole warp (every lane calls it with the same e;
 // every lane gets the result): lane b contributes a^(2^b) if bit b of the

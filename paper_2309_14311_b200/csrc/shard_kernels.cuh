@@ -15,10 +15,11 @@
 #include <cstdint>
 
 #include "step_kernels.cuh"
+#include "tb_config.hpp"
 
 namespace nb200 {
 
-constexpr int kHeadCars = 16;  // halo depth, >= kPlanMax
+constexpr int kHeadCars = kTbHalo;  // halo depth = the deepest launch (k <= kTbHalo)
 constexpr int kConeMax = 256;  // cone slots (one block)
 constexpr int kXchgWords = 2 * kHeadCars + 2 * kConeMax;  // u32 per shard record
 constexpr uint32_t kFlagWords = 64;  // peer exchange: flag words ahead of the receive slots (max shards)

@@ -108,7 +108,7 @@ bool ShardedRing::can_shard(const SimParams& p, unsigned shards) {
   const uint64_t vmax_eff = std::min<uint64_t>(p.v_max, p.road_length - 1);
   const char* ks = std::getenv("NASCH_B200_K");
   const long kreq = ks && *ks ? std::strtol(ks, nullptr, 10) : kPlanMax;
-  uint64_t K = static_cast<uint64_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
+  uint64_t K = static_cast<uint64_t>(std::max<long>(1, std::min<long>(kreq, std::min(kPlanMax, kTbHalo))));
   K = std::min<uint64_t>(K, kConeMax / (vmax_eff + 1));
   const uint64_t min_seg = p.car_count / shards;  // floor partition: smallest segment
   return K >= 2 && p.road_length > K * vmax_eff && p.car_count >= K * (vmax_eff + 1) && min_seg >= 64;
@@ -223,7 +223,7 @@ struct ShardedRing::Impl {
     G = world;
     const char* ks = std::getenv("NASCH_B200_K");
     long kreq = ks && *ks ? std::strtol(ks, nullptr, 10) : kPlanMax;
-    K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, kPlanMax)));
+    K = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq, std::min(kPlanMax, kTbHalo))));
     K = std::min<uint32_t>(K, kConeMax / (vmax_eff + 1));
     lo.resize(G + 1);
     for (unsigned g = 0; g <= G; ++g) lo[g] = static_cast<uint32_t>(uint64_t(g) * n / G);

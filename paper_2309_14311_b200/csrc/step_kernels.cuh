@@ -40,7 +40,7 @@
 
 namespace nb200 {
 
-constexpr int kPlanMax = 16;  // steps per temporal-blocked launch (TB kernel; its halo)
+constexpr int kPlanMax = 32;  // steps per temporal-blocked launch (TB kernel; <= its halo)
 constexpr int kPlanCap = 32;  // plan capacity of Ctl (the distributed-resident epochs)
 
 struct Ctl {
@@ -96,6 +96,12 @@ struct RingArgs {
 };
 
 // ---- vector access helpers ----------------------------------------------
+
+// Bulk prefetch of [p, p + bytes) into L2 (TMA unit; p and bytes multiples
+// of 16): the next tile's state streams in while this tile's steps run.
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
 
 __device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
   uint4 r;
@@ -171,6 +177,17 @@ struct VLanes<uint8_t, 16> {
     *reinterpret_cast<uint4*>(p) = make_uint4(pack4(v), pack4(v + 4), pack4(v + 8), pack4(v + 12));
   }
 };
+template <>
+struct VLanes<uint8_t, 32> {
+  static __device__ __forceinline__ void load(const uint8_t* p, uint32_t* v) {
+    VLanes<uint8_t, 16>::load(p, v);
+    VLanes<uint8_t, 16>::load(p + 16, v + 16);
+  }
+  static __device__ __forceinline__ void store(uint8_t* p, const uint32_t* v) {
+    VLanes<uint8_t, 16>::store(p, v);
+    VLanes<uint8_t, 16>::store(p + 16, v + 16);
+  }
+};
 template <int CPT>
 struct VLanes<uint32_t, CPT> {
   static __device__ __forceinline__ void load(const uint32_t* p, uint32_t* v) {
@@ -203,6 +220,46 @@ __device__ __forceinline__ uint32_t car_rule(uint32_t x, uint32_t xl, uint32_t v
   crossed = nx >= L ? 1u : 0u;
   xnew = crossed ? nx - L : nx;
   return v;
+}
+
+// Sum of small non-negative integers on the FP32 pipe: read as floats, the
+// bit patterns of integers below 2^23 are denormals, whose addition
+// (without flush-to-zero: PTX add.rn.f32, no .ftz) is exact integer
+// addition of the bit patterns.  Moves the temporal-blocked kernel's
+// per-step velocity sums off the integer ALU pipe (its binding pipe) onto
+// the otherwise idle FP32 lanes.  Valid while every partial sum < 2^23.
+__device__ __forceinline__ float fadd_denorm(float a, float b) {
+  float r;
+  asm("add.rn.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+template <int CPT>
+__device__ __forceinline__ uint32_t vsum_fp32(const uint32_t* v) {
+  float t[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) t[c] = __uint_as_float(v[c]);
+#pragma unroll
+  for (int w = 1; w < CPT; w <<= 1) {
+#pragma unroll
+    for (int c = 0; c + w < CPT; c += 2 * w) t[c] = fadd_denorm(t[c], t[c + w]);
+  }
+  return __float_as_uint(t[0]);
+}
+template <int CPT>
+__device__ __forceinline__ uint32_t vsum_imad(const uint32_t* v) {
+  uint32_t t[CPT];
+#pragma unroll
+  for (int c = 0; c < CPT; ++c) t[c] = v[c];
+#pragma unroll
+  for (int w = 1; w < CPT; w <<= 1) {
+#pragma unroll
+    for (int c = 0; c + w < CPT; c += 2 * w) {
+      uint32_t r;
+      asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(t[c]), "r"(1u), "r"(t[c + w]));
+      t[c] = r;
+    }
+  }
+  return t[0];
 }
 
 // Sum of CPT velocities (u8 lanes: two byte dot-products of the packed

@@ -14,14 +14,33 @@ namespace nb200 {
 #define NB_TB_TPB 128
 #endif
 #ifndef NB_TB_CPT
-#define NB_TB_CPT 16
+#define NB_TB_CPT 32
 #endif
 #ifndef NB_TB_MINB
-#define NB_TB_MINB 5
+#define NB_TB_MINB 4
+#endif
+// Halo depth = the deepest temporal blocking a launch may use (k <= HALO).
+#ifndef NB_TB_HALO
+#define NB_TB_HALO 32
 #endif
 
 #ifndef NB_TB_WT
 #define NB_TB_WT 1
+#endif
+
+// Per-step velocity sum of a thread's cars: 0 IADD3 (ALU pipe), 1 FP32
+// denormal adds (FMA pipe, step_kernels.cuh vsum_fp32), 2 IMAD tree.
+#ifndef NB_TB_VSUM
+#define NB_TB_VSUM 1
+#endif
+// Velocity clamp min(v + 1, vmax, gap) as one FMNMX3 (tb_kernel.cuh).
+#ifndef NB_TB_MN3
+#define NB_TB_MN3 1
+#endif
+
+// L2 bulk prefetch of each warp's next tile (tb_kernel.cuh).
+#ifndef NB_TB_PREFETCH
+#define NB_TB_PREFETCH 0
 #endif
 
 // Tile geometry.  Block tiles (WT = false): the block's TPB*CPT cars share
@@ -53,7 +72,7 @@ constexpr int kTbWaves = NB_TB_WAVES;
 
 constexpr int kTbTPB = NB_TB_TPB;                   // threads per tile
 constexpr int kTbCPT = NB_TB_CPT;                   // consecutive cars per thread
-constexpr int kTbHalo = 16;                         // cars ahead re-read per tile (>= K)
+constexpr int kTbHalo = NB_TB_HALO;                 // cars ahead re-read per tile (>= K)
 constexpr bool kTbWT = NB_TB_WT != 0;
 using TbLarge = TbGeom<kTbTPB, kTbCPT, kTbHalo, kTbWT>;
 constexpr uint32_t kTbLoad = TbLarge::kLoad;        // cars spanned per tile

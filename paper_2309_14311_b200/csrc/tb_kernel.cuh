@@ -30,6 +30,25 @@
 
 namespace nb200 {
 
+// The next launch's origin cone (kplan (vmax + 1) cars, one per thread) is
+// simulated by the launch's last block when it fits the block; otherwise
+// by cone_init_kernel<VT, 256> enqueued after the launch (engine.cu).
+__host__ __device__ __forceinline__ bool tb_plan_inline(uint32_t kplan, uint32_t vmax, int tpb) {
+  return kplan * (vmax + 1) <= uint32_t(tpb) && tpb >= 64;
+}
+
+#ifdef NB_TB_TRACE
+// Experiment builds only: %globaltimer per launch (slot = launch index mod
+// 64): [0] first block start, [1] last block start, [2] first block end,
+// [3] last block end (before the ticket), [4] plan start, [5] plan end.
+static __device__ unsigned long long g_tb_trace[64][8];  // per translation unit
+__device__ __forceinline__ unsigned long long tb_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 // The launch body.  PUSH (segmented ring, peer-memory exchange only): the
 // launch's last block also publishes this segment's exchange record for the
 // next launch straight into every segment's receive slots (shard_push,
@@ -42,9 +61,10 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
   constexpr uint32_t STORE = G::kStore;   // cars owned (stored) per block tile
   constexpr uint32_t WSTORE = G::kWarpStore;  // owned per halo unit (warp or block)
   constexpr int NW = TPB / 32;
-  static_assert(HALO >= kPlanMax && HALO % 16 == 0, "halo must cover the plan");
+  static_assert(HALO % 16 == 0 && HALO <= kPlanMax && CPT <= 64, "halo bounds the plan; k <= HALO");
   using Acc = typename std::conditional<sizeof(VT) == 1, uint32_t, unsigned long long>::type;
-  __shared__ uint32_t s_W[kPlanMax], s_E[kPlanMax], s_E2[kPlanMax];
+  // per step j: {E, E2, id of the rank-0 car (N - W, N when W = 0), 0}
+  __shared__ uint4 s_plan[kPlanMax];
   __shared__ uint32_t s_lead[2][NW];
   __shared__ Acc s_acc[kPlanMax][TPB];  // per-thread, per-step velocity sums
 
@@ -52,13 +72,17 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
   const uint32_t N = ra.n, L = ra.L, vmax = ra.vmax, tp = ra.tp;
   const uint64_t t = ctl->t;
   const int b = static_cast<int>(ctl->buf);
-  if (threadIdx.x < kPlanMax) {
-    s_W[threadIdx.x] = ctl->Wk[threadIdx.x];
-    s_E[threadIdx.x] = ctl->Ek[threadIdx.x];
-    s_E2[threadIdx.x] = ctl->E2k[threadIdx.x];
+#ifdef NB_TB_TRACE
+  unsigned long long* trc = g_tb_trace[(t / (k ? k : 1)) % 64];
+  if (threadIdx.x == 0) {
+    const unsigned long long now = tb_now();
+    atomicMin(trc + 0, now);
+    atomicMax(trc + 1, now);
   }
-#pragma unroll
-  for (int j = 0; j < kPlanMax; ++j) s_acc[j][threadIdx.x] = 0;
+#endif
+  if (threadIdx.x < k) s_plan[threadIdx.x] = make_uint4(ctl->Ek[threadIdx.x], ctl->E2k[threadIdx.x],
+                                                        N - ctl->Wk[threadIdx.x], 0u);
+  for (uint32_t j = 0; j < k; ++j) s_acc[j][threadIdx.x] = 0;
   __syncthreads();
   const uint32_t* __restrict__ X = xbuf(ra, b);
   const VT* __restrict__ V = vbuf<VT>(ra, b);
@@ -70,7 +94,10 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
   const uint32_t u0 = WT ? lane * CPT : i0;
   const uint32_t reach = k * vmax;        // farthest any car moves in this launch (< L)
 
-  // P = a^(global id of this thread's first car in its first tile)
+  // P = a^(global id of this thread's first car in its first tile).  The
+  // draw of car c at step j is E_j a^(id_0 + c) = (E_j P) a^c: one mulmod
+  // per thread and step for Q = E_j P, then one per car with the constant
+  // 2 a^c as a constant-bank operand (no per-car multiplier registers).
   uint32_t P = mulmod_d(mulmod_d(ra.agofs, __ldg(ra.blkpow + blockIdx.x)), __ldg(ra.thrpow + threadIdx.x));
   uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
   const uint32_t nl = ra.nl;  // cars stored here (a shard's segment, or the ring)
@@ -83,7 +110,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     // Contiguous in memory: always for a shard (its halo sits inline after
     // nl); on one GPU unless the tile wraps past id N-1.
     const bool fast = ra.sharded || nowrap;
-    uint32_t x[CPT], v[CPT], ap[CPT];
+    uint32_t x[CPT], v[CPT];
     if (fast) {
 #pragma unroll
       for (int q = 0; q < CPT / 4; ++q) {
@@ -103,35 +130,45 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         v[c] = V[id];
       }
     }
-    // 2 * a^id for this thread's cars (doubled for mulmod_x2): a^(first
-    // id) times a^c from the constant table -- independent products, no
-    // dependent chain.  Ids wrapped past N (only in the tile straddling id
-    // N-1) also multiply by a^-N.
-    ap[0] = P << 1;
-#pragma unroll
-    for (int c = 1; c < CPT; ++c) ap[c] = mulmod_d(P, c_pow.lin[c]) << 1;
-    if (!nowrap) {
-#pragma unroll
-      for (int c = 0; c < CPT; ++c)
-        if (base + c >= N) ap[c] = mulmod_d(ap[c] >> 1, ra.an_inv) << 1;
+#if NB_TB_PREFETCH
+    // The warp's cars of its NEXT tile to L2 while this one steps.
+    if (WT && lane == 0 && tile + gridDim.x < ntiles) {
+      const uint32_t nb = (tile + gridDim.x) * STORE + warp * WSTORE;
+      if (ra.gofs + nb + 32u * CPT <= N || ra.sharded) {
+        prefetch_l2_bulk(X + nb, 32u * CPT * 4u);
+        prefetch_l2_bulk(V + nb, 32u * CPT * sizeof(VT));
+      }
     }
+#endif
+    const uint32_t P2 = P << 1;
     P = mulmod_d(P, ra.g);
     // bit c: car c is stored by this tile (all of them but in the halo and
     // at a shard's end)
     const bool own_all = u0 + CPT <= WSTORE && bl + CPT <= nl;
-    uint32_t own = own_all ? (1u << CPT) - 1u : 0u;
+    unsigned long long own = own_all ? ~0ull : 0ull;
     if (!own_all) {
+      own = 0ull;
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) own |= (u0 + c < WSTORE && bl + c < nl) ? (1u << c) : 0u;
+      for (int c = 0; c < CPT; ++c) own |= (u0 + c < WSTORE && bl + c < nl) ? (1ull << c) : 0ull;
     }
     uint32_t xmax = x[0];
 #pragma unroll
     for (int c = 1; c < CPT; ++c) xmax = max(xmax, x[c]);
     const bool plain = nowrap && xmax < L - reach;
+#if NB_TB_MN3
+    // Offset form x[c] = position - c (mod 2^32) for the whole tile: the
+    // headway IMAD then yields the gap x_{c+1} - x_c - 1 directly.
+    // (Measured against a form that also keeps velocity + 1 and position -
+    // c + j, so that min(v+1, vmax, gap) needs no add and the clamp is one
+    // VIADDMNMX: 9 % fewer instructions per step but 1.7 % slower on C3,
+    // round 2.)
+#pragma unroll
+    for (int c = 1; c < CPT; ++c) x[c] -= c;
+#endif
 
     for (uint32_t j = 0; j < k; ++j) {
-      const uint32_t E = s_E[j], E2 = s_E2[j];
-      const uint32_t bound = N - s_W[j];  // id of the rank-0 car (N when W = 0)
+      const uint4 pl = s_plan[j];
+      const uint32_t E = pl.x, E2 = pl.y, bound = pl.z;
       // Slots alternate with the running step count, so one barrier per step
       // suffices (a slot is rewritten only after the next barrier).
       uint32_t xn;
@@ -148,7 +185,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         if (lane == 31) xn = (warp + 1 < NW) ? s_lead[slot][warp + 1] : x[CPT - 1];
       }
       if (plain && !(base < bound && bound <= base + CPT)) {
-        const uint32_t Es = base < bound ? E : E2;
+        const uint32_t Q = mulmod_x2(P2, base < bound ? E : E2);
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           // Balanced between the FMA and ALU pipes (both issue a warp
@@ -158,35 +195,73 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
           // measured +10 % on C3), deceleration flag as the sign of s - tp
           // (ptxas fuses it with the add: LEA.HI.SX32; forcing it onto the
           // FMA pipe as IMAD.HI measured 8 % slower).
-          const uint32_t s = mulmod_x2(ap[c], Es);
+          const uint32_t s = mulmod_x2(c_apow2.v[c], Q);
+#if NB_TB_MN3
+          // gap = x_{c+1} - x_c - 1 from the offset form (the next lane's
+          // car 0 is not offset: minus CPT); tp * (-1) + s keeps s - tp an
+          // IMAD (FMA pipe).  min(v + 1, vmax, gap) is ONE three-input
+          // FMNMX3 on the integers' bit patterns (non-negative integers
+          // order like the floats they encode; the NaN patterns of a gap
+          // above 0x7f800000, or of the halo front car's meaningless gap,
+          // lose every min), with v + 1 as an exact denormal FADD on the FP32
+          // pipe: one ALU instruction where min/min took two.
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn - CPT;
+          const uint32_t gap = x[c] * ra.neg1 + xl;
+          int dec;
+          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(tp * ra.neg1 + s)));
+          float m3;
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(m3)
+              : "f"(fadd_denorm(__uint_as_float(v[c]), __uint_as_float(1u))),
+                "f"(__uint_as_float(vmax)), "f"(__uint_as_float(gap)));
+          v[c] = static_cast<uint32_t>(max(static_cast<int>(__float_as_uint(m3)) + dec, 0));
+#else
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
           const uint32_t d = x[c] * ra.neg1 + xl;
-          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
           int dec;
           asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
+          const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
           v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+#endif
           x[c] += v[c];
         }
         if (own_all) {
+#if NB_TB_VSUM == 1
+          s_acc[j][threadIdx.x] += static_cast<Acc>(vsum_fp32<CPT>(v));
+#elif NB_TB_VSUM == 2
+          s_acc[j][threadIdx.x] += static_cast<Acc>(vsum_imad<CPT>(v));
+#else
           s_acc[j][threadIdx.x] += static_cast<Acc>(VSum<uint32_t, CPT>::sum(v));
+#endif
         } else if (own) {  // a shard's last, partial tile
           Acc sum = 0;
 #pragma unroll
-          for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1u) ? v[c] : 0u;
+          for (int c = 0; c < CPT; ++c) sum += ((own >> c) & 1ull) ? v[c] : 0u;
           s_acc[j][threadIdx.x] += sum;
         }
       } else {
+        // near the origin / at the rank seam / in the tile wrapping past id
+        // N-1: per car, base E or E2 by rank side, a^-N for wrapped ids
+        const uint32_t QE = mulmod_x2(P2, E), QE2 = mulmod_x2(P2, E2);
+        const uint32_t QEw = mulmod_d(QE, ra.an_inv), QE2w = mulmod_d(QE2, ra.an_inv);
         Acc sum = 0;
         uint32_t crs = 0;
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
-          uint32_t id = base + c;
-          if (id >= N) id -= N;
-          const uint32_t s = mulmod_x2(ap[c], id < bound ? E : E2);
-          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
+          const bool wrapped = base + c >= N;
+          const uint32_t id = wrapped ? base + c - N : base + c;
+          const uint32_t q = id < bound ? (wrapped ? QEw : QE) : (wrapped ? QE2w : QE2);
+          const uint32_t s = mulmod_x2(c_apow2.v[c], q);
           uint32_t cr = 0;
+#if NB_TB_MN3
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] + (c + 1) : xn;
+          uint32_t xnew;
+          v[c] = car_any(x[c] + c, xl, v[c], s, L, vmax, tp, xnew, cr);
+          x[c] = xnew - c;
+#else
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
           v[c] = car_any(x[c], xl, v[c], s, L, vmax, tp, x[c], cr);
-          const bool mine = (own >> c) & 1u;
+#endif
+          const bool mine = (own >> c) & 1ull;
           sum += mine ? v[c] : 0u;
           crs += mine ? cr : 0u;
         }
@@ -194,6 +269,10 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         if (crs) atomicAdd(&ra.rec[(t + j) % kRecCap].c, crs);
       }
     }
+#if NB_TB_MN3
+#pragma unroll
+    for (int c = 1; c < CPT; ++c) x[c] += c;
+#endif
     if (fast) {
       // A shard's last tile may spill past nl into its halo/padding region,
       // which the plan kernel rewrites before the next launch reads it.
@@ -207,7 +286,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     } else {
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        if ((own >> c) & 1u) {
+        if ((own >> c) & 1ull) {
           Xo[bl + c] = x[c];
           Vo[bl + c] = static_cast<VT>(v[c]);
         }
@@ -224,7 +303,17 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0 && acc) atomicAdd(&ra.rec[(t + j) % kRecCap].sumv, acc);
   }
+#ifdef NB_TB_TRACE
+  if (threadIdx.x == 0) {
+    const unsigned long long now = tb_now();
+    atomicMin(trc + 2, now);
+    atomicMax(trc + 3, now);
+  }
+#endif
   if (!last_block_done(ctl)) return;
+#ifdef NB_TB_TRACE
+  if (threadIdx.x == 0) trc[4] = tb_now();
+#endif
 
   // Last block: check the plan, advance the control block, plan the next k.
   // One thread per step (k <= kPlanMax <= TPB), earliest mismatch wins.
@@ -252,23 +341,18 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
   }
   __syncthreads();
   const uint32_t Wn = s_Wnext;
-  if (ra.sharded) {
-    // The next plan needs cars of other shards: the exchange + plan kernel
-    // (shard_kernels.cuh) produce it.
-    if (threadIdx.x == 0) {
-      ctl->W = Wn;
-      ctl->t = t + k;
-      ctl->buf = static_cast<unsigned int>(b ^ 1);
-      ctl->ticket = 0;
+  // The next plan: inline when its cone (kplan (vmax + 1) cars) fits this
+  // block; otherwise the host enqueues a 256-thread cone kernel after this
+  // launch (tb_plan_inline), and a segmented ring plans in its exchange
+  // kernel (shard_kernels.cuh), which needs cars of other segments.
+  const bool inline_plan = !ra.sharded && tb_plan_inline(ra.kplan, ra.vmax, TPB);
+  if (inline_plan) {
+    cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
+    for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
+      StepRec* r = ra.rec + ((t + k + j) % kRecCap);
+      r->sumv = 0;
+      r->c = 0;
     }
-    if constexpr (PUSH) shard_push<VT, TPB>(ra, Xo, Vo, Wn, xa);
-    return;
-  }
-  cone_plan<VT, TPB>(ra, Xo, Vo, t + k, Wn, ra.kplan, ctl);
-  for (uint32_t j = threadIdx.x; j < ra.kplan; j += TPB) {
-    StepRec* r = ra.rec + ((t + k + j) % kRecCap);
-    r->sumv = 0;
-    r->c = 0;
   }
   if (threadIdx.x == 0) {
     ctl->W = Wn;
@@ -276,6 +360,11 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     ctl->buf = static_cast<unsigned int>(b ^ 1);
     ctl->ticket = 0;
   }
+  if constexpr (PUSH) shard_push<VT, TPB>(ra, Xo, Vo, Wn, xa);
+#ifdef NB_TB_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) trc[5] = tb_now();
+#endif
 }
 
 template <typename VT, int TPB, int CPT, int HALO, bool WT>

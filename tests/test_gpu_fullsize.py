@@ -6,9 +6,9 @@ of a 2e8-car ring -- at the BASELINE.json size and compares it bit for bit
 with the reference itself (oracle/_ref: the unmodified reference sources,
 its OpenMP Engine on all host cores):
 
-* C3 (L=1e9, N=2e8, p=0.13): 48 steps = three full 16-step launches, every
+* C3 (L=1e9, N=2e8, p=0.13): 96 steps = three full 32-step launches, every
   step's velocity sum and crossing count, final positions and velocities.
-* C5 (L=1e8, N=6e7, p=0.5, k=8 as BASELINE names it, and k=16): 64 steps,
+* C5 (L=1e8, N=6e7, p=0.5, k=8 as BASELINE names it, 16 and 32): 64 steps,
   plus an asynchronous snapshot taken at step 64 while the ring keeps
   stepping.
 * C4: one 64-ring slice of the fundamental-diagram sweep (every density,
@@ -48,16 +48,19 @@ def cores(ref):
 
 
 def test_config3_full_size_three_launches_vs_reference(ref):
-    """C3 exactly as bench.py runs it: 2e8 cars, three full 16-step
-    launches (enqueued one launch at a time, as the timed region does)."""
-    L, N, p, seed, T = 10**9, 2 * 10**8, 0.13, 3, 48
+    """C3 exactly as bench.py runs it: 2e8 cars, three full launches of the
+    default depth (K = 32 steps; enqueued one launch at a time, as the
+    timed region does), including the plan hand-off between launches."""
+    L, N, p, seed = 10**9, 2 * 10**8, 0.13, 3
     x0, v0 = nasch.fill_uniform_state(L, N, 0, seed)
     e = nasch.Engine(params(L, N, 5, p, 1000, seed))
     e.set_checksum(False)
     e.set_state(x0, v0)
-    assert e.steps_per_launch == 16
-    for _ in range(T // 16):
-        e.enqueue(16)
+    K = e.steps_per_launch
+    assert K == 32
+    T = 3 * K
+    for _ in range(3):
+        e.enqueue(K)
     e.synchronize()
     x, v = e.snapshot()
     sumv, wraps = e.sumv_series(), e.wrap_series()
@@ -71,9 +74,10 @@ def test_config3_full_size_three_launches_vs_reference(ref):
     assert (v == r["v"]).all(), "velocities differ"
 
 
-@pytest.mark.parametrize("K", [8, 16])
+@pytest.mark.parametrize("K", [8, 16, 32])
 def test_config5_full_size_vs_reference_with_snapshot(ref, k_env, K):
-    """C5 (jam-dominated, p=0.5) at k=8 (BASELINE's k) and k=16: 64 steps,
+    """C5 (jam-dominated, p=0.5) at k=8 (BASELINE's k), 16 and the default
+    32: 64 steps,
     every step's sums/crossings, and an asynchronous snapshot at step 64
     that completes while 16 further steps run."""
     L, N, p, seed, T = 10**8, 6 * 10**7, 0.5, 5, 64

@@ -98,13 +98,25 @@ def main():
             f.write(f"- `{d['kernel'][:60]}`: " + ", ".join(
                 f"{k} {v:.2f}" for k, v in d["top_stalls_per_issue"].items()) + "\n")
     if a.step_kernel and out:
+        # one capture per launch depth; bench.py picks the one its timed
+        # region runs at
         d = out[0]
-        with open(os.path.join(os.path.dirname(a.out), "ncu_step_kernel.json"), "w") as f:
-            json.dump({"L": a.L, "N": a.N, "steps_per_launch": a.steps_per_launch,
-                       "kernel": d["kernel"], "dram_bytes_per_launch": d["dram_bytes"],
-                       "warp_inst_per_launch": float(d["smsp__inst_executed.sum"]["value"]),
-                       "seconds_per_launch_under_ncu": d["seconds"],
-                       "source": os.path.basename(a.out) + ".json"}, f, indent=1)
+        path = os.path.join(os.path.dirname(a.out), "ncu_step_kernel.json")
+        try:
+            with open(path) as f:
+                prev = json.load(f)
+        except (OSError, ValueError):
+            prev = {}
+        caps = [c for c in prev.get("captures", []) if prev.get("L") == a.L and prev.get("N") == a.N
+                and c.get("steps_per_launch") != a.steps_per_launch]
+        caps.append({"steps_per_launch": a.steps_per_launch, "kernel": d["kernel"],
+                     "dram_bytes_per_launch": d["dram_bytes"],
+                     "warp_inst_per_launch": float(d["smsp__inst_executed.sum"]["value"]),
+                     "seconds_per_launch_under_ncu": d["seconds"],
+                     "source": os.path.basename(a.out) + ".json"})
+        caps.sort(key=lambda c: c["steps_per_launch"])
+        with open(path, "w") as f:
+            json.dump({"L": a.L, "N": a.N, "captures": caps}, f, indent=1)
     print(open(a.out + ".md").read())
 
 
