@@ -241,6 +241,7 @@ struct GpuEnsemble::Impl {
   EnsArgs ea{};
   EnsRing* h_trings = nullptr;
   int tgrid = 1;
+  uint32_t K = kEtK;  // steps per tiled launch (<= kEtK, cone <= 512 cars)
   // pinned staging in the tiled layout (set_state_all32)
   size_t stage_cars = 0;
   uint32_t* h_stage_x = nullptr;
@@ -265,7 +266,7 @@ struct GpuEnsemble::Impl {
   void tlaunch(uint64_t steps) {
     const int pgrid = static_cast<int>((trings.size() + 7) / 8);
     for (uint64_t left = steps; left > 0;) {
-      const uint32_t kq = static_cast<uint32_t>(std::min<uint64_t>(left, kEtK));
+      const uint32_t kq = static_cast<uint32_t>(std::min<uint64_t>(left, K));
       ens_plan_kernel<<<pgrid, 256, 0, stream>>>(ea, kq);
       ens_tb_kernel<kEtTPB><<<tgrid, kEtTPB, 0, stream>>>(ea);
       CKE(cudaGetLastError());
@@ -331,7 +332,10 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
   for (const SimParams& p : rings) {
     const uint64_t vm = std::min<uint64_t>(p.v_max, p.road_length - 1);
     all_tiled = all_tiled && vm <= 31 && p.road_length > kEtK * vm && p.car_count >= kEtK * (vm + 1);
+    // steps per launch: the planner warp simulates K (vmax + 1) <= 512 cone cars
+    d.K = std::min<uint32_t>(d.K, 512u / static_cast<uint32_t>(vm + 1));
   }
+  d.K = std::max<uint32_t>(d.K, 1u);
   if (all_tiled) {
     d.tiled = true;
     uint64_t total = 0;

@@ -21,6 +21,14 @@
 
 namespace nb200 {
 
+// Plain-path car update (tb_kernel.cuh): velocity sums as FP32 denormal
+// adds, min(v + 1, vmax, gap) as one FMNMX3 on offset positions.
+#ifndef NB_ET_VSUM
+#define NB_ET_VSUM 1
+#endif
+#ifndef NB_ET_MN3
+#define NB_ET_MN3 1
+#endif
 constexpr int kEtTPB = 128;
 constexpr int kEtCPT = 16;
 constexpr uint32_t kEtHalo = 16;
@@ -207,6 +215,11 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
     // this thread's ids run consecutively below N (only the ring's last
     // tile has threads that wrap)
     const bool plain = base + CPT <= N && xmax < L - k * vmax;
+#if NB_ET_MN3
+    // offset form x[c] - c for the plain path's FMNMX3 (tb_kernel.cuh)
+#pragma unroll
+    for (int c = 1; c < CPT; ++c) x[c] -= c;
+#endif
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t E = s_plan[warp][1][j], E2 = s_plan[warp][2][j];
       const uint32_t bound = N - s_plan[warp][0][j];
@@ -218,16 +231,32 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           const uint32_t s = mulmod_x2(ap[c], Es);
+#if NB_ET_MN3
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn - CPT;
+          const uint32_t gap = x[c] * ea.neg1 + xl;
+          int dec;
+          asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(tp * ea.neg1 + s)));
+          float m3;
+          asm("min.f32 %0, %1, %2, %3;" : "=f"(m3)
+              : "f"(fadd_denorm(__uint_as_float(v[c]), __uint_as_float(1u))),
+                "f"(__uint_as_float(vmax)), "f"(__uint_as_float(gap)));
+          v[c] = static_cast<uint32_t>(max(static_cast<int>(__float_as_uint(m3)) + dec, 0));
+#else
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
           const uint32_t d = x[c] * ea.neg1 + xl;
           const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
           int dec;
           asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
           v[c] = static_cast<uint32_t>(max(vc + dec, 0));
+#endif
           x[c] += v[c];
         }
         if (own_all) {  // separate branches (as tb_kernel.cuh): no per-car selects
+#if NB_ET_VSUM
+          s_acc[j][threadIdx.x] += vsum_fp32<CPT>(v);
+#else
           s_acc[j][threadIdx.x] += VSum<uint32_t, CPT>::sum(v);
+#endif
         } else if (own) {
           uint32_t sum = 0;
 #pragma unroll
@@ -241,15 +270,25 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
           uint32_t id = base + c;
           while (id >= N) id -= N;
           const uint32_t s = mulmod_x2(ap[c], id < bound ? E : E2);
+#if NB_ET_MN3
+          const uint32_t xc = x[c] + c;
+          const uint32_t xl = (c + 1 < CPT) ? x[c + 1] + (c + 1) : xn;
+#else
+          const uint32_t xc = x[c];
           const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
-          uint32_t d = x[c] * ea.neg1 + xl;
+#endif
+          uint32_t d = xc * ea.neg1 + xl;
           d = min(d, d + L);  // leader past the origin: + L
           const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
           int dec;
           asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(s - tp)));
           v[c] = static_cast<uint32_t>(max(vc + dec, 0));
-          const uint32_t xs = x[c] + v[c];
+          const uint32_t xs = xc + v[c];
+#if NB_ET_MN3
+          x[c] = min(xs, xs - L) - c;
+#else
           x[c] = min(xs, xs - L);
+#endif
           const bool mine = (own >> c) & 1u;
           sum += mine ? v[c] : 0u;
           crs += (mine && xs >= L) ? 1u : 0u;
@@ -259,6 +298,10 @@ __global__ void __launch_bounds__(TPB, NB_ET_MINB) ens_tb_kernel(const EnsArgs e
         if (lane == 0 && crs) atomicAdd(&ea.counts[td.ring].c[j], crs);
       }
     }
+#if NB_ET_MN3
+#pragma unroll
+    for (int c = 1; c < CPT; ++c) x[c] += c;
+#endif
     // Per-step sums of this tile: one atomic per step.
     for (uint32_t j = 0; j < k; ++j) {
       const uint32_t sv = __reduce_add_sync(0xffffffffu, s_acc[j][threadIdx.x]);
