@@ -491,50 +491,90 @@ struct GpuRing::Impl {
 }
 
   // ---- on-device trajectory checksum ---------------------------------
-  unsigned long long* fnv_T[2] = {nullptr, nullptr};
-  unsigned long long* fnv_P[2] = {nullptr, nullptr};
+  // Per step (fnv_kernels.cuh, low-byte decomposition): 8-bit chunk maps,
+  // their composition tree up and walk down (each chunk's incoming low
+  // byte), one exact 64-bit pass per chunk, the chunks' affine maps reduced
+  // and applied -- all graph-captured, no host round trip.
   unsigned long long* fnv_hash = nullptr;
   uint32_t fnv_chunks = 0;
+  std::vector<uint8_t*> fnv_maps;   // level 0: chunk maps; level i+1: groups of 256 of level i
+  std::vector<uint32_t> fnv_count;  // maps per level
+  std::vector<uint8_t*> fnv_lb;     // incoming low byte per map, per level
+  uint8_t* fnv_sub = nullptr;       // cumulative sub-chunk maps (pass C starts)
+  uint32_t fnv_nsub = 0;
+  unsigned long long* fnv_A[2] = {nullptr, nullptr};
+  unsigned long long* fnv_D[2] = {nullptr, nullptr};
   cudaGraphExec_t fnv_graph = nullptr;
 
-  void fnv_enqueue() {
-    const uint32_t nchunks = fnv_chunks;
-    if (vbytes == 1) {
-      fnv_chunk_kernel<uint8_t><<<nchunks, 256, 0, stream>>>(args, fnv_T[0], fnv_P[0]);
-    } else {
-      fnv_chunk_kernel<uint32_t><<<nchunks, 256, 0, stream>>>(args, fnv_T[0], fnv_P[0]);
+  void fnv_alloc() {
+    fnv_chunks = static_cast<uint32_t>((2ull * n + kFnvRowChunk - 1) / kFnvRowChunk);
+    for (uint32_t m = fnv_chunks;;) {
+      uint8_t *maps = nullptr, *lb = nullptr;
+      CK(cudaMalloc(&maps, size_t(m) * 256));
+      CK(cudaMalloc(&lb, m));
+      fnv_maps.push_back(maps);
+      fnv_lb.push_back(lb);
+      fnv_count.push_back(m);
+      if (m <= 256) break;
+      m = (m + 255) / 256;
     }
-    int in = 0;
-    uint32_t n = nchunks;
-    while (n > 1) {
-      const uint32_t m = (n + 1) / 2;
-      fnv_compose_kernel<<<m, 256, 0, stream>>>(fnv_T[in], fnv_P[in], n, fnv_T[in ^ 1], fnv_P[in ^ 1]);
-      in ^= 1;
-      n = m;
+    fnv_nsub = static_cast<uint32_t>((2ull * n + kFnvSubLen - 1) / kFnvSubLen);
+    CK(cudaMalloc(&fnv_sub, size_t(fnv_chunks) * (kFnvSubs - 1) * 256));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaMalloc(&fnv_A[b], size_t(fnv_nsub) * 8));
+      CK(cudaMalloc(&fnv_D[b], size_t(fnv_nsub) * 8));
     }
-    fnv_apply_kernel<<<1, 1, 0, stream>>>(fnv_T[in], fnv_P[in], fnv_hash);
+    CK(cudaFuncSetAttribute(fnv_group8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    CK(cudaFuncSetAttribute(fnv_walk8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
   }
+
+  uint32_t fnv_enqueue() {
+    uint32_t nl = 0;
+    const uint32_t nc = fnv_chunks;
+    const int mgrid = static_cast<int>((nc + kMap8Warps - 1) / kMap8Warps);
+    if (vbytes == 1) fnv_map8_kernel<uint8_t><<<mgrid, 32 * kMap8Warps, 0, stream>>>(args, fnv_maps[0], fnv_sub, nc);
+    else fnv_map8_kernel<uint32_t><<<mgrid, 32 * kMap8Warps, 0, stream>>>(args, fnv_maps[0], fnv_sub, nc);
+    ++nl;
+    const size_t levels = fnv_maps.size();
+    for (size_t i = 0; i + 1 < levels; ++i, ++nl)
+      fnv_group8_kernel<<<fnv_count[i + 1], 256, 65536, stream>>>(fnv_maps[i], fnv_count[i], fnv_maps[i + 1]);
+    for (size_t i = levels; i-- > 0; ++nl) {
+      const int g = static_cast<int>((fnv_count[i] + 255) / 256);
+      fnv_walk8_kernel<<<g, 256, 65536, stream>>>(fnv_maps[i], fnv_count[i], i + 1 < levels ? fnv_lb[i + 1] : nullptr,
+                                                 fnv_hash, fnv_lb[i]);
+    }
+    const uint32_t ns = fnv_nsub;
+    const int agrid = static_cast<int>((ns + kAffTPB - 1) / kAffTPB);
+    if (vbytes == 1)
+      fnv_affine_kernel<uint8_t><<<agrid, kAffTPB, 0, stream>>>(args, fnv_lb[0], fnv_sub, ns, fnv_A[0], fnv_D[0]);
+    else
+      fnv_affine_kernel<uint32_t><<<agrid, kAffTPB, 0, stream>>>(args, fnv_lb[0], fnv_sub, ns, fnv_A[0], fnv_D[0]);
+    ++nl;
+    int in = 0;
+    for (uint32_t m = ns; m > 1; m = (m + 255) / 256, in ^= 1, ++nl)
+      fnv_affine_reduce<<<(m + 255) / 256, 256, 0, stream>>>(fnv_A[in], fnv_D[in], m, fnv_A[in ^ 1], fnv_D[in ^ 1]);
+    fnv_affine_apply<<<1, 1, 0, stream>>>(fnv_A[in], fnv_D[in], fnv_hash);
+    return nl + 1;
+  }
+
+  uint32_t fnv_graph_launches = 0;
 
   // Folds the current state's row into the device digest (one graph launch).
   void fnv_fold() {
     if (!fnv_hash) {
-      fnv_chunks = static_cast<uint32_t>((2ull * n + kFnvChunk - 1) / kFnvChunk);
-      for (int b = 0; b < 2; ++b) {
-        CK(cudaMalloc(&fnv_T[b], size_t(fnv_chunks) * 256 * 8));
-        CK(cudaMalloc(&fnv_P[b], size_t(fnv_chunks) * 8));
-      }
+      fnv_alloc();
       CK(cudaMalloc(&fnv_hash, 8));
       const unsigned long long h = hash;
       CK(cudaMemcpy(fnv_hash, &h, 8, cudaMemcpyHostToDevice));
       cudaGraph_t g;
       CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      fnv_enqueue();
+      fnv_graph_launches = fnv_enqueue();
       CK(cudaStreamEndCapture(stream, &g));
       CK(cudaGraphInstantiate(&fnv_graph, g, 0));
       CK(cudaGraphDestroy(g));
     }
     CK(cudaGraphLaunch(fnv_graph, stream));
-    launches += 2 + static_cast<uint64_t>(std::ceil(std::log2(std::max(1u, fnv_chunks))));
+    launches += fnv_graph_launches;
   }
 
   void pull_hash() {
@@ -825,9 +865,12 @@ GpuRing::Impl::~Impl() {
   for (int b = 0; b < 2; ++b) {
     cudaFree(x[b]);
     cudaFree(v[b]);
-    cudaFree(fnv_T[b]);
-    cudaFree(fnv_P[b]);
+    cudaFree(fnv_A[b]);
+    cudaFree(fnv_D[b]);
   }
+  for (uint8_t* p : fnv_maps) cudaFree(p);
+  for (uint8_t* p : fnv_lb) cudaFree(p);
+  cudaFree(fnv_sub);
   cudaFree(fnv_hash);
   cudaFree(ctl);
   cudaFree(rec);

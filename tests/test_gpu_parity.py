@@ -439,6 +439,23 @@ def test_device_checksum_many_chunks(port):
         assert (g["x"] == o["x"]).all()
 
 
+@pytest.mark.parametrize("L,N,vmax,T", [
+    (5 * 10**6, 1_200_001, 5, 3),    # >= 1e6 cars: 1172 chunk maps, two composition levels
+    (3000, 2000, 5, 25),             # one chunk level; positions < 256 take the one-byte path
+    (200000, 70000, 300, 4),         # u32 velocities above 255: four-byte map path
+    (10**6, 131072, 7, 6)])          # 2N a multiple of the 2048-value chunk
+def test_device_checksum_lowbyte_decomposition(port, L, N, vmax, T):
+    """The per-step digest as 8-bit chunk maps (two starts per register, 128
+    tracked), their composition tree and walk, one exact 64-bit pass per
+    chunk and the affine reduction, against the reference's serial FNV-1a
+    over every step's row."""
+    x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, 5), 13)
+    o = port.run(L, vmax, 0.3, 9, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    g = gpu_run(L, N, vmax, 0.3, 9, T, x0, v0, checksum=True)
+    assert g["checksum"] == o["checksum"], (L, N, vmax)
+    assert (g["x"] == o["x"]).all()
+
+
 @pytest.fixture
 def resident_env():
     old = {k: os.environ.get(k) for k in ("NASCH_B200_RESIDENT", "NASCH_B200_WARPRING")}
