@@ -13,7 +13,8 @@
 // replaced by the exact integer test `s < threshold(p)`: IEEE division is
 // correctly rounded hence monotone in s, so {s : fl(s/m) < p} is a prefix
 // [0, T_p) of the integers, and T_p is found by bisection with the very
-// same binary64 expression (tests/test_minstd.py checks the boundary).
+// same binary64 expression (tests/test_capi_host.py test_threshold_* check
+// the boundary).
 #pragma once
 #include <cstdint>
 

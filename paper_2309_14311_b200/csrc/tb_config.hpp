@@ -30,6 +30,8 @@ namespace nb200 {
 
 // Per-step velocity sum of a thread's cars: 0 IADD3 (ALU pipe), 1 FP32
 // denormal adds (FMA pipe, step_kernels.cuh vsum_fp32), 2 IMAD tree.
+// Measured on C3 (round 2, tools/variant_bench.py): 0 2.14e12, 1 2.18e12,
+// 2 2.06e12 (with NB_TB_MN3); half IADD3 / half FP32 2.11e12.
 #ifndef NB_TB_VSUM
 #define NB_TB_VSUM 1
 #endif

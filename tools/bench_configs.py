@@ -1,7 +1,7 @@
 """Throughput on every BASELINE.json configuration (1 GPU), next to the
 reference's own OpenMP Engine on a bounded sample of the same workload.
 
-  python tools/bench_configs.py [--only C1,C4] [--out profiles/r01_configs.json]
+  python tools/bench_configs.py [--only C1,C4] [--out profiles/r02_configs.json]
 
 C1  L=1e3,  N=200,   p=0.13, 1000 steps, 200 uniform sites from seed 42, v=0
 C2  L=1e6,  N=2e5,   p=0.25, 1e4 steps, v uniform in [0,5]
@@ -11,7 +11,10 @@ C4  4096 rings L=1e5, N_j = 5000 + floor(45000 j/63), p in {0,..,0.7}, 8 seeds,
 C5  L=1e8,  N=6e7,   p=0.5, 2e4 steps, full snapshot every 1000 steps
 
 GPU times are CUDA-event times on the engine stream with the state resident
-(snapshots included for C5); checksum off.  Every run also checks a
+(snapshots included for C5); checksum off, except the C3-checksum /
+C5-checksum rows: the reference's stock semantics, every step's row folded
+into the FNV-1a trajectory digest on the device.  C5 runs at the k = 8
+BASELINE names and at the engine's default depth.  Every run also checks a
 size-independent invariant (sorted positions, exact velocity-sum identity).
 """
 import argparse
@@ -42,14 +45,19 @@ def ev_time(stream, fn):
     return e0.elapsed_time(e1) / 1e3
 
 
-def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None, cores=1):
+def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None, cores=1, k=None,
+         checksum=False):
+    if k:
+        os.environ["NASCH_B200_K"] = str(k)
+    else:
+        os.environ.pop("NASCH_B200_K", None)
     x, v = nasch.fill_uniform_state(L, N, vinit, seed)
     # untimed warm-up as bench.py: >= 512 steps (launch-graph capture on the
     # first chunk, SM clock ramp from idle), capped at T for the small rings
-    warm = max(8, min(512, T))
+    warm = max(8, min(512, T)) if not checksum else 2
     prm = nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T + warm, seed=seed)
     e = nasch.Engine(prm)
-    e.set_checksum(False)
+    e.set_checksum(checksum)
     e.set_state(x, v)
     e.advance(warm)
     snaps = []
@@ -85,10 +93,12 @@ def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None,
     s = e.sumv_series()
     ok = bool((np.diff(xs.astype(np.int64)) > 0).all() and int(vs.sum()) == int(s[-1]))
     out = {"config": name, "L": L, "N": N, "p": p, "steps": T, "gpu_seconds": secs,
-           "gpu_car_updates_per_s": N * T / secs, "steps_per_launch": e.steps_per_launch,
+           "gpu_car_updates_per_s": N * T / secs, "steps_per_launch": 1 if checksum else e.steps_per_launch,
+           "checksum": "on (every step folded on the device)" if checksum else "off",
            "mean_velocity_last": float(s[-1]) / N, "invariants_ok": ok,
            "snapshots": len(snaps)}
     e.close()
+    os.environ.pop("NASCH_B200_K", None)
     if ref is not None and cpu_steps:
         r = ref.run(L, N, 5, p, seed, cpu_steps, workers=cores, x0=x.astype(np.uint64),
                     v0=v.astype(np.uint64), per_step=False, want_state=False)
@@ -112,17 +122,20 @@ def c4(ref=None, cores=1, T=5000):
     ens = nasch.Ensemble(params)
     inits = []
     for r, (N, p, sd) in enumerate(specs):
-        x, v = nasch.fill_uniform_state(L, N, 0, sd)
-        ens.set_state(r, x, v)
-        if r < 64:
-            inits.append((x, v))
+        inits.append(nasch.fill_uniform_state(L, N, 0, sd))
+    ens.set_state_all(np.concatenate([x for x, _ in inits]), np.concatenate([v for _, v in inits]))
+    inits = inits[:64]
+    ens.advance(64)  # warm-up, as bench.py's C4 leg
+    T -= 64
     setup = time.time() - t0
     secs = ev_time(ens.cuda_stream, lambda: (ens.enqueue(T), ens.synchronize()))
+    T += 64
     tot = ens.sumv_totals().astype(np.float64)
     flux = tot / (T * L)
     cars = sum(N for N, _, _ in specs)
     out = {"config": "C4", "rings": len(specs), "L": L, "total_cars": cars, "steps": T,
-           "gpu_seconds": secs, "gpu_car_updates_per_s": cars * T / secs, "setup_seconds": setup,
+           "timed_steps": T - 64, "gpu_seconds": secs, "gpu_car_updates_per_s": cars * (T - 64) / secs,
+           "setup_seconds": setup,
            "flux_min": float(flux.min()), "flux_max": float(flux.max()),
            "flux_p0_density_sweep": [float(f) for f in flux[:64:8]]}
     if ref is not None:
@@ -158,8 +171,8 @@ def c4(ref=None, cores=1, T=5000):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C1,C2,C3,C4,C5")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.json"))
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5,C3-checksum,C5-checksum")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.json"))
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
     torch.cuda.set_device(0)
@@ -182,6 +195,11 @@ def main():
     if "C5" in want:
         res.append(ring("C5", 10**8, 6 * 10**7, 0.5, 20000, 5, 0, snapshot_every=1000,
                         cpu_steps=10, ref=ref, cores=cores))
+        res.append(ring("C5 (k=8)", 10**8, 6 * 10**7, 0.5, 20000, 5, 0, snapshot_every=1000, k=8))
+    if "C3-checksum" in want:
+        res.append(ring("C3-checksum", 10**9, 2 * 10**8, 0.13, 20, 3, 0, checksum=True))
+    if "C5-checksum" in want:
+        res.append(ring("C5-checksum", 10**8, 6 * 10**7, 0.5, 50, 5, 0, checksum=True))
     doc = {"gpu": torch.cuda.get_device_name(0), "cpu_physical_cores": cores, "results": res}
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as f:
