@@ -383,21 +383,24 @@ def c3_leg(args, d: Dist):
     x, v = nasch.fill_uniform_state(L, N, 0, seed)
     log(f"[bench] generated C3 input in {time.time() - t0:.1f}s")
 
-    nccl_id = d.bcast(nasch.nccl_unique_id() if d.rank == 0 else None) if d.world > 1 else None
+    def fresh_id():
+        # one NCCL unique id per communicator (an id's bootstrap root serves
+        # one initialisation; it is not reused for a second communicator)
+        return d.bcast(nasch.nccl_unique_id() if d.rank == 0 else None) if d.world > 1 else None
+
     parity = None
     if d.world > 1 and not args.no_parity:
         t0 = time.time()
-        ok, mode = multi_gpu_parity(d, nccl_id)
+        ok, mode = multi_gpu_parity(d, fresh_id())
         parity = {"ok": ok, "ring": PARITY_RING, "exchange_mode": mode,
                   "checks": "trajectory checksum, whole-ring sumv/wrap series, collective state, "
                             "segment snapshots vs rank 0's single-GPU engine",
                   "seconds": round(time.time() - t0, 2)}
         log(f"[bench] multi-GPU parity self-check: {ok} ({parity['seconds']} s)")
-        nccl_id = d.bcast(nasch.nccl_unique_id() if d.rank == 0 else None)
 
     # ---- device-resident throughput -----------------------------------
     prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=W_run + R * K, seed=seed)
-    eng = (nasch.Engine.distributed(prm, d.rank, d.world, nccl_id) if d.world > 1
+    eng = (nasch.Engine.distributed(prm, d.rank, d.world, fresh_id()) if d.world > 1
            else nasch.Engine(prm))
     eng.set_checksum(False)
     eng.set_state(x, v)
@@ -456,7 +459,7 @@ def c3_leg(args, d: Dist):
     v64 = v.astype(np.uint64)
     del x, v
     prm2 = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=K, seed=seed)
-    eng2 = (nasch.Engine.distributed(prm2, d.rank, d.world, nccl_id) if d.world > 1
+    eng2 = (nasch.Engine.distributed(prm2, d.rank, d.world, fresh_id()) if d.world > 1
             else nasch.Engine(prm2))
     first, count = eng2.shard_range()
     # caller-owned output buffers, already faulted in (a serving loop reuses

@@ -25,7 +25,8 @@
 //
 // No worker can run more than two epochs ahead of any other (plan(e) needs
 // every worker past e-2), which is what makes two plan slots and two state
-// buffers enough.  Every wait is bounded: a CTA waiting more than ~2 s
+// buffers enough.  Every wait is bounded: a CTA waiting longer than
+// NASCH_B200_DR_TIMEOUT_S (default 60 s, wall time by %globaltimer)
 // raises `abort` and Ctl::err = 3, and every other waiter leaves on
 // `abort`, so a fault cannot hang the GPU.
 #pragma once
@@ -91,11 +92,24 @@ __device__ __forceinline__ unsigned int ld_relaxed_u32(const unsigned int* p) {
   return v;
 }
 
+// Bound on any single wait, in %globaltimer nanoseconds (wall time, so it
+// does not depend on the SM clock): NASCH_B200_DR_TIMEOUT_S, default 60 s
+// (engine.cu).  A wait that long means a worker CTA is not running (a
+// time-sliced or preempted GPU, a debugger); the launch then aborts with
+// Ctl::err = 3, reported at the next drain.
+static __constant__ unsigned long long c_dr_timeout_ns = 60ull * 1000000000ull;
+
+__device__ __forceinline__ unsigned long long dr_now_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Thread-0 spin until *p >= target; false when the launch is aborting.
 // Polls with relaxed (L2) loads and fences once on success: an acquire load
 // per poll would invalidate L1 every iteration.
 __device__ __noinline__ bool dr_wait_geq(const unsigned int* p, unsigned int target, DrSync* sync, Ctl* ctl) {
-  const long long start = clock64();
+  const unsigned long long start = dr_now_ns();
   for (uint32_t i = 0;; ++i) {
     if (ld_relaxed_u32(p) >= target) {
       __threadfence();
@@ -103,7 +117,7 @@ __device__ __noinline__ bool dr_wait_geq(const unsigned int* p, unsigned int tar
     }
     if ((i & 63u) == 63u) {
       if (ld_relaxed_u32(&sync->abort)) return false;
-      if (clock64() - start > 4000000000ll) {  // ~2 s at 1.9 GHz
+      if (dr_now_ns() - start > c_dr_timeout_ns) {
         atomicExch(&sync->abort, 1u);
         atomicCAS(&ctl->err, 0u, 3u);
         return false;
@@ -124,7 +138,7 @@ __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) 
 // Thread-0 spin until *p >= a and *q >= b (one acquire fence at the end).
 __device__ __noinline__ bool dr_wait2(const unsigned int* p, unsigned int a, const unsigned int* q, unsigned int b,
                                       DrSync* sync, Ctl* ctl) {
-  const long long start = clock64();
+  const unsigned long long start = dr_now_ns();
   for (uint32_t i = 0;; ++i) {
     const unsigned int vp = ld_relaxed_u32(p), vq = ld_relaxed_u32(q);
     if (vp >= a && vq >= b) {
@@ -133,7 +147,7 @@ __device__ __noinline__ bool dr_wait2(const unsigned int* p, unsigned int a, con
     }
     if ((i & 63u) == 63u) {
       if (ld_relaxed_u32(&sync->abort)) return false;
-      if (clock64() - start > 4000000000ll) {
+      if (dr_now_ns() - start > c_dr_timeout_ns) {
         atomicExch(&sync->abort, 1u);
         atomicCAS(&ctl->err, 0u, 3u);
         return false;
@@ -154,7 +168,7 @@ __device__ __forceinline__ bool dr_block_wait(const unsigned int* p, unsigned in
 
 // Block-wide: until every worker's flag is >= target.
 __device__ __noinline__ bool dr_wait_all(const DrSync* sync, uint32_t G, unsigned int target, Ctl* ctl) {
-  const long long start = clock64();
+  const unsigned long long start = dr_now_ns();
   for (uint32_t i = 0;; ++i) {
     bool ok = true;
     for (uint32_t g = threadIdx.x; g < G; g += blockDim.x) ok = ok && ld_relaxed_u32(&sync->flags[g]) >= target;
@@ -163,7 +177,7 @@ __device__ __noinline__ bool dr_wait_all(const DrSync* sync, uint32_t G, unsigne
       int bad = 0;
       if (threadIdx.x == 0) {
         bad = ld_relaxed_u32(&sync->abort) != 0;
-        if (!bad && clock64() - start > 4000000000ll) {
+        if (!bad && dr_now_ns() - start > c_dr_timeout_ns) {
           atomicExch(const_cast<unsigned int*>(&sync->abort), 1u);
           atomicCAS(&ctl->err, 0u, 3u);
           bad = 1;

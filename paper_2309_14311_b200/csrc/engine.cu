@@ -728,6 +728,10 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
       const uint32_t G = Gw;
       if (occ >= 1 && G + 1 <= uint32_t(sms) * uint32_t(occ)) {
         d.dr = true;
+        // bound on any single inter-CTA wait (dr_kernel.cuh), seconds
+        const long to_s = std::max(1l, env_long("NASCH_B200_DR_TIMEOUT_S", 60));
+        const unsigned long long to_ns = static_cast<unsigned long long>(to_s) * 1000000000ull;
+        CK(cudaMemcpyToSymbol(c_dr_timeout_ns, &to_ns, sizeof to_ns));
         d.tb = d.medium = d.resident = false;
         d.K = Kd;
         d.dr_G = G;
