@@ -11,15 +11,19 @@
 //   scan    exclusive prefix over the block counts (rank of a block's first
 //           car) in two levels: 1024 counts per block, then the group totals
 //   move    block b assembles the NEXT array's cells [4096 b, 4096 b + 4096)
-//           in shared memory from its own cars and the cars of the vmax
-//           cells before it, and writes them with 16-byte stores (no
-//           clearing pass, no byte scatter in HBM); each warp compacts its
-//           cars first (lanes work on cars, not cells); per car: gap to the
-//           next car of the list, the counter-based draw E_t a^rank (a^rank
-//           from three 4096-entry power tables for a lane's first car, then
-//           one multiply by a^32 per car); exact velocity sum and wrap count.
-// Steps are enqueued without a host round trip; the per-step records are
-// drained in batches.  HBM traffic per step: about 3 L bytes.
+//           in shared memory from its own cars, writes them with 16-byte
+//           stores (no clearing pass, no byte scatter in HBM) and counts
+//           them for the next step's scan; each warp compacts its cars
+//           first (lanes work on cars, not cells); per car: gap to the next
+//           car of the list, the counter-based draw E_t a^rank (a^rank from
+//           three 4096-entry power tables for a lane's first car, then one
+//           multiply by a^32 per car); exact velocity sum and wrap count.
+//           Cars landing past the block (<= vmax of them) go to a spill
+//           list:
+//   fixup   stores the spilled cars and adds them to their block's count.
+// The count pass runs only after construction / set_state.  Steps are
+// enqueued without a host round trip; the per-step records are drained in
+// batches.  HBM traffic per step: about 2 L bytes.
 // Bit-identical to the agent engines (tests/test_gpu_grid.py).
 #include <cuda_runtime.h>
 
@@ -144,42 +148,43 @@ __device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
                 __ldg(pw + 8192 + (r >> 24)));
 }
 
-// Gap ahead of the car at x by reading the cell array (any vmax, wraps).
-__device__ __forceinline__ uint32_t gap_scan(const uint8_t* __restrict__ cells, uint32_t x, uint32_t look,
-                                             uint32_t L) {
-  for (uint32_t d = 1; d <= look; ++d) {
-    uint32_t y = x + d;
-    if (y >= L) y -= L;
-    if (cells[y] != kEmpty) return d - 1;
-  }
-  return look;
-}
-
-// Block b owns the OUTPUT cells [B0, B0 + 4096) of the next array and
-// assembles them in shared memory: its own cars (one thread per 16 input
-// cells, as the count kernel) land there unless they pass B0 + 4096 or wrap
-// past L, and the cars of the `look` cells before B0 (mod L), computed once
-// more by warp 0, land there when they cross into it.  The block then
-// writes its 4096 cells with 16-byte stores: no clearing pass and no
-// partial-sector scatter in HBM.  Each car's velocity and crossing are
-// counted by the block that owns its input cell.  Within a warp the cars of
-// its 512 cells are first compacted in shared memory (position order), so
-// every lane works on cars, not on empty cells, and a car's gap is the next
-// entry of the list (the warp's last car reads ahead in the cell array).
-__global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __restrict__ cells,
-                                                             uint8_t* __restrict__ next,
-                                                             const uint32_t* __restrict__ local,
-                                                             const uint32_t* __restrict__ group,
-                                                             GridArgs g, StepRec* rec) {
+// Round 2 form of the move (grid_move2_kernel + grid_fixup_kernel): each
+// block moves only its OWN cars.  A car landing past the block's output
+// cells (at most `look` of them per block: they start within vmax cells of
+// the block's end, or wrap past L) is appended to the block's spill list
+// instead, and grid_fixup_kernel stores the spilled cars after every block
+// has written its cells -- no warp re-simulating the previous block's last
+// cars (a serial chain of global reads the other warps waited on at the
+// barrier).  The block also counts the cars it placed, so the next step's
+// scan needs no separate count pass over the L cells (the fixup adds the
+// spilled cars to their block's count): two passes over the cells per step
+// instead of three.  Draws: Q = E a^rank once per lane, then one mulmod by
+// a^32 per car.
+constexpr uint32_t kSpillMax = 256;  // >= look (vmax <= 254 in the grid engine)
+__global__ void __launch_bounds__(kGridTPB) grid_move2_kernel(const uint8_t* __restrict__ cells,
+                                                              uint8_t* __restrict__ next,
+                                                              const uint32_t* __restrict__ local,
+                                                              const uint32_t* __restrict__ group,
+                                                              GridArgs g, StepRec* rec, uint32_t* counts_next,
+                                                              uint32_t* spill, uint32_t* spill_n) {
   constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
-  static_assert(CPT == 16, "one 16-byte load per thread");
+  constexpr int NW = kGridTPB / 32;
   __shared__ __align__(16) uint8_t s_out[kCellsPerBlock];
-  __shared__ uint32_t s_w[kGridTPB / 32];
-  __shared__ uint16_t s_cx[kGridTPB / 32][32 * CPT];  // a warp's cars: cell offset from B0 ...
-  __shared__ uint8_t s_cv[kGridTPB / 32][32 * CPT];   // ... and velocity, in position order
+  __shared__ __align__(16) uint8_t s_in[kCellsPerBlock];
+  __shared__ uint32_t s_w[NW];
+  __shared__ uint32_t s_nspill, s_cnt;
+  __shared__ uint16_t s_cx[NW][32 * CPT];  // a warp's cars: cell offset from B0, position order
   const uint32_t B0 = blockIdx.x * kCellsPerBlock;
   const uint32_t lo = B0 + threadIdx.x * CPT;
+  // the block's first rank and its draw power, issued before the cells
+  // load so the two global round trips overlap
+  const uint32_t rank0 = __ldg(local + blockIdx.x) + __ldg(group + (blockIdx.x >> 10));
+  const uint32_t Eb = mulmod_d(g.E, apow_rank(g.pw, rank0));  // E a^rank0
   reinterpret_cast<uint4*>(s_out)[threadIdx.x] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  if (threadIdx.x == 0) {
+    s_nspill = 0;
+    s_cnt = 0;
+  }
   uint32_t ws[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
   if (lo + CPT <= g.L) {
     const uint4 w = *reinterpret_cast<const uint4*>(cells + lo);
@@ -192,12 +197,10 @@ __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __re
     for (uint32_t k = 0; k < CPT; ++k)
       if (lo + k < g.L) ws[k / 4] = (ws[k / 4] & ~(0xffu << (8 * (k % 4)))) | (uint32_t(cells[lo + k]) << (8 * (k % 4)));
   }
+  reinterpret_cast<uint4*>(s_in)[threadIdx.x] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
   const uint32_t m16 = occ_bits4(ws[0]) | (occ_bits4(ws[1]) << 4) | (occ_bits4(ws[2]) << 8) | (occ_bits4(ws[3]) << 12);
   const uint32_t occ = __popc(m16);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // Compact the warp's cars (512 cells) into shared memory in position
-  // order, then give lane l the cars l, l + 32, ...: every lane busy, the
-  // gap of all but the warp's last car is the next car in the list.
   uint32_t incl = occ;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -206,81 +209,105 @@ __global__ void __launch_bounds__(kGridTPB) grid_move_kernel(const uint8_t* __re
   }
   const uint32_t wcnt = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) s_w[warp] = incl;
-  {
+  {  // compact the warp's car positions (velocities are read from s_in later)
     uint32_t m = m16, q = incl - occ;
+    const uint32_t off = lo - B0;
     while (m) {
-      const uint32_t k = __ffs(m) - 1u;
+      s_cx[warp][q++] = static_cast<uint16_t>(off + __ffs(m) - 1u);
       m &= m - 1u;
-      s_cx[warp][q] = static_cast<uint16_t>(lo - B0 + k);
-      const uint32_t wk = k < 8 ? (k < 4 ? ws[0] : ws[1]) : (k < 12 ? ws[2] : ws[3]);  // no local array
-      s_cv[warp][q] = static_cast<uint8_t>(wk >> (8 * (k % 4)));
-      ++q;
     }
   }
   __syncthreads();  // also orders the s_out clear before any car lands
-  uint32_t wbase = 0;
-  for (uint32_t w = 0; w < warp; ++w) wbase += s_w[w];
-  const uint32_t rank0 = __ldg(local + blockIdx.x) + __ldg(group + (blockIdx.x >> 10));
+  uint32_t wbase = 0, nfirst = 0xffffffffu;  // cars of earlier warps; first car after this warp
+  for (int w = 0; w < NW; ++w) {
+    const uint32_t cw = s_w[w];
+    if (w < static_cast<int>(warp)) wbase += cw;
+    else if (w > static_cast<int>(warp) && cw && nfirst == 0xffffffffu) nfirst = s_cx[w][0];
+  }
   const uint32_t look = min(g.vmax, g.L - 1);
-  const uint32_t B1 = min(B0 + kCellsPerBlock, g.L);  // end of this block's output cells
+  const uint32_t B1 = min(B0 + kCellsPerBlock, g.L);  // end of this block's cells
   uint32_t sum = 0, wraps = 0;
   if (lane < wcnt) {
-    uint32_t ap = apow_rank(g.pw, rank0 + wbase + lane);
+    // the lane's first draw: E a^(rank0 + wbase + lane), wbase + lane < 4096
+    uint32_t Q = mulmod_d(Eb, __ldg(g.pw + wbase + lane));
     for (uint32_t j = lane; j < wcnt; j += 32) {
-      const uint32_t x = B0 + s_cx[warp][j];
-      const uint32_t ck = s_cv[warp][j];
-      const uint32_t gap = j + 1 < wcnt ? min(static_cast<uint32_t>(s_cx[warp][j + 1]) + B0 - x - 1u, look)
-                                        : gap_scan(cells, x, look, g.L);
-      uint32_t v = min(min(ck + 1, g.vmax), gap);
-      const uint32_t s = mulmod(g.E, ap);  // draw #(t N + rank + 1)
-      ap = mulmod(ap, g.a32);
+      const uint32_t xo = s_cx[warp][j];
+      const uint32_t x = B0 + xo;
+      uint32_t gap;
+      if (j + 1 < wcnt) {
+        gap = min(static_cast<uint32_t>(s_cx[warp][j + 1]) - xo - 1u, look);
+      } else if (nfirst != 0xffffffffu) {  // the next car is in a later warp of the block
+        gap = min(nfirst - xo - 1u, look);
+      } else {  // the block's last car: the cells after the block (wrapping past L)
+        gap = look;
+        for (uint32_t d = 1; d <= look; ++d) {
+          uint32_t y = x + d;
+          if (y >= g.L) y -= g.L;
+          if (__ldg(cells + y) != kEmpty) {
+            gap = d - 1;
+            break;
+          }
+        }
+      }
+      uint32_t v = min(min(static_cast<uint32_t>(s_in[xo]) + 1, g.vmax), gap);
+      const uint32_t s = Q;  // draw #(t N + rank + 1)
+      Q = mulmod_d(Q, g.a32);
       if (s < g.tp && v > 0) --v;
       uint32_t nx = x + v;
-      if (nx >= g.L) {
-        nx -= g.L;
-        ++wraps;
+      const bool wrapped = nx >= g.L;
+      nx -= wrapped ? g.L : 0u;
+      wraps += wrapped;
+      if (nx >= B0 && nx < B1) {
+        s_out[nx - B0] = static_cast<uint8_t>(v);
+      } else {
+        const uint32_t slot = atomicAdd(&s_nspill, 1u);
+        spill[size_t(blockIdx.x) * kSpillMax + slot] = nx;
+        spill[size_t(gridDim.x) * kSpillMax + size_t(blockIdx.x) * kSpillMax + slot] = v;
       }
-      if (nx >= B0 && nx < B1) s_out[nx - B0] = static_cast<uint8_t>(v);
       sum += v;
     }
   }
-  // Warp 0: cars of the `look` cells before B0 (mod L) that land in this
-  // block.  Their ranks count back from the block's first rank (mod N).
-  if (warp == 0 && g.L > kCellsPerBlock) {
-    uint32_t after = 0;  // occupied cells between the current chunk and B0
-    for (uint32_t c0 = 0; c0 < look; c0 += 32) {
-      const uint32_t j = c0 + lane + 1;  // cell B0 - j
-      const uint32_t y = j <= look ? (B0 >= j ? B0 - j : B0 + g.L - j) : 0u;
-      const bool occd = j <= look && cells[y] != kEmpty;
-      const uint32_t bal = __ballot_sync(0xffffffffu, occd);
-      if (occd) {
-        // ranks: cars at B0-1, B0-2, ... are rank0-1, rank0-2, ...
-        const uint32_t nearer = __popc(bal & ((1u << lane) - 1u));  // occupied cells closer to B0
-        uint32_t r = rank0 + g.N - (after + nearer + 1);
-        if (r >= g.N) r -= g.N;
-        const uint32_t cy = cells[y];
-        uint32_t v = min(min(cy + 1, g.vmax), gap_scan(cells, y, look, g.L));
-        const uint32_t sd = mulmod(g.E, apow_rank(g.pw, r));
-        if (sd < g.tp && v > 0) --v;
-        uint32_t nx = y + v;
-        if (nx >= g.L) nx -= g.L;
-        if (nx >= B0 && nx < B1) s_out[nx - B0] = static_cast<uint8_t>(v);
-      }
-      after += __popc(bal);
-    }
-  }
   __syncthreads();
+  uint32_t placed = 0;
   if (B0 + (threadIdx.x + 1) * CPT <= g.L) {
-    reinterpret_cast<uint4*>(next + B0)[threadIdx.x] = reinterpret_cast<const uint4*>(s_out)[threadIdx.x];
+    const uint4 o = reinterpret_cast<const uint4*>(s_out)[threadIdx.x];
+    reinterpret_cast<uint4*>(next + B0)[threadIdx.x] = o;
+    placed = (__popc(__vcmpne4(o.x, 0xffffffffu)) + __popc(__vcmpne4(o.y, 0xffffffffu)) +
+              __popc(__vcmpne4(o.z, 0xffffffffu)) + __popc(__vcmpne4(o.w, 0xffffffffu))) >> 3;
   } else {
-    for (uint32_t k = threadIdx.x * CPT; k < (threadIdx.x + 1) * CPT && B0 + k < g.L; ++k) next[B0 + k] = s_out[k];
+    for (uint32_t k = threadIdx.x * CPT; k < (threadIdx.x + 1) * CPT && B0 + k < g.L; ++k) {
+      next[B0 + k] = s_out[k];
+      placed += s_out[k] != kEmpty;
+    }
   }
   sum = __reduce_add_sync(0xffffffffu, sum);
   wraps = __reduce_add_sync(0xffffffffu, wraps);
+  placed = __reduce_add_sync(0xffffffffu, placed);
   if (lane == 0) {
     StepRec* r = rec + (g.t % kRecCap);
     if (sum) atomicAdd(&r->sumv, static_cast<unsigned long long>(sum));
     if (wraps) atomicAdd(&r->c, wraps);
+    atomicAdd(&s_cnt, placed);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    counts_next[blockIdx.x] = s_cnt;
+    spill_n[blockIdx.x] = s_nspill;
+  }
+}
+
+// The spilled cars of every block into the next array (all blocks' own
+// cells are written by now: stream order) and into their block's count.
+__global__ void grid_fixup_kernel(const uint32_t* __restrict__ spill, const uint32_t* __restrict__ spill_n,
+                                  uint32_t nb, uint8_t* next, uint32_t* counts_next) {
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += gridDim.x * blockDim.x) {
+    const uint32_t n = spill_n[b];
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t nx = spill[size_t(b) * kSpillMax + i];
+      const uint32_t v = spill[size_t(nb) * kSpillMax + size_t(b) * kSpillMax + i];
+      next[nx] = static_cast<uint8_t>(v);
+      atomicAdd(counts_next + nx / kCellsPerBlock, 1u);
+    }
   }
 }
 
@@ -326,6 +353,9 @@ struct GpuGrid::Impl {
   uint8_t* cells[2] = {nullptr, nullptr};
   int cur = 0;
   uint32_t *counts = nullptr, *local = nullptr, *group = nullptr, *xs = nullptr;
+  uint32_t* counts_next = nullptr;  // the next array's block counts (move2 + fixup)
+  uint32_t *spill = nullptr, *spill_n = nullptr;
+  bool counts_valid = false;  // counts[] describe cells[cur]
   uint32_t ng = 0;  // 1024-block groups of the two-level scan
   uint8_t* vs = nullptr;
   StepRec* rec = nullptr;
@@ -352,6 +382,7 @@ struct GpuGrid::Impl {
 
   void compact() {
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+    counts_valid = true;
     scan();
     grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, local, group, xs, vs);
     CKG(cudaGetLastError());
@@ -395,11 +426,19 @@ struct GpuGrid::Impl {
     const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
     const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, powmod(kA, 32), pw, steps_done};
     CKG(cudaMemsetAsync(rec + (steps_done % kRecCap), 0, sizeof(StepRec), stream));
-    grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+    if (!counts_valid) {  // after construction / set_state; later steps count as they move
+      grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
+      ++launches;
+    }
     scan();
-    grid_move_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], local, group, g, rec);
+    grid_move2_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], local, group, g, rec, counts_next,
+                                                   spill, spill_n);
+    grid_fixup_kernel<<<std::max(1u, std::min(1024u, (nb + 255) / 256)), 256, 0, stream>>>(spill, spill_n, nb,
+                                                                                            cells[cur ^ 1], counts_next);
     CKG(cudaGetLastError());
     launches += 4;
+    std::swap(counts, counts_next);
+    counts_valid = true;
     cur ^= 1;
     ++steps_done;
   }
@@ -466,6 +505,9 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   CKG(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) CKG(cudaMalloc(&d.cells[b], d.L));
   CKG(cudaMalloc(&d.counts, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.counts_next, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.spill, size_t(d.nb) * kSpillMax * 2 * 4));
+  CKG(cudaMalloc(&d.spill_n, size_t(d.nb) * 4));
   d.ng = (d.nb + 1023) / 1024;
   CKG(cudaMalloc(&d.local, size_t(d.nb) * 4));
   CKG(cudaMalloc(&d.group, size_t(d.ng) * 4));
@@ -501,6 +543,9 @@ GpuGrid::Impl::~Impl() {
   if (stream) cudaStreamSynchronize(stream);
   for (int b = 0; b < 2; ++b) cudaFree(cells[b]);
   cudaFree(counts);
+  cudaFree(counts_next);
+  cudaFree(spill);
+  cudaFree(spill_n);
   cudaFree(local);
   cudaFree(group);
   cudaFree(xs);
@@ -536,6 +581,7 @@ void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   }
   CKG(cudaMemcpyAsync(d.cells[d.cur], cells.data(), d.L, cudaMemcpyHostToDevice, d.stream));
   CKG(cudaStreamSynchronize(d.stream));
+  d.counts_valid = false;
   d.sumv0 = s;
   d.sumv_host.clear();
   d.wraps_host.clear();
