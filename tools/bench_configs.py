@@ -108,6 +108,47 @@ def ring(name, L, N, p, T, seed, vinit, snapshot_every=0, cpu_steps=0, ref=None,
     return out
 
 
+def _digest(a):
+    """Order-sensitive digest of a u64 array (multiply by odd constants that
+    depend on the index, sum mod 2^64)."""
+    idx = np.arange(len(a), dtype=np.uint64)
+    return int(((a + idx) * np.uint64(0x9E3779B97F4A7C15)).sum(dtype=np.uint64))
+
+
+def c5_segments(G=4, T=20000, every=1000):
+    """C5 as G contiguous car segments on this GPU (the segmented engine,
+    in-process peer-memory exchange) with a snapshot every `every` steps,
+    each snapshot compared (digest of positions and velocities) with the
+    single-GPU engine's at the same step."""
+    L, N, p, seed = 10**8, 6 * 10**7, 0.5, 5
+    x, v = nasch.fill_uniform_state(L, N, 0, seed)
+    prm = nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=T, seed=seed)
+    ref = nasch.Engine(prm)
+    ref.set_checksum(False)
+    ref.set_state(x, v)
+    want = []
+    for _ in range(T // every):
+        ref.advance(every)
+        xs, vs = ref.snapshot()
+        want.append((_digest(xs), _digest(vs)))
+    ref.close()
+    e = nasch.Engine(prm, G, nasch.Engine.CUDA)
+    e.set_checksum(False)
+    e.set_state(x, v)
+    ok = True
+    secs = 0.0
+    for i in range(T // every):
+        secs += ev_time(e.cuda_stream, lambda: e.advance(every))
+        xs, vs, first = e.segment_snapshot()
+        ok = ok and first == 0 and (_digest(xs), _digest(vs)) == want[i]
+    out = {"config": f"C5 ({G} segments, one GPU)", "L": L, "N": N, "p": p, "steps": T,
+           "segments": G, "exchange_mode": e.exchange_mode, "snapshots": T // every,
+           "snapshots_equal_single_gpu": ok, "gpu_seconds_stepping": secs,
+           "gpu_car_updates_per_s": N * T / secs}
+    e.close()
+    return out
+
+
 def c4(ref=None, cores=1, T=5000):
     L = 10**5
     dens = [5000 + (45000 * j) // 63 for j in range(64)]
@@ -171,7 +212,7 @@ def c4(ref=None, cores=1, T=5000):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="C1,C2,C3,C4,C5,C3-checksum,C5-checksum")
+    ap.add_argument("--only", default="C1,C2,C3,C4,C5,C5-segments,C3-checksum,C5-checksum")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.json"))
     ap.add_argument("--no-cpu", action="store_true")
     a = ap.parse_args()
@@ -196,6 +237,8 @@ def main():
         res.append(ring("C5", 10**8, 6 * 10**7, 0.5, 20000, 5, 0, snapshot_every=1000,
                         cpu_steps=10, ref=ref, cores=cores))
         res.append(ring("C5 (k=8)", 10**8, 6 * 10**7, 0.5, 20000, 5, 0, snapshot_every=1000, k=8))
+    if "C5-segments" in want:
+        res.append(c5_segments())
     if "C3-checksum" in want:
         res.append(ring("C3-checksum", 10**9, 2 * 10**8, 0.13, 20, 3, 0, checksum=True))
     if "C5-checksum" in want:
