@@ -329,12 +329,17 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
   // Tiled mode when every ring fits the warp-tile step and its cone plan.
   bool all_tiled = std::getenv("NASCH_B200_ENS_TILED") == nullptr ||
                    std::string(std::getenv("NASCH_B200_ENS_TILED")) != "0";
+  // Steps per launch K <= the halo, shared by all rings: the planner warp
+  // simulates K (vmax + 1) <= 512 cone cars, and every ring must hold a
+  // K-step cone (N >= K (vmax + 1), L > K vmax).  Tiled when K >= 8.
   for (const SimParams& p : rings) {
     const uint64_t vm = std::min<uint64_t>(p.v_max, p.road_length - 1);
-    all_tiled = all_tiled && vm <= 31 && p.road_length > kEtK * vm && p.car_count >= kEtK * (vm + 1);
-    // steps per launch: the planner warp simulates K (vmax + 1) <= 512 cone cars
-    d.K = std::min<uint32_t>(d.K, 512u / static_cast<uint32_t>(vm + 1));
+    all_tiled = all_tiled && vm <= 31;
+    uint64_t k = std::min<uint64_t>(512u / (vm + 1), p.car_count / (vm + 1));
+    if (vm) k = std::min<uint64_t>(k, (p.road_length - 1) / vm);
+    d.K = static_cast<uint32_t>(std::min<uint64_t>(d.K, k));
   }
+  all_tiled = all_tiled && d.K >= 8;
   d.K = std::max<uint32_t>(d.K, 1u);
   if (all_tiled) {
     d.tiled = true;

@@ -30,11 +30,14 @@ namespace nb200 {
 #define NB_ET_MN3 1
 #endif
 constexpr int kEtTPB = 128;
+#ifndef NB_ET_HALO
+#define NB_ET_HALO 32
+#endif
 constexpr int kEtCPT = 16;
-constexpr uint32_t kEtHalo = 16;
+constexpr uint32_t kEtHalo = NB_ET_HALO;              // = the deepest launch
 constexpr uint32_t kEtLoad = 32u * kEtCPT;            // cars spanned by a warp tile
-constexpr uint32_t kEtStore = kEtLoad - kEtHalo;      // 496 owned
-constexpr uint32_t kEtK = 16;                         // steps per launch (<= halo)
+constexpr uint32_t kEtStore = kEtLoad - kEtHalo;      // owned (496 with a 16-car halo)
+constexpr uint32_t kEtK = kEtHalo;                    // steps per launch (<= halo)
 
 struct EnsRing {
   unsigned long long off;         // first car in X / V (multiple of 16)
