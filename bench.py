@@ -21,10 +21,12 @@ value       device throughput, state resident in HBM: N*K / CUDA-event time
             of K steps on the engine's own stream (barrier + synchronize on
             both sides, max over ranks); the median of R passes (the spread
             is in "passes_ms")
-e2e         the same metric through the C ABI with host buffers: set_state
-            from host u64 arrays, advance(K), the whole-ring mean-velocity
-            series and the final state (each rank: its segment) read back to
-            host u64 arrays, wall clock, max over ranks
+e2e         the same metric through the C ABI with host buffers: set_state32
+            from pinned host int32 arrays (BASELINE's state format),
+            advance(K), the whole-ring mean-velocity series and the final
+            state (each rank: its segment) read back to host u64 arrays
+            (the reference's nasch_sim_state format), wall clock, max over
+            ranks
 roofline    SURVEY.md 8(d): 16 algorithmic bytes per car-update (int32 x and
             v read and written once per step) x N*k updates per launch / the
             average duration of the timed region's k-step launches (k =
@@ -455,8 +457,14 @@ def c3_leg(args, d: Dist):
     step_ms = ms / K
 
     # ---- end to end through the C ABI with host buffers ----------------
-    x64 = x.astype(np.uint64)
-    v64 = v.astype(np.uint64)
+    # Input: BASELINE's int32 state in page-locked host memory (a pinned
+    # torch tensor viewed as numpy), uploaded by nasch_sim_set_state32 (the
+    # positions DMA'd straight from it, validated on the host, velocities
+    # narrowed to bytes).  Output: the reference ABI's nasch_sim_state (u64).
+    xin = torch.empty(N, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    vin = torch.empty(N, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    xin[:] = x
+    vin[:] = v
     del x, v
     prm2 = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=K, seed=seed)
     eng2 = (nasch.Engine.distributed(prm2, d.rank, d.world, fresh_id()) if d.world > 1
@@ -473,7 +481,7 @@ def c3_leg(args, d: Dist):
     d.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    eng2.set_state(x64, v64)  # each rank converts and uploads its own segment
+    eng2.set_state(xin, vin)  # each rank validates and uploads its own segment
     t_set = time.perf_counter()
     eng2.advance(K)
     t_adv = time.perf_counter()
@@ -489,9 +497,10 @@ def c3_leg(args, d: Dist):
            "h2d_bytes_per_step": (4 + 1) * N / K,        # u32 x + u8 v per car, all segments
            "d2h_bytes_per_step": ((4 + 1) * N + 8 * K * d.world) / K,  # final state + series
            "breakdown_ms_rank0": {k: round(t, 2) for k, t in parts.items()},
-           "path": "nasch_sim_set_state(u64 host) + nasch_sim_advance(K) + whole-ring mean-velocity "
-                   "series + final state to host u64 (N=1: nasch_sim_state; N>1: each rank "
-                   "nasch_sim_state_segment of its segment), wall clock, max over ranks"}
+           "path": "nasch_sim_set_state32 (BASELINE's int32 state, pinned host arrays) + "
+                   "nasch_sim_advance(K) + whole-ring mean-velocity series + final state to host u64 "
+                   "(N=1: nasch_sim_state, the reference call; N>1: each rank nasch_sim_state_segment "
+                   "of its segment), wall clock, max over ranks"}
 
     # ---- roofline --------------------------------------------------------
     peak, peak_src = peaks()
@@ -539,7 +548,7 @@ def c3_leg(args, d: Dist):
         line["multi_gpu_parity_ok"] = parity["ok"]
         line["multi_gpu_parity"] = parity
     if d.rank == 0 and d.world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_reference_sample(x64, v64)
+        line["cpu_baseline"] = cpu_reference_sample(xin, vin)
     return line
 
 

@@ -601,6 +601,15 @@ struct GpuRing::Impl {
     const uint64_t vlim = std::min<uint64_t>(params.v_max, vmax_eff);
     const int dst = static_cast<int>(buf_host ^ 1u);
     constexpr size_t kChunk = size_t(1) << 24;
+    // u32 positions in page-locked memory (cudaMallocHost / cudaHostRegister,
+    // e.g. a pinned torch tensor) go to the device straight from the
+    // caller's array: validated on the host, no staging copy.
+    bool direct_x = false;
+    if constexpr (std::is_same<T, uint32_t>::value) {
+      cudaPointerAttributes pa{};
+      direct_x = cudaPointerGetAttributes(&pa, hx_in) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+    }
     for (size_t c0 = 0; c0 < n && !err.load(); c0 += kChunk) {
       const size_t c1 = std::min<size_t>(n, c0 + kChunk);
       parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
@@ -608,23 +617,18 @@ struct GpuRing::Impl {
         if constexpr (std::is_same<T, uint64_t>::value) {
           e = narrow_validate(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, hx, hv, vbytes);
         } else {
-          for (size_t i = c0 + a; i < c0 + b && !e; ++i) {
-            const uint64_t xi = hx_in[i], vi = hv_in[i];
-            if (xi >= L) e = 1;
-            else if (i && static_cast<uint64_t>(hx_in[i - 1]) >= xi) e = 2;
-            else if (vi > params.v_max) e = 3;
-            else if (vi > vlim) e = 4;
-            hx[i] = static_cast<uint32_t>(xi);
-            if (vbytes == 1) static_cast<uint8_t*>(hv)[i] = static_cast<uint8_t>(vi);
-            else static_cast<uint32_t*>(hv)[i] = static_cast<uint32_t>(vi);
-          }
+          e = narrow_validate32(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, direct_x ? nullptr : hx, hv,
+                                vbytes);
         }
         if (e) {
           int expected = 0;
           err.compare_exchange_strong(expected, e);
         }
       });
-      CK(cudaMemcpyAsync(x[dst] + c0, hx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, stream));
+      const uint32_t* xsrc = nullptr;
+      if constexpr (std::is_same<T, uint32_t>::value) xsrc = direct_x ? hx_in : hx;
+      else xsrc = hx;
+      CK(cudaMemcpyAsync(x[dst] + c0, xsrc + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, stream));
       CK(cudaMemcpyAsync(static_cast<char*>(v[dst]) + c0 * vbytes, static_cast<char*>(hv) + c0 * vbytes,
                          (c1 - c0) * vbytes, cudaMemcpyHostToDevice, stream));
     }

@@ -226,6 +226,70 @@ void widen_u8(const uint8_t* src, uint64_t* dst, size_t n) {
   widen_u8_scalar(src, dst, n);
 }
 
+#if defined(__x86_64__)
+// 16 cars at a time: u32 rules as masks, velocities narrowed with vpmovdb.
+__attribute__((target("avx512f,avx512bw"))) int narrow32_avx512(const uint32_t* x, const uint32_t* v, size_t lo,
+                                                                size_t hi, uint32_t L, uint32_t vmax, uint32_t vlim,
+                                                                uint32_t* x32, void* vout, int vbytes) {
+  const __m512i vL = _mm512_set1_epi32(static_cast<int>(L));
+  const __m512i vVmax = _mm512_set1_epi32(static_cast<int>(vmax));
+  const __m512i vVlim = _mm512_set1_epi32(static_cast<int>(vlim));
+  size_t i = lo;
+  auto scalar = [&](size_t k) -> int {
+    if (x[k] >= L) return 1;
+    if (k && x[k - 1] >= x[k]) return 2;
+    if (v[k] > vmax) return 3;
+    if (v[k] > vlim) return 4;
+    if (x32) x32[k] = x[k];
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[k] = static_cast<uint8_t>(v[k]);
+    else static_cast<uint32_t*>(vout)[k] = v[k];
+    return 0;
+  };
+  // scalar until i > 0 and a multiple of 16 (aligned streaming stores)
+  for (; i < hi && (i == 0 || (i & 15u)); ++i)
+    if (const int e = scalar(i)) return e;
+  for (; i + 16 <= hi; i += 16) {
+    const __m512i xs = _mm512_loadu_si512(reinterpret_cast<const void*>(x + i));
+    const __m512i vs = _mm512_loadu_si512(reinterpret_cast<const void*>(v + i));
+    const __m512i prevs = _mm512_loadu_si512(reinterpret_cast<const void*>(x + i - 1));
+    const __mmask16 bad = _mm512_cmpge_epu32_mask(xs, vL) | _mm512_cmple_epu32_mask(xs, prevs) |
+                          _mm512_cmpgt_epu32_mask(vs, vVmax) | _mm512_cmpgt_epu32_mask(vs, vVlim);
+    if (bad) {
+      for (size_t k = i; k < i + 16; ++k)
+        if (const int e = scalar(k)) return e;
+    }
+    if (x32) _mm512_stream_si512(reinterpret_cast<__m512i*>(x32 + i), xs);
+    if (vbytes == 1) _mm_stream_si128(reinterpret_cast<__m128i*>(static_cast<uint8_t*>(vout) + i), _mm512_cvtepi32_epi8(vs));
+    else _mm512_stream_si512(reinterpret_cast<__m512i*>(static_cast<uint32_t*>(vout) + i), vs);
+  }
+  _mm_sfence();
+  for (; i < hi; ++i)
+    if (const int e = scalar(i)) return e;
+  return 0;
+}
+#endif
+
+int narrow_validate32(const uint32_t* x, const uint32_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
+                      uint64_t vlim, uint32_t* x32, void* vout, int vbytes) {
+  const uint32_t L32 = static_cast<uint32_t>(L);
+  const uint32_t vmax32 = static_cast<uint32_t>(vmax > 0xffffffffull ? 0xffffffffull : vmax);
+  const uint32_t vlim32 = static_cast<uint32_t>(vlim > 0xffffffffull ? 0xffffffffull : vlim);
+#if defined(__x86_64__)
+  if (have_avx512()) return narrow32_avx512(x, v, lo, hi, L32, vmax32, vlim32, x32, vout, vbytes);
+#endif
+  for (size_t i = lo; i < hi; ++i) {
+    const uint32_t xi = x[i], vi = v[i];
+    if (xi >= L32) return 1;
+    if (i && x[i - 1] >= xi) return 2;
+    if (vi > vmax32) return 3;
+    if (vi > vlim32) return 4;
+    if (x32) x32[i] = xi;
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(vi);
+    else static_cast<uint32_t*>(vout)[i] = vi;
+  }
+  return 0;
+}
+
 int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
                     uint64_t vlim, uint32_t* x32, void* vout, int vbytes) {
 #if defined(__x86_64__)

@@ -22,6 +22,12 @@ void widen_u8(const uint8_t* src, uint64_t* dst, size_t n);
 int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
                     uint64_t vlim, uint32_t* x32, void* vout, int vbytes);
 
+// The same rules for u32 input (nasch_sim_set_state32, BASELINE's int32
+// state); x32 may be null when the positions are uploaded straight from the
+// caller's (page-locked) array.
+int narrow_validate32(const uint32_t* x, const uint32_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
+                      uint64_t vlim, uint32_t* x32, void* vout, int vbytes);
+
 // Persistent host worker pool (host_simd.cpp): job(i) for i in [0, count)
 // on the pool's threads and the caller; returns when all are done.
 unsigned host_threads();

@@ -637,6 +637,52 @@ def test_set_state_validation_rules_and_order():
     assert (xs == ref_x).all() and (vs == ref_v).all()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_set_state32_validation_and_pinned_upload(port, pinned):
+    """set_state32 (u32 arrays; the positions go to the device straight from
+    a page-locked array): same rules and first-violation order as the u64
+    path at every position of the 16-car vector groups, a rejected state
+    leaves the ring untouched, and an accepted one runs like the oracle."""
+    import torch
+    L, N, vmax = 50_000, 20_000, 5
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 22)
+
+    def host(a):
+        if not pinned:
+            return a.copy()
+        t = torch.empty(len(a), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        t[:] = a
+        return t
+
+    e = nasch.Engine(params(L, N, vmax, 0.2, 60, 3))
+    e.set_checksum(False)
+    e.set_state(host(x0), host(v0))
+    e.advance(7)
+    ref_x, ref_v = e.snapshot()
+    msgs = {1: "position out of range", 2: "strictly increasing", 3: "above vmax"}
+    for pos in (0, 1, 15, 16, 17, 31, 32, 4095, N // 2 + 3, N - 17, N - 1):
+        for rule in (1, 2, 3):
+            x, v = host(x0), host(v0)
+            if rule == 1:
+                x[pos] = L + pos
+            elif rule == 2:
+                x[pos] = x[pos - 1] if pos else x[0]
+                if pos == 0:
+                    x[1] = x[0]
+            else:
+                v[pos] = vmax + 1
+            with pytest.raises(nasch.NaschError) as ei:
+                e.set_state(x, v)
+            assert msgs[rule] in str(ei.value), (pos, rule, str(ei.value))
+    xs, vs = e.snapshot()
+    assert (xs == ref_x).all() and (vs == ref_v).all()
+    o = port.run(L, vmax, 0.2, 3, 53, ref_x, ref_v, want_checksum=False,
+                 rng_state=port.jump(port.seeded(3), 7 * N))
+    e.advance(53)
+    xs, vs = e.snapshot()
+    assert (xs == o["x"]).all() and (vs == o["v"]).all()
+
+
 @pytest.mark.parametrize("dr", ["1", "0"])
 def test_long_run_past_record_ring(port, k_env, dr):
     """70,000 steps: past the 65,536-slot device step-record ring and over
