@@ -326,8 +326,13 @@ def nccl_init_summary(path):
     keep = [ln for ln in lines if "nRanks" in ln or "NCCL version" in ln or "Init COMPLETE" in ln]
     for ln in keep[:40]:
         log("[nccl] " + ln)
-    nranks = sorted({int(tok.split()[1]) for ln in keep for tok in [ln[ln.index("nRanks"):]]
-                     if "nRanks" in ln and tok.split()[1].isdigit()})
+    nranks = set()
+    for ln in keep:
+        parts = ln.split()
+        for i, tok in enumerate(parts[:-1]):
+            if tok == "nRanks" and parts[i + 1].isdigit():
+                nranks.add(int(parts[i + 1]))
+    nranks = sorted(nranks)
     return {"init_lines": len(keep), "nranks_seen": nranks, "log": path}
 
 
