@@ -87,6 +87,14 @@ def test_null_arguments(lib):  # test_capi.cpp:92-103
     lib.nasch_sim_free(None)
     assert lib.nasch_sim_set_state(None, None, None, 0) == capi.NASCH_ERR_INVALID
     assert lib.nasch_sim_cuda_stream(None) is None
+    # round-2 extensions: NULL handles and arrays are refused, never followed
+    assert lib.nasch_sim_state_segment(None, None, None, 0, None) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_state_segment_async(None, None, None, 0, None) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_set_state_segment(None, None, None, 0) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_ensemble_set_state_all32(None, None, None, 0) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_state_wait(None) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_exchange_mode(None) == 0
+    assert b"null" in lib.nasch_last_error()
 
 
 def test_invalid_params_cannot_start(lib):  # test_capi.cpp:159-166
@@ -222,3 +230,22 @@ def test_threshold_exhaustive_small_modulus_argument(lib):
         T = lib.nasch_b200_draw_threshold(p)
         s = rng.integers(1, 2147483647, 200000)
         assert ((s < T) == (s.astype(np.float64) / m < p)).all()
+
+
+def test_python_output_buffer_checks():
+    """nasch.py refuses caller buffers the ABI would overrun: wrong dtype,
+    too short, non-contiguous or read-only (snapshot out_x)."""
+    import numpy as np
+    chk = nasch._out_u64
+    ok = np.zeros(10, np.uint64)
+    assert chk(ok, 10, "x") is ok
+    with pytest.raises(TypeError):
+        chk(np.zeros(10, np.uint32), 10, "x")
+    with pytest.raises(ValueError, match="holds 9"):
+        chk(np.zeros(9, np.uint64), 10, "x")
+    with pytest.raises(ValueError, match="contiguous"):
+        chk(np.zeros(20, np.uint64)[::2], 10, "x")
+    ro = np.zeros(10, np.uint64)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError, match="writable"):
+        chk(ro, 10, "x")
