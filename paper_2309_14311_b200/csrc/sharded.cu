@@ -77,8 +77,18 @@ struct NcclApi {
     if (!api.handle) api.open();
     return api;
   }
+  // The NCCL already in the process if there is one (e.g. PyTorch's, which
+  // may be newer than the system's: loading the system copy first would
+  // shadow it -- same soname -- for a later `import torch`), else
+  // NASCH_B200_NCCL_LIB, else the default search path.  Opened RTLD_LOCAL:
+  // our lookups go through dlsym, nothing is exported to the process.
   void open() {
-    handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!handle) {
+      const char* env = std::getenv("NASCH_B200_NCCL_LIB");
+      if (env && *env) handle = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    }
+    if (!handle) handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
     if (!handle) throw std::runtime_error(std::string("cannot load libnccl.so.2: ") + dlerror());
     get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(handle, "ncclGetUniqueId"));
     comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(handle, "ncclCommInitRank"));
@@ -1035,17 +1045,13 @@ struct ShardedRing::Impl {
               for (size_t i = a; i < b; ++i) acc += static_cast<const uint32_t*>(s.hv_stage)[i];
           }
         } else {
-          for (size_t i = a; i < b && !e; ++i) {
-            const uint64_t xi = xs[i], vi = vs[i];
-            if (xi >= L) e = 1;
-            else if (i && static_cast<uint64_t>(xs[i - 1]) >= xi) e = 2;
-            else if (vi > params.v_max) e = 3;
-            else if (vi > vlim) e = 4;
-            s.hx_stage[i] = static_cast<uint32_t>(xi);
-            if (vbytes == 1) static_cast<uint8_t*>(s.hv_stage)[i] = static_cast<uint8_t>(vi);
-            else static_cast<uint32_t*>(s.hv_stage)[i] = static_cast<uint32_t>(vi);
-            acc += vi;
-          }
+          e = narrow_validate32(xs, vs, a, b, L, params.v_max, vlim, s.hx_stage, s.hv_stage, vbytes);
+        }
+        if (!e && !std::is_same<T, uint64_t>::value) {
+          if (vbytes == 1)
+            for (size_t i = a; i < b; ++i) acc += static_cast<const uint8_t*>(s.hv_stage)[i];
+          else
+            for (size_t i = a; i < b; ++i) acc += static_cast<const uint32_t*>(s.hv_stage)[i];
         }
         sum += acc;
         if (e) {
