@@ -95,6 +95,15 @@ struct GpuRing::Impl {
   void* v[2] = {nullptr, nullptr};
   uint32_t* blkpow = nullptr;
   uint32_t* thrpow = nullptr;
+  // Temporal-blocked rings also keep the one-step kernel's geometry: with the
+  // checksum on every step's row is hashed, so they step one launch at a
+  // time with nasch_step_kernel (HBM-bound, ~0.35 ms on 2e8 cars against
+  // ~0.58 ms for a one-step TB launch) and re-plan before the next TB launch.
+  RingArgs args1{};
+  int grid1 = 0;
+  uint32_t* blkpow1 = nullptr;
+  uint32_t* thrpow1 = nullptr;
+  bool plan_stale = false;  // one-step launches ran since the last TB plan
   Ctl* ctl = nullptr;
   StepRec* rec = nullptr;
   unsigned long long* dsum = nullptr;
@@ -214,6 +223,25 @@ struct GpuRing::Impl {
 
   uint32_t steps_per_launch() const { return (resident || dr) ? kResidentChunk : tb ? K : 1u; }
 
+  // One step of a temporal-blocked ring by the one-step kernel (its own grid
+  // and draw-multiplier tables, args1): it advances the control block (t, W,
+  // E, buf) exactly as a 1-step TB launch would, but leaves no plan.
+  void launch_single() {
+    if (vbytes == 1) nasch_step_kernel<uint8_t, kTPB, kCPT1><<<grid1, kTPB, 0, stream>>>(args1);
+    else nasch_step_kernel<uint32_t, kTPB, kCPT1><<<grid1, kTPB, 0, stream>>>(args1);
+    ++launches;
+    plan_stale = true;
+  }
+
+  // The origin-cone plan for the current step (after one-step launches).
+  void replan() {
+    if (vbytes == 1) cone_init_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args);
+    else cone_init_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args);
+    CK(cudaGetLastError());
+    ++launches;
+    plan_stale = false;
+  }
+
   void build_graph() {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
@@ -245,6 +273,7 @@ struct GpuRing::Impl {
       CK(cudaGetLastError());
     }
     W_host = 0;
+    plan_stale = false;
   }
 
   void compute_sumv0() {
@@ -342,6 +371,7 @@ struct GpuRing::Impl {
   // launch.  Keeps the undrained record window well inside kRecCap (each
   // launch's last block zeroes the slots of the next plan).
   void enqueue_steps(uint64_t count) {
+    if (plan_stale) replan();
     const uint64_t per = steps_per_launch();
     if (resident || dr) {  // whole chunks in one launch; no graph needed
       while (count > 0) {
@@ -407,7 +437,8 @@ struct GpuRing::Impl {
     // step per launch, each followed by the on-device FNV fold
     // (fnv_kernels.cuh) -- no host round trip unless a frame is due.
     for (uint64_t k = 0; k < count; ++k) {
-      launch(1);
+      if (tb) launch_single();
+      else launch(1);
       CK(cudaGetLastError());
       ++steps_done;
       fnv_fold();
@@ -491,64 +522,87 @@ struct GpuRing::Impl {
 }
 
   // ---- on-device trajectory checksum ---------------------------------
-  // Per step (fnv_kernels.cuh, low-byte decomposition): 8-bit chunk maps,
-  // their composition tree up and walk down (each chunk's incoming low
-  // byte), one exact 64-bit pass per chunk, the chunks' affine maps reduced
-  // and applied -- all graph-captured, no host round trip.
+  // Per step (fnv_kernels.cuh, nibble decomposition): pass A (low-nibble
+  // chunk maps) and its composition tree up and down (every chunk's incoming
+  // low nibble), pass B (high-nibble maps from it) and its tree (every
+  // chunk's incoming low byte), pass C (one exact 64-bit run per slot), the
+  // slots' affine maps reduced and applied -- all graph-captured, no host
+  // round trip.
   unsigned long long* fnv_hash = nullptr;
-  uint32_t fnv_chunks = 0;
+  uint32_t fnv_nslots = 0, fnv_chunks = 0;
   std::vector<uint8_t*> fnv_maps;   // level 0: chunk maps; level i+1: groups of 256 of level i
+  std::vector<uint8_t*> fnv_pre;    // prefix tables per level
+  std::vector<uint8_t*> fnv_lb;     // incoming nibble per map, levels >= 1
   std::vector<uint32_t> fnv_count;  // maps per level
-  std::vector<uint8_t*> fnv_lb;     // incoming low byte per map, per level
-  uint8_t* fnv_sub = nullptr;       // cumulative sub-chunk maps (pass C starts)
-  uint32_t fnv_nsub = 0;
+  uint8_t* fnv_lo4 = nullptr;       // incoming low nibble per chunk (pass A)
+  uint8_t* fnv_hi4 = nullptr;       // incoming high nibble per chunk (pass B)
+  uint8_t* fnv_sub = nullptr;       // bytes at the slot boundaries inside a chunk (pass B)
+  uint8_t* fnv_top = nullptr;       // the top group's composed map (unused)
   unsigned long long* fnv_A[2] = {nullptr, nullptr};
   unsigned long long* fnv_D[2] = {nullptr, nullptr};
   cudaGraphExec_t fnv_graph = nullptr;
 
   void fnv_alloc() {
-    fnv_chunks = static_cast<uint32_t>((2ull * n + kFnvRowChunk - 1) / kFnvRowChunk);
+    const uint32_t nu = (n + kFnvSlot - 1) / kFnvSlot;
+    const uint32_t npos = (nu + 1 + kFnvSlotsPerChunk - 1) / kFnvSlotsPerChunk * kFnvSlotsPerChunk;  // fnv_row
+    fnv_nslots = 2 * npos;
+    fnv_chunks = fnv_nslots / kFnvSlotsPerChunk;
     for (uint32_t m = fnv_chunks;;) {
-      uint8_t *maps = nullptr, *lb = nullptr;
-      CK(cudaMalloc(&maps, size_t(m) * 256));
+      uint8_t *maps = nullptr, *pre = nullptr, *lb = nullptr;
+      CK(cudaMalloc(&maps, size_t(m) * 16));
+      CK(cudaMalloc(&pre, size_t(m) * 16));
       CK(cudaMalloc(&lb, m));
       fnv_maps.push_back(maps);
+      fnv_pre.push_back(pre);
       fnv_lb.push_back(lb);
       fnv_count.push_back(m);
       if (m <= 256) break;
       m = (m + 255) / 256;
     }
-    fnv_nsub = static_cast<uint32_t>((2ull * n + kFnvSubLen - 1) / kFnvSubLen);
-    CK(cudaMalloc(&fnv_sub, size_t(fnv_chunks) * (kFnvSubs - 1) * 256));
+    CK(cudaMalloc(&fnv_top, 16));
+    CK(cudaMalloc(&fnv_lo4, fnv_chunks));
+    CK(cudaMalloc(&fnv_hi4, fnv_chunks));
+    CK(cudaMalloc(&fnv_sub, size_t(fnv_chunks) * (kFnvSlotsPerChunk - 1) * 16));
     for (int b = 0; b < 2; ++b) {
-      CK(cudaMalloc(&fnv_A[b], size_t(fnv_nsub) * 8));
-      CK(cudaMalloc(&fnv_D[b], size_t(fnv_nsub) * 8));
+      CK(cudaMalloc(&fnv_A[b], size_t(fnv_nslots) * 8));
+      CK(cudaMalloc(&fnv_D[b], size_t(fnv_nslots) * 8));
     }
-    CK(cudaFuncSetAttribute(fnv_group8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
-    CK(cudaFuncSetAttribute(fnv_walk8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+  }
+
+  // Composition tree over fnv_maps[0] (filled by pass A or B): up, then down
+  // from the digest's nibble at `shift`, the level-0 result into `out`.
+  uint32_t fnv_tree(int shift, uint8_t* out) {
+    uint32_t nl = 0;
+    const size_t levels = fnv_maps.size();
+    for (size_t i = 0; i < levels; ++i, ++nl) {
+      const uint32_t groups = (fnv_count[i] + 255) / 256;
+      fnv_up16_kernel<<<(groups + kUpGroups - 1) / kUpGroups, 16 * kUpGroups, 0, stream>>>(
+          fnv_maps[i], fnv_count[i], fnv_pre[i], i + 1 < levels ? fnv_maps[i + 1] : fnv_top);
+    }
+    for (size_t i = levels; i-- > 0; ++nl) {
+      fnv_down16_kernel<<<(fnv_count[i] + 255) / 256, 256, 0, stream>>>(
+          fnv_pre[i], fnv_count[i], i + 1 < levels ? fnv_lb[i + 1] : nullptr, fnv_hash, shift,
+          i == 0 ? out : fnv_lb[i]);
+    }
+    return nl;
   }
 
   uint32_t fnv_enqueue() {
     uint32_t nl = 0;
     const uint32_t nc = fnv_chunks;
-    const int mgrid = static_cast<int>((nc + kMap8Warps - 1) / kMap8Warps);
-    if (vbytes == 1) fnv_map8_kernel<uint8_t><<<mgrid, 32 * kMap8Warps, 0, stream>>>(args, fnv_maps[0], fnv_sub, nc);
-    else fnv_map8_kernel<uint32_t><<<mgrid, 32 * kMap8Warps, 0, stream>>>(args, fnv_maps[0], fnv_sub, nc);
-    ++nl;
-    const size_t levels = fnv_maps.size();
-    for (size_t i = 0; i + 1 < levels; ++i, ++nl)
-      fnv_group8_kernel<<<fnv_count[i + 1], 256, 65536, stream>>>(fnv_maps[i], fnv_count[i], fnv_maps[i + 1]);
-    for (size_t i = levels; i-- > 0; ++nl) {
-      const int g = static_cast<int>((fnv_count[i] + 255) / 256);
-      fnv_walk8_kernel<<<g, 256, 65536, stream>>>(fnv_maps[i], fnv_count[i], i + 1 < levels ? fnv_lb[i + 1] : nullptr,
-                                                 fnv_hash, fnv_lb[i]);
-    }
-    const uint32_t ns = fnv_nsub;
-    const int agrid = static_cast<int>((ns + kAffTPB - 1) / kAffTPB);
+    const int cgrid = static_cast<int>((nc + kFnvTPB - 1) / kFnvTPB);
+    if (vbytes == 1) fnv_nib_kernel<uint8_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, fnv_maps[0], nullptr);
+    else fnv_nib_kernel<uint32_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, fnv_maps[0], nullptr);
+    nl += 1 + fnv_tree(0, fnv_lo4);
+    if (vbytes == 1) fnv_nib_kernel<uint8_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_maps[0], fnv_sub);
+    else fnv_nib_kernel<uint32_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_maps[0], fnv_sub);
+    nl += 1 + fnv_tree(4, fnv_hi4);
+    const uint32_t ns = fnv_nslots;
+    const int sgrid = static_cast<int>((ns + kFnvTPB - 1) / kFnvTPB);
     if (vbytes == 1)
-      fnv_affine_kernel<uint8_t><<<agrid, kAffTPB, 0, stream>>>(args, fnv_lb[0], fnv_sub, ns, fnv_A[0], fnv_D[0]);
+      fnv_exact_kernel<uint8_t><<<sgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_hi4, fnv_sub, fnv_A[0], fnv_D[0]);
     else
-      fnv_affine_kernel<uint32_t><<<agrid, kAffTPB, 0, stream>>>(args, fnv_lb[0], fnv_sub, ns, fnv_A[0], fnv_D[0]);
+      fnv_exact_kernel<uint32_t><<<sgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_hi4, fnv_sub, fnv_A[0], fnv_D[0]);
     ++nl;
     int in = 0;
     for (uint32_t m = ns; m > 1; m = (m + 255) / 256, in ^= 1, ++nl)
@@ -839,6 +893,31 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
     CK(cudaMemcpy(d.dseg, dr_seg.data(), dr_seg.size() * 4, cudaMemcpyHostToDevice));
   }
 
+  if (d.tb) {  // the one-step kernel's geometry (checksum mode, GpuRing::Impl::launch_single)
+    int per1 = 0;
+    if (d.vbytes == 1) {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, nasch_step_kernel<uint8_t, kTPB, kCPT1>, kTPB, 0));
+    } else {
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, nasch_step_kernel<uint32_t, kTPB, kCPT1>, kTPB, 0));
+    }
+    const uint32_t ntiles1 = (d.n + kTile1 - 1) / kTile1;
+    d.grid1 = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(ntiles1, uint64_t(sms) * std::max(per1, 1))));
+    std::vector<uint32_t> blk1(d.grid1), thr1(kTPB);
+    const uint32_t a_tile1 = powmod(kA, kTile1);
+    blk1[0] = 1;
+    for (int b = 1; b < d.grid1; ++b) blk1[b] = mulmod(blk1[b - 1], a_tile1);
+    for (int t = 0; t < kTPB; ++t) thr1[t] = powmod(kA, uint64_t(t) * kCPT1);
+    CK(cudaMalloc(&d.blkpow1, blk1.size() * 4));
+    CK(cudaMalloc(&d.thrpow1, thr1.size() * 4));
+    CK(cudaMemcpy(d.blkpow1, blk1.data(), blk1.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d.thrpow1, thr1.data(), thr1.size() * 4, cudaMemcpyHostToDevice));
+    d.args1 = a;
+    d.args1.blkpow = d.blkpow1;
+    d.args1.thrpow = d.thrpow1;
+    d.args1.g = powmod(kA, uint64_t(d.grid1) * kTile1);
+    d.args1.kplan = 0;
+  }
+
   // init_state (model.cpp:30-40) on the device.
   const int ib = std::max(1, std::min<int>((d.npad + kTPB - 1) / kTPB, 4096));
   for (int b = 0; b < 2; ++b) {
@@ -877,7 +956,11 @@ GpuRing::Impl::~Impl() {
     cudaFree(fnv_D[b]);
   }
   for (uint8_t* p : fnv_maps) cudaFree(p);
+  for (uint8_t* p : fnv_pre) cudaFree(p);
   for (uint8_t* p : fnv_lb) cudaFree(p);
+  cudaFree(fnv_top);
+  cudaFree(fnv_lo4);
+  cudaFree(fnv_hi4);
   cudaFree(fnv_sub);
   cudaFree(fnv_hash);
   cudaFree(ctl);
@@ -885,6 +968,8 @@ GpuRing::Impl::~Impl() {
   cudaFree(dsum);
   cudaFree(blkpow);
   cudaFree(thrpow);
+  cudaFree(blkpow1);
+  cudaFree(thrpow1);
   cudaFree(dplans);
   cudaFree(dsync);
   cudaFree(dmbox);

@@ -118,236 +118,372 @@ __global__ void __launch_bounds__(256) fnv_slice_chunk_kernel(const T* __restric
 }
 
 
-// ---- low-byte decomposition of the row digest (GpuRing) -------------------
+// ---- nibble decomposition of the row digest (GpuRing) ---------------------
 //
-// The 256-start tables above do the 64-bit FNV work 256 times over.  But the
-// only thing a chunk's result needs from the incoming state is its low byte,
-// and the low byte evolves on its own: l -> ((l ^ b) * P) mod 256, with
-// P mod 256 = 0xb3.  So a step's digest is computed in three passes:
-//   A  (fnv_map8_kernel)   per 2048-value chunk, the 8-bit map l_in -> l_out
-//                          of its low byte, for all 256 starts at once: two
-//                          starts per 32-bit register (16-bit lanes, masked
-//                          to 8 bits before each multiply: LOP3 + IMAD per
-//                          byte for two starts), and only 128 starts tracked
-//                          since the map commutes with flipping bit 7
-//                          (F(l ^ 0x80) = F(l) ^ 0x80: both ops carry bit 7
-//                          straight through);
-//   B  (fnv_group8_kernel, fnv_walk8_kernel)  the maps composed 256 at a time
-//                          up a tree, then walked down from the digest's
-//                          known low byte: every chunk's incoming low byte;
-//   C  (fnv_affine_kernel) each chunk once, in exact 64-bit arithmetic, from
-//                          that low byte: h -> P^(8n) h + d_c; the chunks'
-//                          affine maps reduced in a tree (fnv_affine_reduce)
-//                          and applied to the running digest.
-// Pass A does 1/2 of the byte work of the old tables in 8-bit lanes instead
-// of 64-bit products; pass C does the 64-bit work once.
-constexpr uint32_t kFnvRowChunk = 2048;  // row values per chunk
-constexpr uint32_t kFnvP8 = 0xb3u;       // P mod 256
-constexpr uint32_t kFnvP8_5 = (kFnvP8 * kFnvP8 * kFnvP8 * kFnvP8 * kFnvP8) & 0xffu;  // a value's last byte + 4 zero bytes
-constexpr uint32_t kFnvP8_8 = (kFnvP8_5 * kFnvP8 * kFnvP8 * kFnvP8) & 0xffu;       // a < 256 value: 1 byte + 7 zero bytes
-constexpr int kMap8Warps = 8;
-constexpr uint32_t kFnvSubs = 4;                          // pass C threads per chunk
-constexpr uint32_t kFnvSubLen = kFnvRowChunk / kFnvSubs;  // 512 values each
+// The 256-start tables above do the 64-bit FNV work 256 times over.  One byte
+// maps h -> (h xor b) * P, and bit k of the result depends only on bits <= k
+// of h (P is odd, xor is bitwise).  So the low nibble evolves on its own,
+//     l -> ((l xor b) * P) mod 16            (P mod 16 = 3),
+// the low byte on its own once its low nibble is known, and once the low
+// byte is known at every point a run of bytes maps h -> P^(8n) h + d, which
+// is affine.  A step's digest is therefore computed in three passes over the
+// row, each far cheaper than tracking all 256 low bytes:
+//   A  fnv_nib_kernel<VT, 0>  one LANE per chunk (4 slots of 512 values):
+//                             the chunk's low-nibble map for starts 0..7,
+//                             four per register in 8-bit lanes (one LOP3 +
+//                             one IMAD per byte and register); flipping bit 3
+//                             commutes with both operations, F(l ^ 8) =
+//                             F(l) ^ 8, which gives starts 8..15;
+//      fnv_up16 / fnv_down16  the chunk maps composed 256 at a time up a tree
+//                             (each map's prefix table kept), then every
+//                             chunk's true incoming low nibble gathered down
+//                             it from the running digest's;
+//   B  fnv_nib_kernel<VT, 1>  one lane per chunk, from its true low nibble:
+//                             the high nibble's map for starts 0..7 (bit 7
+//                             commutes), two per register in 16-bit lanes,
+//                             and the full byte at each slot boundary;
+//                             composed the same way -> every chunk's true
+//                             incoming low byte;
+//   C  fnv_exact_kernel       one lane per slot, the exact 64-bit FNV of its
+//                             values from its true low byte: the slot maps
+//                             the true state h to P^(8n) h + d; the slots'
+//                             maps reduced in row order (fnv_affine_reduce)
+//                             and applied to the digest.
+// Slots are ID-aligned, so a lane streams its values with 16-byte loads.  The
+// row (rank r = id (head + r) mod N) starts inside unit head / 512, which is
+// split in two: [head, end of that unit), the following units in id order
+// (wrapping), then [unit start, head).  Every array has nu + 1 slots (the
+// last one empty when head is unit-aligned), so the geometry -- and the
+// captured graph -- is the same every step.
+constexpr uint32_t kFnvSlot = 512;          // row values per slot (ID-aligned)
+constexpr uint32_t kFnvSlotsPerChunk = 4;   // slots per pass A/B lane
+constexpr uint32_t kFnvP8 = 0xb3u;          // P mod 256
+constexpr uint32_t kFnvP8_5 = (kFnvP8 * kFnvP8 * kFnvP8 * kFnvP8 * kFnvP8) & 0xffu;  // last data byte + 4 zero bytes
+constexpr uint32_t kFnvP8_8 = (kFnvP8_5 * kFnvP8 * kFnvP8 * kFnvP8) & 0xffu;       // u8 value: 1 byte + 7 zero bytes
+constexpr uint32_t kFnvP4 = kFnvP8 & 0xfu;      // P mod 16 (= 3)
+constexpr uint32_t kFnvP4_5 = kFnvP8_5 & 0xfu;  // (= 3)
+constexpr uint32_t kFnvP4_8 = kFnvP8_8 & 0xfu;  // (= 1)
 
-// Row value k of the current step (k < N: position of rank k, else the
-// velocity of rank k - N; rank r is id (head + r) mod N).
-template <typename VT>
-__device__ __forceinline__ uint32_t fnv_row_value(const uint32_t* X, const VT* V, uint32_t N, uint32_t head,
-                                                  uint64_t k) {
-  const bool pos = k < N;
-  const uint32_t r = static_cast<uint32_t>(pos ? k : k - N);
-  uint32_t id = head + r;
-  if (id >= N) id -= N;
-  return pos ? __ldg(X + id) : static_cast<uint32_t>(__ldg(V + id));
+__host__ __device__ constexpr unsigned long long fnv_pow_c(uint64_t e) {
+  unsigned long long r = 1, b = kFnvP;
+  while (e) {
+    if (e & 1) r *= b;
+    b *= b;
+    e >>= 1;
+  }
+  return r;
+}
+constexpr unsigned long long kFnvPSlot = fnv_pow_c(8ull * kFnvSlot);  // P^(8 * 512): a full slot's slope
+
+struct FnvRow {
+  uint32_t N, head, nu, hu;  // cars, head id, units per array, head unit
+  uint32_t npos;             // slots per array: nu + 1, rounded up to whole chunks (the rest empty)
+};
+
+__device__ __forceinline__ FnvRow fnv_row(uint32_t N, uint32_t W) {
+  FnvRow r;
+  r.N = N;
+  r.head = (N - W) % N;
+  r.nu = (N + kFnvSlot - 1) / kFnvSlot;
+  r.hu = r.head / kFnvSlot;
+  r.npos = (r.nu + 1 + kFnvSlotsPerChunk - 1) / kFnvSlotsPerChunk * kFnvSlotsPerChunk;
+  return r;
 }
 
-// Pass A: one warp per chunk.  Lane t tracks starts t, t+32 (one register)
-// and t+64, t+96 (another).  Out: F[c][l], 256 bytes per chunk.
-template <typename VT>
-__global__ void __launch_bounds__(32 * kMap8Warps) fnv_map8_kernel(const RingArgs ra, uint8_t* F, uint8_t* Fsub,
-                                                                   uint32_t nchunks) {
-  __shared__ uint4 s_bb[kMap8Warps][32];
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  const uint32_t c = blockIdx.x * kMap8Warps + warp;
-  if (c >= nchunks) return;
-  const Ctl* ctl = ra.ctl;
-  const uint32_t N = ra.n;
-  const uint32_t head = (N - ctl->W) % N;
-  const int b = static_cast<int>(ctl->buf);
-  const uint32_t* X = xbuf(ra, b);
-  const VT* V = vbuf<VT>(ra, b);
-  const uint64_t rowlen = 2ull * N;
-  const uint64_t k0 = uint64_t(c) * kFnvRowChunk;
-  const uint32_t cnt = static_cast<uint32_t>(rowlen - k0 < kFnvRowChunk ? rowlen - k0 : kFnvRowChunk);
-  constexpr uint32_t M = 0x00ff00ffu;
-  uint32_t h0 = lane | ((lane + 32u) << 16), h1 = (lane + 64u) | ((lane + 96u) << 16);
-  for (uint32_t base = 0; base < cnt; base += 32) {
-    if (base + lane < cnt) {
-      const uint32_t w = fnv_row_value<VT>(X, V, N, head, k0 + base + lane);
-      s_bb[warp][lane] = make_uint4(__byte_perm(w, 0u, 0x4040u), __byte_perm(w, 0u, 0x4141u),
-                                    __byte_perm(w, 0u, 0x4242u), __byte_perm(w, 0u, 0x4343u));
+// Slot s of the row: array (0 positions, 1 velocities) and id range [a, b).
+__device__ __forceinline__ void fnv_slot(const FnvRow& r, uint32_t s, uint32_t& arr, uint32_t& a, uint32_t& b) {
+  arr = s >= r.npos ? 1u : 0u;
+  const uint32_t t = arr ? s - r.npos : s;
+  if (t == 0) {
+    a = r.head;
+    b = min(r.hu * kFnvSlot + kFnvSlot, r.N);
+  } else if (t >= r.nu) {
+    a = t == r.nu ? r.hu * kFnvSlot : 0u;
+    b = t == r.nu ? r.head : 0u;
+  } else {
+    uint32_t u = r.hu + t;
+    if (u >= r.nu) u -= r.nu;
+    a = u * kFnvSlot;
+    b = min(a + kFnvSlot, r.N);
+  }
+}
+
+// Per-warp staging of the lanes' slots: every lane streams its own slot, so
+// direct per-lane loads would touch 32 cache lines per instruction.  Instead
+// the warp copies 256-byte windows of all 32 slots into shared memory with
+// coalesced 16-byte cp.async copies (a row = one lane's window; rows padded
+// by 16 bytes, so the lanes' 16-byte reads of their own rows hit distinct
+// bank groups), then each lane reads its row.
+constexpr uint32_t kFnvWin = 256;  // bytes per row and window
+struct FnvStage {
+  uint4 tile[32][kFnvWin / 16 + 1];
+  const char* base[32];
+  uint32_t bytes[32];
+};
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Visits the values of ids [a, b) of one array in order: f4(w) for a 4-byte
+// value (positions; u32 velocities), f1(w, k) for byte k of w holding a u8
+// velocity.  Warp-collective (every lane calls it; an idle lane passes an
+// empty range): full slots (ID-aligned, 512 values) go through the staged
+// windows, the few partial ones (the split head slot, the short last unit)
+// value by value afterwards.
+template <typename VT, typename F4, typename F1>
+__device__ __forceinline__ void fnv_slot_values(FnvStage& st, const uint32_t* X, const VT* V, uint32_t arr,
+                                                uint32_t a, uint32_t b, F4&& f4, F1&& f1) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const bool full = b - a == kFnvSlot;
+  const bool wide = arr == 0 || sizeof(VT) == 4;
+  const uint32_t bytes = full ? kFnvSlot * (wide ? 4u : 1u) : 0u;
+  st.base[lane] = wide ? reinterpret_cast<const char*>((arr == 0 ? X : reinterpret_cast<const uint32_t*>(V)) + a)
+                       : reinterpret_cast<const char*>(V) + a;
+  st.bytes[lane] = bytes;
+  __syncwarp();
+  const uint32_t most = __reduce_max_sync(0xffffffffu, bytes);
+  for (uint32_t w = 0; w < most; w += kFnvWin) {
+#pragma unroll
+    for (uint32_t it = 0; it < 32 * (kFnvWin / 16) / 32; ++it) {
+      const uint32_t idx = it * 32 + lane;
+      const uint32_t r = idx / (kFnvWin / 16), u = idx % (kFnvWin / 16);
+      if (w < st.bytes[r]) cp_async16(&st.tile[r][u], st.base[r] + w + 16 * u);
     }
+    cp_async_wait_all();
     __syncwarp();
-    const uint32_t n32 = cnt - base < 32u ? cnt - base : 32u;
-    // positions (and any velocity >= 256): four data bytes, then four zero
-    // bytes folded into the last multiply; u8 velocities: one byte + seven
-    const uint64_t kb = k0 + base;
-    const uint32_t npos = kb >= N ? 0u : (kb + n32 <= N ? n32 : static_cast<uint32_t>(N - kb));
-    const uint32_t nfull = sizeof(VT) == 1 ? npos : n32;
-    auto full = [&](uint32_t j) {
-      const uint4 bb = s_bb[warp][j];
-      h0 = ((h0 ^ bb.x) & M) * kFnvP8;
-      h1 = ((h1 ^ bb.x) & M) * kFnvP8;
-      h0 = ((h0 ^ bb.y) & M) * kFnvP8;
-      h1 = ((h1 ^ bb.y) & M) * kFnvP8;
-      h0 = ((h0 ^ bb.z) & M) * kFnvP8;
-      h1 = ((h1 ^ bb.z) & M) * kFnvP8;
-      h0 = ((h0 ^ bb.w) & M) * kFnvP8_5;
-      h1 = ((h1 ^ bb.w) & M) * kFnvP8_5;
-    };
-    auto one = [&](uint32_t j) {
-      const uint32_t bx = s_bb[warp][j].x;
-      h0 = ((h0 ^ bx) & M) * kFnvP8_8;
-      h1 = ((h1 ^ bx) & M) * kFnvP8_8;
-    };
-    if (nfull == 32) {  // the common case, unrolled
-#pragma unroll
-      for (uint32_t j = 0; j < 32; ++j) full(j);
-    } else if (nfull == 0 && n32 == 32) {
-#pragma unroll
-      for (uint32_t j = 0; j < 32; ++j) one(j);
-    } else {
-      for (uint32_t j = 0; j < nfull; ++j) full(j);
-      for (uint32_t j = nfull; j < n32; ++j) one(j);
-    }
-    __syncwarp();
-    // the map from the chunk's start to each sub-chunk boundary (pass C
-    // runs kFnvSubs threads per chunk from these)
-    const uint32_t done = base + n32;
-    if (done % kFnvSubLen == 0 && done < cnt) {
-      uint8_t* sub = Fsub + (size_t(c) * (kFnvSubs - 1) + done / kFnvSubLen - 1) * 256;
-      const uint32_t g[4] = {h0 & 0xffu, (h0 >> 16) & 0xffu, h1 & 0xffu, (h1 >> 16) & 0xffu};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        sub[lane + 32u * q] = static_cast<uint8_t>(g[q]);
-        sub[(lane + 32u * q) ^ 0x80u] = static_cast<uint8_t>(g[q] ^ 0x80u);
-      }
-    }
-  }
-  uint8_t* out = F + size_t(c) * 256;
-  const uint32_t f[4] = {h0 & 0xffu, (h0 >> 16) & 0xffu, h1 & 0xffu, (h1 >> 16) & 0xffu};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t s = lane + 32u * q;
-    out[s] = static_cast<uint8_t>(f[q]);
-    out[s ^ 0x80u] = static_cast<uint8_t>(f[q] ^ 0x80u);
-  }
-}
-
-// Pass B, up: block g composes maps [256 g, 256 g + 256) of `in` (n maps)
-// into out[g]: thread l follows start l through them (maps staged in
-// shared memory).
-static __global__ void __launch_bounds__(256) fnv_group8_kernel(const uint8_t* in, uint32_t n, uint8_t* out) {
-  extern __shared__ uint8_t s_maps[];  // [256][256]
-  const uint32_t g = blockIdx.x;
-  const uint32_t m = n - 256u * g < 256u ? n - 256u * g : 256u;
-  const uint4* src = reinterpret_cast<const uint4*>(in + size_t(g) * 256 * 256);
-  uint4* dst = reinterpret_cast<uint4*>(s_maps);
-  for (uint32_t i = threadIdx.x; i < m * 16u; i += 256) dst[i] = src[i];
-  __syncthreads();
-  uint32_t l = threadIdx.x;
-  for (uint32_t i = 0; i < m; ++i) l = s_maps[i * 256u + l];
-  out[size_t(g) * 256 + threadIdx.x] = static_cast<uint8_t>(l);
-}
-
-// Pass B, down: block g knows the low byte entering its group (lb_in[g], or
-// the digest's low byte at the top) and walks its <= 256 maps, writing the
-// low byte entering each (lb_out[256 g + i]).
-static __global__ void __launch_bounds__(256) fnv_walk8_kernel(const uint8_t* maps, uint32_t n, const uint8_t* lb_in,
-                                                        const unsigned long long* hash, uint8_t* lb_out) {
-  extern __shared__ uint8_t s_maps[];  // [256][256]
-  const uint32_t g = blockIdx.x;
-  const uint32_t m = n - 256u * g < 256u ? n - 256u * g : 256u;
-  const uint4* src = reinterpret_cast<const uint4*>(maps + size_t(g) * 256 * 256);
-  uint4* dst = reinterpret_cast<uint4*>(s_maps);
-  for (uint32_t i = threadIdx.x; i < m * 16u; i += 256) dst[i] = src[i];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t l = lb_in ? lb_in[g] : static_cast<uint32_t>(*hash & 0xffu);
-    for (uint32_t i = 0; i < m; ++i) {
-      lb_out[256u * g + i] = static_cast<uint8_t>(l);
-      l = s_maps[i * 256u + l];
-    }
-  }
-}
-
-// Pass C: one thread per sub-chunk (kFnvSubLen values) runs the exact
-// 64-bit FNV of its values from the 64-bit state lb (its true incoming low
-// byte, upper bytes 0; a chunk's later sub-chunks read theirs from the
-// cumulative sub-chunk maps of pass A): h_out = P^(8n) lb + d, so the
-// sub-chunk maps the true state h to P^(8n) h + d.  Values staged through
-// shared memory 32 per sub-chunk at a time (coalesced loads, all in flight
-// before the stores; rows padded against bank conflicts).
-constexpr int kAffTPB = 128;
-template <typename VT>
-__global__ void __launch_bounds__(kAffTPB) fnv_affine_kernel(const RingArgs ra, const uint8_t* lb, const uint8_t* Fsub,
-                                                             uint32_t nsub, unsigned long long* A,
-                                                             unsigned long long* D) {
-  __shared__ uint32_t s_v[kAffTPB][33];
-  const Ctl* ctl = ra.ctl;
-  const uint32_t N = ra.n;
-  const uint32_t head = (N - ctl->W) % N;
-  const int b = static_cast<int>(ctl->buf);
-  const uint32_t* X = xbuf(ra, b);
-  const VT* V = vbuf<VT>(ra, b);
-  const uint64_t rowlen = 2ull * N;
-  const uint32_t s0 = blockIdx.x * kAffTPB;
-  const uint32_t s = s0 + threadIdx.x;
-  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  constexpr unsigned long long P4 = kFnvP * kFnvP * kFnvP * kFnvP;
-  unsigned long long h = 0;
-  uint32_t cnt = 0;
-  if (s < nsub) {
-    const uint32_t c = s / kFnvSubs, q = s % kFnvSubs;
-    const uint32_t l = lb[c];
-    h = q == 0 ? l : Fsub[(size_t(c) * (kFnvSubs - 1) + q - 1) * 256 + l];
-    const uint64_t k0 = uint64_t(s) * kFnvSubLen;
-    cnt = static_cast<uint32_t>(rowlen - k0 < kFnvSubLen ? rowlen - k0 : kFnvSubLen);
-  }
-  const unsigned long long h_in = h;
-  for (uint32_t t = 0; t < kFnvSubLen; t += 32) {
-    constexpr int kRows = kAffTPB / (kAffTPB / 32);
-    uint32_t vals[kRows];
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const uint32_t sr = s0 + warp + r * (kAffTPB / 32);
-      const uint64_t k = uint64_t(sr) * kFnvSubLen + t + lane;
-      vals[r] = (sr < nsub && k < rowlen) ? fnv_row_value<VT>(X, V, N, head, k) : 0u;
-    }
-#pragma unroll
-    for (int r = 0; r < kRows; ++r) s_v[warp + r * (kAffTPB / 32)][lane] = vals[r];
-    __syncthreads();
-    const uint32_t m = cnt > t ? (cnt - t < 32u ? cnt - t : 32u) : 0u;
-    for (uint32_t i = 0; i < m; ++i) {
-      const uint32_t w = s_v[threadIdx.x][i];
-      if (w < 256u) {  // velocities (and tiny positions): one data byte
-        h = (h ^ w) * kFnvP;
-        h *= P4 * kFnvP * kFnvP * kFnvP;
+    if (w < bytes) {
+      // partial unrolling: the fully unrolled window (2.3k instructions per
+      // lane in pass B) missed the instruction cache
+      if (wide) {
+#pragma unroll 4
+        for (uint32_t u = 0; u < kFnvWin / 16; ++u) {
+          const uint4 q = st.tile[lane][u];
+          f4(q.x);
+          f4(q.y);
+          f4(q.z);
+          f4(q.w);
+        }
       } else {
-        h = (h ^ (w & 0xffu)) * kFnvP;
-        h = (h ^ ((w >> 8) & 0xffu)) * kFnvP;
-        h = (h ^ ((w >> 16) & 0xffu)) * kFnvP;
-        h = (h ^ (w >> 24)) * kFnvP;
-        h *= P4;
+#pragma unroll 2
+        for (uint32_t u = 0; u < kFnvWin / 16; ++u) {
+          const uint4 q = st.tile[lane][u];
+          f1(q.x, 0); f1(q.x, 1); f1(q.x, 2); f1(q.x, 3);
+          f1(q.y, 0); f1(q.y, 1); f1(q.y, 2); f1(q.y, 3);
+          f1(q.z, 0); f1(q.z, 1); f1(q.z, 2); f1(q.z, 3);
+          f1(q.w, 0); f1(q.w, 1); f1(q.w, 2); f1(q.w, 3);
+        }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
-  if (s < nsub) {
-    const unsigned long long a = fnv_pow(kFnvP, 8ull * cnt);
-    A[s] = a;
-    D[s] = h - a * h_in;
+  if (!full) {
+    for (uint32_t id = a; id < b; ++id) {
+      if (arr == 0) f4(__ldg(X + id));
+      else if (sizeof(VT) == 4) f4(static_cast<uint32_t>(__ldg(V + id)));
+      else f1(static_cast<uint32_t>(__ldg(V + id)), 0);
+    }
   }
+}
+
+// Byte k of w broadcast to the four 8-bit lanes / the two 16-bit lanes.
+__device__ __forceinline__ uint32_t fnv_bcast8(uint32_t w, int k) { return __byte_perm(w, 0u, 0x1111u * k); }
+__device__ __forceinline__ uint32_t fnv_bcast16(uint32_t w, int k) { return __byte_perm(w, 0u, 0x4040u | (0x0101u * k)); }
+
+// Passes A (LEVEL 0) and B (LEVEL 1) of chunk c (slots 4c .. 4c+3).
+// Out: F[c][16] (A: low nibble out per low nibble in; B: high nibble out per
+// high nibble in); B also Fsub[c][q][16], the full byte after slot q < 3 per
+// high nibble in.  Warp-collective (the staging); `live` false: no output.
+template <typename VT, int LEVEL>
+__device__ __forceinline__ void fnv_nib_chunk(FnvStage& st, const FnvRow& row, const uint32_t* X, const VT* V,
+                                              uint32_t c, bool live, const uint8_t* lo4, uint8_t* F,
+                                              uint8_t* Fsub) {
+  const uint32_t nslots = 2 * row.npos;
+  const uint32_t s0 = c * kFnvSlotsPerChunk;
+  uint32_t out[16];
+  if (LEVEL == 0) {
+    constexpr uint32_t M = 0x0f0f0f0fu;
+    uint32_t h0 = 0x03020100u, h1 = 0x07060504u;  // starts 0..3, 4..7
+    auto f4 = [&](uint32_t w) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t bb = fnv_bcast8(w, k);
+        const uint32_t mul = k < 3 ? kFnvP4 : kFnvP4_5;
+        h0 = ((h0 ^ bb) & M) * mul;
+        h1 = ((h1 ^ bb) & M) * mul;
+      }
+    };
+    auto f1 = [&](uint32_t w, int k) {
+      const uint32_t bb = fnv_bcast8(w, k);
+      h0 = ((h0 ^ bb) & M) * kFnvP4_8;
+      h1 = ((h1 ^ bb) & M) * kFnvP4_8;
+    };
+    for (uint32_t q = 0; q < kFnvSlotsPerChunk; ++q) {
+      uint32_t arr = 0, a = 0, b = 0;
+      if (live && s0 + q < nslots) fnv_slot(row, s0 + q, arr, a, b);
+      fnv_slot_values<VT>(st, X, V, arr, a, b, f4, f1);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      out[j] = (h0 >> (8 * j)) & 0xfu;
+      out[j + 4] = (h1 >> (8 * j)) & 0xfu;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[j + 8] = out[j] ^ 8u;
+  } else {
+    constexpr uint32_t M = 0x00ff00ffu;
+    const uint32_t lo = live ? lo4[c] : 0u;
+    // register i: start i in the low half, start i + 4 in the high half
+    uint32_t g[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) g[i] = ((uint32_t(i) << 4) | lo) | ((((uint32_t(i) + 4u) << 4) | lo) << 16);
+    auto f4 = [&](uint32_t w) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t bb = fnv_bcast16(w, k);
+        const uint32_t mul = k < 3 ? kFnvP8 : kFnvP8_5;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) g[i] = ((g[i] ^ bb) & M) * mul;
+      }
+    };
+    auto f1 = [&](uint32_t w, int k) {
+      const uint32_t bb = fnv_bcast16(w, k);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) g[i] = ((g[i] ^ bb) & M) * kFnvP8_8;
+    };
+    auto byte_of = [&](int j) { return (g[j & 3] >> (16 * (j >> 2))) & 0xffu; };
+    for (uint32_t q = 0; q < kFnvSlotsPerChunk; ++q) {
+      uint32_t arr = 0, a = 0, b = 0;
+      if (live && s0 + q < nslots) fnv_slot(row, s0 + q, arr, a, b);
+      fnv_slot_values<VT>(st, X, V, arr, a, b, f4, f1);
+      if (live && q + 1 < kFnvSlotsPerChunk) {
+        uint8_t* sub = Fsub + (size_t(c) * (kFnvSlotsPerChunk - 1) + q) * 16;
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t y = byte_of(j);
+          w[j >> 2] |= y << (8 * (j & 3));
+          w[(j + 8) >> 2] |= (y ^ 0x80u) << (8 * (j & 3));
+        }
+        *reinterpret_cast<uint4*>(sub) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      out[j] = byte_of(j) >> 4;
+      out[j + 8] = out[j] ^ 8u;
+    }
+  }
+  if (!live) return;
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    w[i] = out[4 * i] | (out[4 * i + 1] << 8) | (out[4 * i + 2] << 16) | (out[4 * i + 3] << 24);
+  *reinterpret_cast<uint4*>(F + size_t(c) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Lane = chunk c.  (Pairing a position chunk with a velocity chunk per lane
+// evens the warps' work but halves the warps: measured slower.)
+constexpr uint32_t kFnvTPB = 128;  // 4 warps: 4 x 9 KB staging
+template <typename VT, int LEVEL>
+__global__ void __launch_bounds__(kFnvTPB) fnv_nib_kernel(const RingArgs ra, const uint8_t* lo4, uint8_t* F,
+                                                          uint8_t* Fsub) {
+  __shared__ FnvStage stage[kFnvTPB / 32];
+  FnvStage& st = stage[threadIdx.x / 32];
+  const Ctl* ctl = ra.ctl;
+  const FnvRow row = fnv_row(ra.n, ctl->W);
+  const uint32_t nchunks = 2 * row.npos / kFnvSlotsPerChunk;
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((c & ~31u) >= nchunks) return;  // whole warps only: the staging is warp-collective
+  const int bsel = static_cast<int>(ctl->buf);
+  const uint32_t* X = xbuf(ra, bsel);
+  const VT* V = vbuf<VT>(ra, bsel);
+  fnv_nib_chunk<VT, LEVEL>(st, row, X, V, c, c < nchunks, lo4, F, Fsub);
+}
+
+// Composition tree over maps of 16 nibbles: block = kUpGroups groups of 256
+// maps, thread = (group, start l) following l through its group's maps
+// (staged in shared memory, rows padded so the groups use distinct banks);
+// records pre[m][l], the value entering map m from start l of m's group, and
+// the group's composed map out[g].
+constexpr uint32_t kUpGroups = 8;
+static __global__ void __launch_bounds__(16 * kUpGroups) fnv_up16_kernel(const uint8_t* maps, uint32_t n, uint8_t* pre,
+                                                                        uint8_t* out) {
+  __shared__ uint4 s[kUpGroups][257];
+  const uint32_t g0 = blockIdx.x * kUpGroups;
+  const uint4* src = reinterpret_cast<const uint4*>(maps);
+  for (uint32_t i = threadIdx.x; i < kUpGroups * 256; i += blockDim.x) {
+    const uint32_t m = g0 * 256 + i;
+    s[i / 256][i % 256] = m < n ? src[m] : make_uint4(0, 0, 0, 0);
+  }
+  __syncthreads();
+  const uint32_t gl = threadIdx.x / 16, l = threadIdx.x % 16;
+  const uint32_t g = g0 + gl;
+  if (size_t(g) * 256 >= n) return;
+  const uint32_t cnt = min(256u, n - g * 256);
+  const uint8_t* sm = reinterpret_cast<const uint8_t*>(&s[gl][0]);
+  uint8_t* pg = pre + size_t(g) * 256 * 16 + l;
+  uint32_t v = l;
+  for (uint32_t i = 0; i < cnt; ++i) {
+    pg[i * 16] = static_cast<uint8_t>(v);
+    v = sm[i * 16 + v];
+  }
+  out[size_t(g) * 16 + l] = static_cast<uint8_t>(v);
+}
+
+// Down the tree: lb[m] = pre[m][up[m / 256]], the value entering map m; at
+// the top the value entering the row is the digest's nibble (hash >> shift).
+static __global__ void __launch_bounds__(256) fnv_down16_kernel(const uint8_t* pre, uint32_t n, const uint8_t* up,
+                                                               const unsigned long long* hash, int shift,
+                                                               uint8_t* lb) {
+  const uint32_t m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= n) return;
+  const uint32_t u = up ? up[m / 256] : static_cast<uint32_t>((*hash >> shift) & 0xfu);
+  lb[m] = pre[size_t(m) * 16 + u];
+}
+
+// Pass C: one slot, from its true incoming low byte (chunk start: low and
+// high nibble from passes A and B; later slots: pass B's boundary bytes),
+// the exact 64-bit FNV of its values: the slot maps the true state h to
+// A h + D with A = P^(8n).  Warp-collective.
+template <typename VT>
+__device__ __forceinline__ void fnv_exact_slot(FnvStage& st, const FnvRow& row, const uint32_t* X, const VT* V,
+                                               uint32_t s, bool live, const uint8_t* lo4, const uint8_t* hi4,
+                                               const uint8_t* Fsub, unsigned long long* A, unsigned long long* D) {
+  const uint32_t c = s / kFnvSlotsPerChunk, q = s % kFnvSlotsPerChunk;
+  uint32_t start = 0, arr = 0, a = 0, b = 0;
+  if (live) {
+    const uint32_t hn = hi4[c];
+    start = q == 0 ? (lo4[c] | (hn << 4)) : Fsub[(size_t(c) * (kFnvSlotsPerChunk - 1) + q - 1) * 16 + hn];
+    fnv_slot(row, s, arr, a, b);
+  }
+  unsigned long long h = start;
+  constexpr unsigned long long P8 = fnv_pow_c(8);
+  fnv_slot_values<VT>(st, X, V, arr, a, b, [&](uint32_t w) { h = fnv_value(h, w); },
+                      [&](uint32_t w, int k) { h = (h ^ ((w >> (8 * k)) & 0xffu)) * P8; });
+  if (!live) return;
+  const unsigned long long an = b - a == kFnvSlot ? kFnvPSlot : fnv_pow(kFnvP, 8ull * (b - a));
+  A[s] = an;
+  D[s] = h - an * start;
+}
+
+// Lane = slot s.
+template <typename VT>
+__global__ void __launch_bounds__(kFnvTPB) fnv_exact_kernel(const RingArgs ra, const uint8_t* lo4, const uint8_t* hi4,
+                                                            const uint8_t* Fsub, unsigned long long* A,
+                                                            unsigned long long* D) {
+  __shared__ FnvStage stage[kFnvTPB / 32];
+  FnvStage& st = stage[threadIdx.x / 32];
+  const Ctl* ctl = ra.ctl;
+  const FnvRow row = fnv_row(ra.n, ctl->W);
+  const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if ((s & ~31u) >= 2 * row.npos) return;  // whole warps only
+  const int bsel = static_cast<int>(ctl->buf);
+  const uint32_t* X = xbuf(ra, bsel);
+  const VT* V = vbuf<VT>(ra, bsel);
+  fnv_exact_slot<VT>(st, row, X, V, s, s < 2 * row.npos, lo4, hi4, Fsub, A, D);
 }
 
 // Affine maps h -> A h + D composed in row order, 256 per block:

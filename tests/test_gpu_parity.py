@@ -385,6 +385,33 @@ def test_temporal_blocking_checksum_mode(port, k_env, dr):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("K", ["8", "32"])
+def test_checksum_toggle_switches_step_kernels(port, k_env, K):
+    """A temporal-blocked ring steps with the one-step kernel while the
+    checksum is on (every row hashed) and re-plans its origin cone before the
+    next K-step launch: toggling the checksum mid-run in both directions
+    leaves positions, velocities and every step's sum/crossings equal to the
+    reference's."""
+    os.environ["NASCH_B200_K"] = K
+    os.environ["NASCH_B200_DR"] = "0"
+    L, N, T = 300000, 60000, 137
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 21)
+    o = port.run(L, 5, 0.3, 5, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    e = nasch.Engine(params(L, N, 5, 0.3, T, 5))
+    e.set_state(x0, v0)
+    assert e.steps_per_launch == int(K)
+    on = False
+    for chunk in [10, 7, 33, 5, 1, 40, 3, 38]:
+        e.set_checksum(on)
+        e.advance(chunk)
+        on = not on
+    assert e.steps_done == T
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    e.close()
+
+
 @pytest.mark.parametrize("dr", ["0", "1"])
 def test_temporal_blocking_long_run_vs_reference(ref, k_env, dr):
     """Thousands of steps of a dense jammed ring (many crossings per plan)
@@ -428,9 +455,9 @@ def test_distributed_resident_geometries(port, k_env, kdr):
 
 
 def test_device_checksum_many_chunks(port):
-    """The on-device FNV-1a fold (256-state chunk tables composed in a tree)
-    equals the reference's serial byte-at-a-time digest when a step's row
-    spans many 4096-value chunks and an odd chunk count."""
+    """The on-device FNV-1a fold equals the reference's serial
+    byte-at-a-time digest when a step's row spans many slots and chunks and
+    an odd chunk count."""
     for (L, N, T) in [(10**6, 300001, 12), (9000, 2049, 30)]:
         x0, v0 = nasch.fill_uniform_state(L, N, 5, 6)
         o = port.run(L, 5, 0.3, 2, T, x0.astype(np.uint64), v0.astype(np.uint64))
@@ -440,15 +467,19 @@ def test_device_checksum_many_chunks(port):
 
 
 @pytest.mark.parametrize("L,N,vmax,T", [
-    (5 * 10**6, 1_200_001, 5, 3),    # >= 1e6 cars: 1172 chunk maps, two composition levels
+    (5 * 10**6, 1_200_001, 5, 3),    # >= 1e6 cars: 1173 chunk maps, two composition levels
     (3000, 2000, 5, 25),             # one chunk level; positions < 256 take the one-byte path
-    (200000, 70000, 300, 4),         # u32 velocities above 255: four-byte map path
-    (10**6, 131072, 7, 6)])          # 2N a multiple of the 2048-value chunk
-def test_device_checksum_lowbyte_decomposition(port, L, N, vmax, T):
-    """The per-step digest as 8-bit chunk maps (two starts per register, 128
-    tracked), their composition tree and walk, one exact 64-bit pass per
-    chunk and the affine reduction, against the reference's serial FNV-1a
-    over every step's row."""
+    (200000, 70000, 300, 4),         # u32 velocities above 255: four-byte values everywhere
+    (10**6, 131072, 7, 6),           # N a multiple of the 512-value slot: head unit-aligned steps
+    (700, 300, 5, 40),               # one unit per array: the row is two pieces of one slot each
+    (2 * 10**8, 70_000_001, 5, 2)])  # 68k chunk maps: three composition levels
+def test_device_checksum_nibble_decomposition(port, L, N, vmax, T):
+    """The per-step digest by nibble decomposition (fnv_kernels.cuh): pass A
+    low-nibble chunk maps and their composition tree, pass B high-nibble maps
+    from each chunk's true low nibble and their tree, pass C one exact 64-bit
+    run per ID-aligned slot (the head slot split in two) and the affine
+    reduction, against the reference's serial FNV-1a over every step's row
+    (src/engine.cpp:11-21, :179)."""
     x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, 5), 13)
     o = port.run(L, vmax, 0.3, 9, T, x0.astype(np.uint64), v0.astype(np.uint64))
     g = gpu_run(L, N, vmax, 0.3, 9, T, x0, v0, checksum=True)
