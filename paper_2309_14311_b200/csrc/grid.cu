@@ -5,23 +5,24 @@
 // of the occupant or -1; each step scans the occupied cells in ascending
 // order (= rank order, so draw #(t*N + rank + 1)), brakes to the distance to
 // the next occupied cell, and scatters every car to (x + v) mod L.
-// Here one step is four launches over L one-byte cells (0xff = empty):
-//   count   occupied cells per 4096-cell block (16-byte loads, byte compares
-//           in SIMD-within-a-register form)
-//   scan    exclusive prefix over the block counts (rank of a block's first
-//           car) in two levels: 1024 counts per block, then the group totals
-//   move    block b assembles the NEXT array's cells [4096 b, 4096 b + 4096)
+// Here one step is four launches over L one-byte cells (0xff = empty), in
+// 8192-cell blocks:
+//   fixup   the previous move's spilled cars into the array and their
+//           blocks' counts
+//   scan    exclusive prefix over the block counts (rank of each block's
+//           first car, and a^rank for its draws) in two levels; this step's
+//           record zeroed
+//   move    block b assembles the NEXT array's cells [8192 b, 8192 b + 8192)
 //           in shared memory from its own cars, writes them with 16-byte
 //           stores (no clearing pass, no byte scatter in HBM) and counts
-//           them for the next step's scan; each warp compacts its cars
-//           first (lanes work on cars, not cells); per car: gap to the next
-//           car of the list, the counter-based draw E_t a^rank (a^rank from
-//           three 4096-entry power tables for a lane's first car, then one
-//           multiply by a^32 per car); exact velocity sum and wrap count.
-//           Cars landing past the block (<= vmax of them) go to a spill
-//           list:
-//   fixup   stores the spilled cars and adds them to their block's count.
-// The count pass runs only after construction / set_state.  Steps are
+//           them for the next step's scan; the block compacts its cars into
+//           one list first (threads work on cars, not cells), with the first
+//           car after the block as a sentinel; per car: gap to the next list
+//           entry, the counter-based draw E_t a^rank (one multiply by
+//           a^256 per car), exact velocity sum and wrap count.  Cars landing
+//           past the block (<= vmax of them) go to a spill list, stored by
+//           the next step's fixup (or before a state read).
+// A count pass runs only after construction / set_state.  Steps are
 // enqueued without a host round trip; the per-step records are drained in
 // batches.  HBM traffic per step: about 2 L bytes.
 // Bit-identical to the agent engines (tests/test_gpu_grid.py).
@@ -49,9 +50,10 @@ void check_g(cudaError_t e, const char* what) {
 }
 #define CKG(call) check_g((call), #call)
 
-constexpr uint32_t kCellsPerBlock = 4096;
-constexpr int kGridTPB = 256;  // 16 cells per thread
+constexpr uint32_t kCellsPerBlock = 8192;
+constexpr int kGridTPB = 256;  // 32 cells per thread
 constexpr uint8_t kEmpty = 0xff;
+constexpr uint32_t kSpillMax = 256;  // spilled cars per block: >= look (vmax <= 254 in the grid engine)
 
 
 // Occupied bytes (!= 0xff) among the 16 cells [lo, lo + 16).
@@ -66,12 +68,12 @@ __device__ __forceinline__ uint32_t occupied16(const uint8_t* __restrict__ cells
   return c;
 }
 
-// One thread per 16 consecutive cells of the block (as the move kernel).
+// One thread per 32 consecutive cells of the block (as the move kernel).
 __global__ void __launch_bounds__(kGridTPB) grid_count_kernel(const uint8_t* __restrict__ cells, uint32_t L,
                                                               uint32_t* counts) {
   const uint32_t b = blockIdx.x;
-  const uint32_t lo = b * kCellsPerBlock + threadIdx.x * 16u;
-  uint32_t c = lo < L ? occupied16(cells, lo, L) : 0u;
+  const uint32_t lo = b * kCellsPerBlock + threadIdx.x * 32u;
+  uint32_t c = (lo < L ? occupied16(cells, lo, L) : 0u) + (lo + 16 < L ? occupied16(cells, lo + 16, L) : 0u);
   c = __reduce_add_sync(0xffffffffu, c);
   __shared__ uint32_t s[kGridTPB / 32];
   if ((threadIdx.x & 31) == 0) s[threadIdx.x / 32] = c;
@@ -83,10 +85,7 @@ __global__ void __launch_bounds__(kGridTPB) grid_count_kernel(const uint8_t* __r
   }
 }
 
-// Exclusive scan of the nb block counts in two levels: grid_scan_local
-// (1024 counts per block, warp-shuffle scan) writes each block's local
-// prefix and the 1024-block group totals; grid_scan_top scans the <= 1024
-// group totals.  A block's first rank is local[b] + top[b >> 10].
+// Exclusive scan of 1024 values over one block (warp-shuffle scans).
 __device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s_w, uint32_t* total) {
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   uint32_t incl = v;
@@ -112,27 +111,53 @@ __device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s
   return s_w[warp] + incl - v;
 }
 
+// The draw of the car of rank r: E a^r, a^r from the three power tables
+// pw = [a^j, a^(4096 j), a^(4096^2 j)], j < 4096.
+__device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
+  return mulmod(mulmod(__ldg(pw + (r & 4095u)), __ldg(pw + 4096 + ((r >> 12) & 4095u))),
+                __ldg(pw + 8192 + (r >> 24)));
+}
+
+// The exclusive scan of the block counts in two levels: grid_scan_local
+// (1024 counts per block) writes each block's local prefix and a^prefix and
+// the 1024-block group totals; grid_scan_top scans the group totals (and
+// their a^prefix) and zeroes this step's record.  A block's first rank is
+// local[b] + group[b >> 10]; its draw power plocal[b] * pgroup[b >> 10]
+// reaches the move kernel as two independent loads (round 2: a rank load
+// then three dependent table loads).  (A single-block scan fused with the
+// spill fixup measured 23 us against ~10 us for these two launches.)
 __global__ void __launch_bounds__(1024) grid_scan_local(const uint32_t* counts, uint32_t nb, uint32_t* local,
-                                                        uint32_t* group) {
+                                                        uint32_t* group, const uint32_t* pw, uint32_t* plocal) {
   __shared__ uint32_t s_w[32], s_tot;
   const uint32_t i = blockIdx.x * 1024u + threadIdx.x;
   const uint32_t v = i < nb ? counts[i] : 0u;
   const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
-  if (i < nb) local[i] = ex;
+  if (i < nb) {
+    local[i] = ex;
+    plocal[i] = apow_rank(pw, ex);
+  }
   if (threadIdx.x == 0) group[blockIdx.x] = s_tot;
 }
 
-__global__ void __launch_bounds__(1024) grid_scan_top(uint32_t* group, uint32_t ng) {
+__global__ void __launch_bounds__(1024) grid_scan_top(uint32_t* group, uint32_t ng, const uint32_t* pw,
+                                                      uint32_t* pgroup, StepRec* zero) {
   __shared__ uint32_t s_w[32], s_tot;
   const uint32_t v = threadIdx.x < ng ? group[threadIdx.x] : 0u;
   const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
-  if (threadIdx.x < ng) group[threadIdx.x] = ex;
+  if (threadIdx.x < ng) {
+    group[threadIdx.x] = ex;
+    pgroup[threadIdx.x] = apow_rank(pw, ex);
+  }
+  if (zero && threadIdx.x == 0) {
+    zero->sumv = 0;
+    zero->c = 0;
+  }
 }
 
 struct GridArgs {
   uint32_t L, N, vmax, tp;
   uint32_t E;                 // s0 a^(t N + 1): the draw of the rank-0 car at step t
-  uint32_t a32;               // a^32 (a lane's next car is 32 ranks on)
+  uint32_t astep2;            // 2 a^kGridTPB (a thread's next car is kGridTPB ranks on; doubled: mulmod_x2)
   const uint32_t* pw;         // [3][4096]: a^j, a^(4096 j), a^(4096^2 j)
   unsigned long long t;
 };
@@ -142,156 +167,167 @@ __device__ __forceinline__ uint32_t occ_bits4(uint32_t w) {
   return ((__vcmpne4(w, 0xffffffffu) & 0x01010101u) * 0x01020408u) >> 24;
 }
 
-// The draw of the car of rank r: E a^r, a^r from the three power tables.
-__device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
-  return mulmod(mulmod(__ldg(pw + (r & 4095u)), __ldg(pw + 4096 + ((r >> 12) & 4095u))),
-                __ldg(pw + 8192 + (r >> 24)));
+// Occupied cells of a 4-cell word as 4 bits; with velocities below 128 an
+// occupied byte is one with bit 7 clear (empty = 0xff): ~w & 0x80808080,
+// the four flags gathered by one multiply (bits 7+8k -> 21+k, no carries).
+template <bool SMALLV>
+__device__ __forceinline__ uint32_t occ4(uint32_t w) {
+  if constexpr (SMALLV) {
+    return ((~w & 0x80808080u) * 0x204081u) >> 28;  // bits 7, 15, 23, 31 -> 28..31
+  } else {
+    return occ_bits4(w);
+  }
 }
 
-// Round 2 form of the move (grid_move2_kernel + grid_fixup_kernel): each
-// block moves only its OWN cars.  A car landing past the block's output
-// cells (at most `look` of them per block: they start within vmax cells of
-// the block's end, or wrap past L) is appended to the block's spill list
-// instead, and grid_fixup_kernel stores the spilled cars after every block
-// has written its cells -- no warp re-simulating the previous block's last
-// cars (a serial chain of global reads the other warps waited on at the
-// barrier).  The block also counts the cars it placed, so the next step's
-// scan needs no separate count pass over the L cells (the fixup adds the
-// spilled cars to their block's count): two passes over the cells per step
-// instead of three.  Draws: Q = E a^rank once per lane, then one mulmod by
-// a^32 per car.
-constexpr uint32_t kSpillMax = 256;  // >= look (vmax <= 254 in the grid engine)
-__global__ void __launch_bounds__(kGridTPB) grid_move2_kernel(const uint8_t* __restrict__ cells,
+// Offset from B1 of the first occupied cell at or after B1 (cyclic, read
+// from the current array), searched over max(16, look) cells; the window
+// size when there is none (the gap is then capped at look anyway).
+__device__ __forceinline__ uint32_t grid_next_car(const uint8_t* __restrict__ cells, uint32_t B1, uint32_t L,
+                                                  uint32_t look) {
+  const uint32_t n0 = B1 == L ? 0u : B1;  // B1 is a multiple of the block size, or L
+  if (n0 + 16 <= L) {
+    const uint4 w = *reinterpret_cast<const uint4*>(cells + n0);
+    const uint32_t m = occ_bits4(w.x) | (occ_bits4(w.y) << 4) | (occ_bits4(w.z) << 8) | (occ_bits4(w.w) << 12);
+    if (m) return __ffs(m) - 1u;
+    if (look <= 16) return 16;
+    for (uint32_t d = 16; d < look; ++d)
+      if (cells[(n0 + d) % L] != kEmpty) return d;
+    return look;
+  }
+  const uint32_t win = max(16u, look);
+  for (uint32_t d = 0; d < win; ++d)
+    if (cells[(n0 + d) % L] != kEmpty) return d;
+  return win;
+}
+
+// The move (grid_move3_kernel + grid_fixup_kernel): each block moves only its
+// OWN cars.  A car landing past the block's output cells (at most `look` of
+// them per block: they start within vmax cells of the block's end, or wrap
+// past L) is appended to the block's spill list instead, and
+// grid_fixup_kernel stores the spilled cars after every block has written
+// its cells.  The block also counts the cars it placed, so the next step's
+// scan needs no count pass over the L cells.  Round 3 form: 8192 cells per
+// block (32 per thread) to halve the per-cell share of the block's fixed
+// work; the cars compacted into ONE block-wide list (offsets from B0) with a
+// sentinel after the last car (the first car at or after B1, loaded with the
+// block's cells), so every car's gap is list[j+1] - list[j] - 1 with no warp
+// or block boundary case; thread t takes cars t, t + 256, ... (block-local
+// rank j: draw E a^(rank0 + j) = Eb a^j, one mulmod by a^256 per car).
+template <bool SMALLV>
+__global__ void __launch_bounds__(kGridTPB) grid_move3_kernel(const uint8_t* __restrict__ cells,
                                                               uint8_t* __restrict__ next,
-                                                              const uint32_t* __restrict__ local,
-                                                              const uint32_t* __restrict__ group,
+                                                              const uint32_t* __restrict__ plocal,
+                                                              const uint32_t* __restrict__ pgroup,
                                                               GridArgs g, StepRec* rec, uint32_t* counts_next,
                                                               uint32_t* spill, uint32_t* spill_n) {
-  constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;
+  constexpr uint32_t CPT = kCellsPerBlock / kGridTPB;  // 32
   constexpr int NW = kGridTPB / 32;
   __shared__ __align__(16) uint8_t s_out[kCellsPerBlock];
   __shared__ __align__(16) uint8_t s_in[kCellsPerBlock];
+  __shared__ uint16_t s_list[kCellsPerBlock + 1];  // the block's cars (offsets from B0), then the sentinel
   __shared__ uint32_t s_w[NW];
-  __shared__ uint32_t s_nspill, s_cnt;
-  __shared__ uint16_t s_cx[NW][32 * CPT];  // a warp's cars: cell offset from B0, position order
+  __shared__ uint32_t s_nspill;
   const uint32_t B0 = blockIdx.x * kCellsPerBlock;
   const uint32_t lo = B0 + threadIdx.x * CPT;
-  // the block's first rank and its draw power, issued before the cells
-  // load so the two global round trips overlap
-  const uint32_t rank0 = __ldg(local + blockIdx.x) + __ldg(group + (blockIdx.x >> 10));
-  const uint32_t Eb = mulmod_d(g.E, apow_rank(g.pw, rank0));  // E a^rank0
-  reinterpret_cast<uint4*>(s_out)[threadIdx.x] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-  if (threadIdx.x == 0) {
-    s_nspill = 0;
-    s_cnt = 0;
-  }
-  uint32_t ws[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t look = min(g.vmax, g.L - 1);
+  const uint32_t B1 = min(B0 + kCellsPerBlock, g.L);  // end of this block's cells
+  // every global load first: the cells, the block's draw powers, a^tid
+  uint32_t ws[8];
   if (lo + CPT <= g.L) {
-    const uint4 w = *reinterpret_cast<const uint4*>(cells + lo);
-    ws[0] = w.x;
-    ws[1] = w.y;
-    ws[2] = w.z;
-    ws[3] = w.w;
+    const uint4 u0 = *reinterpret_cast<const uint4*>(cells + lo);
+    const uint4 u1 = *reinterpret_cast<const uint4*>(cells + lo + 16);
+    ws[0] = u0.x; ws[1] = u0.y; ws[2] = u0.z; ws[3] = u0.w;
+    ws[4] = u1.x; ws[5] = u1.y; ws[6] = u1.z; ws[7] = u1.w;
   } else {
 #pragma unroll
-    for (uint32_t k = 0; k < CPT; ++k)
-      if (lo + k < g.L) ws[k / 4] = (ws[k / 4] & ~(0xffu << (8 * (k % 4)))) | (uint32_t(cells[lo + k]) << (8 * (k % 4)));
+    for (uint32_t k = 0; k < 8; ++k) ws[k] = 0xffffffffu;
+    for (uint32_t k = 0; k < CPT && lo + k < g.L; ++k) {
+      const uint32_t sh = 8 * (k % 4);
+#pragma unroll
+      for (uint32_t q = 0; q < 8; ++q)
+        if (q == k / 4) ws[q] = (ws[q] & ~(0xffu << sh)) | (uint32_t(cells[lo + k]) << sh);
+    }
   }
-  reinterpret_cast<uint4*>(s_in)[threadIdx.x] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
-  const uint32_t m16 = occ_bits4(ws[0]) | (occ_bits4(ws[1]) << 4) | (occ_bits4(ws[2]) << 8) | (occ_bits4(ws[3]) << 12);
-  const uint32_t occ = __popc(m16);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t pl = __ldg(plocal + blockIdx.x), pg = __ldg(pgroup + (blockIdx.x >> 10));
+  const uint32_t at = __ldg(g.pw + threadIdx.x);  // a^tid
+  uint32_t sentinel = 0;
+  if (threadIdx.x == 0) {
+    s_nspill = 0;
+    sentinel = (B1 - B0) + grid_next_car(cells, B1, g.L, look);
+  }
+  uint4* so = reinterpret_cast<uint4*>(s_out);
+  so[2 * threadIdx.x] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  so[2 * threadIdx.x + 1] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+  uint4* si = reinterpret_cast<uint4*>(s_in);
+  si[2 * threadIdx.x] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+  si[2 * threadIdx.x + 1] = make_uint4(ws[4], ws[5], ws[6], ws[7]);
+  uint32_t m = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) m |= occ4<SMALLV>(ws[q]) << (4 * q);
+  const uint32_t occ = __popc(m);
   uint32_t incl = occ;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= static_cast<uint32_t>(o)) incl += n;
   }
-  const uint32_t wcnt = __shfl_sync(0xffffffffu, incl, 31);
   if (lane == 31) s_w[warp] = incl;
-  {  // compact the warp's car positions (velocities are read from s_in later)
-    uint32_t m = m16, q = incl - occ;
+  __syncthreads();
+  const uint32_t cw = lane < static_cast<uint32_t>(NW) ? s_w[lane] : 0u;
+  const uint32_t wbase = __reduce_add_sync(0xffffffffu, lane < warp ? cw : 0u);
+  const uint32_t ncars = __reduce_add_sync(0xffffffffu, cw);
+  {  // compaction into the block-wide list
+    uint32_t q = wbase + incl - occ;
     const uint32_t off = lo - B0;
     while (m) {
-      s_cx[warp][q++] = static_cast<uint16_t>(off + __ffs(m) - 1u);
+      s_list[q++] = static_cast<uint16_t>(off + __ffs(m) - 1u);
       m &= m - 1u;
     }
   }
+  if (threadIdx.x == 0) s_list[ncars] = static_cast<uint16_t>(sentinel);
   __syncthreads();  // also orders the s_out clear before any car lands
-  uint32_t wbase = 0, nfirst = 0xffffffffu;  // cars of earlier warps; first car after this warp
-  for (int w = 0; w < NW; ++w) {
-    const uint32_t cw = s_w[w];
-    if (w < static_cast<int>(warp)) wbase += cw;
-    else if (w > static_cast<int>(warp) && cw && nfirst == 0xffffffffu) nfirst = s_cx[w][0];
-  }
-  const uint32_t look = min(g.vmax, g.L - 1);
-  const uint32_t B1 = min(B0 + kCellsPerBlock, g.L);  // end of this block's cells
+  const uint32_t Eb = mulmod_d(mulmod_d(g.E, pl), pg);  // E a^rank0
+  uint32_t Q = mulmod_d(Eb, at);                        // draw of block-local car tid
   uint32_t sum = 0, wraps = 0;
-  if (lane < wcnt) {
-    // the lane's first draw: E a^(rank0 + wbase + lane), wbase + lane < 4096
-    uint32_t Q = mulmod_d(Eb, __ldg(g.pw + wbase + lane));
-    for (uint32_t j = lane; j < wcnt; j += 32) {
-      const uint32_t xo = s_cx[warp][j];
-      const uint32_t x = B0 + xo;
-      uint32_t gap;
-      if (j + 1 < wcnt) {
-        gap = min(static_cast<uint32_t>(s_cx[warp][j + 1]) - xo - 1u, look);
-      } else if (nfirst != 0xffffffffu) {  // the next car is in a later warp of the block
-        gap = min(nfirst - xo - 1u, look);
-      } else {  // the block's last car: the cells after the block (wrapping past L)
-        gap = look;
-        for (uint32_t d = 1; d <= look; ++d) {
-          uint32_t y = x + d;
-          if (y >= g.L) y -= g.L;
-          if (__ldg(cells + y) != kEmpty) {
-            gap = d - 1;
-            break;
-          }
-        }
-      }
-      uint32_t v = min(min(static_cast<uint32_t>(s_in[xo]) + 1, g.vmax), gap);
-      const uint32_t s = Q;  // draw #(t N + rank + 1)
-      Q = mulmod_d(Q, g.a32);
-      if (s < g.tp && v > 0) --v;
-      uint32_t nx = x + v;
-      const bool wrapped = nx >= g.L;
-      nx -= wrapped ? g.L : 0u;
-      wraps += wrapped;
-      if (nx >= B0 && nx < B1) {
-        s_out[nx - B0] = static_cast<uint8_t>(v);
-      } else {
-        const uint32_t slot = atomicAdd(&s_nspill, 1u);
-        spill[size_t(blockIdx.x) * kSpillMax + slot] = nx;
-        spill[size_t(gridDim.x) * kSpillMax + size_t(blockIdx.x) * kSpillMax + slot] = v;
-      }
-      sum += v;
+  for (uint32_t j = threadIdx.x; j < ncars; j += kGridTPB) {
+    const uint32_t xo = s_list[j];
+    const uint32_t gap = min(static_cast<uint32_t>(s_list[j + 1]) - xo - 1u, look);
+    uint32_t v = min(min(static_cast<uint32_t>(s_in[xo]) + 1, g.vmax), gap);
+    const uint32_t s = Q;  // draw #(t N + rank + 1)
+    Q = mulmod_x2(g.astep2, Q);
+    if (s < g.tp && v > 0) --v;
+    uint32_t nx = B0 + xo + v;
+    const bool wrapped = nx >= g.L;
+    nx -= wrapped ? g.L : 0u;
+    wraps += wrapped;
+    if (nx - B0 < B1 - B0) {
+      s_out[nx - B0] = static_cast<uint8_t>(v);
+    } else {
+      const uint32_t slot = atomicAdd(&s_nspill, 1u);
+      spill[size_t(blockIdx.x) * kSpillMax + slot] = nx;
+      spill[size_t(gridDim.x) * kSpillMax + size_t(blockIdx.x) * kSpillMax + slot] = v;
     }
+    sum += v;
   }
   __syncthreads();
-  uint32_t placed = 0;
-  if (B0 + (threadIdx.x + 1) * CPT <= g.L) {
-    const uint4 o = reinterpret_cast<const uint4*>(s_out)[threadIdx.x];
-    reinterpret_cast<uint4*>(next + B0)[threadIdx.x] = o;
-    placed = (__popc(__vcmpne4(o.x, 0xffffffffu)) + __popc(__vcmpne4(o.y, 0xffffffffu)) +
-              __popc(__vcmpne4(o.z, 0xffffffffu)) + __popc(__vcmpne4(o.w, 0xffffffffu))) >> 3;
+  if (lo + CPT <= g.L) {
+    reinterpret_cast<uint4*>(next + lo)[0] = so[2 * threadIdx.x];
+    reinterpret_cast<uint4*>(next + lo)[1] = so[2 * threadIdx.x + 1];
   } else {
-    for (uint32_t k = threadIdx.x * CPT; k < (threadIdx.x + 1) * CPT && B0 + k < g.L; ++k) {
-      next[B0 + k] = s_out[k];
-      placed += s_out[k] != kEmpty;
-    }
+    for (uint32_t k = threadIdx.x * CPT; k < (threadIdx.x + 1) * CPT && B0 + k < g.L; ++k) next[B0 + k] = s_out[k];
   }
   sum = __reduce_add_sync(0xffffffffu, sum);
   wraps = __reduce_add_sync(0xffffffffu, wraps);
-  placed = __reduce_add_sync(0xffffffffu, placed);
   if (lane == 0) {
     StepRec* r = rec + (g.t % kRecCap);
     if (sum) atomicAdd(&r->sumv, static_cast<unsigned long long>(sum));
     if (wraps) atomicAdd(&r->c, wraps);
-    atomicAdd(&s_cnt, placed);
   }
-  __syncthreads();
   if (threadIdx.x == 0) {
-    counts_next[blockIdx.x] = s_cnt;
+    // the cars placed in this block's cells: all of its own but the spilled
+    // ones (grid_fixup_kernel counts those into their destination block)
+    counts_next[blockIdx.x] = ncars - s_nspill;
     spill_n[blockIdx.x] = s_nspill;
   }
 }
@@ -353,10 +389,12 @@ struct GpuGrid::Impl {
   uint8_t* cells[2] = {nullptr, nullptr};
   int cur = 0;
   uint32_t *counts = nullptr, *local = nullptr, *group = nullptr, *xs = nullptr;
+  uint32_t *plocal = nullptr, *pgroup = nullptr;  // a^prefix of the two scan levels
+  uint32_t ng = 0;  // 1024-block groups of the two-level scan
+  bool fixup_pending = false;  // the last move's spilled cars are not yet in cells[cur]
   uint32_t* counts_next = nullptr;  // the next array's block counts (move2 + fixup)
   uint32_t *spill = nullptr, *spill_n = nullptr;
   bool counts_valid = false;  // counts[] describe cells[cur]
-  uint32_t ng = 0;  // 1024-block groups of the two-level scan
   uint8_t* vs = nullptr;
   StepRec* rec = nullptr;
   StepRec* hrec = nullptr;  // pinned [kRecCap]
@@ -375,15 +413,26 @@ struct GpuGrid::Impl {
   unsigned long long* dhash = nullptr;
   ~Impl();
 
-  void scan() {
-    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group);
-    grid_scan_top<<<1, 1024, 0, stream>>>(group, ng);
+  // The last move's spilled cars into cells[cur] and counts (when a state
+  // read comes before the next step).
+  void flush() {
+    if (!fixup_pending) return;
+    grid_fixup_kernel<<<std::max(1u, std::min(1024u, (nb + 255) / 256)), 256, 0, stream>>>(spill, spill_n, nb,
+                                                                                          cells[cur], counts);
+    ++launches;
+    fixup_pending = false;
+  }
+
+  void scan(StepRec* zero) {
+    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group, pw, plocal);
+    grid_scan_top<<<1, 1024, 0, stream>>>(group, ng, pw, pgroup, zero);
   }
 
   void compact() {
+    flush();
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
     counts_valid = true;
-    scan();
+    scan(nullptr);
     grid_compact_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, local, group, xs, vs);
     CKG(cudaGetLastError());
     launches += 4;
@@ -424,21 +473,25 @@ struct GpuGrid::Impl {
   void step() {
     if (steps_done - drained >= kRecCap / 2) drain();
     const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
-    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, powmod(kA, 32), pw, steps_done};
-    CKG(cudaMemsetAsync(rec + (steps_done % kRecCap), 0, sizeof(StepRec), stream));
+    const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, 2 * powmod(kA, kGridTPB), pw, steps_done};
     if (!counts_valid) {  // after construction / set_state; later steps count as they move
+      flush();
       grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
       ++launches;
     }
-    scan();
-    grid_move2_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], local, group, g, rec, counts_next,
-                                                   spill, spill_n);
-    grid_fixup_kernel<<<std::max(1u, std::min(1024u, (nb + 255) / 256)), 256, 0, stream>>>(spill, spill_n, nb,
-                                                                                            cells[cur ^ 1], counts_next);
+    flush();  // the previous move's spilled cars
+    scan(rec + (steps_done % kRecCap));
+    if (vmax < 128)
+      grid_move3_kernel<true><<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], plocal, pgroup, g, rec,
+                                                           counts_next, spill, spill_n);
+    else
+      grid_move3_kernel<false><<<nb, kGridTPB, 0, stream>>>(cells[cur], cells[cur ^ 1], plocal, pgroup, g, rec,
+                                                            counts_next, spill, spill_n);
     CKG(cudaGetLastError());
-    launches += 4;
+    launches += 3;
     std::swap(counts, counts_next);
     counts_valid = true;
+    fixup_pending = true;
     cur ^= 1;
     ++steps_done;
   }
@@ -511,6 +564,8 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   d.ng = (d.nb + 1023) / 1024;
   CKG(cudaMalloc(&d.local, size_t(d.nb) * 4));
   CKG(cudaMalloc(&d.group, size_t(d.ng) * 4));
+  CKG(cudaMalloc(&d.plocal, size_t(d.nb) * 4));
+  CKG(cudaMalloc(&d.pgroup, size_t(d.ng) * 4));
   CKG(cudaMalloc(&d.xs, size_t(d.N) * 4));
   CKG(cudaMalloc(&d.vs, d.N));
   CKG(cudaMalloc(&d.rec, sizeof(StepRec) * kRecCap));
@@ -548,6 +603,8 @@ GpuGrid::Impl::~Impl() {
   cudaFree(spill_n);
   cudaFree(local);
   cudaFree(group);
+  cudaFree(plocal);
+  cudaFree(pgroup);
   cudaFree(xs);
   cudaFree(vs);
   cudaFree(rec);
@@ -582,6 +639,7 @@ void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   CKG(cudaMemcpyAsync(d.cells[d.cur], cells.data(), d.L, cudaMemcpyHostToDevice, d.stream));
   CKG(cudaStreamSynchronize(d.stream));
   d.counts_valid = false;
+  d.fixup_pending = false;  // the loaded state replaces the array
   d.sumv0 = s;
   d.sumv_host.clear();
   d.wraps_host.clear();
