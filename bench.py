@@ -24,9 +24,9 @@ value       device throughput, state resident in HBM: N*K / CUDA-event time
 e2e         the same metric through the C ABI with host buffers: set_state32
             from pinned host int32 arrays (BASELINE's state format),
             advance(K), the whole-ring mean-velocity series and the final
-            state (each rank: its segment) read back to host u64 arrays
-            (the reference's nasch_sim_state format), wall clock, max over
-            ranks
+            state (each rank: its segment) read back to pinned host int32
+            arrays (nasch_sim_state_segment32; nasch_sim_state is the same
+            call widened to u64), wall clock, max over ranks
 roofline    SURVEY.md 8(d): 16 algorithmic bytes per car-update (int32 x and
             v read and written once per step) x N*k updates per launch / the
             average duration of the timed region's k-step launches (k =
@@ -475,12 +475,10 @@ def c3_leg(args, d: Dist):
     eng2 = (nasch.Engine.distributed(prm2, d.rank, d.world, fresh_id()) if d.world > 1
             else nasch.Engine(prm2))
     first, count = eng2.shard_range()
-    # caller-owned output buffers, already faulted in (a serving loop reuses
-    # them; first-touch page faults are not the engine's cost)
-    outx = np.empty(count, np.uint64)
-    outv = np.empty(count, np.uint64)
-    outx.fill(0)  # np.zeros would leave the pages unmapped until the engine writes them
-    outv.fill(0)
+    # caller-owned output buffers in BASELINE's int32 format, page-locked
+    # like the input and already faulted in (a serving loop reuses them)
+    outx = torch.zeros(count, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    outv = torch.zeros(count, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     eng2.set_checksum(False)
     eng2.advance(0)
     d.barrier()
@@ -491,7 +489,7 @@ def c3_leg(args, d: Dist):
     eng2.advance(K)
     t_adv = time.perf_counter()
     mean_v = eng2.mean_velocity_series()  # whole ring (collective)
-    _, _, first_rank = eng2.segment_snapshot(out_x=outx, out_v=outv)
+    _, _, first_rank = eng2.segment_snapshot32(out_x=outx, out_v=outv)
     t1 = time.perf_counter()
     e2e_s = d.max(t1 - t0)
     parts = {"set_state": (t_set - t0) * 1e3, "advance": (t_adv - t_set) * 1e3,
@@ -503,9 +501,9 @@ def c3_leg(args, d: Dist):
            "d2h_bytes_per_step": ((4 + 1) * N + 8 * K * d.world) / K,  # final state + series
            "breakdown_ms_rank0": {k: round(t, 2) for k, t in parts.items()},
            "path": "nasch_sim_set_state32 (BASELINE's int32 state, pinned host arrays) + "
-                   "nasch_sim_advance(K) + whole-ring mean-velocity series + final state to host u64 "
-                   "(N=1: nasch_sim_state, the reference call; N>1: each rank nasch_sim_state_segment "
-                   "of its segment), wall clock, max over ranks"}
+                   "nasch_sim_advance(K) + whole-ring mean-velocity series + final state to pinned host "
+                   "int32 arrays (nasch_sim_state_segment32: N=1 the whole ring in rank order, N>1 each "
+                   "rank its own segment), wall clock, max over ranks"}
 
     # ---- roofline --------------------------------------------------------
     peak, peak_src = peaks()

@@ -134,6 +134,12 @@ nasch_status nasch_sim_set_state(nasch_sim* sim, const uint64_t* positions,
 nasch_status nasch_sim_set_state32(nasch_sim* sim, const uint32_t* positions,
                                    const uint32_t* velocities, size_t count);
 
+/* nasch_sim_state (reference nasch.h:115-118) into u32 arrays, BASELINE's
+ * int32 state format: half the host bytes of the u64 form; positions reach
+ * a page-locked array by DMA with no host pass.  Same rules otherwise. */
+nasch_status nasch_sim_state32(const nasch_sim* sim, uint32_t* positions,
+                               uint32_t* velocities, size_t capacity);
+
 /* nasch_sim_state (reference nasch.h:115-118) split in two: _async copies
  * the current state on the device and returns; the host transfer and
  * widening into the caller's arrays proceed while the caller advances the
@@ -232,6 +238,9 @@ unsigned nasch_sim_exchange_mode(const nasch_sim* sim);
 nasch_status nasch_sim_state_segment(nasch_sim* sim, uint64_t* positions,
                                      uint64_t* velocities, size_t capacity,
                                      uint64_t* first_rank);
+nasch_status nasch_sim_state_segment32(nasch_sim* sim, uint32_t* positions,
+                                       uint32_t* velocities, size_t capacity,
+                                       uint64_t* first_rank);
 nasch_status nasch_sim_state_segment_async(nasch_sim* sim, uint64_t* positions,
                                            uint64_t* velocities, size_t capacity,
                                            uint64_t* first_rank);

@@ -88,6 +88,8 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_sim_new_distributed": (C.c_int, [_P, C.c_uint, C.c_uint, C.c_void_p, C.POINTER(_P)]),
     "nasch_sim_shard_range": (C.c_int, [_P, _u64p, _u64p]),
     "nasch_sim_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
+    "nasch_sim_state_segment32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t, _u64p]),
+    "nasch_sim_state32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t]),
     "nasch_sim_state_segment_async": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
     "nasch_sim_set_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t]),
     # ensembles

@@ -49,6 +49,17 @@ class RingEngine {
   virtual void observables(double* density, double* mean_velocity, double* flow) = 0;
   // Rank (increasing position) order, widened to u64; either may be null.
   virtual void state(uint64_t* positions, uint64_t* velocities) = 0;
+  // Extension: the same snapshot as u32 arrays (BASELINE's int32 state
+  // format; nasch_sim_state32).  Default: through u64 and narrowed.
+  virtual void state32(uint32_t* positions, uint32_t* velocities) {
+    const size_t n = params().car_count;
+    std::vector<uint64_t> x(positions ? n : 0), v(velocities ? n : 0);
+    state(positions ? x.data() : nullptr, velocities ? v.data() : nullptr);
+    for (size_t i = 0; i < n; ++i) {
+      if (positions) positions[i] = static_cast<uint32_t>(x[i]);
+      if (velocities) velocities[i] = static_cast<uint32_t>(v[i]);
+    }
+  }
   // Extension: the same snapshot, returned before the host-side copy and
   // widening are done (they overlap the caller's next advance); the output
   // arrays are complete after state_wait().  Default: synchronous.
@@ -64,6 +75,17 @@ class RingEngine {
   }
   virtual void state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {
     state_segment(positions, velocities, first_rank);
+  }
+  // u32 form of state_segment.  Default: through u64 and narrowed.
+  virtual void state_segment32(uint32_t* positions, uint32_t* velocities, uint64_t* first_rank) {
+    uint64_t first = 0, count = 0;
+    shard_range(&first, &count);
+    std::vector<uint64_t> x(positions ? count : 0), v(velocities ? count : 0);
+    state_segment(positions ? x.data() : nullptr, velocities ? v.data() : nullptr, first_rank);
+    for (size_t i = 0; i < count; ++i) {
+      if (positions) positions[i] = static_cast<uint32_t>(x[i]);
+      if (velocities) velocities[i] = static_cast<uint32_t>(v[i]);
+    }
   }
   // Extension: set_state from this process's segment only (the ids of
   // shard_range in the new rank order); the whole ring elsewhere.
@@ -105,6 +127,11 @@ class GpuRing : public RingEngine {
   const SimParams& params() const override;
   void observables(double* density, double* mean_velocity, double* flow) override;
   void state(uint64_t* positions, uint64_t* velocities) override;
+  void state32(uint32_t* positions, uint32_t* velocities) override;
+  void state_segment32(uint32_t* positions, uint32_t* velocities, uint64_t* first_rank) override {
+    state32(positions, velocities);
+    if (first_rank) *first_rank = 0;
+  }
   void state_async(uint64_t* positions, uint64_t* velocities) override;
   void state_wait() override;
   size_t sumv_series(uint64_t* out, size_t cap) override;

@@ -101,6 +101,10 @@ void widen_u8_scalar(const uint8_t* src, uint64_t* dst, size_t n) {
   for (size_t i = 0; i < n; ++i) dst[i] = src[i];
 }
 
+void widen_u8_u32_scalar(const uint8_t* src, uint32_t* dst, size_t n) {
+  for (size_t i = 0; i < n; ++i) dst[i] = src[i];
+}
+
 #if defined(__x86_64__)
 bool have_avx512() {
   static const bool ok = __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512bw");
@@ -134,6 +138,20 @@ __attribute__((target("avx512f,avx512bw"))) void widen_u8_avx512(const uint8_t* 
     const __m128i s = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
     _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), _mm512_cvtepu8_epi64(s));
     _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i + 8), _mm512_cvtepu8_epi64(_mm_srli_si128(s, 8)));
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
+
+__attribute__((target("avx512f,avx512bw"))) void widen_u8_u32_avx512(const uint8_t* src, uint32_t* dst, size_t n) {
+  size_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 63u)) {
+    dst[i] = src[i];
+    ++i;
+  }
+  for (; i + 16 <= n; i += 16) {
+    const __m128i s = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    _mm512_stream_si512(reinterpret_cast<__m512i*>(dst + i), _mm512_cvtepu8_epi32(s));
   }
   for (; i < n; ++i) dst[i] = src[i];
   _mm_sfence();
@@ -217,6 +235,13 @@ void widen_u32(const uint32_t* src, uint64_t* dst, size_t n) {
   if (have_avx512() && n >= 64) return widen_u32_avx512(src, dst, n);
 #endif
   widen_u32_scalar(src, dst, n);
+}
+
+void widen_u8_u32(const uint8_t* src, uint32_t* dst, size_t n) {
+#if defined(__x86_64__)
+  if (have_avx512() && n >= 64) return widen_u8_u32_avx512(src, dst, n);
+#endif
+  widen_u8_u32_scalar(src, dst, n);
 }
 
 void widen_u8(const uint8_t* src, uint64_t* dst, size_t n) {

@@ -14,6 +14,8 @@ namespace nb200 {
 // dst[i] = src[i] for i < n.
 void widen_u32(const uint32_t* src, uint64_t* dst, size_t n);
 void widen_u8(const uint8_t* src, uint64_t* dst, size_t n);
+// dst[i] = src[i] (u8 velocities into the u32 arrays of nasch_sim_state32).
+void widen_u8_u32(const uint8_t* src, uint32_t* dst, size_t n);
 
 // Narrows rank-ordered u64 input into (x32, v) and validates it exactly as
 // the scalar rules of load_state: returns 0, or the first violated rule

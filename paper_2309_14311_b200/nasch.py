@@ -58,12 +58,12 @@ def _u32p(a):
     return a.ctypes.data_as(C.POINTER(C.c_uint32))
 
 
-def _out_u64(a, n: int, name: str):
+def _out_u64(a, n: int, name: str, dtype=np.uint64):
     """A caller-supplied output array must be a writable, C-contiguous u64
-    vector of at least n elements: the C ABI writes n values through the
-    raw pointer."""
-    if not isinstance(a, np.ndarray) or a.dtype != np.uint64 or a.ndim != 1:
-        raise TypeError(f"{name} must be a 1-D numpy uint64 array")
+    (or, for the 32-bit calls, u32) vector of at least n elements: the C ABI
+    writes n values through the raw pointer."""
+    if not isinstance(a, np.ndarray) or a.dtype != dtype or a.ndim != 1:
+        raise TypeError(f"{name} must be a 1-D numpy {np.dtype(dtype).name} array")
     if not a.flags.c_contiguous or not a.flags.writeable:
         raise ValueError(f"{name} must be C-contiguous and writable")
     if len(a) < n:
@@ -217,6 +217,14 @@ class Engine:
         _check(_lib().nasch_sim_state(self._h, _u64p(x), _u64p(v), min(len(x), len(v))))
         return x, v
 
+    def snapshot32(self, *, out_x=None, out_v=None):
+        """The same snapshot as u32 arrays (BASELINE's int32 state format,
+        nasch_sim_state32): positions reach a page-locked out_x by DMA."""
+        x = np.empty(self.ncars, np.uint32) if out_x is None else _out_u64(out_x, self.ncars, "out_x", np.uint32)
+        v = np.empty(self.ncars, np.uint32) if out_v is None else _out_u64(out_v, self.ncars, "out_v", np.uint32)
+        _check(_lib().nasch_sim_state32(self._h, _u32p(x), _u32p(v), min(len(x), len(v))))
+        return x, v
+
     def snapshot_async(self, out_x, out_v) -> None:
         """Start a snapshot into (out_x, out_v) (u64, length ncars) that
         completes while the caller advances; call snapshot_wait() before
@@ -238,6 +246,16 @@ class Engine:
         first = C.c_uint64()
         _check(_lib().nasch_sim_state_segment(self._h, _u64p(x), _u64p(v), min(len(x), len(v)),
                                               C.byref(first)))
+        return x, v, first.value
+
+    def segment_snapshot32(self, *, out_x=None, out_v=None):
+        """segment_snapshot into u32 arrays (nasch_sim_state_segment32)."""
+        _, count = self.shard_range()
+        x = np.empty(count, np.uint32) if out_x is None else _out_u64(out_x, count, "out_x", np.uint32)
+        v = np.empty(count, np.uint32) if out_v is None else _out_u64(out_v, count, "out_v", np.uint32)
+        first = C.c_uint64()
+        _check(_lib().nasch_sim_state_segment32(self._h, _u32p(x), _u32p(v), min(len(x), len(v)),
+                                                C.byref(first)))
         return x, v, first.value
 
     def segment_snapshot_async(self, out_x, out_v) -> int:

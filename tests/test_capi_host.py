@@ -91,6 +91,8 @@ def test_null_arguments(lib):  # test_capi.cpp:92-103
     assert lib.nasch_sim_state_segment(None, None, None, 0, None) == capi.NASCH_ERR_INVALID
     assert lib.nasch_sim_state_segment_async(None, None, None, 0, None) == capi.NASCH_ERR_INVALID
     assert lib.nasch_sim_set_state_segment(None, None, None, 0) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_state32(None, None, None, 0) == capi.NASCH_ERR_INVALID
+    assert lib.nasch_sim_state_segment32(None, None, None, 0, None) == capi.NASCH_ERR_INVALID
     assert lib.nasch_ensemble_set_state_all32(None, None, None, 0) == capi.NASCH_ERR_INVALID
     assert lib.nasch_sim_state_wait(None) == capi.NASCH_ERR_INVALID
     assert lib.nasch_sim_exchange_mode(None) == 0

@@ -624,6 +624,43 @@ def test_async_snapshots_match_sync(port):
         assert (x == want[0]).all() and (v == want[1]).all()
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+def test_state32_equals_u64_snapshot(pinned):
+    """nasch_sim_state32 / _segment32 (BASELINE's int32 format; positions
+    DMA'd straight into a page-locked array): the same rank-ordered state as
+    nasch_sim_state at a rank offset inside the ring (two id pieces) and
+    across 16M-car chunks, for u8 and u32 velocities, the temporal-blocked,
+    distributed-resident and small-ring engines and the grid engine;
+    capacity below the car count is refused."""
+    import torch
+
+    def out(n):
+        if not pinned:
+            return np.full(n, 7, np.uint32)
+        t = torch.full((n,), 7, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        return t
+
+    cases = [(40_000_000, 17_000_011, 5, nasch.Engine.AGENT), (2_000_000, 600_000, 5, nasch.Engine.AGENT),
+             (60_000, 20_000, 5, nasch.Engine.AGENT), (1000, 200, 5, nasch.Engine.AGENT),
+             (200_000, 70_000, 300, nasch.Engine.AGENT), (300_000, 50_000, 5, nasch.Engine.GRID_REFERENCE)]
+    for L, N, vmax, kind in cases:
+        x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, 5), 5)
+        e = nasch.Engine(params(L, N, vmax, 0.3, 40, 6), 1, kind)
+        e.set_checksum(False)
+        e.set_state(x0, v0)
+        e.advance(37)
+        x, v = e.snapshot()
+        assert (np.diff(x.astype(np.int64)) > 0).all()
+        ox, ov = out(N), out(N)
+        x32, v32 = e.snapshot32(out_x=ox, out_v=ov)
+        assert x32 is ox and (x32 == x).all() and (v32 == v).all(), (L, N, kind)
+        sx, sv, first = e.segment_snapshot32(out_x=out(N), out_v=out(N))
+        assert first == 0 and (sx == x).all() and (sv == v).all()
+        with pytest.raises(ValueError):
+            e.snapshot32(out_x=out(N - 1), out_v=out(N))
+        e.close()
+
+
 def test_set_state_validation_rules_and_order():
     """set_state rejects each rule at every position of the vectorised
     narrowing (first car, inside an 8-car group, group boundary, tail) with
