@@ -104,6 +104,8 @@ struct GpuRing::Impl {
   uint32_t* blkpow1 = nullptr;
   uint32_t* thrpow1 = nullptr;
   bool plan_stale = false;  // one-step launches ran since the last TB plan
+  unsigned long long* dcode = nullptr;  // set_state32: first position-rule violation (device)
+  unsigned long long* hcode = nullptr;  // ... its pinned host copy
   Ctl* ctl = nullptr;
   StepRec* rec = nullptr;
   unsigned long long* dsum = nullptr;
@@ -666,29 +668,54 @@ struct GpuRing::Impl {
       direct_x = cudaPointerGetAttributes(&pa, hx_in) == cudaSuccess && pa.type == cudaMemoryTypeHost;
       cudaGetLastError();
     }
-    // Page-locked u32 positions need no host pass before the copy: all of
-    // them are queued at once, so their DMA (the bulk of the bytes) runs
-    // while the host validates; each chunk's narrowed velocities follow.
-    if (direct_x) {
-      if constexpr (std::is_same<T, uint32_t>::value)
+    // Page-locked u32 positions never pass through the host: all of them
+    // are queued for DMA at once and validated on the device (rules 1-2);
+    // the host only narrows and checks the velocities (rules 3-4) chunk by
+    // chunk behind them, and the earliest violation of either wins.  Host
+    // memory traffic: 2.0 GB instead of 2.8 GB on BASELINE config 3.
+    if constexpr (std::is_same<T, uint32_t>::value) {
+      if (direct_x) {
         CK(cudaMemcpyAsync(x[dst], hx_in, size_t(n) * 4, cudaMemcpyHostToDevice, stream));
+        if (!dcode) {
+          CK(cudaMalloc(&dcode, sizeof(unsigned long long)));
+          CK(cudaMallocHost(&hcode, sizeof(unsigned long long)));
+        }
+        CK(cudaMemsetAsync(dcode, 0xff, sizeof(unsigned long long), stream));
+        validate_positions_kernel<<<148 * 8, 256, 0, stream>>>(x[dst], n, L, dcode);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(hcode, dcode, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+        std::atomic<unsigned long long> vcode{~0ull};
+        for (size_t c0 = 0; c0 < n && vcode.load() == ~0ull; c0 += kChunk) {
+          const size_t c1 = std::min<size_t>(n, c0 + kChunk);
+          parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
+            const uint64_t c = narrow_v32(hv_in, c0 + a, c0 + b, params.v_max, vlim, hv, vbytes);
+            unsigned long long cur_min = vcode.load();
+            while (c < cur_min && !vcode.compare_exchange_weak(cur_min, c)) {
+            }
+          });
+          CK(cudaMemcpyAsync(static_cast<char*>(v[dst]) + c0 * vbytes, static_cast<char*>(hv) + c0 * vbytes,
+                             (c1 - c0) * vbytes, cudaMemcpyHostToDevice, stream));
+        }
+        CK(cudaStreamSynchronize(stream));
+        const unsigned long long code = std::min<unsigned long long>(*hcode, vcode.load());
+        if (code != ~0ull) err.store(static_cast<int>(code & 3u) + 1);
+      }
     }
-    for (size_t c0 = 0; c0 < n && !err.load(); c0 += kChunk) {
+    for (size_t c0 = 0; c0 < n && !err.load() && !direct_x; c0 += kChunk) {
       const size_t c1 = std::min<size_t>(n, c0 + kChunk);
       parallel_chunks(c1 - c0, [&](size_t a, size_t b) {
         int e = 0;
         if constexpr (std::is_same<T, uint64_t>::value) {
           e = narrow_validate(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, hx, hv, vbytes);
         } else {
-          e = narrow_validate32(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, direct_x ? nullptr : hx, hv,
-                                vbytes);
+          e = narrow_validate32(hx_in, hv_in, c0 + a, c0 + b, L, params.v_max, vlim, hx, hv, vbytes);
         }
         if (e) {
           int expected = 0;
           err.compare_exchange_strong(expected, e);
         }
       });
-      if (!direct_x) CK(cudaMemcpyAsync(x[dst] + c0, hx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, stream));
+      CK(cudaMemcpyAsync(x[dst] + c0, hx + c0, (c1 - c0) * 4, cudaMemcpyHostToDevice, stream));
       CK(cudaMemcpyAsync(static_cast<char*>(v[dst]) + c0 * vbytes, static_cast<char*>(hv) + c0 * vbytes,
                          (c1 - c0) * vbytes, cudaMemcpyHostToDevice, stream));
     }
@@ -976,6 +1003,8 @@ GpuRing::Impl::~Impl() {
   cudaFree(thrpow);
   cudaFree(blkpow1);
   cudaFree(thrpow1);
+  cudaFree(dcode);
+  cudaFreeHost(hcode);
   cudaFree(dplans);
   cudaFree(dsync);
   cudaFree(dmbox);

@@ -333,6 +333,56 @@ int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, 
   return 0;
 }
 
+#if defined(__x86_64__)
+__attribute__((target("avx512f,avx512bw"))) uint64_t narrow_v32_avx512(const uint32_t* v, size_t lo, size_t hi,
+                                                                      uint32_t vmax, uint32_t vlim, void* vout,
+                                                                      int vbytes) {
+  const __m512i vVmax = _mm512_set1_epi32(static_cast<int>(vmax));
+  const __m512i vVlim = _mm512_set1_epi32(static_cast<int>(vlim));
+  auto scalar = [&](size_t k) -> uint64_t {
+    if (v[k] > vmax) return 4 * uint64_t(k) + 2;
+    if (v[k] > vlim) return 4 * uint64_t(k) + 3;
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[k] = static_cast<uint8_t>(v[k]);
+    else static_cast<uint32_t*>(vout)[k] = v[k];
+    return ~0ull;
+  };
+  size_t i = lo;
+  for (; i < hi && (i & 15u); ++i)
+    if (const uint64_t c = scalar(i); c != ~0ull) return c;
+  for (; i + 16 <= hi; i += 16) {
+    const __m512i vs = _mm512_loadu_si512(reinterpret_cast<const void*>(v + i));
+    if (_mm512_cmpgt_epu32_mask(vs, vVmax) | _mm512_cmpgt_epu32_mask(vs, vVlim)) {
+      for (size_t k = i; k < i + 16; ++k)
+        if (const uint64_t c = scalar(k); c != ~0ull) return c;
+    }
+    if (vbytes == 1) {
+      _mm_stream_si128(reinterpret_cast<__m128i*>(static_cast<uint8_t*>(vout) + i), _mm512_cvtepi32_epi8(vs));
+    } else {
+      _mm512_storeu_si512(reinterpret_cast<void*>(static_cast<uint32_t*>(vout) + i), vs);
+    }
+  }
+  for (; i < hi; ++i)
+    if (const uint64_t c = scalar(i); c != ~0ull) return c;
+  _mm_sfence();
+  return ~0ull;
+}
+#endif
+
+uint64_t narrow_v32(const uint32_t* v, size_t lo, size_t hi, uint64_t vmax, uint64_t vlim, void* vout, int vbytes) {
+  const uint32_t vmax32 = static_cast<uint32_t>(vmax > 0xffffffffull ? 0xffffffffull : vmax);
+  const uint32_t vlim32 = static_cast<uint32_t>(vlim > 0xffffffffull ? 0xffffffffull : vlim);
+#if defined(__x86_64__)
+  if (have_avx512()) return narrow_v32_avx512(v, lo, hi, vmax32, vlim32, vout, vbytes);
+#endif
+  for (size_t i = lo; i < hi; ++i) {
+    if (v[i] > vmax32) return 4 * uint64_t(i) + 2;
+    if (v[i] > vlim32) return 4 * uint64_t(i) + 3;
+    if (vbytes == 1) static_cast<uint8_t*>(vout)[i] = static_cast<uint8_t>(v[i]);
+    else static_cast<uint32_t*>(vout)[i] = v[i];
+  }
+  return ~0ull;
+}
+
 unsigned host_threads() { return HostPool::get().size(); }
 
 void host_run(unsigned count, std::function<void(unsigned)> job) { HostPool::get().run(count, std::move(job)); }

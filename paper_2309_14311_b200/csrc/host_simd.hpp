@@ -30,6 +30,11 @@ int narrow_validate(const uint64_t* x, const uint64_t* v, size_t lo, size_t hi, 
 int narrow_validate32(const uint32_t* x, const uint32_t* v, size_t lo, size_t hi, uint64_t L, uint64_t vmax,
                       uint64_t vlim, uint32_t* x32, void* vout, int vbytes);
 
+// Velocities only (set_state32 with page-locked positions, which the device
+// validates): narrows v[lo, hi) into vout and returns 4 i + (rule - 1) of the
+// first violation (rule 3: v > vmax, 4: v > vlim), or UINT64_MAX.
+uint64_t narrow_v32(const uint32_t* v, size_t lo, size_t hi, uint64_t vmax, uint64_t vlim, void* vout, int vbytes);
+
 // Persistent host worker pool (host_simd.cpp): job(i) for i in [0, count)
 // on the pool's threads and the caller; returns when all are done.
 unsigned host_threads();

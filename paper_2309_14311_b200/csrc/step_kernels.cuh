@@ -583,6 +583,23 @@ __global__ void init_state_kernel(uint32_t* x, VT* v, uint32_t n, uint32_t npad,
   }
 }
 
+// set_state32's position rules on the device (the positions are uploaded
+// straight from the caller's page-locked array, so the host never reads
+// them): the first violation as 4 i + (rule - 1), rule 1 x >= L, rule 2 not
+// strictly increasing (host: src/model.cpp / acceptance.cpp:118-123 order).
+static __global__ void validate_positions_kernel(const uint32_t* __restrict__ x, uint32_t n, uint32_t L,
+                                          unsigned long long* code) {
+  unsigned long long best = ~0ull;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t xi = __ldg(x + i);
+    if (xi >= L) best = min(best, 4ull * i);
+    else if (i && __ldg(x + i - 1) >= xi) best = min(best, 4ull * i + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(code, best);
+}
+
 // Exact velocity sum of the current state (observables at step 0).
 template <typename VT>
 __global__ void sum_velocity_kernel(const VT* v, uint32_t n, unsigned long long* out) {
