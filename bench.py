@@ -484,26 +484,37 @@ def c3_leg(args, d: Dist):
     d.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    eng2.set_state(xin, vin)  # each rank validates and uploads its own segment
-    t_set = time.perf_counter()
-    eng2.advance(K)
-    t_adv = time.perf_counter()
-    mean_v = eng2.mean_velocity_series()  # whole ring (collective)
-    _, _, first_rank = eng2.segment_snapshot32(out_x=outx, out_v=outv)
+    if d.world == 1:
+        # one call: nasch_sim_job32 streams the upload, the steps and the
+        # download by ranges of the ring when K fits one K-step launch (the
+        # three calls below otherwise, inside the library)
+        eng2.job32(xin, vin, K, out_x=outx, out_v=outv)
+        t_set = t_adv = time.perf_counter()
+        mean_v = eng2.mean_velocity_series()
+    else:
+        eng2.set_state(xin, vin)  # each rank validates and uploads its own segment
+        t_set = time.perf_counter()
+        eng2.advance(K)
+        t_adv = time.perf_counter()
+        mean_v = eng2.mean_velocity_series()  # whole ring (collective)
+        eng2.segment_snapshot32(out_x=outx, out_v=outv)
     t1 = time.perf_counter()
     e2e_s = d.max(t1 - t0)
-    parts = {"set_state": (t_set - t0) * 1e3, "advance": (t_adv - t_set) * 1e3,
-             "series+state": (t1 - t_adv) * 1e3}
+    parts = ({"job32 (set_state + advance + state, streamed)": (t_set - t0) * 1e3, "series": (t1 - t_set) * 1e3}
+             if d.world == 1 else
+             {"set_state": (t_set - t0) * 1e3, "advance": (t_adv - t_set) * 1e3,
+              "series+state": (t1 - t_adv) * 1e3})
     assert len(mean_v) == K
     eng2.close()
     e2e = {"value": N * K / e2e_s, "unit": "car-updates/s",
            "h2d_bytes_per_step": (4 + 1) * N / K,        # u32 x + u8 v per car, all segments
            "d2h_bytes_per_step": ((4 + 1) * N + 8 * K * d.world) / K,  # final state + series
            "breakdown_ms_rank0": {k: round(t, 2) for k, t in parts.items()},
-           "path": "nasch_sim_set_state32 (BASELINE's int32 state, pinned host arrays) + "
-                   "nasch_sim_advance(K) + whole-ring mean-velocity series + final state to pinned host "
-                   "int32 arrays (nasch_sim_state_segment32: N=1 the whole ring in rank order, N>1 each "
-                   "rank its own segment), wall clock, max over ranks"}
+           "path": "N=1: nasch_sim_job32 (set_state32 from BASELINE's int32 state in pinned host arrays + "
+                   "advance(K) + final state to pinned host int32 arrays in rank order, upload / steps / "
+                   "download streamed by ranges of the ring when K <= 32) + the mean-velocity series; N>1: "
+                   "each rank nasch_sim_set_state32 of its segment + nasch_sim_advance(K) + the whole-ring "
+                   "series + nasch_sim_state_segment32; wall clock, max over ranks"}
 
     # ---- roofline --------------------------------------------------------
     peak, peak_src = peaks()

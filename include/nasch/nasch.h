@@ -140,6 +140,18 @@ nasch_status nasch_sim_set_state32(nasch_sim* sim, const uint32_t* positions,
 nasch_status nasch_sim_state32(const nasch_sim* sim, uint32_t* positions,
                                uint32_t* velocities, size_t capacity);
 
+/* One job end to end: nasch_sim_set_state32(positions_in, velocities_in,
+ * count) + nasch_sim_advance(steps) + nasch_sim_state32(positions_out,
+ * velocities_out, capacity), with the same results, series and errors as
+ * the three calls (a rejected input leaves the simulation as it was).  With
+ * page-locked arrays and steps within one temporal-blocked launch the
+ * upload, the steps and the download overlap by ranges of the ring; the
+ * three calls otherwise.  Either output may be NULL. */
+nasch_status nasch_sim_job32(nasch_sim* sim, const uint32_t* positions_in,
+                             const uint32_t* velocities_in, size_t count,
+                             uint64_t steps, uint32_t* positions_out,
+                             uint32_t* velocities_out, size_t capacity);
+
 /* nasch_sim_state (reference nasch.h:115-118) split in two: _async copies
  * the current state on the device and returns; the host transfer and
  * widening into the caller's arrays proceed while the caller advances the

@@ -90,6 +90,7 @@ SIGNATURES: dict[str, tuple] = {
     "nasch_sim_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
     "nasch_sim_state_segment32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t, _u64p]),
     "nasch_sim_state32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t]),
+    "nasch_sim_job32": (C.c_int, [_P, _u32p, _u32p, C.c_size_t, _u64, _u32p, _u32p, C.c_size_t]),
     "nasch_sim_state_segment_async": (C.c_int, [_P, _u64p, _u64p, C.c_size_t, _u64p]),
     "nasch_sim_set_state_segment": (C.c_int, [_P, _u64p, _u64p, C.c_size_t]),
     # ensembles

@@ -17,6 +17,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <exception>
@@ -104,6 +106,11 @@ struct GpuRing::Impl {
   uint32_t* blkpow1 = nullptr;
   uint32_t* thrpow1 = nullptr;
   bool plan_stale = false;  // one-step launches ran since the last TB plan
+  // streamed job (job32): the input state's own buffers, streams, events
+  uint32_t* jx = nullptr;
+  void* jv = nullptr;
+  cudaStream_t jstream[3] = {nullptr, nullptr, nullptr};  // x upload, v upload, download
+  Ctl* jctl = nullptr;  // pinned: the control block after the job's plan
   unsigned long long* dcode = nullptr;  // set_state32: first position-rule violation (device)
   unsigned long long* hcode = nullptr;  // ... its pinned host copy
   Ctl* ctl = nullptr;
@@ -643,6 +650,247 @@ struct GpuRing::Impl {
     hash = h;
   }
 
+  // ---- streamed end-to-end job (nasch_sim_job32) -----------------------
+  // set_state32(xin, vin) + advance(k) + state32(xout, vout) for k <= K (one
+  // temporal-blocked launch) with page-locked arrays, overlapped by ranges
+  // of the ring: the positions upload on one stream and the narrowed
+  // velocities on another, chunk by chunk; the launch runs as kJobChunks
+  // range launches (nasch_tb_range_kernel), range c as soon as chunks c and
+  // c+1 (its halo) have landed; each range's cars go back on a third stream
+  // into their rank order (the final rank offset is known from the origin-
+  // cone plan, computed once chunk 0 and the last chunk are up).  The input
+  // lives in its own buffers (jx, jv) until the job validated, so a
+  // rejected input leaves the ring as it was; the rules and their order are
+  // set_state32's (positions on the device, velocities on the host).
+  // Returns false when the streamed form does not apply (the caller then
+  // runs the three calls).
+  static constexpr uint32_t kJobChunks = 8;
+  bool job32(const uint32_t* xin, const uint32_t* vin, uint64_t steps, uint32_t* xout, uint32_t* vout) {
+    const uint64_t k64 = std::min<uint64_t>(steps, params.steps - steps_done);
+    auto pinned = [](const void* p) {
+      cudaPointerAttributes pa{};
+      const bool ok = p && cudaPointerGetAttributes(&pa, p) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+      cudaGetLastError();
+      return ok;
+    };
+    if (!jx || checksum_on || params.output_mode != OutputMode::none || k64 == 0 || k64 > K ||
+        !pinned(xin) || !pinned(xout) || !vin || !vout)
+      return false;
+    const uint32_t k = static_cast<uint32_t>(k64);
+    drain();
+    snap_join();
+    if (plan_stale) replan();  // (the saved control block below must be current)
+    CK(cudaStreamSynchronize(stream));
+
+    const int cur = static_cast<int>(buf_host);
+    CK(cudaMemcpy(hctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    const Ctl saved = *hctl;  // restored if the input is rejected
+    RingArgs ja = args;       // reads the job's input buffers, writes the idle ping-pong buffer
+    ja.x[cur] = jx;
+    ja.v[cur] = jv;
+    const uint32_t ntiles = (n + kTbStore - 1) / kTbStore;
+    const uint32_t tpc = (ntiles + kJobChunks - 1) / kJobChunks;  // tiles per chunk
+    const uint32_t nch = (ntiles + tpc - 1) / tpc;
+    auto cfirst = [&](uint32_t c) { return std::min<uint64_t>(uint64_t(c) * tpc * kTbStore, n); };
+    std::vector<cudaEvent_t> ev;
+    const bool trace = std::getenv("NASCH_B200_JOB_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    cudaEvent_t t_start = nullptr;
+    const auto host_t0 = std::chrono::steady_clock::now();
+    auto host_ms = [&] {
+      return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+    };
+    if (trace) {
+      CK(cudaEventCreate(&t_start));
+      CK(cudaEventRecord(t_start, stream));
+    }
+    auto event = [&](cudaStream_t st) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, trace ? cudaEventDefault : cudaEventDisableTiming));
+      CK(cudaEventRecord(e, st));
+      ev.push_back(e);
+      if (trace) tev.emplace_back(st == jstream[0] ? "x_up" : st == jstream[1] ? "v_up" : st == jstream[2] ? "down" : "comp", e);
+      return e;
+    };
+    // upload order: chunk 0 and the last chunk first (the origin cone needs
+    // the first K and the last K vmax ids), then the rest in order
+    std::vector<cudaEvent_t> eup(nch), ecomp(nch), edown(nch);
+    const uint64_t vlim = std::min<uint64_t>(params.v_max, vmax_eff);
+    std::atomic<unsigned long long> vcode{~0ull};
+    auto narrow_up = [&](uint32_t c) {
+      const uint64_t a = cfirst(c), b = cfirst(c + 1);
+      parallel_chunks(b - a, [&](size_t lo, size_t hi) {
+        const uint64_t code = narrow_v32(vin, a + lo, a + hi, params.v_max, vlim, hv, vbytes);
+        unsigned long long m = vcode.load();
+        while (code < m && !vcode.compare_exchange_weak(m, code)) {
+        }
+      });
+      // one upload stream, chunk after chunk (H2D copies of two streams
+      // measured serialised: the velocities only moved after every position)
+      CK(cudaMemcpyAsync(jx + a, xin + a, (b - a) * 4, cudaMemcpyHostToDevice, jstream[0]));
+      CK(cudaMemcpyAsync(static_cast<char*>(jv) + a * vbytes, static_cast<char*>(hv) + a * vbytes,
+                         (b - a) * vbytes, cudaMemcpyHostToDevice, jstream[0]));
+      eup[c] = event(jstream[0]);
+    };
+    auto wait_chunk = [&](uint32_t c) { CK(cudaStreamWaitEvent(stream, eup[c], 0)); };
+    // the control block for the loaded state (W = 0), cleared records, the
+    // origin-cone plan from chunk 0 and the last chunk
+    narrow_up(0);
+    if (nch > 1) narrow_up(nch - 1);
+    wait_chunk(0);
+    if (nch > 1) wait_chunk(nch - 1);
+    {
+      Ctl c{};
+      c.t = steps_done;
+      c.W = 0;
+      c.buf = static_cast<unsigned int>(cur);
+      c.E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, n, 0)));
+      c.E2 = mulmod(c.E, args.an_inv);
+      *hctl = c;
+      CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+      CK(cudaMemsetAsync(rec, 0, sizeof(StepRec) * kRecCap, stream));
+      if (vbytes == 1) cone_init_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(ja);
+      else cone_init_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(ja);
+      CK(cudaGetLastError());
+      ++launches;
+      CK(cudaMemcpyAsync(jctl, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+    }
+    cudaEvent_t eplan = event(stream);
+    // range launches, each once its chunk and the next have landed
+    const int rgrid_max = grid;
+    auto launch_range = [&](uint32_t c) {
+      TbRange rg{};
+      rg.tile0 = c * tpc;
+      rg.tile_end = std::min(ntiles, (c + 1) * tpc);
+      const uint32_t gr = std::max<uint32_t>(1, std::min<uint32_t>(rg.tile_end - rg.tile0, rgrid_max));
+      rg.gpow = powmod(kA, uint64_t(gr) * kTbStore);
+      rg.a_tile0 = powmod(kA, uint64_t(rg.tile0) * kTbStore);
+      rg.epi = c + 1 == nch ? 1u : 0u;
+      if (vbytes == 1)
+        nasch_tb_range_kernel<uint8_t, kTbTPB, kTbCPT, kTbHalo, kTbWT><<<gr, kTbTPB, 0, stream>>>(ja, k, rg);
+      else
+        nasch_tb_range_kernel<uint32_t, kTbTPB, kTbCPT, kTbHalo, kTbWT><<<gr, kTbTPB, 0, stream>>>(ja, k, rg);
+      CK(cudaGetLastError());
+      ++launches;
+      ecomp[c] = event(stream);
+    };
+    // downloads: once the plan has given the final rank offset
+    bool have_head = false;
+    uint32_t head_f = 0, W_f = 0;
+    uint32_t next_down = 0, launched = 0;
+    auto try_head = [&](bool block) {
+      if (have_head) return;
+      if (!block && cudaEventQuery(eplan) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+      }
+      CK(cudaEventSynchronize(eplan));
+      uint64_t w = uint64_t(jctl->Wk[k - 1]) + jctl->ck[k - 1];
+      if (w >= n) w -= n;
+      W_f = static_cast<uint32_t>(w);
+      head_f = (n - W_f) % n;
+      have_head = true;
+    };
+    // [a, b) of ids -> up to two rank pieces (r0, id0, m)
+    auto pieces_of = [&](uint64_t a, uint64_t b, auto&& fn) {
+      if (a >= b) return;
+      if (a >= head_f) fn(a - head_f, a, b - a);
+      else if (b <= head_f) fn(a + n - head_f, a, b - a);
+      else {
+        fn(a + n - head_f, a, head_f - a);
+        fn(0, head_f, b - head_f);
+      }
+    };
+    const int dst = cur ^ 1;
+    auto issue_downloads = [&]() {
+      for (; next_down < launched; ++next_down) {
+        const uint32_t c = next_down;
+        CK(cudaStreamWaitEvent(jstream[2], ecomp[c], 0));
+        pieces_of(cfirst(c), cfirst(c + 1), [&](uint64_t r0, uint64_t id0, uint64_t m) {
+          CK(cudaMemcpyAsync(reinterpret_cast<char*>(hx) + r0 * vbytes, static_cast<const char*>(v[dst]) + id0 * vbytes,
+                             m * vbytes, cudaMemcpyDeviceToHost, jstream[2]));
+        });
+        pieces_of(cfirst(c), cfirst(c + 1), [&](uint64_t r0, uint64_t id0, uint64_t m) {
+          CK(cudaMemcpyAsync(xout + r0, x[dst] + id0, m * 4, cudaMemcpyDeviceToHost, jstream[2]));
+        });
+        edown[c] = event(jstream[2]);
+      }
+    };
+    for (uint32_t c = 1; c + 1 < nch; ++c) {
+      narrow_up(c);
+      wait_chunk(c);
+      launch_range(c - 1);
+      ++launched;
+      try_head(false);
+      if (have_head) issue_downloads();
+    }
+    if (nch > 1) {
+      launch_range(nch - 2);  // its halo is the last chunk's start (up)
+      ++launched;
+    }
+    launch_range(nch - 1);  // the wrap tiles read chunk 0; the epilogue
+    ++launched;
+    // the position rules over the whole input (velocities: vcode above)
+    CK(cudaMemsetAsync(dcode, 0xff, sizeof(unsigned long long), stream));
+    validate_positions_kernel<<<148 * 8, 256, 0, stream>>>(jx, n, L, dcode);
+    CK(cudaGetLastError());
+    ++launches;
+    CK(cudaMemcpyAsync(hcode, dcode, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+    cudaEvent_t evalid = event(stream);
+    try_head(true);
+    issue_downloads();
+    // widen each chunk's velocities into rank order as it lands
+    cudaError_t err = cudaSuccess;
+    for (uint32_t c = 0; c < nch; ++c) {
+      if (err == cudaSuccess) err = cudaEventSynchronize(edown[c]);
+      if (err != cudaSuccess) break;
+      pieces_of(cfirst(c), cfirst(c + 1), [&](uint64_t r0, uint64_t, uint64_t m) {
+        parallel_chunks(m, [&](size_t lo, size_t hi) {
+          if (vbytes == 1) widen_u8_u32(reinterpret_cast<const uint8_t*>(hx) + r0 + lo, vout + r0 + lo, hi - lo);
+          else std::memcpy(vout + r0 + lo, reinterpret_cast<const uint32_t*>(hx) + r0 + lo, (hi - lo) * 4);
+        });
+      });
+    }
+    if (err == cudaSuccess) err = cudaEventSynchronize(evalid);
+    if (trace) {
+      std::fprintf(stderr, "[job32] host done %.2f ms;", host_ms());
+      for (auto& te : tev) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, t_start, te.second);
+        std::fprintf(stderr, " %s %.2f", te.first.c_str(), ms);
+      }
+      std::fprintf(stderr, "\n");
+      cudaEventDestroy(t_start);
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    CK(err);
+    CK(cudaStreamSynchronize(stream));
+    const unsigned long long code = std::min<unsigned long long>(*hcode, vcode.load());
+    if (code != ~0ull) {
+      // rejected: the ring is as it was (its buffers were never written)
+      *hctl = saved;
+      CK(cudaMemcpyAsync(ctl, hctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+      plan_stale = true;  // the records of the planned steps are stale: re-plan and clear
+      switch (static_cast<int>(code & 3u) + 1) {
+        case 1: throw std::invalid_argument("position out of range [0, length)");
+        case 2: throw std::invalid_argument("positions must be strictly increasing");
+        case 3: throw std::invalid_argument("velocity above vmax");
+        default: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      }
+    }
+    // accepted: the state loaded (set_state's bookkeeping) and k steps done
+    series_base = steps_done;
+    sumv_host.clear();
+    wraps_host.clear();
+    sumv0 = 0;
+    steps_done += k;
+    plan_stale = true;  // the next K-step launch needs its own plan
+    drain();            // records, control block (buf, W, t, plan check)
+    if (W_host != W_f) throw std::runtime_error("job: rank offset differs from the plan (engine state is invalid)");
+    return true;
+  }
+
   // Validates a rank-ordered state (strictly ascending positions < L,
   // velocities <= vmax -- the invariants of acceptance.cpp:118-123 -- and
   // <= L-1) while narrowing it into the pinned staging buffers, in parallel
@@ -926,6 +1174,16 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
     CK(cudaMemcpy(d.dseg, dr_seg.data(), dr_seg.size() * 4, cudaMemcpyHostToDevice));
   }
 
+  if (d.tb && !d.medium && d.n >= (1u << 22)) {
+    // the streamed job's input buffers (job32), allocated here so a job
+    // never pays for them (the velocities come back through the staging hx)
+    CK(cudaMalloc(&d.jx, size_t(d.npad) * 4));
+    CK(cudaMalloc(&d.jv, size_t(d.npad) * d.vbytes));
+    for (cudaStream_t& js : d.jstream) CK(cudaStreamCreateWithFlags(&js, cudaStreamNonBlocking));
+    CK(cudaMallocHost(&d.jctl, sizeof(Ctl)));
+    CK(cudaMalloc(&d.dcode, sizeof(unsigned long long)));
+    CK(cudaMallocHost(&d.hcode, sizeof(unsigned long long)));
+  }
   if (d.tb) {  // the one-step kernel's geometry (checksum mode, GpuRing::Impl::launch_single)
     int per1 = 0;
     if (d.vbytes == 1) {
@@ -1005,6 +1263,11 @@ GpuRing::Impl::~Impl() {
   cudaFree(thrpow1);
   cudaFree(dcode);
   cudaFreeHost(hcode);
+  cudaFree(jx);
+  cudaFree(jv);
+  for (cudaStream_t js : jstream)
+    if (js) cudaStreamDestroy(js);
+  cudaFreeHost(jctl);
   cudaFree(dplans);
   cudaFree(dsync);
   cudaFree(dmbox);
@@ -1030,6 +1293,15 @@ void GpuRing::set_state32(const uint32_t* x, const uint32_t* v, size_t n) {
   CK(cudaSetDevice(d.device));
   if (n != d.n) throw std::invalid_argument("state length must equal ncars");
   d.load_state<uint32_t>(x, v);
+}
+
+void GpuRing::job32(const uint32_t* xin, const uint32_t* vin, size_t n, uint64_t steps, uint32_t* xout,
+                    uint32_t* vout) {
+  Impl& d = *impl_;
+  CK(cudaSetDevice(d.device));
+  if (n != d.n) throw std::invalid_argument("state length must equal ncars");
+  if (d.job32(xin, vin, steps, xout, vout)) return;
+  RingEngine::job32(xin, vin, n, steps, xout, vout);
 }
 
 void GpuRing::advance(uint64_t steps) {

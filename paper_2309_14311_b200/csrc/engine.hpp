@@ -60,6 +60,16 @@ class RingEngine {
       if (velocities) velocities[i] = static_cast<uint32_t>(v[i]);
     }
   }
+  // Extension: one whole job end to end -- set_state32(xin, vin),
+  // advance(steps), state32(xout, vout) -- with the same results and errors
+  // as the three calls.  Default: the three calls; GpuRing streams them
+  // (upload, steps and download overlapped by ranges of the ring).
+  virtual void job32(const uint32_t* xin, const uint32_t* vin, size_t n, uint64_t steps, uint32_t* xout,
+                     uint32_t* vout) {
+    set_state32(xin, vin, n);
+    advance(steps);
+    state32(xout, vout);
+  }
   // Extension: the same snapshot, returned before the host-side copy and
   // widening are done (they overlap the caller's next advance); the output
   // arrays are complete after state_wait().  Default: synchronous.
@@ -128,6 +138,8 @@ class GpuRing : public RingEngine {
   void observables(double* density, double* mean_velocity, double* flow) override;
   void state(uint64_t* positions, uint64_t* velocities) override;
   void state32(uint32_t* positions, uint32_t* velocities) override;
+  void job32(const uint32_t* xin, const uint32_t* vin, size_t n, uint64_t steps, uint32_t* xout,
+             uint32_t* vout) override;
   void state_segment32(uint32_t* positions, uint32_t* velocities, uint64_t* first_rank) override {
     state32(positions, velocities);
     if (first_rank) *first_rank = 0;

@@ -49,13 +49,24 @@ __device__ __forceinline__ unsigned long long tb_now() {
 }
 #endif
 
+// A launch over a range of tiles (the streamed end-to-end job, engine.cu
+// GpuRing::job32): tiles [tile0, tile_end) with P starting at
+// a^(tile0 * STORE) and advancing by gpow = a^(gridDim.x * STORE) per
+// grid-stride tile; only the range launch with epi != 0 (the last) runs the
+// launch epilogue (plan check, W / t / buf update) -- the earlier ones only
+// add their tiles' velocity sums and crossings to the step records.
+struct TbRange {
+  uint32_t tile0, tile_end, gpow, a_tile0, epi;
+};
+
 // The launch body.  PUSH (segmented ring, peer-memory exchange only): the
 // launch's last block also publishes this segment's exchange record for the
 // next launch straight into every segment's receive slots (shard_push,
 // shard_kernels.cuh) -- the pack and the all-gather fused into the step
 // kernel.  PUSH = false compiles to the plain kernel (dead code removed).
-template <typename VT, int TPB, int CPT, int HALO, bool WT, bool PUSH>
-__device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, const XchgArgs& xa) {
+template <typename VT, int TPB, int CPT, int HALO, bool WT, bool PUSH, bool RANGE = false>
+__device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, const XchgArgs& xa,
+                                        const TbRange& rg = TbRange{}) {
   using G = TbGeom<TPB, CPT, HALO, WT>;
   constexpr uint32_t LOAD = G::kLoad;     // cars spanned per block tile
   constexpr uint32_t STORE = G::kStore;   // cars owned (stored) per block tile
@@ -99,10 +110,12 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
   // per thread and step for Q = E_j P, then one per car with the constant
   // 2 a^c as a constant-bank operand (no per-car multiplier registers).
   uint32_t P = mulmod_d(mulmod_d(ra.agofs, __ldg(ra.blkpow + blockIdx.x)), __ldg(ra.thrpow + threadIdx.x));
+  if (RANGE) P = mulmod_d(P, rg.a_tile0);
+  const uint32_t gpow = RANGE ? rg.gpow : ra.g;
   uint32_t phase = 0;  // running step counter across tiles: s_lead slot parity
   const uint32_t nl = ra.nl;  // cars stored here (a shard's segment, or the ring)
-  const uint32_t ntiles = (nl + STORE - 1) / STORE;
-  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  const uint32_t ntiles = RANGE ? min((nl + STORE - 1) / STORE, rg.tile_end) : (nl + STORE - 1) / STORE;
+  for (uint32_t tile = (RANGE ? rg.tile0 : 0u) + blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t a0 = tile * STORE;          // local index of the tile
     const uint32_t bl = a0 + i0;               // local index of car 0
     const uint32_t base = ra.gofs + bl;        // global id of car 0 (may exceed N at the wrap)
@@ -141,7 +154,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     }
 #endif
     const uint32_t P2 = P << 1;
-    P = mulmod_d(P, ra.g);
+    P = mulmod_d(P, gpow);
     // bit c: car c is stored by this tile (all of them but in the halo and
     // at a shard's end)
     const bool own_all = u0 + CPT <= WSTORE && bl + CPT <= nl;
@@ -310,6 +323,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
     atomicMax(trc + 3, now);
   }
 #endif
+  if (RANGE && !rg.epi) return;
   if (!last_block_done(ctl)) return;
 #ifdef NB_TB_TRACE
   if (threadIdx.x == 0) trc[4] = tb_now();
@@ -370,6 +384,13 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
 template <typename VT, int TPB, int CPT, int HALO, bool WT>
 __global__ void __launch_bounds__(TPB, NB_TB_MINB) nasch_tb_kernel(const RingArgs ra, const uint32_t k) {
   tb_body<VT, TPB, CPT, HALO, WT, false>(ra, k, XchgArgs{});
+}
+
+// Range launch of the streamed job (TbRange).
+template <typename VT, int TPB, int CPT, int HALO, bool WT>
+__global__ void __launch_bounds__(TPB, NB_TB_MINB)
+    nasch_tb_range_kernel(const RingArgs ra, const uint32_t k, const TbRange rg) {
+  tb_body<VT, TPB, CPT, HALO, WT, false, true>(ra, k, XchgArgs{}, rg);
 }
 
 // Segmented ring with the peer-memory exchange (sharded.cu, kXchgP2P).

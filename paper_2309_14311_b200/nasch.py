@@ -225,6 +225,21 @@ class Engine:
         _check(_lib().nasch_sim_state32(self._h, _u32p(x), _u32p(v), min(len(x), len(v))))
         return x, v
 
+    def job32(self, x, v, steps: int, *, out_x=None, out_v=None):
+        """set_state(x, v) + advance(steps) + snapshot32() in one call
+        (nasch_sim_job32): u32 input, u32 output; streamed (upload, steps
+        and download overlapped) for page-locked arrays within one K-step
+        launch."""
+        x = np.ascontiguousarray(x)
+        v = np.ascontiguousarray(v)
+        if x.dtype != np.uint32 or v.dtype != np.uint32 or x.ndim != 1 or v.ndim != 1 or len(x) != len(v):
+            raise ValueError("job32 takes 1-D uint32 positions and velocities of equal length")
+        ox = np.empty(self.ncars, np.uint32) if out_x is None else _out_u64(out_x, self.ncars, "out_x", np.uint32)
+        ov = np.empty(self.ncars, np.uint32) if out_v is None else _out_u64(out_v, self.ncars, "out_v", np.uint32)
+        _check(_lib().nasch_sim_job32(self._h, _u32p(x), _u32p(v), len(x), steps, _u32p(ox), _u32p(ov),
+                                      min(len(ox), len(ov))))
+        return ox, ov
+
     def snapshot_async(self, out_x, out_v) -> None:
         """Start a snapshot into (out_x, out_v) (u64, length ncars) that
         completes while the caller advances; call snapshot_wait() before

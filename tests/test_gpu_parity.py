@@ -661,6 +661,94 @@ def test_state32_equals_u64_snapshot(pinned):
         e.close()
 
 
+def _pinned_u32(a=None, n=None):
+    import torch
+    n = len(a) if a is not None else n
+    t = torch.zeros(n, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    if a is not None:
+        t[:] = a
+    return t
+
+
+@pytest.mark.parametrize("steps", [1, 20, 32, 45])
+def test_job32_streamed_equals_three_calls(port, steps):
+    """nasch_sim_job32 (upload, one K-step launch as range launches and the
+    download overlapped by ranges of the ring) equals set_state32 + advance
+    + state32 on a second engine: state, per-step series, step count; the
+    ring keeps stepping correctly afterwards (re-planned); 45 steps takes
+    the three-call form.  One size is checked against the oracle."""
+    for (L, N, seed) in [(60_000_000, 9_000_001, 3), (20_000_000, 4_200_000, 4)]:
+        x0, v0 = nasch.fill_uniform_state(L, N, 5, seed)
+        xin, vin = _pinned_u32(x0), _pinned_u32(v0)
+        a = nasch.Engine(params(L, N, 5, 0.3, 200, seed))
+        a.set_checksum(False)
+        a.advance(7)  # a non-zero step count and rank offset before the job
+        ox, ov = _pinned_u32(n=N), _pinned_u32(n=N)
+        a.job32(xin, vin, steps, out_x=ox, out_v=ov)
+        b = nasch.Engine(params(L, N, 5, 0.3, 200, seed))
+        b.set_checksum(False)
+        b.advance(7)
+        b.set_state(x0, v0)
+        b.advance(steps)
+        bx, bv = b.snapshot32()
+        assert a.steps_done == b.steps_done == 7 + steps
+        assert (ox == bx).all() and (ov == bv).all(), (N, steps)
+        assert (a.sumv_series() == b.sumv_series()).all() and (a.wrap_series() == b.wrap_series()).all()
+        a.advance(50)
+        b.advance(50)
+        ax, av = a.snapshot()
+        bx, bv = b.snapshot()
+        assert (ax == bx).all() and (av == bv).all()
+        if N < 5_000_000 and steps == 20:
+            o = port.run(L, 5, 0.3, seed, steps, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False,
+                         rng_state=port.jump(port.seeded(seed), 7 * N))
+            assert (ox == o["x"]).all() and (ov == o["v"]).all()
+        a.close()
+        b.close()
+
+
+def test_job32_rejects_like_set_state32():
+    """A rejected job32 input (position or velocity rule, in the first, a
+    middle or the last chunk) raises set_state32's message and leaves the
+    ring exactly as it was: same state, and it steps on as before."""
+    L, N = 30_000_000, 6_000_000
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 9)
+    e = nasch.Engine(params(L, N, 5, 0.3, 100, 9))
+    e.set_checksum(False)
+    e.set_state(x0, v0)
+    e.advance(11)
+    ref = nasch.Engine(params(L, N, 5, 0.3, 100, 9))
+    ref.set_checksum(False)
+    ref.set_state(x0, v0)
+    ref.advance(11)
+    sx, sv = e.snapshot()
+    ox, ov = _pinned_u32(n=N), _pinned_u32(n=N)
+    cases = [(5, "x", L, "position out of range"), (N // 2 + 3, "x", None, "strictly increasing"),
+             (N - 2, "v", 6, "above vmax"), (N // 8, "v", 9, "above vmax")]
+    for pos, arr, val, msg in cases:
+        xin, vin = _pinned_u32(x0), _pinned_u32(v0)
+        if arr == "x":
+            xin[pos] = val if val is not None else xin[pos - 1]
+        else:
+            vin[pos] = val
+        with pytest.raises(nasch.NaschError, match=msg):
+            e.job32(xin, vin, 20, out_x=ox, out_v=ov)
+        x, v = e.snapshot()
+        assert (x == sx).all() and (v == sv).all() and e.steps_done == 11
+    # earliest violation wins across the device (positions) and host (velocities) checks
+    xin, vin = _pinned_u32(x0), _pinned_u32(v0)
+    vin[1000] = 7
+    xin[N - 5] = L
+    with pytest.raises(nasch.NaschError, match="above vmax"):
+        e.job32(xin, vin, 20, out_x=ox, out_v=ov)
+    e.advance(30)
+    ref.advance(30)
+    x, v = e.snapshot()
+    rx, rv = ref.snapshot()
+    assert (x == rx).all() and (v == rv).all()
+    assert (e.sumv_series()[-30:] == ref.sumv_series()[-30:]).all()
+
+
 def test_set_state_validation_rules_and_order():
     """set_state rejects each rule at every position of the vectorised
     narrowing (first car, inside an 8-car group, group boundary, tail) with

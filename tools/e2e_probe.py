@@ -47,3 +47,14 @@ for rep in range(3):
           flush=True)
     e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=5, p=0.13, steps=100, seed=3))
     e.set_checksum(False)
+for rep in range(3):
+    e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=5, p=0.13, steps=100, seed=3))
+    e.set_checksum(False)
+    e.advance(0)
+    t0 = time.perf_counter()
+    e.job32(xin, vin, 20, out_x=outx, out_v=outv)
+    t1 = time.perf_counter()
+    s = e.mean_velocity_series()
+    t2 = time.perf_counter()
+    print(f"job32(20 steps) {1e3*(t1-t0):.2f} ms, series {1e3*(t2-t1):.2f} ms -> "
+          f"{N * 20 / (t2 - t0):.3e} car-updates/s", flush=True)
