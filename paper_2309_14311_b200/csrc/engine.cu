@@ -664,7 +664,7 @@ struct GpuRing::Impl {
   // set_state32's (positions on the device, velocities on the host).
   // Returns false when the streamed form does not apply (the caller then
   // runs the three calls).
-  static constexpr uint32_t kJobChunks = 8;
+  static constexpr uint32_t kJobChunks = 16;  // 4: 41 ms, 8: 35-43, 12: 33, 16: 32, 24: 32, 32: 33 on C3 (NASCH_B200_JOB_CHUNKS)
   bool job32(const uint32_t* xin, const uint32_t* vin, uint64_t steps, uint32_t* xout, uint32_t* vout) {
     const uint64_t k64 = std::min<uint64_t>(steps, params.steps - steps_done);
     auto pinned = [](const void* p) {
@@ -689,7 +689,8 @@ struct GpuRing::Impl {
     ja.x[cur] = jx;
     ja.v[cur] = jv;
     const uint32_t ntiles = (n + kTbStore - 1) / kTbStore;
-    const uint32_t tpc = (ntiles + kJobChunks - 1) / kJobChunks;  // tiles per chunk
+    const uint32_t chunks = static_cast<uint32_t>(std::max<long>(2, env_long("NASCH_B200_JOB_CHUNKS", kJobChunks)));
+    const uint32_t tpc = (ntiles + chunks - 1) / chunks;  // tiles per chunk
     const uint32_t nch = (ntiles + tpc - 1) / tpc;
     auto cfirst = [&](uint32_t c) { return std::min<uint64_t>(uint64_t(c) * tpc * kTbStore, n); };
     std::vector<cudaEvent_t> ev;
