@@ -186,6 +186,7 @@ class ShardedRing : public RingEngine {
   void observables(double* density, double* mean_velocity, double* flow) override;
   void state(uint64_t* positions, uint64_t* velocities) override;
   void state_segment(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) override;
+  void state_segment32(uint32_t* positions, uint32_t* velocities, uint64_t* first_rank) override;
   void state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) override;
   void state_wait() override;
   void set_state_segment(const uint64_t* x, const uint64_t* v, size_t n) override;

@@ -821,6 +821,53 @@ struct ShardedRing::Impl {
     CKS(err);
   }
 
+  // u32 form (nasch_sim_state_segment32): positions by DMA straight into a
+  // page-locked caller array (else through the staging), u8 velocities
+  // widened to u32 on the host as each piece lands.
+  void segment_to_host32(Shard& s, uint32_t* positions, uint32_t* velocities) {
+    ensure_stage(s);
+    cudaPointerAttributes pa{};
+    const bool direct_x =
+        positions && cudaPointerGetAttributes(&pa, positions) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const uint32_t* dx = s.x[buf_host];
+    const void* dv = s.v[buf_host];
+    constexpr uint32_t kChunk = 1u << 24;
+    std::vector<cudaEvent_t> evs;
+    for (uint32_t c0 = 0; c0 < s.nl; c0 += kChunk) {
+      const uint32_t m = std::min<uint32_t>(kChunk, s.nl - c0);
+      cudaEvent_t ev;
+      CKS(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      if (velocities)
+        CKS(cudaMemcpyAsync(static_cast<char*>(s.hv_stage) + size_t(c0) * vbytes,
+                            static_cast<const char*>(dv) + size_t(c0) * vbytes, size_t(m) * vbytes,
+                            cudaMemcpyDeviceToHost, s.stream));
+      if (positions)
+        CKS(cudaMemcpyAsync((direct_x ? positions : s.hx_stage) + c0, dx + c0, size_t(m) * 4,
+                            cudaMemcpyDeviceToHost, s.stream));
+      CKS(cudaEventRecord(ev, s.stream));
+      evs.push_back(ev);
+    }
+    cudaError_t err = cudaSuccess;
+    for (size_t i = 0; i < evs.size(); ++i) {
+      if (err == cudaSuccess) err = cudaEventSynchronize(evs[i]);
+      if (err == cudaSuccess) {
+        const size_t c0 = i * size_t(kChunk), m = std::min<size_t>(kChunk, s.nl - c0);
+        parallel_chunks(m, [&](size_t a, size_t b) {
+          a += c0;
+          b += c0;
+          if (positions && !direct_x) std::memcpy(positions + a, s.hx_stage + a, (b - a) * 4);
+          if (velocities) {
+            if (vbytes == 1) widen_u8_u32(static_cast<const uint8_t*>(s.hv_stage) + a, velocities + a, b - a);
+            else std::memcpy(velocities + a, static_cast<const uint32_t*>(s.hv_stage) + a, (b - a) * 4);
+          }
+        });
+      }
+      cudaEventDestroy(evs[i]);
+    }
+    CKS(err);
+  }
+
   void snap_join() {
     if (snap_thread.joinable()) snap_thread.join();
     if (snap_error) {
@@ -1284,6 +1331,21 @@ void ShardedRing::state_segment(uint64_t* positions, uint64_t* velocities, uint6
     return;
   }
   d.state_segment(positions, velocities, first_rank, false);
+}
+
+void ShardedRing::state_segment32(uint32_t* positions, uint32_t* velocities, uint64_t* first_rank) {
+  Impl& d = *impl_;
+  if (!d.use_nccl) {
+    RingEngine::state_segment32(positions, velocities, first_rank);
+    return;
+  }
+  d.check_poison();
+  d.snap_join();
+  d.drain();
+  Impl::Shard& s = d.sh[0];
+  CKS(cudaSetDevice(s.device));
+  if (first_rank) *first_rank = d.segment_first_rank();
+  d.segment_to_host32(s, positions, velocities);
 }
 
 void ShardedRing::state_segment_async(uint64_t* positions, uint64_t* velocities, uint64_t* first_rank) {

@@ -231,6 +231,8 @@ def test_distributed_whole_ring_calls_and_segment_snapshots(port, xchg, tmp_path
     sx, sv, first = e.segment_snapshot()
     r = (first + np.arange(N, dtype=np.uint64)) % np.uint64(N)
     assert (sx == o["x"][r]).all() and (sv == o["v"][r]).all()
+    sx32, sv32, first32 = e.segment_snapshot32()  # nasch_sim_state_segment32
+    assert first32 == first and (sx32 == sx).all() and (sv32 == sv).all()
     ax = np.empty(N, np.uint64)
     av = np.empty(N, np.uint64)
     first2 = e.segment_snapshot_async(ax, av)
@@ -276,4 +278,6 @@ def test_in_process_shards_segment_api(port):
         e.advance(T)
         sx, sv, first = e.segment_snapshot()
         assert first == 0 and (sx == o["x"]).all() and (sv == o["v"]).all()
+        sx32, sv32, first32 = e.segment_snapshot32()
+        assert first32 == 0 and (sx32 == sx).all() and (sv32 == sv).all()
         e.close()
