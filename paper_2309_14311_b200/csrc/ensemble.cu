@@ -213,6 +213,62 @@ uint32_t bits_for(uint64_t max_value) {
 
 }  // namespace
 
+// set_state_all32 with page-locked positions: the concatenated input goes up
+// in one DMA (velocities narrowed to u8 on the host) and one block per ring
+// scatters its cars into the tiled layout's idle buffer (buf ^ 1), checks
+// the position rules (first violation as 4 (global index) + rule - 1, by
+// atomicMin) and sums the velocities; ens_commit_kernel then makes the idle
+// buffer current, only if no rule failed, so a rejected state leaves every
+// ring as it was.
+__global__ void __launch_bounds__(256) ens_load_kernel(const EnsArgs ea, const unsigned long long* __restrict__ start,
+                                                       const uint32_t* __restrict__ in_x,
+                                                       const uint8_t* __restrict__ in_v, uint32_t* sums,
+                                                       unsigned long long* code) {
+  __shared__ uint32_t s_sum[8];
+  const uint32_t r = blockIdx.x;
+  const EnsRing R = ea.rings[r];
+  const unsigned long long g0 = start[r];
+  uint32_t* X = ea.X[R.buf ^ 1u] + R.off;
+  uint8_t* V = ea.V[R.buf ^ 1u] + R.off;
+  unsigned long long best = ~0ull;
+  uint32_t sum = 0;
+  for (uint32_t i = threadIdx.x; i < R.n; i += blockDim.x) {
+    const uint32_t xi = __ldg(in_x + g0 + i);
+    const uint8_t vi = __ldg(in_v + g0 + i);
+    X[i] = xi;
+    V[i] = vi;
+    sum += vi;
+    if (xi >= R.L) best = min(best, 4ull * (g0 + i));
+    else if (i && __ldg(in_x + g0 + i - 1) >= xi) best = min(best, 4ull * (g0 + i) + 1);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+    sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_sum[threadIdx.x / 32] = sum;
+    if (best != ~0ull) atomicMin(code, best);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < 8; ++w) t += s_sum[w];
+    sums[r] = t;
+  }
+}
+
+__global__ void ens_commit_kernel(const EnsArgs ea, const uint32_t* sums, const unsigned long long* code,
+                                  unsigned long long host_code) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= ea.nrings || *code != ~0ull || host_code != ~0ull) return;
+  EnsRing& R = ea.rings[r];
+  R.buf ^= 1u;
+  R.W = 0;
+  R.k = 0;
+  R.last_sumv = sums[r];
+}
+
 struct GpuEnsemble::Impl {
   std::vector<SimParams> params;
   int device = 0;
@@ -246,6 +302,13 @@ struct GpuEnsemble::Impl {
   size_t stage_cars = 0;
   uint32_t* h_stage_x = nullptr;
   uint8_t* h_stage_v = nullptr;
+  // set_state_all32 with page-locked positions (ens_load_kernel)
+  uint32_t* d_in_x = nullptr;
+  uint8_t* d_in_v = nullptr;
+  unsigned long long* d_start = nullptr;
+  uint32_t* d_sums = nullptr;
+  unsigned long long* d_code = nullptr;
+  unsigned long long* h_code = nullptr;
 
   void tpull() {
     if (!dirty) return;
@@ -368,6 +431,17 @@ GpuEnsemble::GpuEnsemble(const std::vector<SimParams>& rings) : impl_(new Impl) 
     d.stage_cars = total;
     CKE(cudaMallocHost(&d.h_stage_x, total * 4));
     CKE(cudaMallocHost(&d.h_stage_v, total));
+    {
+      std::vector<unsigned long long> st(rings.size() + 1, 0);
+      for (size_t r = 0; r < rings.size(); ++r) st[r + 1] = st[r] + rings[r].car_count;
+      CKE(cudaMalloc(&d.d_in_x, std::max<size_t>(1, st.back()) * 4));
+      CKE(cudaMalloc(&d.d_in_v, std::max<size_t>(1, st.back())));
+      CKE(cudaMalloc(&d.d_start, st.size() * sizeof(unsigned long long)));
+      CKE(cudaMemcpy(d.d_start, st.data(), st.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+      CKE(cudaMalloc(&d.d_sums, rings.size() * 4));
+      CKE(cudaMalloc(&d.d_code, sizeof(unsigned long long)));
+      CKE(cudaMallocHost(&d.h_code, sizeof(unsigned long long)));
+    }
     std::memset(d.h_stage_x, 0, total * 4);
     std::memset(d.h_stage_v, 0, total);
     for (int b = 0; b < 2; ++b) {
@@ -499,6 +573,12 @@ GpuEnsemble::Impl::~Impl() {
   cudaFreeHost(h_trings);
   cudaFreeHost(h_stage_x);
   cudaFreeHost(h_stage_v);
+  cudaFree(d_in_x);
+  cudaFree(d_in_v);
+  cudaFree(d_start);
+  cudaFree(d_sums);
+  cudaFree(d_code);
+  cudaFreeHost(h_code);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -579,6 +659,45 @@ void GpuEnsemble::set_state_all32(const uint32_t* x, const uint32_t* v, size_t t
     return;
   }
   d.tpull();
+  cudaPointerAttributes pa{};
+  const bool direct_x = cudaPointerGetAttributes(&pa, x) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();
+  if (direct_x) {
+    // positions: one DMA straight from the caller, scattered and checked on
+    // the device; velocities: narrowed (rules 3-4) on the host, one DMA
+    CKE(cudaMemcpyAsync(d.d_in_x, x, total * 4, cudaMemcpyHostToDevice, d.stream));
+    std::atomic<unsigned long long> vcode{~0ull};
+    const unsigned jobs = static_cast<unsigned>(std::min<size_t>(R, 4 * size_t(host_threads())));
+    host_run(jobs, [&](unsigned j) {
+      for (size_t r = j; r < R; r += jobs) {
+        const uint64_t c = narrow_v32(v, start[r], start[r + 1], d.params[r].v_max, d.trings[r].vmax,
+                                      d.h_stage_v, 1);
+        unsigned long long m = vcode.load();
+        while (c < m && !vcode.compare_exchange_weak(m, c)) {
+        }
+      }
+    });
+    const unsigned long long hc = vcode.load();
+    CKE(cudaMemcpyAsync(d.d_in_v, d.h_stage_v, total, cudaMemcpyHostToDevice, d.stream));
+    CKE(cudaMemsetAsync(d.d_code, 0xff, sizeof(unsigned long long), d.stream));
+    ens_load_kernel<<<static_cast<unsigned>(R), 256, 0, d.stream>>>(d.ea, d.d_start, d.d_in_x, d.d_in_v, d.d_sums,
+                                                                     d.d_code);
+    ens_commit_kernel<<<static_cast<unsigned>((R + 255) / 256), 256, 0, d.stream>>>(d.ea, d.d_sums, d.d_code, hc);
+    CKE(cudaGetLastError());
+    d.launches += 2;
+    CKE(cudaMemcpyAsync(d.h_code, d.d_code, sizeof(unsigned long long), cudaMemcpyDeviceToHost, d.stream));
+    CKE(cudaStreamSynchronize(d.stream));
+    d.dirty = true;  // the device ring records changed (committed) or not; re-read them
+    const unsigned long long code = std::min<unsigned long long>(*d.h_code, hc);
+    switch (code == ~0ull ? 0 : static_cast<int>(code & 3u) + 1) {
+      case 1: throw std::invalid_argument("position out of range [0, length)");
+      case 2: throw std::invalid_argument("positions must be strictly increasing");
+      case 3: throw std::invalid_argument("velocity above vmax");
+      case 4: throw std::invalid_argument("velocity above length-1 (B200 engine restriction)");
+      default: break;
+    }
+    return;
+  }
   const size_t pad = d.stage_cars;
   // rings validated and packed into the tiled layout in parallel; the
   // lowest failing ring's rule is reported

@@ -145,3 +145,60 @@ def test_tiled_ensemble_random_rings(port, tiled_env):
         assert (x == o["x"]).all() and (v == o["v"]).all(), (r, specs[r])
         assert int(tot[r]) == int(o["sumv"].sum()), r
         assert int(last[r]) == int(o["sumv"][-1]), r
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_ensemble_set_state_all32_pinned_and_rejects(port, pinned):
+    """set_state_all32 (every ring in one call): from page-locked arrays the
+    positions are scattered into the tiled layout and checked on the device
+    (ens_load_kernel / ens_commit_kernel), from pageable ones on the host;
+    both give the oracle's trajectories, the same first-violation message
+    (earliest car over all rings, rule order within a car), and a rejected
+    state leaves every ring as it was."""
+    import torch
+
+    def host(a):
+        if not pinned:
+            return np.array(a, np.uint32)
+        t = torch.empty(len(a), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+        t[:] = a
+        return t
+
+    specs = [(30000 + 1000 * i, 5000 + 1000 * i, 5, 0.1 * (i % 6), 60, 100 + i) for i in range(24)]
+    xs, vs = zip(*[nasch.fill_uniform_state(L, N, 5, sd) for (L, N, _, _, _, sd) in specs])
+    xc, vc = np.concatenate(xs), np.concatenate(vs)
+    ens = nasch.Ensemble([mk(*s) for s in specs])
+    ens.set_state_all(host(xc), host(vc))
+    ens.advance(13)
+    before = [ens.snapshot(r) for r in range(len(specs))]
+    starts = np.cumsum([0] + [s[1] for s in specs])
+    cases = [(int(starts[5]) + 3, "x", "position out of range"), (int(starts[11]) + 7, "x2", "strictly increasing"),
+             (int(starts[2]) + 9, "v", "above vmax"), (int(starts[20]) + 1, "v", "above vmax")]
+    for pos, what, msg in cases:
+        x, v = host(xc), host(vc)
+        if what == "x":
+            x[pos] = 10**6
+        elif what == "x2":
+            x[pos] = x[pos - 1]
+        else:
+            v[pos] = 6
+        with pytest.raises(nasch.NaschError, match=msg):
+            ens.set_state_all(x, v)
+        for r in range(len(specs)):
+            bx, bv = ens.snapshot(r)
+            assert (bx == before[r][0]).all() and (bv == before[r][1]).all(), (msg, r)
+    # the earlier car wins across rings and checks (a velocity in ring 3 before a position in ring 9)
+    x, v = host(xc), host(vc)
+    v[int(starts[3]) + 2] = 7
+    x[int(starts[9]) + 1] = 10**6
+    with pytest.raises(nasch.NaschError, match="above vmax"):
+        ens.set_state_all(x, v)
+    ens.set_state_all(host(xc), host(vc))
+    ens.advance(60)
+    for r, (L, N, vmax, p, T, sd) in enumerate(specs):
+        # set_state keeps the step count: the stream continues at draw 13 N
+        o = port.run(L, vmax, p, sd, T - 13, np.asarray(xs[r], np.uint64), np.asarray(vs[r], np.uint64),
+                     want_checksum=False, rng_state=port.jump(port.seeded(sd), 13 * N))
+        x, v = ens.snapshot(r)
+        assert ens.steps_done(r) == T
+        assert (x == o["x"]).all() and (v == o["v"]).all(), r
