@@ -354,6 +354,26 @@ struct GpuRing::Impl {
     return vbytes == 1 ? static_cast<const uint8_t*>(hv)[i] : static_cast<const uint32_t*>(hv)[i];
   }
 
+  // output = pgm: the frame as its raster row only, built on the device
+  // from the current state (a memset and a scatter of N zero bytes into an
+  // L-byte row), then copied to the host -- L bytes per frame instead of
+  // 16 N bytes of u64 positions and velocities rendered on the host.
+  uint8_t* draster = nullptr;
+  void record_frame_raster() {
+    if (!draster) CK(cudaMalloc(&draster, L));
+    const int cur = static_cast<int>(buf_host);
+    CK(cudaMemsetAsync(draster, 0xff, L, stream));
+    raster_kernel<<<std::max(1u, std::min(148u * 8u, (n + 255) / 256)), 256, 0, stream>>>(x[cur], n, draster);
+    CK(cudaGetLastError());
+    ++launches;
+    Frame f;
+    f.step = steps_done;
+    f.raster.resize(L);
+    CK(cudaMemcpyAsync(f.raster.data(), draster, L, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    frames.push_back(std::move(f));
+  }
+
   void record_frame_staged() {
     Frame f;
     f.step = steps_done;
@@ -372,6 +392,10 @@ struct GpuRing::Impl {
   void record_frame_if_due() {
     if (!frame_due()) return;
     drain();
+    if (params.output_mode == OutputMode::pgm) {
+      record_frame_raster();
+      return;
+    }
     fetch_rank_order();
     record_frame_staged();
   }
@@ -428,7 +452,10 @@ struct GpuRing::Impl {
         }
         enqueue_steps(chunk);
         left -= chunk;
-        if (frame_due()) {
+        if (frame_due() && params.output_mode == OutputMode::pgm) {
+          drain();
+          record_frame_raster();
+        } else if (frame_due()) {
           // overlapped with the next chunk: device copy now, host copy and
           // widening into the frame on the snapshot thread
           frames.emplace_back();
@@ -452,9 +479,7 @@ struct GpuRing::Impl {
       ++steps_done;
       fnv_fold();
       if (frame_due()) {
-        drain();
-        fetch_rank_order();
-        record_frame_staged();
+        record_frame_if_due();
       } else if (steps_done - drained > kRecCap / 2) {
         drain();
       }
@@ -1264,6 +1289,7 @@ GpuRing::Impl::~Impl() {
   cudaFree(thrpow1);
   cudaFree(dcode);
   cudaFreeHost(hcode);
+  cudaFree(draster);
   cudaFree(jx);
   cudaFree(jv);
   for (cudaStream_t js : jstream)

@@ -194,6 +194,10 @@ void write_pgm_file(const std::vector<Frame>& frames, uint64_t road_length,
   out << "P5\n" << road_length << ' ' << frames.size() << "\n255\n";
   std::vector<char> row(road_length);
   for (const Frame& f : frames) {
+    if (f.raster.size() == road_length) {  // rasterised on the device
+      out.write(reinterpret_cast<const char*>(f.raster.data()), static_cast<std::streamsize>(road_length));
+      continue;
+    }
     std::fill(row.begin(), row.end(), '\xff');
     for (uint64_t x : f.positions) row[x] = '\0';
     out.write(row.data(), static_cast<std::streamsize>(row.size()));

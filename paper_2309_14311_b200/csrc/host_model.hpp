@@ -63,6 +63,10 @@ struct Frame {
   uint64_t step = 0;
   std::vector<uint64_t> positions;
   std::vector<uint64_t> velocities;
+  // output = pgm on the single-GPU engine: the frame's space-time row as
+  // the P5 writer emits it (0 occupied, 255 empty), rasterised on the device
+  // (positions / velocities are then not kept: only the ascii writer reads them)
+  std::vector<uint8_t> raster;
 };
 
 void write_ascii_file(const std::vector<Frame>& frames, const std::string& path);

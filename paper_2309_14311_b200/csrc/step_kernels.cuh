@@ -600,6 +600,13 @@ static __global__ void validate_positions_kernel(const uint32_t* __restrict__ x,
   if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(code, best);
 }
 
+// The space-time raster row of a frame (src/io.cpp:186-216: a P5 row of L
+// pixels, 0 where a car stands, 255 elsewhere), from the ID-ordered
+// positions: the row was set to 255 first (cudaMemsetAsync).
+static __global__ void raster_kernel(const uint32_t* __restrict__ x, uint32_t n, uint8_t* row) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) row[__ldg(x + i)] = 0;
+}
+
 // Exact velocity sum of the current state (observables at step 0).
 template <typename VT>
 __global__ void sum_velocity_kernel(const VT* v, uint32_t n, unsigned long long* out) {

@@ -158,6 +158,36 @@ def test_frames_and_writers(tmp_path):  # test_engine.cpp:238-279, test_capi.cpp
     assert data.startswith(b"P5\n50 4\n255\n") and len(data) == len(b"P5\n50 4\n255\n") + 200
 
 
+@pytest.mark.parametrize("L,N", [(300_000, 60_000), (10_000_000, 2_500_000)])
+def test_pgm_raster_on_device_matches_reference(tmp_path, L, N):
+    """output = pgm on the distributed-resident (60k cars) and temporal-
+    blocked (2.5M cars) engines: frames are rasterised on the device (one
+    L-byte row each) and the P5 file equals the reference library's
+    (src/io.cpp:186-216) byte for byte."""
+    import ctypes as C
+    ref_so = os.path.join(os.path.dirname(O.__file__), "_ref", "libnasch_ref.so")
+    ref = C.CDLL(ref_so)
+    ref.nasch_params_parse.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_void_p]
+    ref.nasch_sim_new.argtypes = [C.c_void_p, C.c_uint, C.POINTER(C.c_void_p)]
+    ref.nasch_sim_run.argtypes = [C.c_void_p]
+    ref.nasch_sim_write_pgm.argtypes = [C.c_void_p, C.c_char_p]
+    ref.nasch_sim_free.argtypes = [C.c_void_p]
+    text = f"length={L}\nncars={N}\nvmax=5\np=0.3\nsteps=40\nseed=5\nstride=10\noutput=pgm"
+    hp, hs = C.c_void_p(), C.c_void_p()
+    assert ref.nasch_params_parse(text.encode(), C.byref(hp), None) == 0
+    assert ref.nasch_sim_new(hp, 8, C.byref(hs)) == 0
+    assert ref.nasch_sim_run(hs) == 0
+    assert ref.nasch_sim_write_pgm(hs, str(tmp_path / "ref.pgm").encode()) == 0
+    ref.nasch_sim_free(hs)
+    p, _ = nasch.SimParams.parse(text)
+    e = nasch.Engine(p)
+    e.set_checksum(False)
+    e.run()
+    assert e.frame_count == 4
+    e.write_pgm(str(tmp_path / "ours.pgm"))
+    assert open(tmp_path / "ours.pgm", "rb").read() == open(tmp_path / "ref.pgm", "rb").read()
+
+
 def test_frames_match_reference(tmp_path):
     """ASCII frame bytes equal the reference library's (acceptance.cpp:331-378)."""
     import ctypes as C
