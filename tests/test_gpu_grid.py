@@ -75,3 +75,24 @@ def test_grid_device_checksum_many_chunks(port):
     assert g.checksum == o["checksum"]
     x, v = g.snapshot()
     assert (x == o["x"]).all() and (v == o["v"]).all()
+
+
+@pytest.mark.parametrize("L,N,vmax,p,T", [
+    (8192 * 6 + 3, 9000, 9, 0.3, 50),     # a 3-cell tail block: cars jump over it into block 0
+    (8192 * 5 + 100, 12000, 40, 0.2, 40),  # look > 16: the next car after a block searched past the window
+    (60000, 4000, 200, 0.1, 30),           # velocities >= 128: occupancy by byte compare, not bit 7
+    (8192 * 3, 24576, 5, 0.5, 20)])        # every cell occupied, L a multiple of the block
+def test_grid_block_geometry_edges_vs_oracle(port, L, N, vmax, p, T):
+    """grid_move3_kernel's 8192-cell blocks at their edges, against the
+    oracle: spills into a non-adjacent block, the long next-car search,
+    the byte-compare occupancy path and a full road."""
+    x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, 5), 11)
+    o = port.run(L, vmax, p, 4, T, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    g = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=4), 1, GRID)
+    g.set_checksum(False)
+    g.set_state(x0, v0)
+    g.advance(T // 2)
+    g.advance(T - T // 2)
+    x, v = g.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
