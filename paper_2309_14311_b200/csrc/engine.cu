@@ -43,7 +43,7 @@
 #include "tb_kernel.cuh"
 #include "resident_kernel.cuh"
 #include "dr_kernel.cuh"
-#include "fnv_kernels.cuh"
+#include "fnv_pipeline.cuh"
 
 namespace nb200 {
 
@@ -564,115 +564,14 @@ struct GpuRing::Impl {
   // chunk's incoming low byte), pass C (one exact 64-bit run per slot), the
   // slots' affine maps reduced and applied -- all graph-captured, no host
   // round trip.
-  unsigned long long* fnv_hash = nullptr;
-  uint32_t fnv_nslots = 0, fnv_chunks = 0;
-  std::vector<uint8_t*> fnv_maps;   // level 0: chunk maps; level i+1: groups of 256 of level i
-  std::vector<uint8_t*> fnv_pre;    // prefix tables per level
-  std::vector<uint8_t*> fnv_lb;     // incoming nibble per map, levels >= 1
-  std::vector<uint32_t> fnv_count;  // maps per level
-  uint8_t* fnv_lo4 = nullptr;       // incoming low nibble per chunk (pass A)
-  uint8_t* fnv_hi4 = nullptr;       // incoming high nibble per chunk (pass B)
-  uint8_t* fnv_sub = nullptr;       // bytes at the slot boundaries inside a chunk (pass B)
-  uint8_t* fnv_top = nullptr;       // the top group's composed map (unused)
-  unsigned long long* fnv_A[2] = {nullptr, nullptr};
-  unsigned long long* fnv_D[2] = {nullptr, nullptr};
-  cudaGraphExec_t fnv_graph = nullptr;
-
-  void fnv_alloc() {
-    const uint32_t nu = (n + kFnvSlot - 1) / kFnvSlot;
-    const uint32_t npos = (nu + 1 + kFnvSlotsPerChunk - 1) / kFnvSlotsPerChunk * kFnvSlotsPerChunk;  // fnv_row
-    fnv_nslots = 2 * npos;
-    fnv_chunks = fnv_nslots / kFnvSlotsPerChunk;
-    for (uint32_t m = fnv_chunks;;) {
-      uint8_t *maps = nullptr, *pre = nullptr, *lb = nullptr;
-      CK(cudaMalloc(&maps, size_t(m) * 16));
-      CK(cudaMalloc(&pre, size_t(m) * 16));
-      CK(cudaMalloc(&lb, m));
-      fnv_maps.push_back(maps);
-      fnv_pre.push_back(pre);
-      fnv_lb.push_back(lb);
-      fnv_count.push_back(m);
-      if (m <= 256) break;
-      m = (m + 255) / 256;
-    }
-    CK(cudaMalloc(&fnv_top, 16));
-    CK(cudaMalloc(&fnv_lo4, fnv_chunks));
-    CK(cudaMalloc(&fnv_hi4, fnv_chunks));
-    CK(cudaMalloc(&fnv_sub, size_t(fnv_chunks) * (kFnvSlotsPerChunk - 1) * 16));
-    for (int b = 0; b < 2; ++b) {
-      CK(cudaMalloc(&fnv_A[b], size_t(fnv_nslots) * 8));
-      CK(cudaMalloc(&fnv_D[b], size_t(fnv_nslots) * 8));
-    }
-  }
-
-  // Composition tree over fnv_maps[0] (filled by pass A or B): up, then down
-  // from the digest's nibble at `shift`, the level-0 result into `out`.
-  uint32_t fnv_tree(int shift, uint8_t* out) {
-    uint32_t nl = 0;
-    const size_t levels = fnv_maps.size();
-    for (size_t i = 0; i < levels; ++i, ++nl) {
-      const uint32_t groups = (fnv_count[i] + 255) / 256;
-      fnv_up16_kernel<<<(groups + kUpGroups - 1) / kUpGroups, 16 * kUpGroups, 0, stream>>>(
-          fnv_maps[i], fnv_count[i], fnv_pre[i], i + 1 < levels ? fnv_maps[i + 1] : fnv_top);
-    }
-    for (size_t i = levels; i-- > 0; ++nl) {
-      fnv_down16_kernel<<<(fnv_count[i] + 255) / 256, 256, 0, stream>>>(
-          fnv_pre[i], fnv_count[i], i + 1 < levels ? fnv_lb[i + 1] : nullptr, fnv_hash, shift,
-          i == 0 ? out : fnv_lb[i]);
-    }
-    return nl;
-  }
-
-  uint32_t fnv_enqueue() {
-    uint32_t nl = 0;
-    const uint32_t nc = fnv_chunks;
-    const int cgrid = static_cast<int>((nc + kFnvTPB - 1) / kFnvTPB);
-    if (vbytes == 1) fnv_nib_kernel<uint8_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, fnv_maps[0], nullptr);
-    else fnv_nib_kernel<uint32_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, fnv_maps[0], nullptr);
-    nl += 1 + fnv_tree(0, fnv_lo4);
-    if (vbytes == 1) fnv_nib_kernel<uint8_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_maps[0], fnv_sub);
-    else fnv_nib_kernel<uint32_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_maps[0], fnv_sub);
-    nl += 1 + fnv_tree(4, fnv_hi4);
-    const uint32_t ns = fnv_nslots;
-    const int sgrid = static_cast<int>((ns + kFnvTPB - 1) / kFnvTPB);
-    if (vbytes == 1)
-      fnv_exact_kernel<uint8_t><<<sgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_hi4, fnv_sub, fnv_A[0], fnv_D[0]);
-    else
-      fnv_exact_kernel<uint32_t><<<sgrid, kFnvTPB, 0, stream>>>(args, fnv_lo4, fnv_hi4, fnv_sub, fnv_A[0], fnv_D[0]);
-    ++nl;
-    int in = 0;
-    for (uint32_t m = ns; m > 1; m = (m + 255) / 256, in ^= 1, ++nl)
-      fnv_affine_reduce<<<(m + 255) / 256, 256, 0, stream>>>(fnv_A[in], fnv_D[in], m, fnv_A[in ^ 1], fnv_D[in ^ 1]);
-    fnv_affine_apply<<<1, 1, 0, stream>>>(fnv_A[in], fnv_D[in], fnv_hash);
-    return nl + 1;
-  }
-
-  uint32_t fnv_graph_launches = 0;
+  FnvRowDigest digest;
 
   // Folds the current state's row into the device digest (one graph launch).
-  void fnv_fold() {
-    if (!fnv_hash) {
-      fnv_alloc();
-      CK(cudaMalloc(&fnv_hash, 8));
-      const unsigned long long h = hash;
-      CK(cudaMemcpy(fnv_hash, &h, 8, cudaMemcpyHostToDevice));
-      cudaGraph_t g;
-      CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-      fnv_graph_launches = fnv_enqueue();
-      CK(cudaStreamEndCapture(stream, &g));
-      CK(cudaGraphInstantiate(&fnv_graph, g, 0));
-      CK(cudaGraphDestroy(g));
-    }
-    CK(cudaGraphLaunch(fnv_graph, stream));
-    launches += fnv_graph_launches;
-  }
+  void fnv_fold() { launches += digest.fold(args, n, vbytes, stream, hash); }
 
   void pull_hash() {
-    if (!fnv_hash) return;
-    unsigned long long h = 0;
-    CK(cudaMemcpyAsync(&h, fnv_hash, 8, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    hash = h;
+    uint64_t h = 0;
+    if (digest.pull(stream, &h)) hash = h;
   }
 
   // ---- streamed end-to-end job (nasch_sim_job32) -----------------------
@@ -1265,21 +1164,10 @@ GpuRing::Impl::~Impl() {
   if (snap_stream) cudaStreamDestroy(snap_stream);
   if (stream) cudaStreamSynchronize(stream);
   if (graph) cudaGraphExecDestroy(graph);
-  if (fnv_graph) cudaGraphExecDestroy(fnv_graph);
   for (int b = 0; b < 2; ++b) {
     cudaFree(x[b]);
     cudaFree(v[b]);
-    cudaFree(fnv_A[b]);
-    cudaFree(fnv_D[b]);
   }
-  for (uint8_t* p : fnv_maps) cudaFree(p);
-  for (uint8_t* p : fnv_pre) cudaFree(p);
-  for (uint8_t* p : fnv_lb) cudaFree(p);
-  cudaFree(fnv_top);
-  cudaFree(fnv_lo4);
-  cudaFree(fnv_hi4);
-  cudaFree(fnv_sub);
-  cudaFree(fnv_hash);
   cudaFree(ctl);
   cudaFree(rec);
   cudaFree(dsum);

@@ -36,7 +36,7 @@
 
 #include "engine.hpp"
 #include "minstd.hpp"
-#include "fnv_kernels.cuh"
+#include "fnv_pipeline.cuh"
 #include "step_kernels.cuh"
 
 namespace nb200 {
@@ -406,11 +406,11 @@ struct GpuGrid::Impl {
   bool checksum_on = true;
   std::vector<uint64_t> sumv_host, wraps_host;
   std::vector<Frame> frames;
-  // on-device checksum (fnv_kernels.cuh): chunk maps of the compacted,
-  // rank-ordered row, composed and applied to a device digest
-  unsigned long long* fT[2] = {nullptr, nullptr};
-  unsigned long long* fP[2] = {nullptr, nullptr};
-  unsigned long long* dhash = nullptr;
+  // on-device checksum: the nibble-decomposed digest (fnv_pipeline.cuh) of
+  // the compacted, rank-ordered row
+  FnvRowDigest digest;
+  Ctl* dctl = nullptr;   // the compacted row's control block: W = 0, buf = 0
+  RingArgs rowargs{};    // (xs, vs) as a RingArgs for the digest kernels
   ~Impl();
 
   // The last move's spilled cars into cells[cur] and counts (when a state
@@ -441,32 +441,21 @@ struct GpuGrid::Impl {
   // Folds the current row (positions, then velocities) into the device
   // digest: no transfer of the state.
   void hash_step() {
-    const uint32_t nch = (N + kFnvChunk - 1) / kFnvChunk;
-    if (!dhash) {
-      for (int b = 0; b < 2; ++b) {
-        CKG(cudaMalloc(&fT[b], size_t(2) * nch * 256 * sizeof(unsigned long long)));
-        CKG(cudaMalloc(&fP[b], size_t(2) * nch * sizeof(unsigned long long)));
-      }
-      CKG(cudaMalloc(&dhash, sizeof(unsigned long long)));
-      CKG(cudaMemcpyAsync(dhash, &hash, sizeof hash, cudaMemcpyHostToDevice, stream));
+    if (!dctl) {
+      CKG(cudaMalloc(&dctl, sizeof(Ctl)));
+      CKG(cudaMemset(dctl, 0, sizeof(Ctl)));
+      rowargs.x[0] = rowargs.x[1] = xs;
+      rowargs.v[0] = rowargs.v[1] = vs;
+      rowargs.n = N;
+      rowargs.ctl = dctl;
     }
-    compact();
-    fnv_slice_chunk_kernel<uint32_t><<<nch, 256, 0, stream>>>(xs, N, fT[0], fP[0]);
-    fnv_slice_chunk_kernel<uint8_t><<<nch, 256, 0, stream>>>(vs, N, fT[0] + size_t(nch) * 256, fP[0] + nch);
-    int in = 0;
-    for (uint32_t m = 2 * nch; m > 1; m = (m + 1) / 2) {
-      fnv_compose_kernel<<<(m + 1) / 2, 256, 0, stream>>>(fT[in], fP[in], m, fT[in ^ 1], fP[in ^ 1]);
-      in ^= 1;
-    }
-    fnv_apply_kernel<<<1, 1, 0, stream>>>(fT[in], fP[in], dhash);
-    CKG(cudaGetLastError());
-    launches += 4;
+    compact();  // the row in rank order: xs, vs (head id 0)
+    launches += digest.fold(rowargs, N, 1, stream, hash);
   }
 
   void pull_hash() {
-    if (!dhash) return;
-    CKG(cudaMemcpyAsync(&hash, dhash, sizeof hash, cudaMemcpyDeviceToHost, stream));
-    CKG(cudaStreamSynchronize(stream));
+    uint64_t h = 0;
+    if (digest.pull(stream, &h)) hash = h;
   }
 
   // One step, enqueued: no host round trip (records drained in batches).
@@ -609,11 +598,7 @@ GpuGrid::Impl::~Impl() {
   cudaFree(vs);
   cudaFree(rec);
   cudaFree(pw);
-  for (int b = 0; b < 2; ++b) {
-    cudaFree(fT[b]);
-    cudaFree(fP[b]);
-  }
-  cudaFree(dhash);
+  cudaFree(dctl);
   cudaFreeHost(hrec);
   cudaFreeHost(hx);
   cudaFreeHost(hv);
