@@ -244,7 +244,8 @@ struct GpuRing::Impl {
 
   // The origin-cone plan for the current step (after one-step launches).
   void replan() {
-    if (vbytes == 1) cone_init_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args);
+    if (dr) cone_init_kernel<uint8_t, kDrTPB><<<1, kDrTPB, 0, stream>>>(args);  // the DR planner's width
+    else if (vbytes == 1) cone_init_kernel<uint8_t, 256><<<1, 256, 0, stream>>>(args);
     else cone_init_kernel<uint32_t, 256><<<1, 256, 0, stream>>>(args);
     CK(cudaGetLastError());
     ++launches;
@@ -469,6 +470,11 @@ struct GpuRing::Impl {
       if (sync) drain();
       return;
     }
+    if (dump_rows() > 0) {
+      checksum_batched(count);
+      if (sync) drain();
+      return;
+    }
     // The checksum folds every step's row (src/engine.cpp:173-181): one
     // step per launch, each followed by the on-device FNV fold
     // (fnv_kernels.cuh) -- no host round trip unless a frame is due.
@@ -485,6 +491,94 @@ struct GpuRing::Impl {
       }
     }
     if (sync) drain();
+  }
+
+  // ---- checksum batches (rings up to ~1M cars) -------------------------
+  // The digest is one FNV-1a over every step's row laid end to end, so k
+  // rows can be digested in ONE pass of the pipeline (FnvRowDigest over the
+  // positions-only array of 2 N k u32 values) instead of one pass per step,
+  // whose ~20 launches dominate a small ring's step (C1: 89 us per step,
+  // slower than the reference's CPU).  Small rings dump their rows from the
+  // resident kernels (RingArgs::dump, k steps per launch); medium rings step
+  // with the one-step kernel and dump_row_kernel.
+  static constexpr uint64_t kDumpBytes = uint64_t(64) << 20;
+  static constexpr uint64_t kDumpMaxRows = 4096;
+  uint32_t* dstage = nullptr;  // [rows][2N] u32 rank-ordered rows
+  Ctl* dctl0 = nullptr;        // W = 0, buf = 0: the batch as one row
+
+  static constexpr uint64_t kDumpGraphRows = 512;
+  cudaGraphExec_t gbatch = nullptr;
+  uint64_t gbatch_launches = 0;
+
+  // k one-step launches, each followed by the dump of its row (slot i)
+  void enqueue_dumped_steps(uint64_t k) {
+    const int g = static_cast<int>(std::min<uint64_t>(148 * 8, (n + 255) / 256));
+    for (uint64_t i = 0; i < k; ++i) {
+      launch_single();
+      if (vbytes == 1) dump_row_kernel<uint8_t><<<g, 256, 0, stream>>>(args, dstage + i * 2 * n);
+      else dump_row_kernel<uint32_t><<<g, 256, 0, stream>>>(args, dstage + i * 2 * n);
+      ++launches;
+    }
+  }
+
+  uint64_t dump_rows() const {
+    if (!(resident || ((tb || dr) && grid1 > 0))) return 0;
+    const uint64_t rows = std::min<uint64_t>(kDumpMaxRows, kDumpBytes / (8ull * n));
+    return rows >= 8 ? rows : 0;
+  }
+
+  void checksum_batched(uint64_t count) {
+    const uint64_t B = dump_rows();
+    if (!dstage) {
+      CK(cudaMalloc(&dstage, size_t(B) * 2 * n * 4));
+      CK(cudaMalloc(&dctl0, sizeof(Ctl)));
+      CK(cudaMemset(dctl0, 0, sizeof(Ctl)));
+    }
+    RingArgs rowargs{};
+    rowargs.x[0] = rowargs.x[1] = dstage;
+    rowargs.v[0] = rowargs.v[1] = dstage;
+    rowargs.ctl = dctl0;
+    rowargs.fnv_pos_only = 1;
+    while (count > 0) {
+      uint64_t k = std::min(count, B);
+      if (params.output_mode != OutputMode::none) {
+        const uint64_t stride = params.output_stride;
+        k = std::min(k, (steps_done / stride + 1) * stride - steps_done);  // up to the next frame step
+      }
+      if (steps_done - drained + k > kRecCap / 2) drain();
+      if (resident) {
+        const uint32_t* keep = args.dump;
+        args.dump = dstage;
+        launch(static_cast<uint32_t>(k));
+        args.dump = const_cast<uint32_t*>(keep);
+      } else if (k == B && B <= kDumpGraphRows) {
+        // full batches replay one captured graph of B (step, dump) pairs:
+        // the per-kernel launch latency, not the work, sets a medium ring's
+        // step time here
+        if (!gbatch) {
+          cudaGraph_t gr;
+          CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+          const uint64_t l0 = launches;
+          enqueue_dumped_steps(B);
+          gbatch_launches = launches - l0;
+          launches = l0;
+          CK(cudaStreamEndCapture(stream, &gr));
+          CK(cudaGraphInstantiate(&gbatch, gr, 0));
+          CK(cudaGraphDestroy(gr));
+        }
+        CK(cudaGraphLaunch(gbatch, stream));
+        launches += gbatch_launches;
+        plan_stale = true;
+      } else {
+        enqueue_dumped_steps(k);
+      }
+      CK(cudaGetLastError());
+      steps_done += k;
+      rowargs.n = static_cast<uint32_t>(2 * n * k);
+      launches += digest.fold_direct(rowargs, rowargs.n, static_cast<uint32_t>(2 * n * B), 4, stream, hash);
+      count -= k;
+      if (frame_due()) record_frame_if_due();
+    }
   }
 
   // Starts an asynchronous rank-ordered snapshot into (positions,
@@ -1109,7 +1203,7 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
     CK(cudaMalloc(&d.dcode, sizeof(unsigned long long)));
     CK(cudaMallocHost(&d.hcode, sizeof(unsigned long long)));
   }
-  if (d.tb) {  // the one-step kernel's geometry (checksum mode, GpuRing::Impl::launch_single)
+  if (d.tb || d.dr) {  // the one-step kernel's geometry (checksum mode, GpuRing::Impl::launch_single)
     int per1 = 0;
     if (d.vbytes == 1) {
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, nasch_step_kernel<uint8_t, kTPB, kCPT1>, kTPB, 0));
@@ -1178,6 +1272,9 @@ GpuRing::Impl::~Impl() {
   cudaFree(dcode);
   cudaFreeHost(hcode);
   cudaFree(draster);
+  cudaFree(dstage);
+  cudaFree(dctl0);
+  if (gbatch) cudaGraphExecDestroy(gbatch);
   cudaFree(jx);
   cudaFree(jv);
   for (cudaStream_t js : jstream)

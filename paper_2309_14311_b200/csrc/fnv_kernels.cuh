@@ -178,10 +178,12 @@ constexpr unsigned long long kFnvPSlot = fnv_pow_c(8ull * kFnvSlot);  // P^(8 * 
 struct FnvRow {
   uint32_t N, head, nu, hu;  // cars, head id, units per array, head unit
   uint32_t npos;             // slots per array: nu + 1, rounded up to whole chunks (the rest empty)
+  uint32_t pos_only;         // no velocity part: its slots are empty
 };
 
-__device__ __forceinline__ FnvRow fnv_row(uint32_t N, uint32_t W) {
+__device__ __forceinline__ FnvRow fnv_row(uint32_t N, uint32_t W, uint32_t pos_only = 0) {
   FnvRow r;
+  r.pos_only = pos_only;
   r.N = N;
   r.head = (N - W) % N;
   r.nu = (N + kFnvSlot - 1) / kFnvSlot;
@@ -194,7 +196,9 @@ __device__ __forceinline__ FnvRow fnv_row(uint32_t N, uint32_t W) {
 __device__ __forceinline__ void fnv_slot(const FnvRow& r, uint32_t s, uint32_t& arr, uint32_t& a, uint32_t& b) {
   arr = s >= r.npos ? 1u : 0u;
   const uint32_t t = arr ? s - r.npos : s;
-  if (t == 0) {
+  if (arr && r.pos_only) {
+    a = b = 0;
+  } else if (t == 0) {
     a = r.head;
     b = min(r.hu * kFnvSlot + kFnvSlot, r.N);
   } else if (t >= r.nu) {
@@ -393,7 +397,7 @@ __global__ void __launch_bounds__(kFnvTPB) fnv_nib_kernel(const RingArgs ra, con
   __shared__ FnvStage stage[kFnvTPB / 32];
   FnvStage& st = stage[threadIdx.x / 32];
   const Ctl* ctl = ra.ctl;
-  const FnvRow row = fnv_row(ra.n, ctl->W);
+  const FnvRow row = fnv_row(ra.n, ctl->W, ra.fnv_pos_only);
   const uint32_t nchunks = 2 * row.npos / kFnvSlotsPerChunk;
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   if ((c & ~31u) >= nchunks) return;  // whole warps only: the staging is warp-collective
@@ -477,7 +481,7 @@ __global__ void __launch_bounds__(kFnvTPB) fnv_exact_kernel(const RingArgs ra, c
   __shared__ FnvStage stage[kFnvTPB / 32];
   FnvStage& st = stage[threadIdx.x / 32];
   const Ctl* ctl = ra.ctl;
-  const FnvRow row = fnv_row(ra.n, ctl->W);
+  const FnvRow row = fnv_row(ra.n, ctl->W, ra.fnv_pos_only);
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if ((s & ~31u) >= 2 * row.npos) return;  // whole warps only
   const int bsel = static_cast<int>(ctl->buf);

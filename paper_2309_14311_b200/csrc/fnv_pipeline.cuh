@@ -46,22 +46,28 @@ class FnvRowDigest {
   // describing the row: the kernels read buf and W from args.ctl).  Returns
   // the kernel launches the graph made.
   uint32_t fold(const RingArgs& args, uint32_t n, int vbytes, cudaStream_t stream, uint64_t host_hash) {
-    if (!hash_) {
-      n_ = n;
-      vbytes_ = vbytes;
-      alloc();
-      ck(cudaMalloc(&hash_, 8), "cudaMalloc(digest)");
-      const unsigned long long h = host_hash;
-      ck(cudaMemcpy(hash_, &h, 8, cudaMemcpyHostToDevice), "cudaMemcpy(digest)");
+    if (!hash_) start(n, vbytes, host_hash);
+    if (!graph_) {
       cudaGraph_t g;
       ck(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-      launches_ = enqueue(args, stream);
+      launches_ = enqueue(args, n, stream);
       ck(cudaStreamEndCapture(stream, &g), "cudaStreamEndCapture");
       ck(cudaGraphInstantiate(&graph_, g, 0), "cudaGraphInstantiate");
       ck(cudaGraphDestroy(g), "cudaGraphDestroy");
     }
     ck(cudaGraphLaunch(graph_, stream), "cudaGraphLaunch(digest)");
     return launches_;
+  }
+
+  // The same fold without a graph, for a row of n <= capacity values whose
+  // length changes from call to call (checksum batches of small rings: the
+  // rows of k steps laid end to end); the first call sizes the buffers for
+  // `capacity` values.
+  uint32_t fold_direct(const RingArgs& args, uint32_t n, uint32_t capacity, int vbytes, cudaStream_t stream,
+                       uint64_t host_hash) {
+    if (!hash_) start(capacity, vbytes, host_hash);
+    if (n > n_) throw std::logic_error("digest row longer than its capacity");
+    return enqueue(args, n, stream);
   }
 
   // The device digest into *out (synchronises the stream); false before the
@@ -80,10 +86,23 @@ class FnvRowDigest {
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
   }
 
+  void start(uint32_t n, int vbytes, uint64_t host_hash) {
+    n_ = n;
+    vbytes_ = vbytes;
+    alloc();
+    ck(cudaMalloc(&hash_, 8), "cudaMalloc(digest)");
+    const unsigned long long h = host_hash;
+    ck(cudaMemcpy(hash_, &h, 8, cudaMemcpyHostToDevice), "cudaMemcpy(digest)");
+  }
+
+  // slots and chunks of a row of n values (fnv_row)
+  static uint32_t slots_of(uint32_t n) {
+    const uint32_t nu = (n + kFnvSlot - 1) / kFnvSlot;
+    return 2 * ((nu + 1 + kFnvSlotsPerChunk - 1) / kFnvSlotsPerChunk * kFnvSlotsPerChunk);
+  }
+
   void alloc() {
-    const uint32_t nu = (n_ + kFnvSlot - 1) / kFnvSlot;
-    const uint32_t npos = (nu + 1 + kFnvSlotsPerChunk - 1) / kFnvSlotsPerChunk * kFnvSlotsPerChunk;  // fnv_row
-    nslots_ = 2 * npos;
+    nslots_ = slots_of(n_);
     chunks_ = nslots_ / kFnvSlotsPerChunk;
     for (uint32_t m = chunks_;;) {
       uint8_t *maps = nullptr, *pre = nullptr, *lb = nullptr;
@@ -107,40 +126,47 @@ class FnvRowDigest {
     }
   }
 
-  // Composition tree over maps_[0] (filled by pass A or B): up, then down
-  // from the digest's nibble at `shift`, the level-0 result into `out`.
-  uint32_t tree(int shift, uint8_t* out, cudaStream_t stream) {
+  // Composition tree over maps_[0] (filled by pass A or B; `chunks` maps):
+  // up, then down from the digest's nibble at `shift`, the level-0 result
+  // into `out`.
+  uint32_t tree(uint32_t chunks, int shift, uint8_t* out, cudaStream_t stream) {
     uint32_t nl = 0;
-    const size_t levels = maps_.size();
+    std::vector<uint32_t> count;
+    for (uint32_t m = chunks;; m = (m + 255) / 256) {
+      count.push_back(m);
+      if (m <= 256) break;
+    }
+    const size_t levels = count.size();
     for (size_t i = 0; i < levels; ++i, ++nl) {
-      const uint32_t groups = (count_[i] + 255) / 256;
+      const uint32_t groups = (count[i] + 255) / 256;
       fnv_up16_kernel<<<(groups + kUpGroups - 1) / kUpGroups, 16 * kUpGroups, 0, stream>>>(
-          maps_[i], count_[i], pre_[i], i + 1 < levels ? maps_[i + 1] : top_);
+          maps_[i], count[i], pre_[i], i + 1 < levels ? maps_[i + 1] : top_);
     }
     for (size_t i = levels; i-- > 0; ++nl) {
-      fnv_down16_kernel<<<(count_[i] + 255) / 256, 256, 0, stream>>>(
-          pre_[i], count_[i], i + 1 < levels ? lb_[i + 1] : nullptr, hash_, shift, i == 0 ? out : lb_[i]);
+      fnv_down16_kernel<<<(count[i] + 255) / 256, 256, 0, stream>>>(
+          pre_[i], count[i], i + 1 < levels ? lb_[i + 1] : nullptr, hash_, shift, i == 0 ? out : lb_[i]);
     }
     return nl;
   }
 
-  uint32_t enqueue(const RingArgs& args, cudaStream_t stream) {
+  uint32_t enqueue(const RingArgs& args, uint32_t n, cudaStream_t stream) {
     uint32_t nl = 0;
-    const int cgrid = static_cast<int>((chunks_ + kFnvTPB - 1) / kFnvTPB);
+    const uint32_t nslots = slots_of(n), chunks = nslots / kFnvSlotsPerChunk;
+    const int cgrid = static_cast<int>((chunks + kFnvTPB - 1) / kFnvTPB);
     if (vbytes_ == 1) fnv_nib_kernel<uint8_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, maps_[0], nullptr);
     else fnv_nib_kernel<uint32_t, 0><<<cgrid, kFnvTPB, 0, stream>>>(args, nullptr, maps_[0], nullptr);
-    nl += 1 + tree(0, lo4_, stream);
+    nl += 1 + tree(chunks, 0, lo4_, stream);
     if (vbytes_ == 1) fnv_nib_kernel<uint8_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, lo4_, maps_[0], sub_);
     else fnv_nib_kernel<uint32_t, 1><<<cgrid, kFnvTPB, 0, stream>>>(args, lo4_, maps_[0], sub_);
-    nl += 1 + tree(4, hi4_, stream);
-    const int sgrid = static_cast<int>((nslots_ + kFnvTPB - 1) / kFnvTPB);
+    nl += 1 + tree(chunks, 4, hi4_, stream);
+    const int sgrid = static_cast<int>((nslots + kFnvTPB - 1) / kFnvTPB);
     if (vbytes_ == 1)
       fnv_exact_kernel<uint8_t><<<sgrid, kFnvTPB, 0, stream>>>(args, lo4_, hi4_, sub_, A_[0], D_[0]);
     else
       fnv_exact_kernel<uint32_t><<<sgrid, kFnvTPB, 0, stream>>>(args, lo4_, hi4_, sub_, A_[0], D_[0]);
     ++nl;
     int in = 0;
-    for (uint32_t m = nslots_; m > 1; m = (m + 255) / 256, in ^= 1, ++nl)
+    for (uint32_t m = nslots; m > 1; m = (m + 255) / 256, in ^= 1, ++nl)
       fnv_affine_reduce<<<(m + 255) / 256, 256, 0, stream>>>(A_[in], D_[in], m, A_[in ^ 1], D_[in ^ 1]);
     fnv_affine_apply<<<1, 1, 0, stream>>>(A_[in], D_[in], hash_);
     ck(cudaGetLastError(), "digest kernels");

@@ -66,6 +66,15 @@ __global__ void __launch_bounds__(TPB, 1) ring_resident_kernel(const RingArgs ra
       const uint32_t ac = c < 256 ? apw[c] : powmod(kA, c);
       E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
       W = Wn;
+      if (ra.dump) {  // checksum batch: step st-1's row in rank order
+        uint32_t* row = ra.dump + size_t(st - 1) * 2u * N;
+        for (uint32_t id = first; id < first + cnt; ++id) {
+          uint32_t r = id + W;
+          if (r >= N) r -= N;
+          row[r] = sx[id];
+          row[N + r] = sv[id];
+        }
+      }
     }
     if (st == steps) break;
     const uint32_t E2 = mulmod_d(E, ra.an_inv);
@@ -247,6 +256,18 @@ __global__ void __launch_bounds__(32, 1) ring_warp_kernel(const RingArgs ra, con
       E = mulmod_d(E, wrap ? ac : mulmod_d(ra.an, ac));
     }
     W = Wn;
+    if (ra.dump) {  // checksum batch: this step's row in rank order
+      uint32_t* row = ra.dump + size_t(st) * 2u * N;
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) {
+        if ((live >> c) & 1u) {
+          uint32_t r = first + c + W;
+          if (r >= N) r -= N;
+          row[r] = x[c];
+          row[N + r] = v[c];
+        }
+      }
+    }
   }
 #pragma unroll
   for (int c = 0; c < CPW; ++c) {

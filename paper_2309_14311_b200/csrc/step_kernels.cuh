@@ -93,6 +93,14 @@ struct RingArgs {
   // -1 as a launch parameter: ptxas cannot fold it, so x * neg1 + xl stays
   // one IMAD on the FMA pipe instead of an IADD3 on the (busier) ALU pipe.
   uint32_t neg1 = 0xffffffffu;
+  // Checksum mode on small rings (engine.cu, GpuRing::Impl::advance): the
+  // small-ring kernels write each step's rank-ordered row -- N positions,
+  // then N velocities, as u32 -- to dump + 2N * (step within the launch),
+  // for one digest over a batch of rows.  nullptr: off.
+  uint32_t* dump = nullptr;
+  // The row digest (fnv_kernels.cuh) over positions only: the velocity
+  // slots are empty (a dump batch is one flat array of u32 values).
+  uint32_t fnv_pos_only = 0;
 };
 
 // ---- vector access helpers ----------------------------------------------
@@ -605,6 +613,24 @@ static __global__ void validate_positions_kernel(const uint32_t* __restrict__ x,
 // positions: the row was set to 255 first (cudaMemsetAsync).
 static __global__ void raster_kernel(const uint32_t* __restrict__ x, uint32_t n, uint8_t* row) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) row[__ldg(x + i)] = 0;
+}
+
+// The current state's rank-ordered row into a dump slot (2N u32 values:
+// positions, then velocities), for checksum batches of rings stepped by
+// the one-step kernel.
+template <typename VT>
+__global__ void dump_row_kernel(const RingArgs ra, uint32_t* row) {
+  const Ctl* ctl = ra.ctl;
+  const uint32_t N = ra.n, W = ctl->W;
+  const int b = static_cast<int>(ctl->buf);
+  const uint32_t* X = xbuf(ra, b);
+  const VT* V = vbuf<VT>(ra, b);
+  for (uint32_t id = blockIdx.x * blockDim.x + threadIdx.x; id < N; id += gridDim.x * blockDim.x) {
+    uint32_t r = id + W;
+    if (r >= N) r -= N;
+    row[r] = __ldg(X + id);
+    row[N + r] = static_cast<uint32_t>(__ldg(V + id));
+  }
 }
 
 // Exact velocity sum of the current state (observables at step 0).

@@ -415,6 +415,47 @@ def test_temporal_blocking_checksum_mode(port, k_env, dr):
     assert_same(g, o)
 
 
+@pytest.mark.parametrize("L,N,T,dr", [
+    (1000, 200, 5000, "1"),        # one-warp ring: 4096-row batches, a partial one
+    (12000, 3000, 700, "1"),       # one-CTA ring
+    (100000, 20000, 1000, "1"),    # distributed-resident ring: one-step kernel + row dumps
+    (300000, 60000, 300, "0")])    # temporal-blocked medium ring, the same
+def test_checksum_batches_vs_reference(port, k_env, L, N, T, dr):
+    """Rings up to ~1M cars digest their rows in batches (the rows of up to
+    4096 steps laid end to end, one pass of the nibble pipeline): the
+    checksum equals the reference's step-by-step FNV-1a over advance calls
+    that split batches, with the checksum toggled off and on between them
+    (the DR / TB rings then re-plan), and the state and series stay exact."""
+    os.environ["NASCH_B200_DR"] = dr
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 3)
+    o = port.run(L, 5, 0.3, 7, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    e = nasch.Engine(params(L, N, 5, 0.3, T, 7))
+    e.set_state(x0, v0)
+    for chunk in (T // 3, 1, T // 5):
+        e.advance(chunk)
+    e.advance(T)
+    assert e.steps_done == T
+    assert e.checksum == o["checksum"], (N, dr)
+    x, v = e.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    e.close()
+    # checksum off for a stretch: the DR / TB kernels re-plan after the one-step launches
+    T2 = min(T, 400)
+    o2 = port.run(L, 5, 0.3, 7, T2, x0.astype(np.uint64), v0.astype(np.uint64), want_checksum=False)
+    e = nasch.Engine(params(L, N, 5, 0.3, T2, 7))
+    e.set_state(x0, v0)
+    e.advance(T2 // 4)
+    e.set_checksum(False)
+    e.advance(T2 // 4)
+    e.set_checksum(True)
+    e.advance(T2)
+    x, v = e.snapshot()
+    assert (x == o2["x"]).all() and (v == o2["v"]).all()
+    assert (e.sumv_series() == o2["sumv"]).all()
+    e.close()
+
+
 @pytest.mark.parametrize("K", ["8", "32"])
 def test_checksum_toggle_switches_step_kernels(port, k_env, K):
     """A temporal-blocked ring steps with the one-step kernel while the
