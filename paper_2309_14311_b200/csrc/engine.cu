@@ -440,6 +440,15 @@ struct GpuRing::Impl {
   void advance(uint64_t steps, bool sync) {
     const uint64_t count = std::min(steps, params.steps - steps_done);
     if (count == 0) return;
+    // Small rings whose every few steps are hashed or recorded: rows dumped
+    // by the step kernels, digested and turned into frames a batch at a time
+    // (frames alone only on the resident rings: a medium ring's multi-step
+    // launches and its device raster are faster than dumping every row)
+    if (dump_rows() > 0 && (checksum_on || (params.output_mode != OutputMode::none && resident))) {
+      dump_batched(count);
+      if (sync) drain();
+      return;
+    }
     if (!checksum_on) {
       // Run at full speed between frame steps (every output_stride steps,
       // src/engine.cpp:81-86); each frame is one rank-ordered D2H.
@@ -467,11 +476,6 @@ struct GpuRing::Impl {
           snap_start(f.positions.data(), f.velocities.data());
         }
       }
-      if (sync) drain();
-      return;
-    }
-    if (dump_rows() > 0) {
-      checksum_batched(count);
       if (sync) drain();
       return;
     }
@@ -527,7 +531,9 @@ struct GpuRing::Impl {
     return rows >= 8 ? rows : 0;
   }
 
-  void checksum_batched(uint64_t count) {
+  uint32_t* hrows = nullptr;   // pinned: frame rows copied down from a batch
+
+  void dump_batched(uint64_t count) {
     const uint64_t B = dump_rows();
     if (!dstage) {
       CK(cudaMalloc(&dstage, size_t(B) * 2 * n * 4));
@@ -540,11 +546,7 @@ struct GpuRing::Impl {
     rowargs.ctl = dctl0;
     rowargs.fnv_pos_only = 1;
     while (count > 0) {
-      uint64_t k = std::min(count, B);
-      if (params.output_mode != OutputMode::none) {
-        const uint64_t stride = params.output_stride;
-        k = std::min(k, (steps_done / stride + 1) * stride - steps_done);  // up to the next frame step
-      }
+      const uint64_t k = std::min(count, B);
       if (steps_done - drained + k > kRecCap / 2) drain();
       if (resident) {
         const uint32_t* keep = args.dump;
@@ -573,11 +575,37 @@ struct GpuRing::Impl {
         enqueue_dumped_steps(k);
       }
       CK(cudaGetLastError());
+      const uint64_t before = steps_done;
       steps_done += k;
-      rowargs.n = static_cast<uint32_t>(2 * n * k);
-      launches += digest.fold_direct(rowargs, rowargs.n, static_cast<uint32_t>(2 * n * B), 4, stream, hash);
+      if (checksum_on) {
+        rowargs.n = static_cast<uint32_t>(2 * n * k);
+        launches += digest.fold_direct(rowargs, rowargs.n, static_cast<uint32_t>(2 * n * B), 4, stream, hash);
+      }
+      if (params.output_mode != OutputMode::none) record_batch_frames(before, k);
       count -= k;
-      if (frame_due()) record_frame_if_due();
+    }
+  }
+
+  // Frames (src/engine.cpp:81-86: steps s with s % stride == 0, s < T) among
+  // the batch's rows (row j = the state after step before + j + 1), copied
+  // down in one span and widened to the reference's u64 frames.
+  void record_batch_frames(uint64_t before, uint64_t k) {
+    const uint64_t stride = params.output_stride;
+    uint64_t s = (before / stride + 1) * stride;
+    if (s > before + k || s >= params.steps) return;
+    const uint64_t last = std::min<uint64_t>(before + k, params.steps - 1) / stride * stride;
+    const uint64_t j0 = s - before - 1, j1 = last - before - 1;
+    if (!hrows) CK(cudaMallocHost(&hrows, size_t(dump_rows()) * 2 * n * 4));
+    CK(cudaMemcpyAsync(hrows, dstage + j0 * 2 * n, size_t(j1 - j0 + 1) * 2 * n * 4, cudaMemcpyDeviceToHost,
+                       stream));
+    CK(cudaStreamSynchronize(stream));
+    for (; s <= last; s += stride) {
+      const uint32_t* row = hrows + (s - before - 1 - j0) * 2 * n;
+      Frame f;
+      f.step = s;
+      f.positions.assign(row, row + n);
+      f.velocities.assign(row + n, row + 2 * n);
+      frames.push_back(std::move(f));
     }
   }
 
@@ -1274,6 +1302,7 @@ GpuRing::Impl::~Impl() {
   cudaFree(draster);
   cudaFree(dstage);
   cudaFree(dctl0);
+  cudaFreeHost(hrows);
   if (gbatch) cudaGraphExecDestroy(gbatch);
   cudaFree(jx);
   cudaFree(jv);
