@@ -505,7 +505,7 @@ struct GpuRing::Impl {
   // slower than the reference's CPU).  Small rings dump their rows from the
   // resident kernels (RingArgs::dump, k steps per launch); medium rings step
   // with the one-step kernel and dump_row_kernel.
-  static constexpr uint64_t kDumpBytes = uint64_t(64) << 20;
+  static constexpr uint64_t kDumpBytes = uint64_t(256) << 20;
   static constexpr uint64_t kDumpMaxRows = 4096;
   uint32_t* dstage = nullptr;  // [rows][2N] u32 rank-ordered rows
   Ctl* dctl0 = nullptr;        // W = 0, buf = 0: the batch as one row
