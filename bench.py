@@ -65,6 +65,7 @@ BYTES_MOVED_PER_UPDATE = 10  # u32 x + u8 v, read once and written once per laun
 SURVEY_BYTES_PER_UPDATE = 16  # int32 x and v read+written per step
 CPU_SAMPLE_SECONDS = 25.0
 MIN_WARMUP_STEPS = 512
+CK_STEPS = 10  # the checksum-on leg (C3 with the reference's per-step FNV-1a)
 C4_MIN_WARMUP_STEPS = 64
 PARITY_RING = dict(L=10**7, N=2 * 10**6, p=0.13, vmax=5, seed=17, steps=48, init_seed=11)
 
@@ -406,7 +407,7 @@ def c3_leg(args, d: Dist):
         log(f"[bench] multi-GPU parity self-check: {ok} ({parity['seconds']} s)")
 
     # ---- device-resident throughput -----------------------------------
-    prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=W_run + R * K, seed=seed)
+    prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=W_run + R * K + 2 + CK_STEPS, seed=seed)
     eng = (nasch.Engine.distributed(prm, d.rank, d.world, fresh_id()) if d.world > 1
            else nasch.Engine(prm))
     eng.set_checksum(False)
@@ -457,6 +458,26 @@ def c3_leg(args, d: Dist):
         ok = bool(len(sumv) == W_run + R * K and all(w == allw[0] for w in allw)
                   and int(sumv.max()) <= vmax * N)
     ok = d.all_true(ok)
+    # The reference's stock semantics on the same engine: the checksum on,
+    # every step's rank-ordered row folded into the FNV-1a digest on the
+    # device; one GPU (the segmented ring keeps the slower
+    # round-1 digest)
+    checksum_leg = None
+    if d.world == 1:
+        eng.set_checksum(True)
+        eng.advance(2)  # the digest's buffers and graph, outside the timing
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record(stream)
+        eng.enqueue(CK_STEPS)
+        c1.record(stream)
+        eng.synchronize()
+        torch.cuda.synchronize()
+        ck_ms = c0.elapsed_time(c1)
+        checksum_leg = {"value": N * CK_STEPS / (ck_ms / 1e3), "unit": "car-updates/s",
+                        "ms_per_step": ck_ms / CK_STEPS, "steps": CK_STEPS,
+                        "note": "checksum on (nasch_sim_new's default, the reference cannot turn it off): "
+                                "one-step kernel + the nibble-decomposed FNV-1a of every step's row on the device"}
     eng.close()
     value = N * K / (ms / 1000.0)  # whole ring, max over ranks
     step_ms = ms / K
@@ -555,6 +576,7 @@ def c3_leg(args, d: Dist):
                                  "the binding roof is integer issue (issue_bound, DESIGN.md 4.1)"},
             "issue_bound": issue_bound(launch_ms, k_launch, N, clocks, d.world),
             "e2e": e2e,
+            **({"checksum_on": checksum_leg} if checksum_leg else {}),
             "gpu_launches": int(launches),
             "clocks": clocks,
             "invariants_ok": ok}
