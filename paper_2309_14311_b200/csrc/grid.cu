@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -37,6 +38,7 @@
 #include "engine.hpp"
 #include "minstd.hpp"
 #include "fnv_pipeline.cuh"
+#include "grid_bits.cuh"
 #include "step_kernels.cuh"
 
 namespace nb200 {
@@ -126,11 +128,15 @@ __device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
 // reaches the move kernel as two independent loads (round 2: a rank load
 // then three dependent table loads).  (A single-block scan fused with the
 // spill fixup measured 23 us against ~10 us for these two launches.)
+// (Bit-plane form: a block's cars are those in its words plus the cars the
+// previous block carried over its end, still in `carry`.)
 __global__ void __launch_bounds__(1024) grid_scan_local(const uint32_t* counts, uint32_t nb, uint32_t* local,
-                                                        uint32_t* group, const uint32_t* pw, uint32_t* plocal) {
+                                                        uint32_t* group, const uint32_t* pw, uint32_t* plocal,
+                                                        const uint4* carry) {
   __shared__ uint32_t s_w[32], s_tot;
   const uint32_t i = blockIdx.x * 1024u + threadIdx.x;
-  const uint32_t v = i < nb ? counts[i] : 0u;
+  uint32_t v = i < nb ? counts[i] : 0u;
+  if (carry && i < nb) v += __popc(carry[(i + nb - 1) % nb].x);
   const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
   if (i < nb) {
     local[i] = ex;
@@ -411,7 +417,68 @@ struct GpuGrid::Impl {
   FnvRowDigest digest;
   Ctl* dctl = nullptr;   // the compacted row's control block: W = 0, buf = 0
   RingArgs rowargs{};    // (xs, vs) as a RingArgs for the digest kernels
+  // Bit-plane form (grid_bits.cuh; vmax <= 7 and L a multiple of 32): the
+  // planes are the state the steps run on, cells[cur] a view unpacked for
+  // the readers (state, frames, checksum).
+  bool bitmode = false;
+  uint4* planes[2] = {nullptr, nullptr};
+  uint4* carry[2] = {nullptr, nullptr};  // per block: the cars carried over its end by the last move
+  uint32_t* bcounts[2] = {nullptr, nullptr};
+  int pcur = 0;
+  uint32_t nwords = 0, nbb = 0, ngb = 0;
+  bool planes_valid = false;  // planes[pcur] (+ carry[pcur]) hold the current state
+  bool cells_valid = true;    // cells[cur] holds the current state
   ~Impl();
+
+  // cells[cur] -> planes (after construction / set_state).
+  void pack() {
+    gridbits::grid_pack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(cells[cur], nwords, planes[pcur]);
+    CKG(cudaMemsetAsync(carry[pcur], 0, size_t(nbb) * sizeof(uint4), stream));
+    gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, bcounts[pcur]);
+    CKG(cudaGetLastError());
+    launches += 2;
+    planes_valid = true;
+  }
+
+  // planes -> cells[cur] for the readers.
+  void ensure_cells() {
+    if (!bitmode || cells_valid) return;
+    gridbits::grid_unpack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(planes[pcur], carry[pcur], nwords, nbb,
+                                                                          cells[cur]);
+    CKG(cudaGetLastError());
+    ++launches;
+    cells_valid = true;
+    counts_valid = false;
+  }
+
+  template <int VMAX>
+  void launch_bitmove(const gridbits::BitArgs& g) {
+    gridbits::grid_bitmove_kernel<VMAX><<<nbb, gridbits::kTPB, 0, stream>>>(
+        planes[pcur], planes[pcur ^ 1], carry[pcur], carry[pcur ^ 1], plocal, pgroup, g, rec, bcounts[pcur ^ 1]);
+  }
+
+  void step_bits() {
+    if (steps_done - drained >= kRecCap / 2) drain();
+    if (!planes_valid) pack();
+    const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
+    const gridbits::BitArgs g{nwords, deceleration_threshold(params.p), E, 2 * kA, pw, steps_done};
+    grid_scan_local<<<ngb, 1024, 0, stream>>>(bcounts[pcur], nbb, local, group, pw, plocal, carry[pcur]);
+    grid_scan_top<<<1, 1024, 0, stream>>>(group, ngb, pw, pgroup, rec + (steps_done % kRecCap));
+    switch (vmax) {
+      case 1: launch_bitmove<1>(g); break;
+      case 2: launch_bitmove<2>(g); break;
+      case 3: launch_bitmove<3>(g); break;
+      case 4: launch_bitmove<4>(g); break;
+      case 5: launch_bitmove<5>(g); break;
+      case 6: launch_bitmove<6>(g); break;
+      default: launch_bitmove<7>(g); break;
+    }
+    CKG(cudaGetLastError());
+    launches += 3;
+    pcur ^= 1;
+    cells_valid = false;
+    ++steps_done;
+  }
 
   // The last move's spilled cars into cells[cur] and counts (when a state
   // read comes before the next step).
@@ -424,11 +491,12 @@ struct GpuGrid::Impl {
   }
 
   void scan(StepRec* zero) {
-    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group, pw, plocal);
+    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group, pw, plocal, nullptr);
     grid_scan_top<<<1, 1024, 0, stream>>>(group, ng, pw, pgroup, zero);
   }
 
   void compact() {
+    ensure_cells();
     flush();
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
     counts_valid = true;
@@ -460,6 +528,7 @@ struct GpuGrid::Impl {
 
   // One step, enqueued: no host round trip (records drained in batches).
   void step() {
+    if (bitmode) return step_bits();
     if (steps_done - drained >= kRecCap / 2) drain();
     const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
     const GridArgs g{L, N, vmax, deceleration_threshold(params.p), E, 2 * powmod(kA, kGridTPB), pw, steps_done};
@@ -571,6 +640,20 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   }
   CKG(cudaMallocHost(&d.hx, size_t(d.N) * 4));
   CKG(cudaMallocHost(&d.hv, d.N));
+  {
+    const char* force = std::getenv("NASCH_B200_GRID_BYTES");  // 1: the byte-per-cell kernels whatever vmax and L
+    d.bitmode = d.vmax <= 7 && d.L % 32 == 0 && !(force && force[0] == '1');
+  }
+  if (d.bitmode) {
+    d.nwords = d.L / 32;
+    d.nbb = (d.nwords + gridbits::kWordsPerBlock - 1) / gridbits::kWordsPerBlock;
+    d.ngb = (d.nbb + 1023) / 1024;
+    for (int b = 0; b < 2; ++b) {
+      CKG(cudaMalloc(&d.planes[b], size_t(d.nwords) * sizeof(uint4)));
+      CKG(cudaMalloc(&d.carry[b], size_t(d.nbb) * sizeof(uint4)));
+      CKG(cudaMalloc(&d.bcounts[b], size_t(d.nbb) * 4));
+    }
+  }
   CKG(cudaMemsetAsync(d.cells[0], kEmpty, d.L, d.stream));
   grid_init_kernel<<<std::max(1u, std::min(4096u, (d.N + 255) / 256)), 256, 0, d.stream>>>(d.cells[0], d.L, d.N);
   CKG(cudaGetLastError());
@@ -599,6 +682,11 @@ GpuGrid::Impl::~Impl() {
   cudaFree(rec);
   cudaFree(pw);
   cudaFree(dctl);
+  for (int b = 0; b < 2; ++b) {
+    cudaFree(planes[b]);
+    cudaFree(carry[b]);
+    cudaFree(bcounts[b]);
+  }
   cudaFreeHost(hrec);
   cudaFreeHost(hx);
   cudaFreeHost(hv);
@@ -625,6 +713,8 @@ void GpuGrid::set_state(const uint64_t* x, const uint64_t* v, size_t n) {
   CKG(cudaStreamSynchronize(d.stream));
   d.counts_valid = false;
   d.fixup_pending = false;  // the loaded state replaces the array
+  d.planes_valid = false;
+  d.cells_valid = true;
   d.sumv0 = s;
   d.sumv_host.clear();
   d.wraps_host.clear();

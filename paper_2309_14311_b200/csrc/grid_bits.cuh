@@ -1,0 +1,265 @@
+// grid_bits.cuh -- the cell-array engine (src/model.cpp:99-129) in bit planes,
+// for vmax <= 7 and L a multiple of 32: 32 cells per uint4 {occupied, v bit 0,
+// v bit 1, v bit 2}, half a byte per cell instead of one, and the whole rule
+// but the draws evaluated for 32 cells at once with bitwise operations
+// ("multi-spin coding"):
+//   gap >= d        F_d = ~(occ >> 1) & ... & ~(occ >> d) (funnel shifts across
+//                   the next word: the lookahead is at most vmax cells)
+//   min(v+1, vmax, gap) >= d     T_{d-1} & F_d, T_d = cars with v >= d
+//                   (thermometer form from the three binary planes)
+//   random slowdown v' >= d      vc_{d+1} | (vc_d & ~dec)
+//   move            cars with v' = d exactly shifted up d cells; the bits that
+//                   leave the word go to the next word (register, shuffle,
+//                   shared memory, or the block's carry word in HBM, which the
+//                   next block ORs into its first word when it loads it next
+//                   step -- no fixup pass)
+// Only the draws are per car: rank order is ascending bit order, so a thread
+// walks the set bits of its words with Q <- Q a (one mulmod_x2 per car) from
+// Q = E a^(rank of its first car), the rank from the block scan of popcounts.
+// The velocity sum is the sum of the thermometer popcounts, the wrap count the
+// popcount of the last word's overflow.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "minstd.hpp"
+#include "step_kernels.cuh"
+
+namespace nb200 {
+namespace gridbits {
+
+constexpr int kTPB = 256;
+#ifndef NB_GRID_WPT
+#define NB_GRID_WPT 2
+#endif
+constexpr int kWPT = NB_GRID_WPT;  // 32-cell words per thread
+constexpr uint32_t kWordsPerBlock = kTPB * kWPT;
+
+struct BitArgs {
+  uint32_t nwords;     // L / 32
+  uint32_t tp;         // deceleration threshold
+  uint32_t E;          // s0 a^(t N + 1)
+  uint32_t a2;         // 2 a
+  const uint32_t* pw;  // [2][4096]: a^j, a^(4096 j)
+  unsigned long long t;
+};
+
+// Cars with velocity >= D from the binary planes (D = 0: every car).
+template <int D>
+__device__ __forceinline__ uint32_t thermo(uint32_t o, uint32_t p0, uint32_t p1, uint32_t p2) {
+  if constexpr (D == 0) return o;
+  if constexpr (D == 1) return p0 | p1 | p2;
+  if constexpr (D == 2) return p1 | p2;
+  if constexpr (D == 3) return p2 | (p1 & p0);
+  if constexpr (D == 4) return p2;
+  if constexpr (D == 5) return p2 & (p0 | p1);
+  if constexpr (D == 6) return p2 & p1;
+  return p2 & p1 & p0;
+}
+
+// One word: the new velocities' thermometer masks vp[1..VMAX] from the word,
+// the next word's occupancy and the deceleration mask.
+template <int VMAX>
+__device__ __forceinline__ void word_rule(uint32_t o, uint32_t p0, uint32_t p1, uint32_t p2, uint32_t nx,
+                                          uint32_t (&vc)[VMAX + 2]) {
+  uint32_t F = 0xffffffffu;
+  vc[0] = o;
+  vc[VMAX + 1] = 0;
+#pragma unroll
+  for (int d = 1; d <= VMAX; ++d) {
+    F &= ~__funnelshift_r(o, nx, d);  // cell i + d empty, for every i at once
+    uint32_t T;
+    switch (d - 1) {
+      case 0: T = thermo<0>(o, p0, p1, p2); break;
+      case 1: T = thermo<1>(o, p0, p1, p2); break;
+      case 2: T = thermo<2>(o, p0, p1, p2); break;
+      case 3: T = thermo<3>(o, p0, p1, p2); break;
+      case 4: T = thermo<4>(o, p0, p1, p2); break;
+      case 5: T = thermo<5>(o, p0, p1, p2); break;
+      default: T = thermo<6>(o, p0, p1, p2); break;
+    }
+    vc[d] = T & F;  // min(v + 1, vmax, gap) >= d
+  }
+}
+
+// The move of one step over the bit planes.  Block b owns words
+// [b kWordsPerBlock, ...), thread t the kWPT consecutive words from
+// (b kTPB + t) kWPT.
+template <int VMAX>
+__global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                                            const uint4* __restrict__ carry_in,
+                                                            uint4* __restrict__ carry_out,
+                                                            const uint32_t* __restrict__ plocal,
+                                                            const uint32_t* __restrict__ pgroup, BitArgs g,
+                                                            StepRec* rec, uint32_t* counts_next) {
+  constexpr int NW = kTPB / 32;
+  __shared__ uint32_t s_cnt[NW], s_first[NW + 1], s_hi[NW];
+  const uint32_t b = blockIdx.x, nbb = gridDim.x;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint32_t w0 = (b * kTPB + threadIdx.x) * kWPT;
+  const uint32_t lastw = min((b + 1) * kWordsPerBlock, g.nwords) - 1u;  // the block's last live word
+  const bool has_last = w0 <= lastw && lastw < w0 + kWPT;
+  // every global load first
+  uint32_t o[kWPT], p0[kWPT], p1[kWPT], p2[kWPT];
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) {
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (w0 + k < g.nwords) u = __ldg(in + w0 + k);
+    o[k] = u.x; p0[k] = u.y; p1[k] = u.z; p2[k] = u.w;
+  }
+  uint32_t nxt_global = 0;
+  if (has_last) {  // the first word after the block (cyclic), with the cars carried into it last step
+    const uint32_t wn = b + 1 == nbb ? 0u : (b + 1) * kWordsPerBlock;
+    nxt_global = __ldg(in + wn).x | __ldg(carry_in + b).x;
+  }
+  if (threadIdx.x == 0) {  // the cars the previous block carried over its end last step
+    const uint4 c = __ldg(carry_in + (b + nbb - 1) % nbb);
+    o[0] |= c.x; p0[0] |= c.y; p1[0] |= c.z; p2[0] |= c.w;
+  }
+  const uint32_t pl = __ldg(plocal + b), pg = __ldg(pgroup + (b >> 10));
+  // ranks: block scan of the popcounts
+  uint32_t cnt = 0;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) cnt += __popc(o[k]);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= static_cast<uint32_t>(s)) incl += n;
+  }
+  if (lane == 31) s_cnt[warp] = incl;
+  if (lane == 0) s_first[warp] = o[0];
+  __syncthreads();
+  const uint32_t cw = lane < static_cast<uint32_t>(NW) ? s_cnt[lane] : 0u;
+  const uint32_t wbase = __reduce_add_sync(0xffffffffu, lane < warp ? cw : 0u);
+  const uint32_t ncars = __reduce_add_sync(0xffffffffu, cw);
+  const uint32_t j0 = wbase + incl - cnt;  // block-local rank of this thread's first car
+  uint32_t nxt_thread = __shfl_down_sync(0xffffffffu, o[0], 1);
+  if (lane == 31) nxt_thread = warp + 1 < static_cast<uint32_t>(NW) ? s_first[warp + 1] : 0u;
+  const uint32_t Eb = mulmod_d(mulmod_d(g.E, pl), pg);  // E a^(rank of the block's first car)
+  uint32_t Q = mulmod_d(mulmod_d(Eb, __ldg(g.pw + (j0 & 4095u))), __ldg(g.pw + 4096 + (j0 >> 12)));
+
+  uint32_t no[kWPT], n0[kWPT], n1[kWPT], n2[kWPT];  // the next array's words
+  uint32_t ho = 0, h0 = 0, h1 = 0, h2 = 0;          // bits leaving the previous word
+  uint32_t co = 0, c0 = 0, c1 = 0, c2 = 0;          // ... leaving the block's last word
+  uint32_t sumv = 0;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k) {
+    uint32_t nx = k + 1 < kWPT ? o[k + 1 < kWPT ? k + 1 : k] : nxt_thread;
+    if (w0 + k == lastw) nx = nxt_global;
+    uint32_t vc[VMAX + 2];
+    word_rule<VMAX>(o[k], p0[k], p1[k], p2[k], nx, vc);
+    // the draws, one per car in ascending cell order (model.cpp:51: always consumed)
+    uint32_t dec = 0;
+    for (uint32_t m = o[k]; m;) {
+      const uint32_t s = Q;
+      Q = mulmod_x2(g.a2, Q);
+      const uint32_t bit = m & (0u - m);
+      if (s < g.tp) dec |= bit;
+      m ^= bit;
+    }
+    uint32_t lo_o, lo_0 = 0, lo_1 = 0, lo_2 = 0, hi_o = 0, hi_0 = 0, hi_1 = 0, hi_2 = 0;
+    uint32_t vnext = 0;  // v' >= d + 1
+    uint32_t stay = 0;
+#pragma unroll
+    for (int d = VMAX; d >= 1; --d) {
+      const uint32_t vp = vc[d + 1] | (vc[d] & ~dec);  // v' >= d
+      sumv += __popc(vp);
+      const uint32_t X = vp & ~vnext;  // v' == d
+      vnext = vp;
+      const uint32_t l = X << d, h = X >> (32 - d);
+      stay |= l;
+      hi_o |= h;
+      if (d & 1) { lo_0 |= l; hi_0 |= h; }
+      if (d & 2) { lo_1 |= l; hi_1 |= h; }
+      if (d & 4) { lo_2 |= l; hi_2 |= h; }
+    }
+    lo_o = stay | (o[k] & ~vnext);  // v' == 0 stays
+    no[k] = lo_o | ho; n0[k] = lo_0 | h0; n1[k] = lo_1 | h1; n2[k] = lo_2 | h2;
+    ho = hi_o; h0 = hi_0; h1 = hi_1; h2 = hi_2;
+    if (w0 + k == lastw) { co = hi_o; c0 = hi_0; c1 = hi_1; c2 = hi_2; }
+  }
+  // the last word's overflow to the next thread's first word (<= 7 bits a plane)
+  const uint32_t pk = ho | (h0 << 7) | (h1 << 14) | (h2 << 21);
+  uint32_t pin = __shfl_up_sync(0xffffffffu, pk, 1);
+  if (lane == 31) s_hi[warp] = pk;
+  __syncthreads();
+  if (lane == 0) pin = warp ? s_hi[warp - 1] : 0u;
+  no[0] |= pin & 0x7fu; n0[0] |= (pin >> 7) & 0x7fu; n1[0] |= (pin >> 14) & 0x7fu; n2[0] |= (pin >> 21) & 0x7fu;
+#pragma unroll
+  for (int k = 0; k < kWPT; ++k)
+    if (w0 + k <= lastw) out[w0 + k] = make_uint4(no[k], n0[k], n1[k], n2[k]);
+  sumv = __reduce_add_sync(0xffffffffu, sumv);
+  if (lane == 0 && sumv) atomicAdd(&rec[g.t % kRecCap].sumv, static_cast<unsigned long long>(sumv));
+  if (has_last) {
+    carry_out[b] = make_uint4(co, c0, c1, c2);
+    counts_next[b] = ncars - __popc(co);  // the cars left in the block's own cells
+    if (b + 1 == nbb && co) atomicAdd(&rec[g.t % kRecCap].c, static_cast<unsigned int>(__popc(co)));
+  }
+}
+
+// cells (one byte per cell, 0xff = empty) -> planes; one thread per word.
+__global__ void grid_pack_kernel(const uint8_t* __restrict__ cells, uint32_t nwords, uint4* __restrict__ planes) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nwords) return;
+  const uint4* src = reinterpret_cast<const uint4*>(cells) + 2 * size_t(i);
+  const uint4 a = src[0], c = src[1];
+  const uint32_t ws[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  uint32_t o = 0, q0 = 0, q1 = 0, q2 = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t w = ws[q];
+    o |= (((__vcmpne4(w, 0xffffffffu) & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+    q0 |= (((w & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+    q1 |= ((((w >> 1) & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+    q2 |= ((((w >> 2) & 0x01010101u) * 0x01020408u) >> 24) << (4 * q);
+  }
+  planes[i] = make_uint4(o, q0 & o, q1 & o, q2 & o);
+}
+
+// planes (+ the carry words not yet folded in) -> cells; one thread per word.
+__global__ void grid_unpack_kernel(const uint4* __restrict__ planes, const uint4* __restrict__ carry,
+                                   uint32_t nwords, uint32_t nbb, uint8_t* __restrict__ cells) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nwords) return;
+  uint4 u = planes[i];
+  if (i % kWordsPerBlock == 0) {
+    const uint4 c = carry[(i / kWordsPerBlock + nbb - 1) % nbb];
+    u.x |= c.x; u.y |= c.y; u.z |= c.z; u.w |= c.w;
+  }
+  uint32_t ws[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const uint32_t e = (~u.x >> (4 * q)) & 0xfu, a = (u.y >> (4 * q)) & 0xfu, c = (u.z >> (4 * q)) & 0xfu,
+                   d = (u.w >> (4 * q)) & 0xfu;
+    // nibble bit i -> bit 8 i
+    ws[q] = (((e * 0x204081u) & 0x01010101u) * 0xffu) | ((a * 0x204081u) & 0x01010101u) |
+            (((c * 0x204081u) & 0x01010101u) << 1) | (((d * 0x204081u) & 0x01010101u) << 2);
+  }
+  uint4* dst = reinterpret_cast<uint4*>(cells) + 2 * size_t(i);
+  dst[0] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+  dst[1] = make_uint4(ws[4], ws[5], ws[6], ws[7]);
+}
+
+// Cars per block of kWordsPerBlock words.
+__global__ void __launch_bounds__(kTPB) grid_bitcount_kernel(const uint4* __restrict__ planes, uint32_t nwords,
+                                                             uint32_t* counts) {
+  __shared__ uint32_t s[kTPB / 32];
+  uint32_t c = 0;
+  for (int k = 0; k < kWPT; ++k) {
+    const uint32_t w = (blockIdx.x * kTPB + threadIdx.x) * kWPT + k;
+    if (w < nwords) c += __popc(planes[w].x);
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x / 32] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int w = 0; w < kTPB / 32; ++w) t += s[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+}  // namespace gridbits
+}  // namespace nb200

@@ -96,3 +96,61 @@ def test_grid_block_geometry_edges_vs_oracle(port, L, N, vmax, p, T):
     x, v = g.snapshot()
     assert (x == o["x"]).all() and (v == o["v"]).all()
     assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
+
+
+# --- bit-plane form (csrc/grid_bits.cuh): vmax <= 7 and L a multiple of 32 ---
+
+@pytest.mark.parametrize("L,N,vmax,p,T", [
+    (32, 5, 7, 0.3, 100),                  # one word: the carry returns into the word it left
+    (64, 64, 3, 0.5, 10),                  # every cell occupied
+    (96, 1, 7, 0.0, 200),                  # one car, no noise: laps of the ring through every carry
+    (16384, 3000, 5, 0.13, 80),            # exactly one 512-word block
+    (16384 + 32, 3500, 7, 0.4, 80),        # a one-word tail block
+    (16384 * 2 + 96, 20000, 6, 0.5, 60),   # a partial tail block, jammed
+    (32000, 200, 1, 0.9, 100),             # vmax = 1
+    (32768 * 3, 30000, 4, 0.25, 64),       # whole blocks at 4 words per thread too
+    (999968, 200000, 5, 0.25, 100)])       # ~61 blocks, C2's density
+def test_grid_bit_planes_vs_oracle(port, L, N, vmax, p, T):
+    """grid_bitmove_kernel against the oracle: word, warp, block and ring
+    seams, a mid-run state read (planes unpacked, stepping continues from the
+    planes) and the per-step series."""
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 21)
+    o = port.run(L, vmax, p, 6, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    g = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=6), 1, GRID)
+    g.set_state(x0, v0)
+    g.advance(T // 3)
+    xm, vm = g.snapshot()
+    assert (xm[1:] > xm[:-1]).all() and int(vm.sum()) == int(g.sumv_series()[-1])
+    g.advance(T - T // 3)
+    x, v = g.snapshot()
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
+    assert g.checksum == o["checksum"]
+
+
+def test_grid_bit_planes_equal_agent_and_bytes_random_sweep(monkeypatch):
+    """Random rings with L a multiple of 32: the bit-plane grid, the
+    byte-per-cell grid (NASCH_B200_GRID_BYTES=1) and the agent engine agree
+    on every step's state (checksum), the series and the observables."""
+    rd = random.Random(20261021)
+    for trial in range(30):
+        L = 32 * (1 + rd.randrange(40))
+        N = 1 + rd.randrange(L)
+        vmax = 1 + rd.randrange(7)
+        p = rd.randrange(10001) / 10000.0
+        T = 1 + rd.randrange(120)
+        prm = nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=rd.getrandbits(64))
+        a = nasch.Engine(prm, 1, nasch.Engine.AGENT)
+        g = nasch.Engine(prm, 1, GRID)
+        monkeypatch.setenv("NASCH_B200_GRID_BYTES", "1")
+        gb = nasch.Engine(prm, 1, GRID)
+        monkeypatch.delenv("NASCH_B200_GRID_BYTES")
+        for e in (a, g, gb):
+            e.run()
+        assert a.checksum == g.checksum == gb.checksum, trial
+        xa, va = a.snapshot()
+        for e in (g, gb):
+            xg, vg = e.snapshot()
+            assert (xa == xg).all() and (va == vg).all()
+            assert (a.sumv_series() == e.sumv_series()).all()
+            assert a.observables() == e.observables()
