@@ -128,15 +128,11 @@ __device__ __forceinline__ uint32_t apow_rank(const uint32_t* pw, uint32_t r) {
 // reaches the move kernel as two independent loads (round 2: a rank load
 // then three dependent table loads).  (A single-block scan fused with the
 // spill fixup measured 23 us against ~10 us for these two launches.)
-// (Bit-plane form: a block's cars are those in its words plus the cars the
-// previous block carried over its end, still in `carry`.)
 __global__ void __launch_bounds__(1024) grid_scan_local(const uint32_t* counts, uint32_t nb, uint32_t* local,
-                                                        uint32_t* group, const uint32_t* pw, uint32_t* plocal,
-                                                        const uint4* carry) {
+                                                        uint32_t* group, const uint32_t* pw, uint32_t* plocal) {
   __shared__ uint32_t s_w[32], s_tot;
   const uint32_t i = blockIdx.x * 1024u + threadIdx.x;
-  uint32_t v = i < nb ? counts[i] : 0u;
-  if (carry && i < nb) v += __popc(carry[(i + nb - 1) % nb].x);
+  const uint32_t v = i < nb ? counts[i] : 0u;
   const uint32_t ex = block_excl_scan_1024(v, s_w, &s_tot);
   if (i < nb) {
     local[i] = ex;
@@ -424,8 +420,9 @@ struct GpuGrid::Impl {
   uint4* planes[2] = {nullptr, nullptr};
   uint4* carry[2] = {nullptr, nullptr};  // per block: the cars carried over its end by the last move
   uint32_t* bcounts[2] = {nullptr, nullptr};
+  uint32_t* prank = nullptr;  // a^(rank of each block's first car), kept current by the moves
   int pcur = 0;
-  uint32_t nwords = 0, nbb = 0, ngb = 0;
+  uint32_t nwords = 0, nbb = 0;
   bool planes_valid = false;  // planes[pcur] (+ carry[pcur]) hold the current state
   bool cells_valid = true;    // cells[cur] holds the current state
   ~Impl();
@@ -435,8 +432,10 @@ struct GpuGrid::Impl {
     gridbits::grid_pack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(cells[cur], nwords, planes[pcur]);
     CKG(cudaMemsetAsync(carry[pcur], 0, size_t(nbb) * sizeof(uint4), stream));
     gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, bcounts[pcur]);
+    gridbits::grid_bits_scan_kernel<<<1, gridbits::kTPB, 0, stream>>>(bcounts[pcur], carry[pcur], nbb, pw,
+                                                                     prank, rec + (steps_done % kRecCap));
     CKG(cudaGetLastError());
-    launches += 2;
+    launches += 3;
     planes_valid = true;
   }
 
@@ -454,16 +453,21 @@ struct GpuGrid::Impl {
   template <int VMAX>
   void launch_bitmove(const gridbits::BitArgs& g) {
     gridbits::grid_bitmove_kernel<VMAX><<<nbb, gridbits::kTPB, 0, stream>>>(
-        planes[pcur], planes[pcur ^ 1], carry[pcur], carry[pcur ^ 1], plocal, pgroup, g, rec, bcounts[pcur ^ 1]);
+        planes[pcur], planes[pcur ^ 1], carry[pcur], carry[pcur ^ 1], prank, g, rec);
   }
 
   void step_bits() {
     if (steps_done - drained >= kRecCap / 2) drain();
     if (!planes_valid) pack();
     const uint32_t E = mulmod(seeded(params.seed), powmod(kA, draw_exponent(steps_done, N, 0)));
-    const gridbits::BitArgs g{nwords, deceleration_threshold(params.p), E, 2 * kA, pw, steps_done};
-    grid_scan_local<<<ngb, 1024, 0, stream>>>(bcounts[pcur], nbb, local, group, pw, plocal, carry[pcur]);
-    grid_scan_top<<<1, 1024, 0, stream>>>(group, ngb, pw, pgroup, rec + (steps_done % kRecCap));
+    gridbits::BitArgs g{nwords, deceleration_threshold(params.p), E, 2 * kA, 1u, 2u,
+                        {1u, 2u, 4u, 8u, 16u, 32u, 64u, 128u}, {}, {}, pw, steps_done};
+    const uint32_t ainv1 = powmod(kA, kOrder - 1);  // a^-1 (Fermat)
+    g.apw[0] = g.ainv[0] = 1;
+    for (int k = 1; k < 8; ++k) {
+      g.apw[k] = mulmod(g.apw[k - 1], kA);
+      g.ainv[k] = mulmod(g.ainv[k - 1], ainv1);
+    }
     switch (vmax) {
       case 1: launch_bitmove<1>(g); break;
       case 2: launch_bitmove<2>(g); break;
@@ -474,7 +478,7 @@ struct GpuGrid::Impl {
       default: launch_bitmove<7>(g); break;
     }
     CKG(cudaGetLastError());
-    launches += 3;
+    ++launches;
     pcur ^= 1;
     cells_valid = false;
     ++steps_done;
@@ -491,7 +495,7 @@ struct GpuGrid::Impl {
   }
 
   void scan(StepRec* zero) {
-    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group, pw, plocal, nullptr);
+    grid_scan_local<<<ng, 1024, 0, stream>>>(counts, nb, local, group, pw, plocal);
     grid_scan_top<<<1, 1024, 0, stream>>>(group, ng, pw, pgroup, zero);
   }
 
@@ -647,12 +651,12 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   if (d.bitmode) {
     d.nwords = d.L / 32;
     d.nbb = (d.nwords + gridbits::kWordsPerBlock - 1) / gridbits::kWordsPerBlock;
-    d.ngb = (d.nbb + 1023) / 1024;
     for (int b = 0; b < 2; ++b) {
       CKG(cudaMalloc(&d.planes[b], size_t(d.nwords) * sizeof(uint4)));
       CKG(cudaMalloc(&d.carry[b], size_t(d.nbb) * sizeof(uint4)));
       CKG(cudaMalloc(&d.bcounts[b], size_t(d.nbb) * 4));
     }
+    CKG(cudaMalloc(&d.prank, size_t(d.nbb) * 4));
   }
   CKG(cudaMemsetAsync(d.cells[0], kEmpty, d.L, d.stream));
   grid_init_kernel<<<std::max(1u, std::min(4096u, (d.N + 255) / 256)), 256, 0, d.stream>>>(d.cells[0], d.L, d.N);
@@ -687,6 +691,7 @@ GpuGrid::Impl::~Impl() {
     cudaFree(carry[b]);
     cudaFree(bcounts[b]);
   }
+  cudaFree(prank);
   cudaFreeHost(hrec);
   cudaFreeHost(hx);
   cudaFreeHost(hv);

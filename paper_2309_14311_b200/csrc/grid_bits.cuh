@@ -41,7 +41,11 @@ struct BitArgs {
   uint32_t tp;         // deceleration threshold
   uint32_t E;          // s0 a^(t N + 1)
   uint32_t a2;         // 2 a
-  const uint32_t* pw;  // [2][4096]: a^j, a^(4096 j)
+  uint32_t one, two;   // 1 and 2 as launch parameters: keep the compare IMADs (FMA pipe; the kernel is ALU-pipe bound)
+  uint32_t p2[8];      // 2^d, likewise
+  uint32_t apw[8];     // a^k
+  uint32_t ainv[8];    // a^-k
+  const uint32_t* pw;  // [3][4096]: a^j, a^(4096 j), a^(4096^2 j)
   unsigned long long t;
 };
 
@@ -83,29 +87,94 @@ __device__ __forceinline__ void word_rule(uint32_t o, uint32_t p0, uint32_t p1, 
   }
 }
 
+// a^r from the three power tables pw = [a^j, a^(4096 j), a^(4096^2 j)], j < 4096.
+__device__ __forceinline__ uint32_t apow3(const uint32_t* pw, uint32_t r) {
+  return mulmod(mulmod(__ldg(pw + (r & 4095u)), __ldg(pw + 4096 + ((r >> 12) & 4095u))),
+                __ldg(pw + 8192 + (r >> 24)));
+}
+
+// The exclusive scan of the blocks' car counts by ONE block of kTPB threads:
+// prank[b] = a^(rank of block b's first car), a block's cars being those in
+// its words plus the ones the previous block carried over its end.  Runs
+// after a pack only (the moves keep prank current themselves, below).
+// Thread t scans a contiguous range of blocks.
+__device__ __forceinline__ void scan_blocks(const uint32_t* counts, const uint4* carry, uint32_t nbb,
+                                            const uint32_t* __restrict__ pw, uint32_t* prank, uint32_t* s_scan) {
+  constexpr int B = 16;  // entries in flight per thread: the loads of a batch are independent
+  const uint32_t per = (nbb + kTPB - 1) / kTPB;
+  const uint32_t i0 = min(threadIdx.x * per, nbb), i1 = min(i0 + per, nbb);
+  uint32_t sum = 0;
+  for (uint32_t base = i0; base < i1; base += B) {
+    uint32_t c[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t i = base + j;
+      c[j] = i < i1 ? __ldcg(counts + i) + __popc(__ldcg(&carry[(i ? i : nbb) - 1].x)) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) sum += c[j];
+  }
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl = sum;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, s);
+    if (lane >= static_cast<uint32_t>(s)) incl += n;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  uint32_t r = incl - sum;
+  for (uint32_t w = 0; w < warp; ++w) r += s_scan[w];
+  for (uint32_t base = i0; base < i1; base += B) {
+    uint32_t c[B], rr[B];
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      const uint32_t i = base + j;
+      c[j] = i < i1 ? __ldcg(counts + i) + __popc(__ldcg(&carry[(i ? i : nbb) - 1].x)) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j) {
+      rr[j] = r;
+      r += c[j];
+    }
+#pragma unroll
+    for (int j = 0; j < B; ++j)
+      if (base + j < i1) prank[base + j] = apow3(pw, rr[j]);
+  }
+}
+
+__global__ void __launch_bounds__(kTPB) grid_bits_scan_kernel(const uint32_t* counts, const uint4* carry,
+                                                              uint32_t nbb, const uint32_t* pw, uint32_t* prank,
+                                                              StepRec* zero) {
+  __shared__ uint32_t s_scan[kTPB / 32];
+  scan_blocks(counts, carry, nbb, pw, prank, s_scan);
+  if (threadIdx.x == 0) {
+    zero->sumv = 0;
+    zero->c = 0;
+  }
+}
+
 // The move of one step over the bit planes.  Block b owns words
 // [b kWordsPerBlock, ...), thread t the kWPT consecutive words from
-// (b kTPB + t) kWPT.
-template <int VMAX>
-__global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
-                                                            const uint4* __restrict__ carry_in,
-                                                            uint4* __restrict__ carry_out,
-                                                            const uint32_t* __restrict__ plocal,
-                                                            const uint32_t* __restrict__ pgroup, BitArgs g,
-                                                            StepRec* rec, uint32_t* counts_next) {
+// (b kTPB + t) kWPT.  PARTIAL: the ring's last block when it is not whole
+// (dead words read as empty, the last live word anywhere in the block).
+template <int VMAX, bool PARTIAL>
+__device__ __forceinline__ void bitmove_block(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                              const uint4* __restrict__ carry_in, uint4* __restrict__ carry_out,
+                                              uint32_t* prank, const BitArgs& g, StepRec* rec, uint32_t* s_cnt,
+                                              uint32_t* s_first, uint32_t* s_hi) {
   constexpr int NW = kTPB / 32;
-  __shared__ uint32_t s_cnt[NW], s_first[NW + 1], s_hi[NW];
   const uint32_t b = blockIdx.x, nbb = gridDim.x;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint32_t w0 = (b * kTPB + threadIdx.x) * kWPT;
-  const uint32_t lastw = min((b + 1) * kWordsPerBlock, g.nwords) - 1u;  // the block's last live word
-  const bool has_last = w0 <= lastw && lastw < w0 + kWPT;
+  const uint32_t lastw = PARTIAL ? g.nwords - 1u : (b + 1) * kWordsPerBlock - 1u;  // the block's last live word
+  const bool has_last = PARTIAL ? (w0 <= lastw && lastw < w0 + kWPT) : threadIdx.x == kTPB - 1;
   // every global load first
   uint32_t o[kWPT], p0[kWPT], p1[kWPT], p2[kWPT];
 #pragma unroll
   for (int k = 0; k < kWPT; ++k) {
     uint4 u = make_uint4(0, 0, 0, 0);
-    if (w0 + k < g.nwords) u = __ldg(in + w0 + k);
+    if (!PARTIAL || w0 + k <= lastw) u = __ldg(in + w0 + k);
     o[k] = u.x; p0[k] = u.y; p1[k] = u.z; p2[k] = u.w;
   }
   uint32_t nxt_global = 0;
@@ -113,11 +182,13 @@ __global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restr
     const uint32_t wn = b + 1 == nbb ? 0u : (b + 1) * kWordsPerBlock;
     nxt_global = __ldg(in + wn).x | __ldg(carry_in + b).x;
   }
-  if (threadIdx.x == 0) {  // the cars the previous block carried over its end last step
-    const uint4 c = __ldg(carry_in + (b + nbb - 1) % nbb);
-    o[0] |= c.x; p0[0] |= c.y; p1[0] |= c.z; p2[0] |= c.w;
+  const uint4 cprev = __ldg(carry_in + (b + nbb - 1) % nbb);  // the cars the previous block carried over its end
+  const uint32_t wrapped = __popc(__ldg(carry_in + nbb - 1).x);
+  if (threadIdx.x == 0) {
+    o[0] |= cprev.x; p0[0] |= cprev.y; p1[0] |= cprev.z; p2[0] |= cprev.w;
   }
-  const uint32_t pl = __ldg(plocal + b), pg = __ldg(pgroup + (b >> 10));
+  // a^(rank of the block's first car): last step's, times a^wrapped a^-carried
+  const uint32_t pr = mulmod_d(mulmod_d(__ldcg(prank + b), g.apw[wrapped]), g.ainv[__popc(cprev.x)]);
   // ranks: block scan of the popcounts
   uint32_t cnt = 0;
 #pragma unroll
@@ -133,30 +204,37 @@ __global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restr
   __syncthreads();
   const uint32_t cw = lane < static_cast<uint32_t>(NW) ? s_cnt[lane] : 0u;
   const uint32_t wbase = __reduce_add_sync(0xffffffffu, lane < warp ? cw : 0u);
-  const uint32_t ncars = __reduce_add_sync(0xffffffffu, cw);
   const uint32_t j0 = wbase + incl - cnt;  // block-local rank of this thread's first car
   uint32_t nxt_thread = __shfl_down_sync(0xffffffffu, o[0], 1);
-  if (lane == 31) nxt_thread = warp + 1 < static_cast<uint32_t>(NW) ? s_first[warp + 1] : 0u;
-  const uint32_t Eb = mulmod_d(mulmod_d(g.E, pl), pg);  // E a^(rank of the block's first car)
+  if (lane == 31) nxt_thread = warp + 1 < static_cast<uint32_t>(NW) ? s_first[warp + 1] : nxt_global;
+  const uint32_t Eb = mulmod_d(g.E, pr);  // E a^(rank of the block's first car)
   uint32_t Q = mulmod_d(mulmod_d(Eb, __ldg(g.pw + (j0 & 4095u))), __ldg(g.pw + 4096 + (j0 >> 12)));
 
   uint32_t no[kWPT], n0[kWPT], n1[kWPT], n2[kWPT];  // the next array's words
   uint32_t ho = 0, h0 = 0, h1 = 0, h2 = 0;          // bits leaving the previous word
   uint32_t co = 0, c0 = 0, c1 = 0, c2 = 0;          // ... leaving the block's last word
   uint32_t sumv = 0;
+  const uint32_t ntp = 0u - g.tp;
 #pragma unroll
   for (int k = 0; k < kWPT; ++k) {
     uint32_t nx = k + 1 < kWPT ? o[k + 1 < kWPT ? k + 1 : k] : nxt_thread;
-    if (w0 + k == lastw) nx = nxt_global;
+    if (PARTIAL && w0 + k == lastw) nx = nxt_global;
     uint32_t vc[VMAX + 2];
     word_rule<VMAX>(o[k], p0[k], p1[k], p2[k], nx, vc);
-    // the draws, one per car in ascending cell order (model.cpp:51: always consumed)
+    // The draws, one per car in ascending cell order (model.cpp:51: always
+    // consumed).  s < tp as bit 31 of s - tp (both below 2^31), moved to bit 0
+    // by a multiply-high and selected by a multiply-add: three FMA-pipe
+    // instructions (1 and 2 are launch parameters so that they stay IMADs)
+    // instead of ISETP + SEL + LOP3 on the ALU pipe, which bounds the kernel.
     uint32_t dec = 0;
     for (uint32_t m = o[k]; m;) {
       const uint32_t s = Q;
       Q = mulmod_x2(g.a2, Q);
+      uint32_t lt;
+      asm("{ .reg .u32 t; mad.lo.u32 t, %1, %2, %3; mul.hi.u32 %0, t, %4; }"
+          : "=r"(lt) : "r"(s), "r"(g.one), "r"(ntp), "r"(g.two));
       const uint32_t bit = m & (0u - m);
-      if (s < g.tp) dec |= bit;
+      dec += lt * bit;
       m ^= bit;
     }
     uint32_t lo_o, lo_0 = 0, lo_1 = 0, lo_2 = 0, hi_o = 0, hi_0 = 0, hi_1 = 0, hi_2 = 0;
@@ -168,7 +246,9 @@ __global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restr
       sumv += __popc(vp);
       const uint32_t X = vp & ~vnext;  // v' == d
       vnext = vp;
-      const uint32_t l = X << d, h = X >> (32 - d);
+      // X >> (32 - d) as the high word of X 2^d (2^d a launch parameter: an
+      // IMAD.HI on the FMA pipe, not a shift on the ALU pipe)
+      const uint32_t l = X << d, h = __umulhi(X, g.p2[d]);
       stay |= l;
       hi_o |= h;
       if (d & 1) { lo_0 |= l; hi_0 |= h; }
@@ -178,8 +258,9 @@ __global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restr
     lo_o = stay | (o[k] & ~vnext);  // v' == 0 stays
     no[k] = lo_o | ho; n0[k] = lo_0 | h0; n1[k] = lo_1 | h1; n2[k] = lo_2 | h2;
     ho = hi_o; h0 = hi_0; h1 = hi_1; h2 = hi_2;
-    if (w0 + k == lastw) { co = hi_o; c0 = hi_0; c1 = hi_1; c2 = hi_2; }
+    if (PARTIAL && w0 + k == lastw) { co = hi_o; c0 = hi_0; c1 = hi_1; c2 = hi_2; }
   }
+  if (!PARTIAL) { co = ho; c0 = h0; c1 = h1; c2 = h2; }  // read by the has_last thread only
   // the last word's overflow to the next thread's first word (<= 7 bits a plane)
   const uint32_t pk = ho | (h0 << 7) | (h1 << 14) | (h2 << 21);
   uint32_t pin = __shfl_up_sync(0xffffffffu, pk, 1);
@@ -189,14 +270,41 @@ __global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restr
   no[0] |= pin & 0x7fu; n0[0] |= (pin >> 7) & 0x7fu; n1[0] |= (pin >> 14) & 0x7fu; n2[0] |= (pin >> 21) & 0x7fu;
 #pragma unroll
   for (int k = 0; k < kWPT; ++k)
-    if (w0 + k <= lastw) out[w0 + k] = make_uint4(no[k], n0[k], n1[k], n2[k]);
+    if (!PARTIAL || w0 + k <= lastw) out[w0 + k] = make_uint4(no[k], n0[k], n1[k], n2[k]);
   sumv = __reduce_add_sync(0xffffffffu, sumv);
   if (lane == 0 && sumv) atomicAdd(&rec[g.t % kRecCap].sumv, static_cast<unsigned long long>(sumv));
   if (has_last) {
     carry_out[b] = make_uint4(co, c0, c1, c2);
-    counts_next[b] = ncars - __popc(co);  // the cars left in the block's own cells
     if (b + 1 == nbb && co) atomicAdd(&rec[g.t % kRecCap].c, static_cast<unsigned int>(__popc(co)));
   }
+  if (threadIdx.x == 0) {
+    prank[b] = pr;
+    if (b == 0) {  // the next step's record
+      StepRec* nr = rec + ((g.t + 1) % kRecCap);
+      nr->sumv = 0;
+      nr->c = 0;
+    }
+  }
+}
+
+// One step is ONE launch.  No scan between steps: cars never overtake, so the
+// rank of a block's first car changes from one step to the next by the cars
+// that wrapped past the ring's end (they take the lowest ranks) minus the
+// cars the previous block carried over this block's start (they precede the
+// block's own cars) -- both are popcounts of last step's carry words, which
+// the block reads anyway.  Each block keeps a^(its rank) in prank[b] and
+// advances it by a^wrapped a^-carried.
+template <int VMAX>
+__global__ void __launch_bounds__(kTPB) grid_bitmove_kernel(const uint4* __restrict__ in, uint4* __restrict__ out,
+                                                            const uint4* __restrict__ carry_in,
+                                                            uint4* __restrict__ carry_out, uint32_t* prank,
+                                                            BitArgs g, StepRec* rec) {
+  constexpr int NW = kTPB / 32;
+  __shared__ uint32_t s_cnt[NW], s_first[NW + 1], s_hi[NW];
+  if ((blockIdx.x + 1) * kWordsPerBlock <= g.nwords)
+    bitmove_block<VMAX, false>(in, out, carry_in, carry_out, prank, g, rec, s_cnt, s_first, s_hi);
+  else
+    bitmove_block<VMAX, true>(in, out, carry_in, carry_out, prank, g, rec, s_cnt, s_first, s_hi);
 }
 
 // cells (one byte per cell, 0xff = empty) -> planes; one thread per word.

@@ -6,9 +6,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2309_14311_b200 import nasch  # noqa: E402
 
-L, N = 10**8, 2 * 10**7
+L, N = 10**8, int(sys.argv[1]) if len(sys.argv) > 1 else 2 * 10**7
+p = float(sys.argv[2]) if len(sys.argv) > 2 else 0.13
 x, v = nasch.fill_uniform_state(L, N, 5, 3)
-e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=5, p=0.13, steps=12, seed=3), 1,
+e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=5, p=p, steps=12, seed=3), 1,
                  nasch.Engine.GRID_REFERENCE)
 e.set_checksum(False)
 e.set_state(x, v)
