@@ -423,6 +423,7 @@ struct GpuGrid::Impl {
   uint32_t* prank = nullptr;  // a^(rank of each block's first car), kept current by the moves
   int pcur = 0;
   uint32_t nwords = 0, nbb = 0;
+  int wpt = 2;  // words per thread of the move kernel (grid_bits.cuh)
   bool planes_valid = false;  // planes[pcur] (+ carry[pcur]) hold the current state
   bool cells_valid = true;    // cells[cur] holds the current state
   ~Impl();
@@ -431,7 +432,7 @@ struct GpuGrid::Impl {
   void pack() {
     gridbits::grid_pack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(cells[cur], nwords, planes[pcur]);
     CKG(cudaMemsetAsync(carry[pcur], 0, size_t(nbb) * sizeof(uint4), stream));
-    gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, bcounts[pcur]);
+    gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, wpt, bcounts[pcur]);
     gridbits::grid_bits_scan_kernel<<<1, gridbits::kTPB, 0, stream>>>(bcounts[pcur], carry[pcur], nbb, pw,
                                                                      prank, rec + (steps_done % kRecCap));
     CKG(cudaGetLastError());
@@ -442,18 +443,24 @@ struct GpuGrid::Impl {
   // planes -> cells[cur] for the readers.
   void ensure_cells() {
     if (!bitmode || cells_valid) return;
-    gridbits::grid_unpack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(planes[pcur], carry[pcur], nwords, nbb,
-                                                                          cells[cur]);
+    gridbits::grid_unpack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(
+        planes[pcur], carry[pcur], nwords, nbb, gridbits::words_per_block(wpt), cells[cur]);
     CKG(cudaGetLastError());
     ++launches;
     cells_valid = true;
     counts_valid = false;
   }
 
+  template <int VMAX, int WPT>
+  void launch_bitmove_w(const gridbits::BitArgs& g) {
+    gridbits::grid_bitmove_kernel<VMAX, WPT><<<nbb, gridbits::kTPB, 0, stream>>>(
+        planes[pcur], planes[pcur ^ 1], carry[pcur], carry[pcur ^ 1], prank, g, rec);
+  }
   template <int VMAX>
   void launch_bitmove(const gridbits::BitArgs& g) {
-    gridbits::grid_bitmove_kernel<VMAX><<<nbb, gridbits::kTPB, 0, stream>>>(
-        planes[pcur], planes[pcur ^ 1], carry[pcur], carry[pcur ^ 1], prank, g, rec);
+    if (wpt == 4) launch_bitmove_w<VMAX, 4>(g);
+    else if (wpt == 2) launch_bitmove_w<VMAX, 2>(g);
+    else launch_bitmove_w<VMAX, 1>(g);
   }
 
   void step_bits() {
@@ -650,7 +657,14 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
   }
   if (d.bitmode) {
     d.nwords = d.L / 32;
-    d.nbb = (d.nwords + gridbits::kWordsPerBlock - 1) / gridbits::kWordsPerBlock;
+    // enough blocks for a few waves of the 148 SMs before more words per thread
+    d.wpt = d.nwords >= 4u * 256 * 148 * 4 ? 4 : d.nwords >= 2u * 256 * 148 * 2 ? 2 : 1;
+    if (const char* w = std::getenv("NASCH_B200_GRID_WPT")) {  // 1, 2 or 4: geometry experiments and tests
+      const int v = std::atoi(w);
+      if (v == 1 || v == 2 || v == 4) d.wpt = v;
+    }
+    const uint32_t wpb = gridbits::words_per_block(d.wpt);
+    d.nbb = (d.nwords + wpb - 1) / wpb;
     for (int b = 0; b < 2; ++b) {
       CKG(cudaMalloc(&d.planes[b], size_t(d.nwords) * sizeof(uint4)));
       CKG(cudaMalloc(&d.carry[b], size_t(d.nbb) * sizeof(uint4)));

@@ -154,3 +154,22 @@ def test_grid_bit_planes_equal_agent_and_bytes_random_sweep(monkeypatch):
             assert (xa == xg).all() and (va == vg).all()
             assert (a.sumv_series() == e.sumv_series()).all()
             assert a.observables() == e.observables()
+
+
+@pytest.mark.parametrize("wpt", [1, 2, 4])
+def test_grid_bit_planes_words_per_thread(port, monkeypatch, wpt):
+    """Every instantiation of the move kernel (1, 2 or 4 words per thread;
+    the engine picks by ring size, NASCH_B200_GRID_WPT forces one) on rings
+    with a partial tail block for that geometry, against the oracle."""
+    monkeypatch.setenv("NASCH_B200_GRID_WPT", str(wpt))
+    for L, N, vmax, p, T in [(256 * wpt * 32 * 2 + 64, 9000 * wpt, 5, 0.3, 50),
+                             (256 * wpt * 32, 2000 * wpt, 7, 0.6, 40), (96, 40, 2, 0.2, 30)]:
+        x0, v0 = nasch.fill_uniform_state(L, N, vmax, 31)
+        o = port.run(L, vmax, p, 8, T, x0.astype(np.uint64), v0.astype(np.uint64))
+        g = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=8), 1, GRID)
+        g.set_state(x0, v0)
+        g.run()
+        x, v = g.snapshot()
+        assert (x == o["x"]).all() and (v == o["v"]).all()
+        assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
+        assert g.checksum == o["checksum"]
