@@ -4,8 +4,10 @@ GPU, csrc/grid.cu) against its HBM roofline, one GPU.
   python tools/grid_bench.py [--out profiles/r01_grid.json]
 
 One step reads the L cells and writes the L cells of the next array:
-algorithmic bytes per step = 2 L (one byte per cell; round 1 also made a
-count pass and was quoted against 3 L, reported too as hbm_frac_3L).
+algorithmic bytes per step = 2 L at one byte per cell (round 1 also made a
+count pass and was quoted against 3 L, reported too as hbm_frac_3L).  The
+bit-plane form (csrc/grid_bits.cuh; vmax <= 7, L % 32 == 0) moves half a
+byte per cell each way; its rows are still quoted against 2 L / 3 L.
 CUDA-event time on the engine stream, state resident, checksum off."""
 import argparse
 import json
