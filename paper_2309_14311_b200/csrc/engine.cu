@@ -778,6 +778,7 @@ struct GpuRing::Impl {
       CK(cudaMemcpyAsync(static_cast<char*>(jv) + a * vbytes, static_cast<char*>(hv) + a * vbytes,
                          (b - a) * vbytes, cudaMemcpyHostToDevice, jstream[0]));
       eup[c] = event(jstream[0]);
+      if (trace) std::fprintf(stderr, "[job32] chunk %u enqueued at host %.2f ms\n", c, host_ms());
     };
     auto wait_chunk = [&](uint32_t c) { CK(cudaStreamWaitEvent(stream, eup[c], 0)); };
     // the control block for the loaded state (W = 0), cleared records, the

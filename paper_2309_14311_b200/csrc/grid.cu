@@ -414,8 +414,9 @@ struct GpuGrid::Impl {
   Ctl* dctl = nullptr;   // the compacted row's control block: W = 0, buf = 0
   RingArgs rowargs{};    // (xs, vs) as a RingArgs for the digest kernels
   // Bit-plane form (grid_bits.cuh; vmax <= 7 and L a multiple of 32): the
-  // planes are the state the steps run on, cells[cur] a view unpacked for
-  // the readers (state, frames, checksum).
+  // planes are the state the steps run on; cells[cur] only carries a loaded
+  // state to the pack.  The readers (state, frames, checksum) compact their
+  // rank-ordered row from the planes.
   bool bitmode = false;
   uint4* planes[2] = {nullptr, nullptr};
   uint4* carry[2] = {nullptr, nullptr};  // per block: the cars carried over its end by the last move
@@ -438,17 +439,6 @@ struct GpuGrid::Impl {
     CKG(cudaGetLastError());
     launches += 3;
     planes_valid = true;
-  }
-
-  // planes -> cells[cur] for the readers.
-  void ensure_cells() {
-    if (!bitmode || cells_valid) return;
-    gridbits::grid_unpack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(
-        planes[pcur], carry[pcur], nwords, nbb, gridbits::words_per_block(wpt), cells[cur]);
-    CKG(cudaGetLastError());
-    ++launches;
-    cells_valid = true;
-    counts_valid = false;
   }
 
   template <int VMAX, int WPT>
@@ -507,7 +497,17 @@ struct GpuGrid::Impl {
   }
 
   void compact() {
-    ensure_cells();
+    if (bitmode && !cells_valid) {  // the row straight from the planes (cells[cur] is stale)
+      const uint32_t wpb = gridbits::words_per_block(wpt);
+      gridbits::grid_bits_rowcount_kernel<<<nb, 256, 0, stream>>>(planes[pcur], carry[pcur], nwords, nbb, wpb,
+                                                                  counts);
+      scan(nullptr);
+      gridbits::grid_bits_row_kernel<<<nb, 256, 0, stream>>>(planes[pcur], carry[pcur], nwords, nbb, wpb, local,
+                                                             group, xs, vs);
+      CKG(cudaGetLastError());
+      launches += 4;
+      return;
+    }
     flush();
     grid_count_kernel<<<nb, kGridTPB, 0, stream>>>(cells[cur], L, counts);
     counts_valid = true;

@@ -326,28 +326,65 @@ __global__ void grid_pack_kernel(const uint8_t* __restrict__ cells, uint32_t nwo
   planes[i] = make_uint4(o, q0 & o, q1 & o, q2 & o);
 }
 
-// planes (+ the carry words not yet folded in) -> cells; one thread per word.
-__global__ void grid_unpack_kernel(const uint4* __restrict__ planes, const uint4* __restrict__ carry,
-                                   uint32_t nwords, uint32_t nbb, uint32_t wpb, uint8_t* __restrict__ cells) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= nwords) return;
-  uint4 u = planes[i];
-  if (i % wpb == 0) {
-    const uint4 c = carry[(i / wpb + nbb - 1) % nbb];
+// The readers' rank-ordered row (state, frames, checksum) straight from the
+// planes, in 256-word (8192-cell) blocks like the byte form's compaction:
+// a word's cars are its own plus, for the first word of a move block, the
+// cars the previous move block carried over its end (still in `carry`).
+__device__ __forceinline__ uint4 word_with_carry(const uint4* __restrict__ planes, const uint4* __restrict__ carry,
+                                                 uint32_t w, uint32_t nbb, uint32_t wpb) {
+  uint4 u = planes[w];
+  if (w % wpb == 0) {
+    const uint4 c = carry[(w / wpb + nbb - 1) % nbb];
     u.x |= c.x; u.y |= c.y; u.z |= c.z; u.w |= c.w;
   }
-  uint32_t ws[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const uint32_t e = (~u.x >> (4 * q)) & 0xfu, a = (u.y >> (4 * q)) & 0xfu, c = (u.z >> (4 * q)) & 0xfu,
-                   d = (u.w >> (4 * q)) & 0xfu;
-    // nibble bit i -> bit 8 i
-    ws[q] = (((e * 0x204081u) & 0x01010101u) * 0xffu) | ((a * 0x204081u) & 0x01010101u) |
-            (((c * 0x204081u) & 0x01010101u) << 1) | (((d * 0x204081u) & 0x01010101u) << 2);
+  return u;
+}
+
+__global__ void __launch_bounds__(256) grid_bits_rowcount_kernel(const uint4* __restrict__ planes,
+                                                                 const uint4* __restrict__ carry, uint32_t nwords,
+                                                                 uint32_t nbb, uint32_t wpb, uint32_t* counts) {
+  __shared__ uint32_t s[8];
+  const uint32_t w = blockIdx.x * 256u + threadIdx.x;
+  uint32_t c = w < nwords ? __popc(word_with_carry(planes, carry, w, nbb, wpb).x) : 0u;
+  c = __reduce_add_sync(0xffffffffu, c);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x / 32] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t t = 0;
+    for (int k = 0; k < 8; ++k) t += s[k];
+    counts[blockIdx.x] = t;
   }
-  uint4* dst = reinterpret_cast<uint4*>(cells) + 2 * size_t(i);
-  dst[0] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
-  dst[1] = make_uint4(ws[4], ws[5], ws[6], ws[7]);
+}
+
+// local/group: the two-level exclusive scan of the row counts (grid.cu).
+__global__ void __launch_bounds__(256) grid_bits_row_kernel(const uint4* __restrict__ planes,
+                                                            const uint4* __restrict__ carry, uint32_t nwords,
+                                                            uint32_t nbb, uint32_t wpb,
+                                                            const uint32_t* __restrict__ local,
+                                                            const uint32_t* __restrict__ group, uint32_t* xs,
+                                                            uint8_t* vs) {
+  __shared__ uint32_t s_w[8];
+  const uint32_t w = blockIdx.x * 256u + threadIdx.x;
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint4 u = make_uint4(0, 0, 0, 0);
+  if (w < nwords) u = word_with_carry(planes, carry, w, nbb, wpb);
+  const uint32_t cnt = __popc(u.x);
+  uint32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += n;
+  }
+  if (lane == 31) s_w[warp] = incl;
+  __syncthreads();
+  uint32_t r = local[blockIdx.x] + group[blockIdx.x >> 10] + incl - cnt;
+  for (uint32_t k = 0; k < warp; ++k) r += s_w[k];
+  for (uint32_t m = u.x; m; m &= m - 1u) {
+    const uint32_t pos = __ffs(m) - 1u;
+    xs[r] = w * 32u + pos;
+    vs[r] = static_cast<uint8_t>(((u.y >> pos) & 1u) | (((u.z >> pos) & 1u) << 1) | (((u.w >> pos) & 1u) << 2));
+    ++r;
+  }
 }
 
 // Cars per block of kTPB wpt words.
