@@ -420,7 +420,7 @@ struct GpuGrid::Impl {
   bool bitmode = false;
   uint4* planes[2] = {nullptr, nullptr};
   uint4* carry[2] = {nullptr, nullptr};  // per block: the cars carried over its end by the last move
-  uint32_t* bcounts[2] = {nullptr, nullptr};
+  uint32_t* bcounts = nullptr;  // cars per move block, for the scan after a pack
   uint32_t* prank = nullptr;  // a^(rank of each block's first car), kept current by the moves
   int pcur = 0;
   uint32_t nwords = 0, nbb = 0;
@@ -433,8 +433,8 @@ struct GpuGrid::Impl {
   void pack() {
     gridbits::grid_pack_kernel<<<(nwords + 255) / 256, 256, 0, stream>>>(cells[cur], nwords, planes[pcur]);
     CKG(cudaMemsetAsync(carry[pcur], 0, size_t(nbb) * sizeof(uint4), stream));
-    gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, wpt, bcounts[pcur]);
-    gridbits::grid_bits_scan_kernel<<<1, gridbits::kTPB, 0, stream>>>(bcounts[pcur], carry[pcur], nbb, pw,
+    gridbits::grid_bitcount_kernel<<<nbb, gridbits::kTPB, 0, stream>>>(planes[pcur], nwords, wpt, bcounts);
+    gridbits::grid_bits_scan_kernel<<<1, gridbits::kTPB, 0, stream>>>(bcounts, carry[pcur], nbb, pw,
                                                                      prank, rec + (steps_done % kRecCap));
     CKG(cudaGetLastError());
     launches += 3;
@@ -668,8 +668,8 @@ GpuGrid::GpuGrid(const SimParams& p) : impl_(new Impl) {
     for (int b = 0; b < 2; ++b) {
       CKG(cudaMalloc(&d.planes[b], size_t(d.nwords) * sizeof(uint4)));
       CKG(cudaMalloc(&d.carry[b], size_t(d.nbb) * sizeof(uint4)));
-      CKG(cudaMalloc(&d.bcounts[b], size_t(d.nbb) * 4));
     }
+    CKG(cudaMalloc(&d.bcounts, size_t(d.nbb) * 4));
     CKG(cudaMalloc(&d.prank, size_t(d.nbb) * 4));
   }
   CKG(cudaMemsetAsync(d.cells[0], kEmpty, d.L, d.stream));
@@ -703,8 +703,8 @@ GpuGrid::Impl::~Impl() {
   for (int b = 0; b < 2; ++b) {
     cudaFree(planes[b]);
     cudaFree(carry[b]);
-    cudaFree(bcounts[b]);
   }
+  cudaFree(bcounts);
   cudaFree(prank);
   cudaFreeHost(hrec);
   cudaFreeHost(hx);

@@ -173,3 +173,37 @@ def test_grid_bit_planes_words_per_thread(port, monkeypatch, wpt):
         assert (x == o["x"]).all() and (v == o["v"]).all()
         assert (g.sumv_series() == o["sumv"]).all() and (g.wrap_series() == o["wraps"]).all()
         assert g.checksum == o["checksum"]
+
+
+@pytest.mark.parametrize("mode", ["ascii", "pgm"])
+def test_grid_bit_planes_frames_match_reference_grid_engine(tmp_path, mode):
+    """Frames recorded from the bit planes (the row compacted on the device,
+    steps in between on the planes) written as ascii / pgm: byte-equal to the
+    files of the reference library's own grid engine (src/engine.cpp:186-196,
+    src/io.cpp:140-216)."""
+    import ctypes as C
+    import os
+    import oracle as O
+    ref = C.CDLL(os.path.join(os.path.dirname(O.__file__), "_ref", "libnasch_ref.so"))
+    ref.nasch_params_parse.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_void_p]
+    ref.nasch_sim_new_kind.argtypes = [C.c_void_p, C.c_uint, C.c_int, C.POINTER(C.c_void_p)]
+    ref.nasch_sim_run.argtypes = [C.c_void_p]
+    ref.nasch_sim_checksum.argtypes = [C.c_void_p]
+    ref.nasch_sim_checksum.restype = C.c_uint64
+    writer = getattr(ref, "nasch_sim_write_" + mode)
+    writer.argtypes = [C.c_void_p, C.c_char_p]
+    ref.nasch_sim_free.argtypes = [C.c_void_p]
+    text = f"length=640\nncars=150\nvmax=5\np=0.35\nsteps=90\nseed=12\nstride=9\noutput={mode}"
+    hp, hs = C.c_void_p(), C.c_void_p()
+    assert ref.nasch_params_parse(text.encode(), C.byref(hp), None) == 0
+    assert ref.nasch_sim_new_kind(hp, 1, GRID, C.byref(hs)) == 0
+    assert ref.nasch_sim_run(hs) == 0
+    assert writer(hs, str(tmp_path / "ref.out").encode()) == 0
+    ref_checksum = ref.nasch_sim_checksum(hs)
+    ref.nasch_sim_free(hs)
+    p, _ = nasch.SimParams.parse(text)
+    g = nasch.Engine(p, 1, GRID)
+    g.run()
+    assert g.frame_count == 10 and g.checksum == ref_checksum
+    getattr(g, "write_" + mode)(str(tmp_path / "ours.out"))
+    assert open(tmp_path / "ours.out", "rb").read() == open(tmp_path / "ref.out", "rb").read()
