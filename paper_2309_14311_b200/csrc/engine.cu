@@ -3,7 +3,8 @@
 //
 // Mode selection (per simulation, fixed at construction):
 //   warp ring -- N <= 512: ring_warp_kernel, one warp, cars in registers,
-//                whole chunks of steps per launch (resident_kernel.cuh).
+//                whole chunks of steps per launch (resident_kernel.cuh);
+//                256 < N <= 512: ring_quad_kernel, the same on four warps.
 //   resident  -- N <= 4096: ring_resident_kernel, one CTA, shared memory.
 //   DR        -- 4096 < N <= ~560k: ring_dr_kernel, the ring in registers
 //                across all SMs, a planner CTA one epoch ahead
@@ -83,6 +84,8 @@ struct GpuRing::Impl {
   bool tb = false;  // temporal-blocked mode
   bool resident = false;  // small ring: one CTA runs whole chunks of steps
   bool warp_ring = true;  // tiny rings (N <= 512): one warp, cars in registers
+  bool quad_all = false;  // NASCH_B200_QUADRING=2: every N <= 512 on four warps (tests)
+  bool quad_ring = true;  // 256 < N <= 512 (and ragged 128 < N <= 256): four warps (ring_quad_kernel)
   bool medium = false;    // TB with 512-car tiles (medium rings)
   bool dr = false;        // distributed-resident medium ring (dr_kernel.cuh)
   uint32_t dr_G = 0, dr_cpt = 0;
@@ -192,6 +195,18 @@ struct GpuRing::Impl {
 
   // One launch advancing k steps (k == 1 in single-step mode; any k in
   // resident mode).
+  // ring_quad_kernel: CPW = 1, 2 or 4 cars per thread on four warps.
+  template <typename VT>
+  void launch_quad(uint32_t k) {
+    const uint32_t cpw = n <= 128 ? 1 : n <= 256 ? 2 : 4;  // (NASCH_B200_QUADRING=2 sends every N <= 512 here)
+    const bool exact = n % cpw == 0;
+    if (cpw == 1) ring_quad_kernel<VT, 1, true><<<1, 128, 0, stream>>>(args, k);
+    else if (cpw == 2 && exact) ring_quad_kernel<VT, 2, true><<<1, 128, 0, stream>>>(args, k);
+    else if (cpw == 2) ring_quad_kernel<VT, 2, false><<<1, 128, 0, stream>>>(args, k);
+    else if (exact) ring_quad_kernel<VT, 4, true><<<1, 128, 0, stream>>>(args, k);
+    else ring_quad_kernel<VT, 4, false><<<1, 128, 0, stream>>>(args, k);
+  }
+
   void launch(uint32_t k) {
     if (dr) {
       launch_dr<uint8_t>(k);  // DR needs K(vmax+1) <= 256: u8 velocities
@@ -200,7 +215,12 @@ struct GpuRing::Impl {
     } else if (resident) {
       // Block width by ring size: a per-step barrier across 32 warps costs
       // more than a few extra cars per thread on a tiny ring (C1: 200 cars).
-      if (vbytes == 1) {
+      // (measured, tools/c1_probe.py: four warps 283 ns per step at N = 500
+      // against 513 on one warp with 16 cars per lane; N = 203: 264 / 321;
+      // N = 200, the EXACT one-warp instantiation: 273 / 250; N = 100: 265 / 195)
+      if (quad_ring && n <= 512 && (quad_all || n > 256 || (n > 128 && n % 8 != 0))) {
+        if (vbytes == 1) launch_quad<uint8_t>(k); else launch_quad<uint32_t>(k);
+      } else if (vbytes == 1) {
         if (warp_ring && n <= 128) {
           if (n % 4 == 0) ring_warp_kernel<uint8_t, 4, true><<<1, 32, 0, stream>>>(args, k);
           else ring_warp_kernel<uint8_t, 4><<<1, 32, 0, stream>>>(args, k);
@@ -1079,6 +1099,8 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // (NASCH_B200_RESIDENT=0 forces the one-step-per-launch kernel instead).
   d.resident = !d.tb && d.n <= kResidentMaxCars && env_long("NASCH_B200_RESIDENT", 1) != 0;
   d.warp_ring = env_long("NASCH_B200_WARPRING", 1) != 0;
+  d.quad_ring = env_long("NASCH_B200_QUADRING", 1) != 0;
+  d.quad_all = env_long("NASCH_B200_QUADRING", 1) == 2;
   // Medium rings: the distributed-resident kernel (dr_kernel.cuh) keeps the
   // ring in registers on every SM for whole chunks of steps
   // (NASCH_B200_DR=0 disables it).

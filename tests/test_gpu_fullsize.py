@@ -137,11 +137,14 @@ def test_config4_slice_full_length_vs_reference(ref):
     assert [int(t) for t in last] == [w[1] for w in want]
 
 
+@pytest.mark.parametrize("quad", ["0", "2"])
 @pytest.mark.parametrize("N", [200, 203, 509])
-def test_warp_ring_past_record_ring_ragged_chunks(port, N):
-    """The one-warp kernel (N <= 512; 200 is the EXACT instantiation) over
+def test_warp_ring_past_record_ring_ragged_chunks(port, monkeypatch, N, quad):
+    """The one-warp kernel (N <= 512; 200 is the EXACT instantiation) and the
+    four-warp kernel (NASCH_B200_QUADRING=2: every N <= 512) over
     69,901 steps -- past the 65,536-slot device step-record ring -- in
     chunks that are not multiples of 32, against the oracle."""
+    monkeypatch.setenv("NASCH_B200_QUADRING", quad)
     L, p, seed = 5 * N, 0.13, 42
     chunks = [31, 1000, 65537, 3333]
     T = sum(chunks)
@@ -158,3 +161,23 @@ def test_warp_ring_past_record_ring_ragged_chunks(port, N):
     assert len(sumv) == T
     assert (sumv == o["sumv"]).all() and (wraps == o["wraps"]).all()
     assert (x == o["x"]).all() and (v == o["v"]).all()
+
+
+@pytest.mark.parametrize("N,vmax", [(65, 3), (128, 5), (129, 5), (256, 7), (257, 2), (384, 5), (511, 5), (512, 300)])
+def test_quad_ring_every_instantiation_vs_oracle(port, monkeypatch, N, vmax):
+    """ring_quad_kernel (four warps, 1 / 2 / 4 cars per thread, exact and
+    ragged, u8 and u32 velocities) with the checksum on (row dumps) and a
+    chunked advance, against the oracle."""
+    monkeypatch.setenv("NASCH_B200_QUADRING", "2")
+    L, p, seed, T = 4 * N + 3, 0.3, 9, 700
+    x0, v0 = nasch.fill_uniform_state(L, N, min(vmax, 5), 13)
+    e = nasch.Engine(params(L, N, vmax, p, T, seed))
+    e.set_state(x0, v0)
+    e.advance(333)
+    e.advance(T - 333)
+    x, v = e.snapshot()
+    o = port.run(L, vmax, p, seed, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    assert e.checksum == o["checksum"]
+    e.close()
