@@ -41,6 +41,16 @@ namespace nb200 {
 #endif
 
 // L2 bulk prefetch of each warp's next tile (tb_kernel.cuh).
+// 1: a warp tile whose cars all take the plain path keeps its positions
+// relative to the warp's first car (< 2^24, so FP32 adds on the bit patterns
+// are exact): the headway and the move become FADDs on the FP32 lanes instead
+// of two IMADs on the FMA-heavy pipe.  Bit-exact (parity suite green), but
+// measured 0.7 % SLOWER on C3 and C5 (2.156e12 vs 2.171e12, 2.074e12 vs
+// 2.091e12; tools/ab_libs.py, round 2): the FMA-heavy pipe is not what holds
+// the kernel back.  Off.
+#ifndef NB_TB_FREL
+#define NB_TB_FREL 0
+#endif
 #ifndef NB_TB_PREFETCH
 #define NB_TB_PREFETCH 0
 #endif

@@ -178,6 +178,22 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
 #pragma unroll
     for (int c = 1; c < CPT; ++c) x[c] -= c;
 #endif
+    // Relative form (warp tiles whose cars are all plain): positions minus
+    // the warp's first car's, all below 2^24 for the whole launch, so the
+    // FP32 add of two bit patterns is their exact integer sum.
+    bool frel = false;
+    uint32_t xb = 0;
+#if NB_TB_FREL && NB_TB_MN3
+    if (WT) {
+      xb = __shfl_sync(0xffffffffu, x[0], 0);
+      const uint32_t xtop = __shfl_sync(0xffffffffu, x[CPT - 1], 31);
+      frel = __all_sync(0xffffffffu, plain) && xtop - xb < (1u << 24) - reach - 2u * CPT - vmax - 64u;
+      if (frel) {
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) x[c] -= xb;
+      }
+    }
+#endif
 
     for (uint32_t j = 0; j < k; ++j) {
       const uint4 pl = s_plan[j];
@@ -189,7 +205,7 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         xn = __shfl_down_sync(0xffffffffu, x[0], 1);
         // warp tiles: the front car of the warp's halo has no leader (its
         // error reaches at most k <= HALO cars back by the launch's end)
-        if (lane == 31) xn = x[CPT - 1];
+        if (lane == 31) xn = frel ? x[CPT - 1] + CPT + vmax + 1u : x[CPT - 1];  // (relative form: a free road ahead)
       } else {
         const uint32_t slot = phase++ & 1u;
         if (lane == 0) s_lead[slot][warp] = x[0];
@@ -199,6 +215,26 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
       }
       if (plain && !(base < bound && bound <= base + CPT)) {
         const uint32_t Q = mulmod_x2(P2, base < bound ? E : E2);
+#if NB_TB_FREL && NB_TB_MN3
+        if (frel) {
+          // the same car update with the headway and the move as exact FP32
+          // adds of the (relative, < 2^24) positions' bit patterns
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            const uint32_t s = mulmod_x2(c_apow2.v[c], Q);
+            const uint32_t xl = (c + 1 < CPT) ? x[c + 1 < CPT ? c + 1 : c] : xn - CPT;
+            const float gap = fadd_denorm(__uint_as_float(xl), -__uint_as_float(x[c]));
+            int dec;
+            asm("mul.hi.s32 %0, %1, 1;" : "=r"(dec) : "r"(static_cast<int>(tp * ra.neg1 + s)));
+            float m3;
+            asm("min.f32 %0, %1, %2, %3;" : "=f"(m3)
+                : "f"(fadd_denorm(__uint_as_float(v[c]), __uint_as_float(1u))),
+                  "f"(__uint_as_float(vmax)), "f"(gap));
+            v[c] = static_cast<uint32_t>(max(static_cast<int>(__float_as_uint(m3)) + dec, 0));
+            x[c] = __float_as_uint(fadd_denorm(__uint_as_float(x[c]), __uint_as_float(v[c])));
+          }
+        } else
+#endif
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           // Balanced between the FMA and ALU pipes (both issue a warp
@@ -258,6 +294,11 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         const uint32_t QEw = mulmod_d(QE, ra.an_inv), QE2w = mulmod_d(QE2, ra.an_inv);
         Acc sum = 0;
         uint32_t crs = 0;
+        if (frel) {  // the rank seam inside a relative tile: absolute for this step
+          xn += xb;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) x[c] += xb;
+        }
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           const bool wrapped = base + c >= N;
@@ -280,7 +321,15 @@ __device__ __forceinline__ void tb_body(const RingArgs& ra, const uint32_t k, co
         }
         s_acc[j][threadIdx.x] += sum;
         if (crs) atomicAdd(&ra.rec[(t + j) % kRecCap].c, crs);
+        if (frel) {
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) x[c] -= xb;
+        }
       }
+    }
+    if (frel) {
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) x[c] += xb;
     }
 #if NB_TB_MN3
 #pragma unroll
