@@ -5,7 +5,8 @@
 //   warp ring -- N <= 512: ring_warp_kernel, one warp, cars in registers,
 //                whole chunks of steps per launch (resident_kernel.cuh);
 //                256 < N <= 512: ring_quad_kernel, the same on four warps.
-//   resident  -- N <= 4096: ring_resident_kernel, one CTA, shared memory.
+//   resident  -- N <= 4096: ring_resident_kernel, one CTA, shared memory
+//                (only where the distributed-resident kernel does not apply).
 //   DR        -- 4096 < N <= ~560k: ring_dr_kernel, the ring in registers
 //                across all SMs, a planner CTA one epoch ahead
 //                (dr_kernel.cuh, cone_warp.cuh).
@@ -1105,7 +1106,12 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   // ring in registers on every SM for whole chunks of steps
   // (NASCH_B200_DR=0 disables it).
   std::vector<uint32_t> dr_seg;
-  if (d.n > kResidentMaxCars && env_long("NASCH_B200_DR", 1) != 0) {
+  // From 513 cars up (NASCH_B200_DR_MIN raises it): 0.44 us per step from
+  // 600 cars on, where the one-CTA shared-memory kernel takes 0.9-1.3 us
+  // (tools/small_ring_sweep.py); that kernel remains the path of rings the DR
+  // conditions below exclude (u32 velocities, L <= 2 K vmax).
+  const long dr_min = std::max(512l, env_long("NASCH_B200_DR_MIN", 512));
+  if (d.n > uint64_t(dr_min) && env_long("NASCH_B200_DR", 1) != 0) {
     // 32-step epochs (C2: 4.0e11 vs 3.4e11 at 16 with the four-warp cone)
     const long kreq_dr = env_long("NASCH_B200_K", kDrKMax);
     uint32_t Kd = static_cast<uint32_t>(std::max<long>(1, std::min<long>(kreq_dr, kDrKMax)));

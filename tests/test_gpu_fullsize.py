@@ -181,3 +181,25 @@ def test_quad_ring_every_instantiation_vs_oracle(port, monkeypatch, N, vmax):
     assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
     assert e.checksum == o["checksum"]
     e.close()
+
+
+@pytest.mark.parametrize("dr_min", ["512", "4096"])
+@pytest.mark.parametrize("N", [513, 600, 2000, 4096])
+def test_rings_of_513_to_4096_cars_both_engines_vs_oracle(port, monkeypatch, N, dr_min):
+    """513..4096 cars: the distributed-resident kernel (default from 513 cars:
+    0.44 us per step against 0.9-1.3 on one CTA) and the one-CTA shared-memory
+    kernel (NASCH_B200_DR_MIN=4096; still the path of u32-velocity rings),
+    checksum on, chunked advance, against the oracle."""
+    monkeypatch.setenv("NASCH_B200_DR_MIN", dr_min)
+    L, p, seed, T = 4 * N + 1, 0.25, 17, 300
+    x0, v0 = nasch.fill_uniform_state(L, N, 5, 19)
+    e = nasch.Engine(params(L, N, 5, p, T, seed))
+    e.set_state(x0, v0)
+    e.advance(101)
+    e.advance(T - 101)
+    x, v = e.snapshot()
+    o = port.run(L, 5, p, seed, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    assert e.checksum == o["checksum"]
+    e.close()

@@ -22,7 +22,7 @@ rd = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 port = O.Port()
 GRID = nasch.Engine.GRID_REFERENCE
 t_end = time.time() + budget
-ngrid = nquad = 0
+ngrid = nquad = nmid = 0
 
 
 def compare(e, o, what):
@@ -76,4 +76,24 @@ while time.time() < t_end:
     compare(e, o, ("quad", L, N, vmax, p, T, seed))
     e.close()
     nquad += 1
-print(f"fuzz ok: {ngrid} grid cases, {nquad} four-warp cases", flush=True)
+    # 513..4096 cars: the distributed-resident kernel (one-CTA kernel where it does not apply)
+    os.environ.pop("NASCH_B200_QUADRING", None)
+    if ngrid % 8 == 0:
+        N = rd.randrange(513, 4097)
+        L = N + rd.randrange(0, 5 * N)
+        vmax = rd.choice([1, 3, 5, 7, 300])
+        p = rd.choice([0.0, 1.0, rd.random()])
+        T = rd.randrange(1, 200)
+        seed = rd.getrandbits(63)
+        x0, v0 = port.fill_uniform_state(L, N, min(vmax, L - 1, rd.randrange(0, 6)), rd.getrandbits(32))
+        x0, v0 = np.asarray(x0, np.uint64), np.asarray(v0, np.uint64)
+        o = port.run(L, vmax, p, seed, T, x0, v0)
+        e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=seed))
+        e.set_state(x0, v0)
+        k = rd.randrange(0, T + 1)
+        e.advance(k)
+        e.advance(T - k)
+        compare(e, o, ("mid", L, N, vmax, p, T, seed))
+        e.close()
+        nmid += 1
+print(f"fuzz ok: {ngrid} grid cases, {nquad} four-warp cases, {nmid} rings of 513..4096 cars", flush=True)
