@@ -1196,7 +1196,11 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
   }
   // Temporal-blocked kernels: several block waves (tb_config.hpp kTbWaves);
   // the one-step kernel stays persistent (HBM-bound, one wave).
-  const uint32_t waves = d.tb ? static_cast<uint32_t>(std::max<long>(1, env_long("NASCH_B200_WAVES", kTbWaves))) : 1u;
+  // Block tiles (0.56M-2.3M cars): 2 waves -- fewer, longer-lived blocks pay
+  // the per-block plan load and velocity-sum reduction less often (measured,
+  // tools/tile_ab.py: N = 1e6 1.88 -> 1.69 us per step, 2e6 2.96 -> 2.54).
+  const uint32_t waves =
+      d.tb ? static_cast<uint32_t>(std::max<long>(1, env_long("NASCH_B200_WAVES", d.medium ? 2 : kTbWaves))) : 1u;
   d.grid = static_cast<int>(std::max<uint64_t>(
       1, std::min<uint64_t>(ntiles, uint64_t(sms) * std::max(per_sm, 1) * waves)));
   // Test knob: force a grid size, to show results do not depend on the
