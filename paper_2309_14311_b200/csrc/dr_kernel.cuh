@@ -296,7 +296,11 @@ constexpr uint32_t dr_capacity() {
   return (TPB / 32) * (32u * CPT - kDrHalo);
 }
 
-template <typename VT, int TPB, int CPT>
+// QDRAW: the draw of car c of a thread as (E a^id0) a^c -- one product per
+// thread and step times the constant-bank 2 a^c, as in nasch_tb_kernel --
+// instead of a per-car multiplier register pair and id (three registers per
+// car): what lets 32 cars per thread fit, i.e. rings up to ~1.17M cars.
+template <typename VT, int TPB, int CPT, bool QDRAW = false>
 __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, const DrArgs da, const uint32_t steps) {
   using Acc = typename std::conditional<sizeof(VT) == 1, uint32_t, unsigned long long>::type;
   constexpr int NW = TPB / 32;
@@ -324,21 +328,39 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
   // Cars past S are the halo (the next segment's first cars; slots past
   // those replicate the last one and are never used).
   const uint32_t span = S + kDrHalo;
-  uint32_t idc[CPT], ap[CPT], apB[CPT], x[CPT], v[CPT];
+  constexpr int NM = QDRAW ? 1 : CPT;  // per-car multipliers and ids only without QDRAW
+  uint32_t idc[NM], ap[NM], apB[NM], x[CPT], v[CPT];
   uint32_t own = 0;
+  uint32_t P2 = 0;  // QDRAW: 2 a^base
+  if constexpr (QDRAW) {
+    P2 = (wactive ? powmod(kA, base) : 1u) << 1;  // once per launch
 #pragma unroll
-  for (int c = 0; c < CPT; ++c) {
-    const uint32_t li = min(i0 + c, span - 1);
-    uint32_t id = lo + li;
-    const bool wrapped = id >= N;
-    if (wrapped) id -= N;
-    idc[c] = id;
-    uint32_t a = wactive ? powmod(kA, id) : 1u;  // once per launch
-    ap[c] = a << 1;                              // ids below the rank seam
-    apB[c] = mulmod(a, ra.an_inv) << 1;          // at or past it
-    own |= (u0 + c < OW && i0 + c < S) ? (1u << c) : 0u;
+    for (int c = 0; c < CPT; ++c) own |= (u0 + c < OW && i0 + c < S) ? (1u << c) : 0u;
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+      const uint32_t li = min(i0 + c, span - 1);
+      uint32_t id = lo + li;
+      const bool wrapped = id >= N;
+      if (wrapped) id -= N;
+      idc[c] = id;
+      uint32_t a = wactive ? powmod(kA, id) : 1u;  // once per launch
+      ap[c] = a << 1;                              // ids below the rank seam
+      apB[c] = mulmod(a, ra.an_inv) << 1;          // at or past it
+      own |= (u0 + c < OW && i0 + c < S) ? (1u << c) : 0u;
+    }
   }
-  const bool own_all = own == (1u << CPT) - 1u;
+  // the id of slot c (halo slots past the span replicate its last car)
+  auto slot_id = [&](int c) {
+    if constexpr (QDRAW) {
+      uint32_t id = lo + min(i0 + static_cast<uint32_t>(c), span - 1);
+      if (id >= N) id -= N;
+      return id;
+    } else {
+      return idc[c];
+    }
+  };
+  const bool own_all = CPT == 32 ? own == 0xffffffffu : own == (1u << (CPT & 31)) - 1u;
   const bool nowrap = base + CPT <= N;  // ids of this thread's cars run consecutively
   const uint32_t nE = (steps + da.K - 1) / da.K;
   for (uint32_t i = threadIdx.x; i < kDrKMax * NW; i += TPB) (&s_wacc[0][0])[i] = 0;
@@ -366,8 +388,9 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
       const VT* V = vbuf<VT>(ra, bi);
 #pragma unroll
       for (int c = 0; c < CPT; ++c) {
-        x[c] = __ldcg(X + idc[c]);
-        v[c] = static_cast<uint32_t>(__ldcg(V + idc[c]));
+        const uint32_t id = slot_id(c);
+        x[c] = __ldcg(X + id);
+        v[c] = static_cast<uint32_t>(__ldcg(V + id));
       }
     } else {
       // Halo slots: the next warp's first cars (shared memory, written at
@@ -407,9 +430,10 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
         const bool tplain = plain && !(base < bound && bound <= base + CPT);
         if (__all_sync(0xffffffffu, tplain)) {
           const uint32_t Es = base < bound ? E : E2;
+          const uint32_t Qs = QDRAW ? mulmod_x2(P2, Es) : 0u;
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
-            const uint32_t s = mulmod_x2(ap[c], Es);
+            const uint32_t s = QDRAW ? mulmod_x2(c_apow2.v[c], Qs) : mulmod_x2(ap[QDRAW ? 0 : c], Es);
             const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
             const uint32_t d = x[c] * ra.neg1 + xl;
             const int vc = static_cast<int>(min(min(v[c] + 1, vmax), d - 1));
@@ -432,9 +456,19 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
           // and position modulo L as unsigned min's (L < 2^31).
           Acc sum = 0;
           uint32_t crs = 0;
+          // QDRAW: base E or E2 by rank side, a^-N for ids wrapped past N-1
+          const uint32_t QE = QDRAW ? mulmod_x2(P2, E) : 0u, QE2 = QDRAW ? mulmod_x2(P2, E2) : 0u;
+          const uint32_t QEw = QDRAW ? mulmod_d(QE, ra.an_inv) : 0u, QE2w = QDRAW ? mulmod_d(QE2, ra.an_inv) : 0u;
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
-            const uint32_t s = mulmod_x2(idc[c] < bound ? ap[c] : apB[c], E);
+            uint32_t s;
+            if constexpr (QDRAW) {
+              const bool wrapped = base + c >= N;
+              const uint32_t id = wrapped ? base + c - N : base + c;
+              s = mulmod_x2(c_apow2.v[c], id < bound ? (wrapped ? QEw : QE) : (wrapped ? QE2w : QE2));
+            } else {
+              s = mulmod_x2(idc[c] < bound ? ap[c] : apB[c], E);
+            }
             const uint32_t xl = (c + 1 < CPT) ? x[c + 1] : xn;
             uint32_t d = x[c] * ra.neg1 + xl;
             d = min(d, d + L);  // leader past the origin: + L
@@ -493,8 +527,9 @@ __global__ void __launch_bounds__(TPB, 1) ring_dr_kernel(const RingArgs ra, cons
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
           if ((own >> c) & 1u) {
-            Xo[idc[c]] = x[c];
-            Vo[idc[c]] = static_cast<VT>(v[c]);
+            const uint32_t id = slot_id(c);
+            Xo[id] = x[c];
+            Vo[id] = static_cast<VT>(v[c]);
           }
         }
       }

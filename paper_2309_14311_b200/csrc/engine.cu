@@ -165,12 +165,12 @@ struct GpuRing::Impl {
   StepRec* hrec = nullptr;
   Ctl* hctl = nullptr;
 
-  template <typename VT, int TPB, int CPT>
+  template <typename VT, int TPB, int CPT, bool QDRAW = false>
   void launch_dr_cpt(uint32_t k) {
     DrArgs da{dplans, dmbox, dsync, dseg, dr_G, K};
     void* kargs[] = {&args, &da, &k};
     CK(cudaMemsetAsync(dsync, 0, (2 + dr_G) * sizeof(unsigned int), stream));
-    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, TPB, CPT>),
+    CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&ring_dr_kernel<VT, TPB, CPT, QDRAW>),
                                    dim3(dr_G + 1), dim3(TPB), kargs, 0, stream));
   }
   template <typename VT>
@@ -178,7 +178,10 @@ struct GpuRing::Impl {
     switch (dr_geom) {
       case 0: launch_dr_cpt<VT, kDrTPB, 4>(k); break;
       case 1: launch_dr_cpt<VT, kDrTPB, 8>(k); break;
-      default: launch_dr_cpt<VT, kDrTPB, 16>(k); break;
+      case 2: launch_dr_cpt<VT, kDrTPB, 16>(k); break;
+      case 3: launch_dr_cpt<VT, kDrTPB, 20, true>(k); break;
+      case 4: launch_dr_cpt<VT, kDrTPB, 24, true>(k); break;
+      default: launch_dr_cpt<VT, kDrTPB, 32, true>(k); break;
     }
   }
 
@@ -1128,13 +1131,21 @@ GpuRing::GpuRing(const SimParams& params) : impl_(new Impl) {
     // blocks with 4 or 8 cars per thread measured 3-4 % slower on C2);
     // NASCH_B200_DR_GEOM forces one (index) for experiments
     struct G2 { int tpb; uint32_t cpt; uint32_t cap; const void* fn; };
-    const G2 geoms[3] = {
+    // (20 / 24 / 32 cars per thread: the draw as one per-thread base times
+    // 2 a^c, QDRAW in dr_kernel.cuh -- rings of 0.56M..1.17M cars)
+    const G2 geoms[6] = {
         {kDrTPB, 4, dr_capacity<kDrTPB, 4>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 4>)},
         {kDrTPB, 8, dr_capacity<kDrTPB, 8>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 8>)},
-        {kDrTPB, 16, dr_capacity<kDrTPB, 16>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>)}};
+        {kDrTPB, 16, dr_capacity<kDrTPB, 16>(), reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 16>)},
+        {kDrTPB, 20, dr_capacity<kDrTPB, 20>(),
+         reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 20, true>)},
+        {kDrTPB, 24, dr_capacity<kDrTPB, 24>(),
+         reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 24, true>)},
+        {kDrTPB, 32, dr_capacity<kDrTPB, 32>(),
+         reinterpret_cast<const void*>(&ring_dr_kernel<uint8_t, kDrTPB, 32, true>)}};
     const long gforce = env_long("NASCH_B200_DR_GEOM", -1);
     int gi = -1;
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 6; ++i)
       if ((gforce < 0 || gforce == i) && gi < 0 && segsz <= geoms[i].cap) gi = i;
     if (gi >= 0) cptd = geoms[gi].cpt;
     if (coop && sms >= 2 && cptd && Kd >= 2 && d.vbytes == 1 && uint64_t(d.L) > 2ull * Kd * d.vmax_eff) {

@@ -203,3 +203,28 @@ def test_rings_of_513_to_4096_cars_both_engines_vs_oracle(port, monkeypatch, N, 
     assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
     assert e.checksum == o["checksum"]
     e.close()
+
+
+@pytest.mark.parametrize("L,N,vmax,p,T", [
+    (5 * 20000, 20000, 5, 0.3, 70),       # forced onto few, mostly empty 32-car threads
+    (3 * 640000, 640000, 5, 0.25, 64),    # 20 cars per thread (564k..715k cars), density 1/3
+    (2 * 800000, 800000, 7, 0.1, 48),     # 24 cars per thread (..865k cars)
+    (1150000 + 7, 1150000, 3, 0.5, 40)])  # near its capacity, an almost full road
+def test_dr_32_cars_per_thread_vs_oracle(port, monkeypatch, L, N, vmax, p, T):
+    """ring_dr_kernel<u8,256,20|24|32,QDRAW> (draws from one per-thread base
+    times 2 a^c; rings of 0.56M..1.17M cars, or NASCH_B200_DR_GEOM=3..5) against the
+    oracle: state, both series, checksum, a chunked advance across launches."""
+    if N < 564000:
+        monkeypatch.setenv("NASCH_B200_DR_GEOM", "5")
+    x0, v0 = nasch.fill_uniform_state(L, N, vmax, 23)
+    e = nasch.Engine(params(L, N, vmax, p, T, 29))
+    assert e.steps_per_launch > 32  # the distributed-resident engine
+    e.set_state(x0, v0)
+    e.advance(33)
+    e.advance(T - 33)
+    x, v = e.snapshot()
+    o = port.run(L, vmax, p, 29, T, x0.astype(np.uint64), v0.astype(np.uint64))
+    assert (x == o["x"]).all() and (v == o["v"]).all()
+    assert (e.sumv_series() == o["sumv"]).all() and (e.wrap_series() == o["wraps"]).all()
+    assert e.checksum == o["checksum"]
+    e.close()
