@@ -48,9 +48,11 @@ def cores(ref):
 
 
 def test_config3_full_size_three_launches_vs_reference(ref):
-    """C3 exactly as bench.py runs it: 2e8 cars, three full launches of the
+    """C3 exactly as bench.py runs it: 2e8 cars, two full launches of the
     default depth (K = 32 steps; enqueued one launch at a time, as the
-    timed region does), including the plan hand-off between launches."""
+    timed region does) and a shorter third one (8 steps), i.e. 72 steps and
+    both plan hand-offs between launches (the reference's side of the check
+    costs ~1.8 s per step on 16 cores)."""
     L, N, p, seed = 10**9, 2 * 10**8, 0.13, 3
     x0, v0 = nasch.fill_uniform_state(L, N, 0, seed)
     e = nasch.Engine(params(L, N, 5, p, 1000, seed))
@@ -58,9 +60,9 @@ def test_config3_full_size_three_launches_vs_reference(ref):
     e.set_state(x0, v0)
     K = e.steps_per_launch
     assert K == 32
-    T = 3 * K
-    for _ in range(3):
-        e.enqueue(K)
+    T = 2 * K + 8
+    for k in (K, K, 8):
+        e.enqueue(k)
     e.synchronize()
     x, v = e.snapshot()
     sumv, wraps = e.sumv_series(), e.wrap_series()
@@ -72,6 +74,17 @@ def test_config3_full_size_three_launches_vs_reference(ref):
     assert (wraps == r["wraps"]).all(), "per-step crossing counts differ"
     assert (x == r["x"]).all(), "positions differ"
     assert (v == r["v"]).all(), "velocities differ"
+
+
+_C5 = {}
+
+
+def c5_reference(ref, L, N, p, seed, T, x0, v0):
+    """The reference's 64 steps of C5, run once for the three K's (it does not
+    depend on K): ~30 s on 16 cores."""
+    if "r" not in _C5:
+        _C5["r"] = ref.run(L, N, 5, p, seed, T, x0=x0.astype(np.uint64), v0=v0.astype(np.uint64), workers=cores(ref))
+    return _C5["r"]
 
 
 @pytest.mark.parametrize("K", [8, 16, 32])
@@ -96,8 +109,7 @@ def test_config5_full_size_vs_reference_with_snapshot(ref, k_env, K):
     e.synchronize()
     sumv, wraps = e.sumv_series()[:T], e.wrap_series()[:T]
     e.close()
-    r = ref.run(L, N, 5, p, seed, T, x0=x0.astype(np.uint64), v0=v0.astype(np.uint64),
-                workers=cores(ref))
+    r = c5_reference(ref, L, N, p, seed, T, x0, v0)
     assert (sumv == r["sumv"]).all() and (wraps == r["wraps"]).all()
     assert (sx == r["x"]).all() and (sv == r["v"]).all()
 
