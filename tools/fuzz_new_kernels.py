@@ -22,7 +22,7 @@ rd = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 port = O.Port()
 GRID = nasch.Engine.GRID_REFERENCE
 t_end = time.time() + budget
-ngrid = nquad = nmid = 0
+ngrid = nquad = nmid = nq = 0
 
 
 def compare(e, o, what):
@@ -96,4 +96,25 @@ while time.time() < t_end:
         compare(e, o, ("mid", L, N, vmax, p, T, seed))
         e.close()
         nmid += 1
-print(f"fuzz ok: {ngrid} grid cases, {nquad} four-warp cases, {nmid} rings of 513..4096 cars", flush=True)
+    # the distributed-resident kernel at 20 / 24 / 32 cars per thread (QDRAW), forced on medium rings
+    if ngrid % 16 == 0:
+        os.environ["NASCH_B200_DR_GEOM"] = rd.choice(["3", "4", "5"])
+        N = rd.randrange(4200, 60000)
+        L = N + rd.randrange(0, 5 * N)
+        vmax = rd.choice([1, 3, 5, 7])
+        p = rd.choice([0.0, 1.0, rd.random()])
+        T = rd.randrange(1, 120)
+        seed = rd.getrandbits(63)
+        x0, v0 = port.fill_uniform_state(L, N, min(vmax, L - 1, rd.randrange(0, 6)), rd.getrandbits(32))
+        x0, v0 = np.asarray(x0, np.uint64), np.asarray(v0, np.uint64)
+        o = port.run(L, vmax, p, seed, T, x0, v0)
+        e = nasch.Engine(nasch.SimParams(length=L, ncars=N, vmax=vmax, p=p, steps=T, seed=seed))
+        e.set_state(x0, v0)
+        k = rd.randrange(0, T + 1)
+        e.advance(k)
+        e.advance(T - k)
+        compare(e, o, ("qdraw", os.environ["NASCH_B200_DR_GEOM"], L, N, vmax, p, T, seed))
+        e.close()
+        os.environ.pop("NASCH_B200_DR_GEOM", None)
+        nq += 1
+print(f"fuzz ok: {nq} QDRAW rings, {ngrid} grid cases, {nquad} four-warp cases, {nmid} rings of 513..4096 cars", flush=True)
